@@ -1,0 +1,381 @@
+"""Pins for the fp64 oracle (CPU only).  Each test fixes an oracle function against something
+other than itself: NumPy/SciPy brute force with a materialised P, a library routine (torch SDPA
+in fp64), a closed form, an invariant, or a value the paper prints (tests/golden/*, cited).
+Each pin is chosen so a plausible slip (dropped term, wrong sign/index, transposed operand,
+off-by-one block edge) fails it."""
+import itertools
+import math
+
+import numpy as np
+import pytest
+import scipy.special
+import torch
+
+from conftest import golden_lines
+from paper_2603_05503_b200 import inputs
+
+
+def _rand(n, d, seed):
+    rng = np.random.default_rng(seed)
+    return rng.standard_normal((n, d)), rng.standard_normal((n, d)), rng.standard_normal((n, d))
+
+
+def _block_of(n, b):
+    return np.arange(n) // b
+
+
+def brute_masked(q, k, v, scale, b, mask):
+    """Materialised P with -inf outside kept blocks, SciPy softmax (independent of the oracle)."""
+    n = q.shape[0]
+    logits = scale * (q @ k.T)
+    if mask is not None:
+        blk = _block_of(n, b)
+        keep = mask[blk[:, None], blk[None, :]].astype(bool)
+        logits = np.where(keep, logits, -np.inf)
+    p = scipy.special.softmax(logits, axis=1)
+    return p @ v, scipy.special.logsumexp(logits, axis=1), p
+
+
+# ---------------------------------------------------------------- a7: masked attention
+@pytest.mark.parametrize("n,b,d", [(256, 64, 64), (250, 64, 64), (200, 32, 16)])
+def test_masked_attention_equals_brute_force(orc, n, b, d):
+    q, k, v = _rand(n, d, 1)
+    nb = orc.num_blocks(n, b)
+    rng = np.random.default_rng(7)
+    mask = (rng.random((nb, nb)) < 0.5).astype(np.uint8)
+    mask[np.arange(nb), np.arange(nb)] = 1
+    if n == 256:
+        mask = inputs.TINY_HAND_MASK.copy()
+    scale = 1.0 / math.sqrt(d)
+    out, lse = orc.masked_attention_rows(q, k, v, scale, b, mask)
+    ref, ref_lse, p = brute_masked(q, k, v, scale, b, mask)
+    assert np.max(np.abs(out - ref)) < 1e-12
+    assert np.max(np.abs(lse - ref_lse)) < 1e-12
+    # row sums over kept keys are 1 (P:505-507 'row ... sums up to 1' applied to kept support)
+    logits = scale * (q @ k.T)
+    blk = _block_of(n, b)
+    keep = mask[blk[:, None], blk[None, :]].astype(bool)
+    rs = np.where(keep, np.exp(logits - lse[:, None]), 0.0).sum(axis=1)
+    assert np.max(np.abs(rs - 1.0)) < 1e-12
+    # each output coordinate lies in [min, max] of the kept V rows (convex combination)
+    for i in range(0, n, 17):
+        vk = v[keep[i]]
+        assert np.all(out[i] <= vk.max(axis=0) + 1e-12) and np.all(out[i] >= vk.min(axis=0) - 1e-12)
+
+
+def test_all_ones_mask_equals_library_dense_attention(orc):
+    """All-ones plan == dense attention computed by torch SDPA in fp64."""
+    n, d, b = 250, 64, 64
+    q, k, v = _rand(n, d, 3)
+    scale = 1.0 / math.sqrt(d)
+    out, _ = orc.masked_attention_rows(q, k, v, scale, b, np.ones((4, 4), np.uint8))
+    out2, _ = orc.masked_attention_rows(q, k, v, scale, b, None)
+    t = lambda a: torch.from_numpy(a)[None, None]
+    ref = torch.nn.functional.scaled_dot_product_attention(t(q), t(k), t(v), scale=scale)[0, 0].numpy()
+    assert np.max(np.abs(out - ref)) < 1e-12
+    assert np.array_equal(out, out2)
+
+
+def test_exact_block_structure_sparse_equals_dense(orc):
+    """Logits ~ -inf outside a block pattern + the matching mask -> sparse == dense."""
+    n, b, d = 256, 64, 64
+    nb = 4
+    mask = inputs.TINY_HAND_MASK
+    rng = np.random.default_rng(5)
+    A = math.sqrt(90.0 * math.sqrt(d))  # sigma*A^2 = 90: off-pattern weight e^-90 relative
+    blk = _block_of(n, b)
+    q = 0.05 * rng.standard_normal((n, d))
+    k = 0.05 * rng.standard_normal((n, d))
+    q[:, :nb] += A * mask[blk]                    # row r's indicator of kept columns
+    k[:, :nb] += A * np.eye(nb)[blk]               # column c's one-hot
+    v = rng.standard_normal((n, d))
+    scale = 1.0 / math.sqrt(d)
+    sparse, _ = orc.masked_attention_rows(q, k, v, scale, b, mask)
+    dense, _ = orc.masked_attention_rows(q, k, v, scale, b, None)
+    assert np.max(np.abs(sparse - dense)) < 1e-12
+
+
+def test_single_block_row_is_convex_combination_of_that_block(orc):
+    n, b, d = 256, 64, 8
+    q, k, v = _rand(n, d, 9)
+    mask = np.eye(4, dtype=np.uint8)[[2, 0, 3, 1]]
+    out, _ = orc.masked_attention_rows(q, k, v, 0.3, b, mask)
+    for i in range(n):
+        c = int(np.argmax(mask[i // b]))
+        vb = v[c * b:(c + 1) * b]
+        assert np.all(out[i] <= vb.max(0) + 1e-12) and np.all(out[i] >= vb.min(0) - 1e-12)
+
+
+# ---------------------------------------------------------------- a8: anchor rows
+def test_anchor_rows_and_nearest(orc):
+    for line in golden_lines("worked_examples.txt"):
+        if line.startswith("anchors"):
+            lhs, rhs = line.split("|")
+            _, H, kA = lhs.split()
+            assert orc.anchor_rows(int(H), int(kA)) == [int(x) for x in rhs.split()]
+    assert orc.anchor_rows(30, 30) == list(range(30))
+    # brute-force nearest with explicit tie rule (lower anchor)
+    for H in (1, 5, 8, 30, 45):
+        for kA in range(1, H + 1):
+            a = orc.anchor_rows(H, kA)
+            for i in range(H):
+                dist = [abs(i - x) for x in a]
+                assert orc.nearest_anchor(H, kA, i) == dist.index(min(dist))
+            # max distance bound of a centred equispaced placement
+            assert max(min(abs(i - x) for x in a) for i in range(H)) <= math.ceil(H / (2 * kA))
+
+
+def test_anchor_sparsity_matches_paper_table(orc):
+    """1 - k/H reproduces Table tab:anchor_bench's sparsity column."""
+    H = 30
+    n = 21 * 30 * 52
+    for line in golden_lines("anchor_bench_sparsity.txt"):
+        kA, pct = line.split()
+        kA = int(kA)
+        # kept area of a REPETITIVE cell: F*k*W queries x N keys
+        cell = orc.compile_cell(np.zeros((256, 256)), n, 128, 21, H, 52, 1, similarity=1.0,
+                                gamma=0.87, anchor_k=kA)
+        assert cell["kind"] == 1
+        assert round(100 * orc.sparsity_of_cell(cell["kept_area"], n), 1) == float(pct)
+
+
+def test_anchor_k_equals_H_is_dense_and_repetitive_workload_exact(orc):
+    F, H, W, d = 2, 6, 5, 8
+    n = F * H * W
+    q, k, v = _rand(n, d, 11)
+    dense, _ = orc.masked_attention_rows(q, k, v, 0.4, 64, None)
+    full, _ = orc.anchor_attention_rows(F, H, W, q, k, v, 0.4, H)
+    assert np.max(np.abs(full - dense)) < 1e-14
+    # queries depending only on (f, j): every spatial row is identical -> anchors exact
+    rng = np.random.default_rng(3)
+    base = rng.standard_normal((F, 1, W, d))
+    qr = np.broadcast_to(base, (F, H, W, d)).reshape(n, d)
+    dense_r, _ = orc.masked_attention_rows(qr, k, v, 0.4, 64, None)
+    for kA in (1, 2, 5):
+        out, _ = orc.anchor_attention_rows(F, H, W, qr, k, v, 0.4, kA)
+        assert np.max(np.abs(out - dense_r)) < 1e-12
+
+
+def test_anchor_broadcast_is_positionwise_copy_of_nearest_anchor(orc):
+    F, H, W, d = 2, 7, 4, 4
+    n = F * H * W
+    q, k, v = _rand(n, d, 12)
+    out, _ = orc.anchor_attention_rows(F, H, W, q, k, v, 0.5, 3)
+    dense, _ = orc.masked_attention_rows(q, k, v, 0.5, 64, None)
+    a = orc.anchor_rows(H, 3)
+    for f in range(F):
+        for i in range(H):
+            m = orc.nearest_anchor(H, 3, i)
+            for j in range(W):
+                t = f * H * W + i * W + j
+                s = f * H * W + a[m] * W + j
+                assert np.array_equal(out[t], out[s])
+                assert np.max(np.abs(out[t] - dense[s])) < 1e-14
+
+
+# ---------------------------------------------------------------- a2/a3: LSE and block energy
+def test_lse_and_energy_against_materialised_P(orc):
+    n, b, d = 250, 64, 16
+    q, k, _ = _rand(n, d, 21)
+    scale = 0.7
+    lse = orc.row_lse(q, k, scale)
+    assert np.max(np.abs(lse - scipy.special.logsumexp(scale * q @ k.T, axis=1))) < 1e-12
+    E = orc.block_energy(q, k, scale, b)
+    p = scipy.special.softmax(scale * q @ k.T, axis=1)
+    nb = 4
+    ref = np.zeros((nb, nb))
+    for r in range(nb):
+        rows = slice(r * b, min((r + 1) * b, n))
+        for c in range(nb):
+            ref[r, c] = p[rows, c * b:min((c + 1) * b, n)].sum() / p[rows].shape[0]
+    assert np.max(np.abs(E - ref)) < 1e-12
+    assert np.max(np.abs(E.sum(axis=1) - 1.0)) < 1e-12      # P:507 rows sum to 1 (ragged too)
+    E2 = orc.block_energy(q, k, scale, b, lse=lse)
+    assert np.max(np.abs(E2 - E)) < 1e-15
+
+
+def test_energy_uniform_and_block_diagonal_closed_forms(orc):
+    n, b, d = 250, 64, 16
+    # q = 0 -> every P_ij = 1/N -> E_rc = |J_c| / N
+    q = np.zeros((n, d))
+    k = np.random.default_rng(1).standard_normal((n, d))
+    E = orc.block_energy(q, k, 1.0, b)
+    sizes = np.array([64, 64, 64, 58])
+    assert np.max(np.abs(E - sizes[None, :] / n)) < 1e-15
+    # block-diagonal P (each query attends inside its own block) -> E = I
+    blk = _block_of(n, b)
+    A = math.sqrt(200.0)
+    q = np.zeros((n, d)); k = np.zeros((n, d))
+    q[:, :4] = A * np.eye(4)[blk]
+    k[:, :4] = A * np.eye(4)[blk]
+    E = orc.block_energy(q, k, 1.0, b)
+    assert np.max(np.abs(E - np.eye(4))) < 1e-12
+
+
+# ---------------------------------------------------------------- a4: selection
+def test_selection_worked_examples(orc):
+    for line in golden_lines("worked_examples.txt"):
+        if not line.startswith("select"):
+            continue
+        lhs, e, kept = line.split("|")
+        eps = float(lhs.split()[1])
+        e = np.array([float(x) for x in e.split()])
+        exp = np.zeros(e.size, np.uint8)
+        exp[[int(x) for x in kept.split()]] = 1
+        assert np.array_equal(orc.select(e, eps), exp)
+
+
+def test_selection_is_minimal_against_subset_brute_force(orc):
+    """Eq. eq:row_energy_constraint solved exactly (P:533 'optimally solves'), N_B <= 12."""
+    rng = np.random.default_rng(0)
+    for trial in range(300):
+        nb = int(rng.integers(1, 11))
+        e = rng.dirichlet(np.full(nb, rng.uniform(0.2, 3.0)))
+        eps = float(rng.uniform(0.5, 0.999))
+        kept = orc.select(e, eps)
+        best = None
+        for size in range(1, nb + 1):
+            if any(e[list(s)].sum() >= eps for s in itertools.combinations(range(nb), size)):
+                best = size
+                break
+        if best is None:          # unreachable eps (rounding) -> keep everything (Q5)
+            assert kept.sum() == nb
+        else:
+            assert kept.sum() == best
+            assert e[kept.astype(bool)].sum() >= eps
+        assert kept.sum() >= 1
+
+
+def test_selection_tie_order_and_prefix_monotone(orc):
+    e = np.full(10, 0.1)
+    assert list(np.nonzero(orc.select(e, 0.35))[0]) == [0, 1, 2, 3]
+    rng = np.random.default_rng(4)
+    e = rng.dirichlet(np.ones(30))
+    prev = orc.select(e, 0.5)
+    for eps in (0.6, 0.8, 0.9, 0.99):
+        cur = orc.select(e, eps)
+        assert np.all(cur >= prev)
+        prev = cur
+
+
+# ---------------------------------------------------------------- a1: eps schedule
+def test_epsilon_schedule_paper_values(orc):
+    for line in golden_lines("epsilon_schedule.txt"):
+        name, n, T, A, C, k, t, val, tol = line.split()
+        A = orc.A_of_N(float(n)) if A == "A(N)" else float(A)
+        e = orc.epsilon(int(t), int(T), A, float(C), float(k))
+        assert abs(e - float(val)) <= float(tol), name
+    # closed form of the fitted level at the paper's geometry: 0.796 + 1.41e-6 * 32760
+    assert abs(orc.A_of_N(32760) - 0.8421916) < 1e-12
+    # non-increasing in t for C >= A, k >= 0
+    A = orc.A_of_N(75600)
+    seq = [orc.epsilon(t, 50, A, 0.99, 16) for t in range(50)]
+    assert all(x >= y for x, y in zip(seq, seq[1:]))
+
+
+# ---------------------------------------------------------------- a5/a6: counts and compile
+def test_threshold_worked_examples_and_min_count(orc):
+    assert orc.min_count(0.5, 64) == 32
+    assert orc.min_count(0.6, 2) == 2 and orc.min_count(0.5, 2) == 1
+    for line in golden_lines("worked_examples.txt"):
+        if not line.startswith("threshold"):
+            continue
+        lhs, cnt, exp = line.split("|")
+        _, nd, rho = lhs.split()
+        cnt = np.array([int(x) for x in cnt.split()], np.uint16)
+        nb = cnt.size
+        counts = np.zeros((nb, nb), np.uint16)
+        counts[:] = cnt
+        cell = orc.compile_cell(counts, nb * 4, 4, 1, 1, nb * 4, orc.min_count(float(rho), int(nd)))
+        assert list(cell["mask"][0]) == [int(x) for x in exp.split()]
+
+
+def test_accumulate_is_count_of_kept(orc):
+    rng = np.random.default_rng(1)
+    masks = (rng.random((64, 5, 5)) < 0.4).astype(np.uint8)
+    cnt = np.zeros((5, 5), np.uint16)
+    for m in masks:
+        orc.accumulate(m, cnt)
+    assert np.array_equal(cnt, masks.sum(0))
+    # mean >= rho <=> count >= min_count (Eq. eq:mask_mean / eq:mask_threshold)
+    for rho in (0.1, 0.5, 0.77, 1.0):
+        mc = orc.min_count(rho, 64)
+        assert np.array_equal(cnt >= mc, masks.mean(0) >= rho)
+
+
+def _decode(iv, nb):
+    row = np.zeros(nb, np.uint8)
+    for s, e in iv:
+        row[s:e] = 1
+    return row
+
+
+def test_intervals_worked_examples_and_round_trip(orc):
+    for line in golden_lines("worked_examples.txt"):
+        if not line.startswith("intervals"):
+            continue
+        _, bits, exp = line.split("|")
+        bits = np.array([int(x) for x in bits.split()], np.uint16)
+        nb = bits.size
+        counts = np.tile(bits, (nb, 1))
+        cell = orc.compile_cell(counts, nb * 2, 2, 1, 1, nb * 2, 1)
+        got = cell["ivl"][cell["ivl_row_ptr"][0]:cell["ivl_row_ptr"][1]].ravel().tolist()
+        assert got == [int(x) for x in exp.split()]
+    rng = np.random.default_rng(2)
+    for trial in range(200):
+        nb = int(rng.integers(1, 40))
+        counts = (rng.random((nb, nb)) < rng.random()).astype(np.uint16) * 3
+        cell = orc.compile_cell(counts, nb * 8 - int(rng.integers(0, 8)), 8, 1, 1, 1, 2)
+        mask = cell["mask"]
+        for r in range(nb):
+            iv = cell["ivl"][cell["ivl_row_ptr"][r]:cell["ivl_row_ptr"][r + 1]]
+            assert np.array_equal(_decode(iv, nb), mask[r])            # decode(compile) = id
+            assert all(iv[x][1] < iv[x + 1][0] for x in range(len(iv) - 1))  # non-adjacent
+            idx = cell["blk_idx"][cell["blk_row_ptr"][r]:cell["blk_row_ptr"][r + 1]]
+            assert list(idx) == list(np.nonzero(mask[r])[0])
+            if counts[r].max() < 2:                                     # repaired row (Q7)
+                assert mask[r].sum() == 1 and mask[r][int(np.argmax(counts[r]))] == 1
+            else:
+                assert np.array_equal(mask[r], (counts[r] >= 2).astype(np.uint8))
+
+
+def test_area_and_repetitive_rule(orc):
+    n, b = 4 * 64, 64
+    cell = orc.compile_cell(np.eye(4, dtype=np.uint16), n, b, 4, 8, 8, 1)
+    assert orc.sparsity_of_cell(cell["kept_area"], n) == 0.75
+    ragged = orc.compile_cell(np.ones((4, 4), np.uint16), 250, 64, 2, 5, 25, 1)
+    assert ragged["kept_area"] == 250 * 250                              # all-ones = N^2
+    z = np.ones((4, 4), np.uint16)
+    assert orc.compile_cell(z, 256, 64, 4, 8, 8, 1, similarity=0.87, gamma=0.87)["kind"] == 0
+    rep = orc.compile_cell(z, 256, 64, 4, 8, 8, 1, similarity=0.8700001, gamma=0.87, anchor_k=2)
+    assert rep["kind"] == 1 and rep["kept_area"] == 4 * 2 * 8 * 256 and rep["blk_idx"].size == 0
+
+
+def test_geometry(orc):
+    for line in golden_lines("worked_examples.txt"):
+        if line.startswith("token"):
+            lhs, v = line.split("|")
+            _, H, W, f, i, j = lhs.split()
+            assert orc.token_index(int(H), int(W), int(f), int(i), int(j)) == int(v)
+    assert orc.num_blocks(32760, 128) == 256 and 32760 - 255 * 128 == 120   # P:1139 ragged tail
+    assert orc.num_blocks(75600, 128) == 591
+
+
+def test_work_list_is_sorted_permutation(orc):
+    rng = np.random.default_rng(3)
+    n, b, F, W = 250, 64, 2, 25
+    nb = 4
+    kinds = np.array([0, 1, 0, 0], np.uint8)
+    ak = np.array([0, 2, 0, 0], np.int32)
+    nnz = rng.integers(1, nb + 1, size=(4, nb)).astype(np.int32)
+    wl = orc.work_list(n, b, F, W, kinds, ak, nnz)
+    nu = (F * 2 * W + 127) // 128
+    assert wl.size == 3 * nb + nu
+    items = []
+    for code in wl:
+        kind, h, idx = int(code) >> 31, (int(code) >> 20) & 0x7FF, int(code) & 0xFFFFF
+        cost = nb if kind else int(nnz[h, idx])
+        items.append((-cost, h, kind, idx))
+    assert items == sorted(items)
+    assert sorted((h, k, i) for _, h, k, i in items) == sorted(
+        [(h, 0, r) for h in (0, 2, 3) for r in range(nb)] + [(1, 1, u) for u in range(nu)])
