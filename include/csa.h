@@ -1,0 +1,203 @@
+/*
+ * csa.h -- C ABI of the B200 (sm_100a) calibrated-sparse-attention hot path.
+ *
+ * Paper: "Accelerating Text-to-Video Generation with Calibrated Sparse Attention"
+ * (arxiv 2603.05503), cited as P:<line> of PAPER.md (section / equation).
+ *
+ * Three operations, in the order the method runs them:
+ *   csa_calib_accumulate  -- calibration statistics: row LSE, block energy E_{r,c}
+ *                            (Eq. eq:block_energy), per-prompt energy selection at eps(t)
+ *                            (Eq. eq:row_energy_constraint), keep-count accumulation
+ *                            (numerator of Eq. eq:mask_mean).
+ *   csa_compile_plan      -- rho threshold (Eq. eq:mask_threshold), repetitive-head override
+ *                            (P:624-626), skip lists / block lists (1D form P:947-950),
+ *                            kept area (sparsity metric P:728);  csa_build_work_list orders one
+ *                            launch's (head, query-block) items.
+ *   csa_sparse_attn_fwd   -- block-sparse attention forward over the kept blocks and
+ *                            anchor-row attention + broadcast for repetitive heads.
+ *
+ * Conventions (all entry points):
+ *   - Ownership: the caller owns every buffer (e.g. torch.empty on the device); the library never
+ *     allocates device memory, never frees, and keeps no pointer past the enqueued work.
+ *   - Asynchrony: work is enqueued on `stream`; no host synchronisation, except
+ *     csa_validate_plan (documented).  Pointers are DEVICE pointers unless stated otherwise.
+ *   - Errors: host-side argument checks return a status; csa_last_error() gives a thread-local
+ *     detail string.  Device-side corruption is detected only by csa_validate_plan.
+ *     Non-finite inputs are not scanned; NaN propagates.
+ *   - Geometry (Eq. eq:indices P:196-204): N = frames*rows*cols video tokens in
+ *     row-major (f, i, j) order; N_B = ceil(N / block); the last block may be ragged.
+ *   - Tensors: bf16, layout [batch, N, heads, head_dim] given by element strides; head_dim
+ *     contiguous; base and strides 16-byte aligned (TMA).
+ *   - Supported: sm_100 devices; head_dim in {64, 128}; block in {64, 128}; N_B <= 2047.
+ */
+#ifndef CSA_H
+#define CSA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CSA_API __attribute__((visibility("default")))
+#else
+#define CSA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* csa_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    CSA_OK = 0,
+    CSA_ERR_INVALID_ARGUMENT = 1,   /* shape / stride / alignment / range error */
+    CSA_ERR_UNSUPPORTED = 2,        /* head_dim, block, size limit or device not supported */
+    CSA_ERR_CORRUPT_PLAN = 3,       /* csa_validate_plan found an inconsistent plan */
+    CSA_ERR_CUDA = 4,               /* a CUDA runtime/driver call failed (see csa_last_error) */
+    CSA_ERR_INSUFFICIENT_CAPACITY = 5
+} csa_status_t;
+
+/* Video token grid and block size (128x128 blocks). */
+typedef struct {
+    int32_t frames; /* F */
+    int32_t rows;   /* H, spatial rows per frame */
+    int32_t cols;   /* W, tokens per spatial row */
+    int32_t block;  /* B (query and key block size, "B x B") */
+} csa_layout_t;
+
+/* bf16 tensor [batch, N, heads, head_dim]; strides in ELEMENTS; head_dim stride is 1. */
+typedef struct {
+    void* ptr;
+    int64_t stride_b;
+    int64_t stride_n;
+    int64_t stride_h;
+} csa_tensor_t;
+
+/* Compiled plan for n_cells cells (a cell is one (t, l, h); cell id chosen by the
+ * caller, e.g. (t*L + l)*H + h).  Every pointer is a caller-allocated device buffer.
+ *   kind        [n_cells]                0 = MASK, 1 = REPETITIVE (anchor rows)
+ *   anchor_k    [n_cells]                anchor rows per frame (REPETITIVE only)
+ *   mask_bits   [n_cells][N_B][ceil(N_B/32)] kept bit (r,c) = word c/32 bit c%32 (LSB first)
+ *   blk_base    [n_cells + 1]            cell offset into blk_idx; blk_base[n_cells] = total
+ *   blk_row_ptr [n_cells][N_B + 1]       CSR row pointers relative to blk_base[cell]
+ *   blk_idx     [blk_capacity]           kept key-block indices c, ascending per row
+ *   ivl_base    [n_cells + 1]            cell offset (in intervals) into ivl
+ *   ivl_row_ptr [n_cells][N_B + 1]       interval row pointers relative to ivl_base[cell]
+ *   ivl         [2 * ivl_capacity]       skip-list intervals (start, end) half-open, maximal runs
+ *   kept_area   [n_cells]                sum over kept (r,c) of |I_r||J_c|; REPETITIVE: F*k*W*N
+ * REPETITIVE cells have empty rows (row_ptr all 0) and mask_bits all 0 ("instead"). */
+typedef struct {
+    int64_t n_cells;
+    uint8_t* kind;
+    int32_t* anchor_k;
+    uint32_t* mask_bits;
+    int64_t* blk_base;
+    int32_t* blk_row_ptr;
+    uint16_t* blk_idx;
+    int64_t* ivl_base;
+    int32_t* ivl_row_ptr;
+    uint16_t* ivl;
+    int64_t* kept_area;
+    int64_t blk_capacity; /* elements of blk_idx */
+    int64_t ivl_capacity; /* intervals (pairs) of ivl */
+} csa_plan_t;
+
+/* Which workspace a call needs (csa_workspace_size). */
+enum { CSA_WS_CALIB = 0, CSA_WS_COMPILE = 1, CSA_WS_WORK_LIST = 2, CSA_WS_ATTN = 3 };
+
+/* ------------------------------------------------------------------------------------------
+ * csa_calib_accumulate -- one calibration prompt at one (t, l), all heads.
+ * For each head h and query block r:
+ *   lse_i   = log sum_{j<N} exp(softmax_scale * q_i.k_j)              (dense P, Eq. eq:p)
+ *             -- taken from lse_in when given (the dense calibration run's own statistic);
+ *   E_{r,c} = (1/|I_r|) sum_{i in I_r} sum_{j in J_c} exp(s_ij - lse_i)  (Eq. eq:block_energy;
+ *             divides by the actual |I_r| of a ragged last block), P never materialised;
+ *   M_p[r,.] = shortest prefix of (E desc, c asc) whose fp64 sequential sum of the fp32 E values
+ *             reaches eps (keep all if never reached; >= 1 block);
+ *   keep_count[h][r][c] += M_p[r][c]  (uint16, saturating at 65535).
+ * Arguments:
+ *   q, k        bf16 [1, N, n_heads, head_dim] (batch index 0 only: conditional branch)
+ *   lse_in      optional fp32 [n_heads][N] natural-log row LSE; NULL -> computed in-kernel
+ *   eps         eps(t) computed by the caller (Eq. eq:epsilon_schedule), 0 < eps
+ *   keep_count  uint16 [n_heads][N_B][N_B], accumulated in place
+ *   energy_out  optional fp32 [n_heads][N_B][N_B] (the exact values the selection consumed)
+ *   lse_out     optional fp32 [n_heads][N] (natural log; the values pass B used)
+ * Workspace: csa_workspace_size(CSA_WS_CALIB, ...) bytes (may be 0 -> NULL allowed). */
+CSA_API csa_status_t csa_calib_accumulate(csa_layout_t L, int32_t n_heads, int32_t head_dim,
+                                  float softmax_scale, csa_tensor_t q, csa_tensor_t k,
+                                  const float* lse_in, double eps, uint16_t* keep_count,
+                                  float* energy_out, float* lse_out, void* workspace,
+                                  size_t workspace_bytes, csa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * csa_compile_plan -- keep counts -> plan, for cells [0, n_cells).
+ *   M[r,c] = keep_count[cell][r][c] >= min_count (Eq. eq:mask_threshold in count space:
+ *            min_count = smallest integer >= rho*|D|, computed by the caller);
+ *   a row emptied by the threshold re-keeps argmax_c count (tie -> lowest c);
+ *   similarity (optional fp64 [n_cells]): s[cell] > gamma -> REPETITIVE with anchor_k rows.
+ * Two phases on the same plan struct:
+ *   phase 0 (COUNT): writes kind, anchor_k, mask_bits, row pointers, kept_area, blk_base,
+ *                    ivl_base (blk_idx / ivl may be NULL).  The caller reads blk_base[n_cells]
+ *                    and ivl_base[n_cells] to size blk_idx / ivl.
+ *   phase 1 (FILL):  writes blk_idx and ivl (writes beyond the capacities are dropped; a plan
+ *                    filled with too small a capacity fails csa_validate_plan).
+ * keep_count: uint16 [n_cells][N_B][N_B]. */
+CSA_API csa_status_t csa_compile_plan(csa_layout_t L, int64_t n_cells, const uint16_t* keep_count,
+                              int32_t min_count, const double* similarity, double gamma,
+                              int32_t anchor_k, int32_t phase, const csa_plan_t* plan,
+                              void* workspace, size_t workspace_bytes, csa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * csa_build_work_list -- items of one attention launch over heads [0, n_heads) whose cells are
+ * cell_base + h.  MASK head: items (h, r), r < N_B, cost = kept blocks of row r; REPETITIVE
+ * head: items (h, u), u < ceil(F*k*W/128) anchor-query tiles, cost = N_B.
+ * order 0: longest-first, ties (h asc, kind asc, index asc) -- a total order (unique output);
+ * order 1: natural (h asc, index asc).
+ * Encoding: kind<<31 | h<<20 | (r or u).  work_list: uint32 [capacity]; n_work: device int32.
+ * Requires n_heads <= 2048 and at most 32768 items. */
+CSA_API csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan, int64_t cell_base,
+                                 int32_t n_heads, int32_t order, uint32_t* work_list,
+                                 int32_t capacity, int32_t* n_work, void* workspace,
+                                 size_t workspace_bytes, csa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * csa_sparse_attn_fwd -- calibrated sparse attention of one layer at one timestep.
+ * For batch b, head h (cell = cell_base + h), query token i in block r:
+ *   MASK:       o_i = sum_{j in K_r} softmax_{j in K_r}(softmax_scale q_i.k_j) v_j with
+ *               K_r = U_{c: M[r,c]=1} J_c (skipped blocks excluded from numerator and
+ *               normaliser; skipped K/V blocks are never loaded), P:647-653;
+ *   REPETITIVE: o[f,i,j] = dense attention of q[f, a(i), j] over all N keys, a(i) the nearest
+ *               of the anchor rows floor((2m+1)H/(2k)) (tie -> lower).
+ * The batch shares the plan (CFG branches).
+ *   q, k, v, o  bf16 [batch, N, n_heads, head_dim]
+ *   lse_out     optional fp32 [batch][n_heads][N], natural log over the kept keys
+ *   work_list   items from csa_build_work_list; n_work device int32 (count)
+ *   max_work    host upper bound of *n_work (sizes the persistent grid)
+ * Workspace: csa_workspace_size(CSA_WS_ATTN, ...) bytes. */
+CSA_API csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
+                                 int32_t head_dim, float softmax_scale, csa_tensor_t q,
+                                 csa_tensor_t k, csa_tensor_t v, csa_tensor_t o, float* lse_out,
+                                 const csa_plan_t* plan, int64_t cell_base,
+                                 const uint32_t* work_list, const int32_t* n_work,
+                                 int32_t max_work, void* workspace, size_t workspace_bytes,
+                                 csa_stream_t stream);
+
+/* Workspace bytes for `which` (CSA_WS_*). */
+CSA_API size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_t head_dim);
+
+/* Structural check of cells [0, n_cells) of a plan (row pointers monotone, indices ascending and
+ * < N_B, MASK rows non-empty, intervals maximal/ordered and consistent with blk_idx, bases within
+ * capacities).  Synchronises `stream`.  CSA_OK or CSA_ERR_CORRUPT_PLAN. */
+CSA_API csa_status_t csa_validate_plan(const csa_plan_t* plan, csa_layout_t L, int64_t n_cells,
+                               csa_stream_t stream);
+
+/* Thread-local detail of the last error returned on this thread ("" if none). */
+CSA_API const char* csa_last_error(void);
+
+/* Library version string. */
+CSA_API const char* csa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CSA_H */

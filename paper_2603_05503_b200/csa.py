@@ -1,0 +1,280 @@
+"""Python binding of libcsa.so (include/csa.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C ABI; this module only turns
+torch tensors into pointers/strides and owns the plan buffers' allocation (torch, device memory).
+There is no CPU fallback: importing this module without a built libcsa.so raises, and every call
+needs CUDA tensors on an sm_100 device.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import math
+import os
+
+import torch
+
+from .inputs import Layout
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcsa.so")
+
+CSA_OK = 0
+_STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "UNSUPPORTED", 3: "CORRUPT_PLAN", 4: "CUDA",
+           5: "INSUFFICIENT_CAPACITY"}
+
+
+class CsaError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        super().__init__(f"{where}: CSA_{_STATUS.get(status, status)}: {detail}")
+        self.status = status
+
+
+class _LayoutT(ctypes.Structure):
+    _fields_ = [("frames", ctypes.c_int32), ("rows", ctypes.c_int32), ("cols", ctypes.c_int32),
+                ("block", ctypes.c_int32)]
+
+
+class _TensorT(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("stride_b", ctypes.c_int64),
+                ("stride_n", ctypes.c_int64), ("stride_h", ctypes.c_int64)]
+
+
+class _PlanT(ctypes.Structure):
+    _fields_ = [("n_cells", ctypes.c_int64), ("kind", ctypes.c_void_p),
+                ("anchor_k", ctypes.c_void_p), ("mask_bits", ctypes.c_void_p),
+                ("blk_base", ctypes.c_void_p), ("blk_row_ptr", ctypes.c_void_p),
+                ("blk_idx", ctypes.c_void_p), ("ivl_base", ctypes.c_void_p),
+                ("ivl_row_ptr", ctypes.c_void_p), ("ivl", ctypes.c_void_p),
+                ("kept_area", ctypes.c_void_p), ("blk_capacity", ctypes.c_int64),
+                ("ivl_capacity", ctypes.c_int64)]
+
+
+EXPORTS = ["csa_calib_accumulate", "csa_compile_plan", "csa_build_work_list",
+           "csa_sparse_attn_fwd", "csa_workspace_size", "csa_validate_plan", "csa_last_error",
+           "csa_version"]
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libcsa.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; "
+                          f"g.build()'` (nvcc, sm_100a).  There is no CPU fallback.")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, st = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int
+    L.csa_last_error.restype = ctypes.c_char_p
+    L.csa_version.restype = ctypes.c_char_p
+    L.csa_workspace_size.restype = ctypes.c_size_t
+    L.csa_workspace_size.argtypes = [i32, _LayoutT, i32, i32]
+    L.csa_calib_accumulate.restype = st
+    L.csa_calib_accumulate.argtypes = [_LayoutT, i32, i32, ctypes.c_float, _TensorT, _TensorT, vp,
+                                       ctypes.c_double, vp, vp, vp, vp, ctypes.c_size_t, vp]
+    L.csa_compile_plan.restype = st
+    L.csa_compile_plan.argtypes = [_LayoutT, i64, vp, i32, vp, ctypes.c_double, i32, i32,
+                                   ctypes.POINTER(_PlanT), vp, ctypes.c_size_t, vp]
+    L.csa_build_work_list.restype = st
+    L.csa_build_work_list.argtypes = [_LayoutT, ctypes.POINTER(_PlanT), i64, i32, i32, vp, i32, vp,
+                                      vp, ctypes.c_size_t, vp]
+    L.csa_sparse_attn_fwd.restype = st
+    L.csa_sparse_attn_fwd.argtypes = [_LayoutT, i32, i32, i32, ctypes.c_float, _TensorT, _TensorT,
+                                      _TensorT, _TensorT, vp, ctypes.POINTER(_PlanT), i64, vp, vp,
+                                      i32, vp, ctypes.c_size_t, vp]
+    L.csa_validate_plan.restype = st
+    L.csa_validate_plan.argtypes = [ctypes.POINTER(_PlanT), _LayoutT, i64, vp]
+    _lib = L
+    return L
+
+
+def _check(status: int, where: str) -> None:
+    if status != CSA_OK:
+        raise CsaError(status, where, lib().csa_last_error().decode())
+
+
+def _layout(lay: Layout) -> _LayoutT:
+    return _LayoutT(lay.F, lay.H, lay.W, lay.B)
+
+
+def _tensor(t: torch.Tensor | None) -> _TensorT:
+    if t is None:
+        return _TensorT(None, 0, 0, 0)
+    if t.dtype != torch.bfloat16 or not t.is_cuda or t.dim() != 4 or t.stride(3) != 1:
+        raise ValueError("expected a CUDA bf16 tensor [batch, N, heads, head_dim], head_dim "
+                         "contiguous")
+    return _TensorT(t.data_ptr(), t.stride(0), t.stride(1), t.stride(2))
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def default_scale(d: int) -> float:
+    """softmax scale 1/sqrt(d)."""
+    return 1.0 / math.sqrt(d)
+
+
+# ------------------------------------------------------------------------------- calibration
+def calib_accumulate(lay: Layout, q: torch.Tensor, k: torch.Tensor, eps: float,
+                     keep_count: torch.Tensor, lse_in: torch.Tensor | None = None,
+                     energy_out: torch.Tensor | None = None, lse_out: torch.Tensor | None = None,
+                     scale: float | None = None, stream=None) -> None:
+    """csa_calib_accumulate: one prompt at one (t, l), all heads of q/k [1, N, H, d]."""
+    _, n, heads, d = q.shape
+    assert n == lay.N and keep_count.dtype == torch.uint16 and keep_count.is_contiguous()
+    assert keep_count.numel() == heads * lay.NB * lay.NB
+    for t, shape in ((lse_in, heads * n), (lse_out, heads * n),
+                     (energy_out, heads * lay.NB * lay.NB)):
+        if t is not None:
+            assert t.dtype == torch.float32 and t.is_contiguous() and t.numel() == shape
+    sc = default_scale(d) if scale is None else scale
+    _check(lib().csa_calib_accumulate(_layout(lay), heads, d, sc, _tensor(q), _tensor(k),
+                                      _ptr(lse_in), float(eps), _ptr(keep_count),
+                                      _ptr(energy_out), _ptr(lse_out), None, 0, _stream(stream)),
+           "csa_calib_accumulate")
+
+
+# ------------------------------------------------------------------------------- plan
+@dataclasses.dataclass
+class Plan:
+    """Device buffers of a compiled plan (see csa_plan_t in include/csa.h)."""
+
+    lay: Layout
+    n_cells: int
+    kind: torch.Tensor
+    anchor_k: torch.Tensor
+    mask_bits: torch.Tensor
+    blk_base: torch.Tensor
+    blk_row_ptr: torch.Tensor
+    blk_idx: torch.Tensor
+    ivl_base: torch.Tensor
+    ivl_row_ptr: torch.Tensor
+    ivl: torch.Tensor
+    kept_area: torch.Tensor
+    kind_host: list | None = None
+    anchor_k_host: list | None = None
+
+    def struct(self) -> _PlanT:
+        return _PlanT(self.n_cells, self.kind.data_ptr(), self.anchor_k.data_ptr(),
+                      self.mask_bits.data_ptr(), self.blk_base.data_ptr(),
+                      self.blk_row_ptr.data_ptr(),
+                      self.blk_idx.data_ptr() if self.blk_idx.numel() else None,
+                      self.ivl_base.data_ptr(), self.ivl_row_ptr.data_ptr(),
+                      self.ivl.data_ptr() if self.ivl.numel() else None,
+                      self.kept_area.data_ptr(), self.blk_idx.numel(), self.ivl.numel() // 2)
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (
+            self.kind, self.anchor_k, self.mask_bits, self.blk_base, self.blk_row_ptr,
+            self.blk_idx, self.ivl_base, self.ivl_row_ptr, self.ivl, self.kept_area))
+
+    def items(self, cell_base: int, n_heads: int) -> int:
+        """Work items of one launch (host-side count used to size the persistent grid)."""
+        tot = 0
+        for h in range(n_heads):
+            c = cell_base + h
+            if self.kind_host[c]:
+                tot += (self.lay.F * self.anchor_k_host[c] * self.lay.W + 127) // 128
+            else:
+                tot += self.lay.NB
+        return tot
+
+
+def compile_plan(lay: Layout, keep_count: torch.Tensor, min_count: int,
+                 similarity: torch.Tensor | None = None, gamma: float = 0.87, anchor_k: int = 5,
+                 stream=None) -> Plan:
+    """csa_compile_plan phase 0 (count) -> size read-back -> phase 1 (fill)."""
+    dev = keep_count.device
+    nb = lay.NB
+    n_cells = keep_count.numel() // (nb * nb)
+    assert keep_count.dtype == torch.uint16 and keep_count.is_contiguous()
+    if similarity is not None:
+        assert similarity.dtype == torch.float64 and similarity.numel() == n_cells
+    w32 = (nb + 31) // 32
+    e = torch.empty
+    p = Plan(lay, n_cells,
+             kind=e(n_cells, dtype=torch.uint8, device=dev),
+             anchor_k=e(n_cells, dtype=torch.int32, device=dev),
+             mask_bits=e(n_cells * nb * w32, dtype=torch.int32, device=dev),
+             blk_base=e(n_cells + 1, dtype=torch.int64, device=dev),
+             blk_row_ptr=e(n_cells * (nb + 1), dtype=torch.int32, device=dev),
+             blk_idx=e(0, dtype=torch.uint16, device=dev),
+             ivl_base=e(n_cells + 1, dtype=torch.int64, device=dev),
+             ivl_row_ptr=e(n_cells * (nb + 1), dtype=torch.int32, device=dev),
+             ivl=e(0, dtype=torch.uint16, device=dev),
+             kept_area=e(n_cells, dtype=torch.int64, device=dev))
+    s = p.struct()
+    _check(lib().csa_compile_plan(_layout(lay), n_cells, _ptr(keep_count), int(min_count),
+                                  _ptr(similarity), float(gamma), int(anchor_k), 0,
+                                  ctypes.byref(s), None, 0, _stream(stream)), "csa_compile_plan(0)")
+    tot_b = int(p.blk_base[n_cells].item())
+    tot_i = int(p.ivl_base[n_cells].item())
+    p.blk_idx = e(max(tot_b, 1), dtype=torch.uint16, device=dev)
+    p.ivl = e(max(2 * tot_i, 2), dtype=torch.uint16, device=dev)
+    s = p.struct()
+    _check(lib().csa_compile_plan(_layout(lay), n_cells, None, int(min_count), None, float(gamma),
+                                  int(anchor_k), 1, ctypes.byref(s), None, 0, _stream(stream)),
+           "csa_compile_plan(1)")
+    p.kind_host = p.kind.cpu().tolist()
+    p.anchor_k_host = p.anchor_k.cpu().tolist()
+    return p
+
+
+def validate_plan(plan: Plan, n_cells: int | None = None, stream=None) -> None:
+    s = plan.struct()
+    _check(lib().csa_validate_plan(ctypes.byref(s), _layout(plan.lay),
+                                   plan.n_cells if n_cells is None else n_cells, _stream(stream)),
+           "csa_validate_plan")
+
+
+@dataclasses.dataclass
+class WorkList:
+    items: torch.Tensor   # uint32 codes (stored as int32)
+    n_work: torch.Tensor  # device int32 [1]
+    max_work: int
+
+
+def build_work_list(plan: Plan, cell_base: int, n_heads: int, order: int = 0,
+                    stream=None) -> WorkList:
+    cap = plan.items(cell_base, n_heads)
+    items = torch.empty(max(cap, 1), dtype=torch.int32, device=plan.kind.device)
+    n_work = torch.empty(1, dtype=torch.int32, device=plan.kind.device)
+    s = plan.struct()
+    _check(lib().csa_build_work_list(_layout(plan.lay), ctypes.byref(s), cell_base, n_heads, order,
+                                     _ptr(items), cap, _ptr(n_work), None, 0, _stream(stream)),
+           "csa_build_work_list")
+    return WorkList(items, n_work, cap)
+
+
+# ------------------------------------------------------------------------------- attention
+def sparse_attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: Plan,
+                    work: WorkList, cell_base: int = 0, out: torch.Tensor | None = None,
+                    lse_out: torch.Tensor | None = None, scale: float | None = None,
+                    stream=None) -> torch.Tensor:
+    """csa_sparse_attn_fwd on q/k/v [batch, N, heads, d] (bf16, CUDA)."""
+    b, n, heads, d = q.shape
+    assert n == plan.lay.N and k.shape == q.shape and v.shape == q.shape
+    if out is None:
+        out = torch.empty_like(q)
+    if lse_out is not None:
+        assert lse_out.dtype == torch.float32 and lse_out.is_contiguous()
+        assert lse_out.numel() == b * heads * n
+    sc = default_scale(d) if scale is None else scale
+    s = plan.struct()
+    _check(lib().csa_sparse_attn_fwd(_layout(plan.lay), b, heads, d, sc, _tensor(q), _tensor(k),
+                                     _tensor(v), _tensor(out), _ptr(lse_out), ctypes.byref(s),
+                                     cell_base, _ptr(work.items), _ptr(work.n_work), work.max_work,
+                                     None, 0, _stream(stream)), "csa_sparse_attn_fwd")
+    return out
+
+
+def version() -> str:
+    return lib().csa_version().decode()

@@ -1,0 +1,305 @@
+// api.cu -- the C ABI of include/csa.h: argument validation, TMA descriptor encoding, launches.
+// No allocation, no host synchronisation (except csa_validate_plan), thread-local error text.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include <cudaTypedefs.h>
+
+#include "csa_internal.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+csa_status_t fail(csa_status_t st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+csa_status_t ok() {
+    g_err.clear();
+    return CSA_OK;
+}
+
+csa_status_t cuda_fail(cudaError_t e, const char* what) {
+    return fail(CSA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+struct DeviceInfo {
+    int sms = 0;
+    bool sm100 = false;
+};
+
+csa_status_t device_info(DeviceInfo* out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    int major = 0, minor = 0, sms = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    out->sms = sms;
+    out->sm100 = (major == 10 && minor == 0);
+    if (!out->sm100)
+        return fail(CSA_ERR_UNSUPPORTED, "device is sm_%d%d; this library is built for sm_100a",
+                    major, minor);
+    return CSA_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 4-D map over [batch, N, heads, D] bf16 (dims innermost first: d, h, n, b), box (64,1,rows,1),
+// SWIZZLE_128B, out-of-bounds rows zero-filled (ragged last block).
+csa_status_t make_map(CUtensorMap* map, const csa_tensor_t& t, int32_t batch, int32_t n,
+                      int32_t heads, int32_t d, int32_t box_rows, const char* name) {
+    auto enc = encode_fn();
+    if (!enc) return fail(CSA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    if (!t.ptr) return fail(CSA_ERR_INVALID_ARGUMENT, "%s: null pointer", name);
+    if (reinterpret_cast<uintptr_t>(t.ptr) % 16)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "%s: base not 16-byte aligned", name);
+    int64_t sb = t.stride_b, sn = t.stride_n, sh = t.stride_h;
+    if (batch == 1) sb = sn * n;  // unused dimension: any legal stride
+    if (heads == 1) sh = d;
+    if (sn <= 0 || sh <= 0 || sb <= 0 || (sn * 2) % 16 || (sh * 2) % 16 || (sb * 2) % 16)
+        return fail(CSA_ERR_INVALID_ARGUMENT,
+                    "%s: strides (b=%lld n=%lld h=%lld elements) must be positive and 16-byte "
+                    "multiples", name, (long long)t.stride_b, (long long)t.stride_n,
+                    (long long)t.stride_h);
+    cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)heads, (cuuint64_t)n, (cuuint64_t)batch};
+    cuuint64_t strides[3] = {(cuuint64_t)(sh * 2), (cuuint64_t)(sn * 2), (cuuint64_t)(sb * 2)};
+    cuuint32_t box[4] = {64, 1, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, t.ptr, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "%s: cuTensorMapEncodeTiled failed (%d)", name,
+                    (int)r);
+    return CSA_OK;
+}
+
+csa_status_t check_layout(const csa_layout_t& L, int32_t head_dim, int32_t n_heads) {
+    if (L.frames <= 0 || L.rows <= 0 || L.cols <= 0)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "layout: frames/rows/cols must be positive");
+    if (L.block != 64 && L.block != 128)
+        return fail(CSA_ERR_UNSUPPORTED, "layout: block %d not in {64, 128}", L.block);
+    const int64_t n = (int64_t)L.frames * L.rows * L.cols;
+    if (n >= (1LL << 31)) return fail(CSA_ERR_UNSUPPORTED, "layout: N too large");
+    if ((n + L.block - 1) / L.block > csa::kMaxBlocks)
+        return fail(CSA_ERR_UNSUPPORTED, "layout: N_B > %d", csa::kMaxBlocks);
+    if (head_dim != 0 && head_dim != 64 && head_dim != 128)
+        return fail(CSA_ERR_UNSUPPORTED, "head_dim %d not in {64, 128}", head_dim);
+    if (n_heads < 0 || n_heads > 2048)
+        return fail(CSA_ERR_UNSUPPORTED, "n_heads %d outside [0, 2048]", n_heads);
+    return CSA_OK;
+}
+
+bool plan_ptrs_ok(const csa_plan_t* p, bool need_lists) {
+    if (!p || !p->kind || !p->anchor_k || !p->mask_bits || !p->blk_base || !p->blk_row_ptr ||
+        !p->ivl_base || !p->ivl_row_ptr || !p->kept_area)
+        return false;
+    if (need_lists && (!p->blk_idx || !p->ivl)) return false;
+    return true;
+}
+
+__device__ uint32_t g_validate_flag;
+std::mutex g_validate_mu;
+
+}  // namespace
+
+extern "C" {
+
+const char* csa_last_error(void) { return g_err.c_str(); }
+
+const char* csa_version(void) { return "csa-b200 0.1 (sm_100a)"; }
+
+size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_t head_dim) {
+    (void)which;
+    (void)L;
+    (void)n_heads;
+    (void)head_dim;
+    return 0;  // every kernel of this version is workspace-free
+}
+
+csa_status_t csa_calib_accumulate(csa_layout_t L, int32_t n_heads, int32_t head_dim,
+                                  float softmax_scale, csa_tensor_t q, csa_tensor_t k,
+                                  const float* lse_in, double eps, uint16_t* keep_count,
+                                  float* energy_out, float* lse_out, void* workspace,
+                                  size_t workspace_bytes, csa_stream_t stream) {
+    (void)workspace;
+    (void)workspace_bytes;
+    csa_status_t st = check_layout(L, head_dim, n_heads);
+    if (st != CSA_OK) return st;
+    if (n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "n_heads must be >= 1");
+    if (!(softmax_scale > 0.0f)) return fail(CSA_ERR_INVALID_ARGUMENT, "softmax_scale <= 0");
+    if (!(eps > 0.0)) return fail(CSA_ERR_INVALID_ARGUMENT, "eps must be > 0");
+    if (!keep_count) return fail(CSA_ERR_INVALID_ARGUMENT, "keep_count is null");
+    DeviceInfo di;
+    if ((st = device_info(&di)) != CSA_OK) return st;
+    const csa::Geo g = csa::make_geo(L);
+    CUtensorMap tq, tk;
+    if ((st = make_map(&tq, q, 1, g.N, n_heads, head_dim, g.B, "q")) != CSA_OK) return st;
+    if ((st = make_map(&tk, k, 1, g.N, n_heads, head_dim, g.B, "k")) != CSA_OK) return st;
+    csa::CalibArgs a;
+    a.g = g;
+    a.n_heads = n_heads;
+    a.scale_log2 = softmax_scale * 1.4426950408889634f;
+    a.lse_in = lse_in;
+    a.eps = eps;
+    a.keep_count = keep_count;
+    a.energy_out = energy_out;
+    a.lse_out = lse_out;
+    cudaError_t e = csa::launch_calib(a, head_dim, tq, tk, di.sms, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "calib launch");
+    return ok();
+}
+
+csa_status_t csa_compile_plan(csa_layout_t L, int64_t n_cells, const uint16_t* keep_count,
+                              int32_t min_count, const double* similarity, double gamma,
+                              int32_t anchor_k, int32_t phase, const csa_plan_t* plan,
+                              void* workspace, size_t workspace_bytes, csa_stream_t stream) {
+    (void)workspace;
+    (void)workspace_bytes;
+    csa_status_t st = check_layout(L, 0, 0);
+    if (st != CSA_OK) return st;
+    if (n_cells < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "n_cells must be >= 1");
+    if (phase != 0 && phase != 1) return fail(CSA_ERR_INVALID_ARGUMENT, "phase must be 0 or 1");
+    if (!plan_ptrs_ok(plan, phase == 1)) return fail(CSA_ERR_INVALID_ARGUMENT, "plan: null buffer");
+    if (plan->n_cells < n_cells) return fail(CSA_ERR_INVALID_ARGUMENT, "plan holds fewer cells");
+    if (phase == 0 && !keep_count) return fail(CSA_ERR_INVALID_ARGUMENT, "keep_count is null");
+    if (similarity && (anchor_k < 1 || anchor_k > L.rows))
+        return fail(CSA_ERR_INVALID_ARGUMENT, "anchor_k %d outside [1, rows=%d]", anchor_k, L.rows);
+    const csa::Geo g = csa::make_geo(L);
+    const csa::PlanDev p = csa::to_dev(*plan);
+    cudaError_t e = phase == 0 ? csa::launch_plan_count(g, n_cells, keep_count, min_count,
+                                                        similarity, gamma, anchor_k, p,
+                                                        (cudaStream_t)stream)
+                               : csa::launch_plan_fill(g, n_cells, p, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "compile launch");
+    return ok();
+}
+
+csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan, int64_t cell_base,
+                                 int32_t n_heads, int32_t order, uint32_t* work_list,
+                                 int32_t capacity, int32_t* n_work, void* workspace,
+                                 size_t workspace_bytes, csa_stream_t stream) {
+    (void)workspace;
+    (void)workspace_bytes;
+    csa_status_t st = check_layout(L, 0, n_heads);
+    if (st != CSA_OK) return st;
+    if (n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "n_heads must be >= 1");
+    if (order != 0 && order != 1) return fail(CSA_ERR_INVALID_ARGUMENT, "order must be 0 or 1");
+    if (!plan_ptrs_ok(plan, false) || !work_list || !n_work)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "null buffer");
+    if (cell_base < 0 || cell_base + n_heads > plan->n_cells)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "cells [%lld, %lld) outside the plan",
+                    (long long)cell_base, (long long)(cell_base + n_heads));
+    const csa::Geo g = csa::make_geo(L);
+    cudaError_t e = csa::launch_work_list(g, csa::to_dev(*plan), cell_base, n_heads, order,
+                                          work_list, capacity, n_work, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "work list launch");
+    return ok();
+}
+
+csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
+                                 int32_t head_dim, float softmax_scale, csa_tensor_t q,
+                                 csa_tensor_t k, csa_tensor_t v, csa_tensor_t o, float* lse_out,
+                                 const csa_plan_t* plan, int64_t cell_base,
+                                 const uint32_t* work_list, const int32_t* n_work,
+                                 int32_t max_work, void* workspace, size_t workspace_bytes,
+                                 csa_stream_t stream) {
+    (void)workspace;
+    (void)workspace_bytes;
+    csa_status_t st = check_layout(L, head_dim, n_heads);
+    if (st != CSA_OK) return st;
+    if (batch < 1 || n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "batch/n_heads < 1");
+    if (!(softmax_scale > 0.0f)) return fail(CSA_ERR_INVALID_ARGUMENT, "softmax_scale <= 0");
+    if (!plan_ptrs_ok(plan, true) || !work_list || !n_work)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "null plan / work list");
+    if (cell_base < 0 || cell_base + n_heads > plan->n_cells)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "cells outside the plan");
+    if (max_work < 0) return fail(CSA_ERR_INVALID_ARGUMENT, "max_work < 0");
+    if (!o.ptr || reinterpret_cast<uintptr_t>(o.ptr) % 16 || o.stride_n % 8 ||
+        (n_heads > 1 && o.stride_h % 8) || (batch > 1 && o.stride_b % 8))
+        return fail(CSA_ERR_INVALID_ARGUMENT, "o: null or not 16-byte aligned");
+    if (!q.ptr || q.stride_n % 8 || (n_heads > 1 && q.stride_h % 8))
+        return fail(CSA_ERR_INVALID_ARGUMENT, "q: null or strides not 16-byte multiples");
+    DeviceInfo di;
+    if ((st = device_info(&di)) != CSA_OK) return st;
+    if (max_work == 0) return ok();
+    const csa::Geo g = csa::make_geo(L);
+    CUtensorMap tq, tk, tv;
+    if ((st = make_map(&tq, q, batch, g.N, n_heads, head_dim, g.B, "q")) != CSA_OK) return st;
+    if ((st = make_map(&tk, k, batch, g.N, n_heads, head_dim, g.B, "k")) != CSA_OK) return st;
+    if ((st = make_map(&tv, v, batch, g.N, n_heads, head_dim, g.B, "v")) != CSA_OK) return st;
+    csa::AttnArgs a;
+    a.g = g;
+    a.batch = batch;
+    a.n_heads = n_heads;
+    a.scale_log2 = softmax_scale * 1.4426950408889634f;
+    a.q = static_cast<const __nv_bfloat16*>(q.ptr);
+    a.o = static_cast<__nv_bfloat16*>(o.ptr);
+    a.q_sb = q.stride_b;
+    a.q_sn = q.stride_n;
+    a.q_sh = q.stride_h;
+    a.o_sb = o.stride_b;
+    a.o_sn = o.stride_n;
+    a.o_sh = o.stride_h;
+    a.lse_out = lse_out;
+    a.plan = csa::to_dev(*plan);
+    a.cell_base = cell_base;
+    a.work_list = work_list;
+    a.n_work = n_work;
+    const int64_t items = (int64_t)max_work * batch;
+    const int grid = (int)(items < di.sms ? items : di.sms);
+    cudaError_t e = csa::launch_attn(a, head_dim, tq, tk, tv, grid, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "attention launch");
+    return ok();
+}
+
+csa_status_t csa_validate_plan(const csa_plan_t* plan, csa_layout_t L, int64_t n_cells,
+                               csa_stream_t stream) {
+    csa_status_t st = check_layout(L, 0, 0);
+    if (st != CSA_OK) return st;
+    if (!plan_ptrs_ok(plan, true) || n_cells < 1 || n_cells > plan->n_cells)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "plan / n_cells");
+    std::lock_guard<std::mutex> lk(g_validate_mu);
+    uint32_t* flag = nullptr;
+    cudaError_t e = cudaGetSymbolAddress(reinterpret_cast<void**>(&flag), g_validate_flag);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetSymbolAddress");
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((e = cudaMemsetAsync(flag, 0, sizeof(uint32_t), s)) != cudaSuccess)
+        return cuda_fail(e, "memset");
+    if ((e = csa::launch_validate(csa::make_geo(L), n_cells, csa::to_dev(*plan), flag, s)) !=
+        cudaSuccess)
+        return cuda_fail(e, "validate launch");
+    uint32_t h = 0;
+    if ((e = cudaMemcpyAsync(&h, flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s)) !=
+        cudaSuccess)
+        return cuda_fail(e, "memcpy");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "sync");
+    if (h) return fail(CSA_ERR_CORRUPT_PLAN, "plan check failed (flags 0x%x)", h);
+    return ok();
+}
+
+}  // extern "C"

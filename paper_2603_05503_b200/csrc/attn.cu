@@ -1,0 +1,441 @@
+// attn.cu -- a7 + a8: calibrated block-sparse attention forward on sm_100a.
+//
+// What it computes:
+//   MASK cells: for query block r, softmax(scale Q_r K^T) V restricted to the keys of
+//     the kept key blocks c of row r (Eq. eq:p / eq:pv) -- skipped blocks excluded
+//     from numerator and normaliser (reading Q1) and never loaded.  Online softmax over the kept
+//     tiles in ascending c.
+//   REPETITIVE cells: only the k anchor spatial rows of every frame are
+//     computed, densely against all N keys; row (f,i,j) receives row (f, a(i), j) (Q9, Q10).
+//
+// Design: persistent, one CTA per SM, 12 warps.
+//   warp 0      producer: Q tile (TMA, or an in-warp gather of anchor rows), then the kept K/V
+//               tiles of the item's block list through a FIFO ring of smem slots (TMA, SW128).
+//   warp 1      MMA issuer (one thread): S_j = Q K_j^T into S[j&1] (TMEM), then
+//               O[(j-1)&1] += P_{j-1} V_{j-1} with P read from TMEM (TS-MMA).
+//   warp 2      TMEM allocator (512 columns: S0 S1 O0 O1).
+//   warps 4-7   softmax group 0: even tiles of the item's list   } each keeps its own (m, l, O);
+//   warps 8-11  softmax group 1: odd tiles                          } merged in the epilogue.
+// One thread owns one query row (= one TMEM lane).  Lazy rescale: O is rescaled only when the
+// running max grows by more than 2^8.
+#include <cstdint>
+
+#include "csa_internal.cuh"
+#include "tiles.cuh"
+
+namespace csa {
+namespace {
+
+constexpr int kThreads = 384;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+template <int BK, int D>
+struct AttnSmem {
+    using C = TileCfg<BK, D>;
+    static constexpr int kSlots = (BK == 128 && D == 128) ? 5 : 8;
+    static constexpr int kQOff = 0;
+    static constexpr int kKVOff = 2 * C::kQBytes;
+    static constexpr int kBarOff = kKVOff + kSlots * C::kKVBytes;
+    // barriers: q_full[2] q_empty[2] kv_full[S] kv_empty[S] s_full[2] p_full[2] o_full o_empty
+    static constexpr int kNumBars = 4 + 2 * kSlots + 4 + 2;
+    static constexpr int kRowOff = kBarOff + kNumBars * 8;           // m[2][128], l[2][128]
+    static constexpr int kTmemPtrOff = kRowOff + 4 * 128 * 4;
+    static constexpr int kBytes = kTmemPtrOff + 16;
+    static constexpr int kAlloc = kBytes;  // base is 1 KiB aligned (__align__ on the extern)
+    static_assert(kAlloc <= 232448, "smem");
+};
+
+struct Item {
+    uint32_t kind;  // 0 MASK, 1 REPETITIVE
+    int32_t h, idx, b;
+    int64_t cell;
+};
+
+__device__ __forceinline__ Item decode_item(const AttnArgs& a, int32_t item) {
+    const uint32_t code = a.work_list[item / a.batch];
+    Item it;
+    it.kind = code >> 31;
+    it.h = (int32_t)((code >> 20) & 0x7FFu);
+    it.idx = (int32_t)(code & 0xFFFFFu);
+    it.b = item % a.batch;
+    it.cell = a.cell_base + it.h;
+    return it;
+}
+
+// Kept key-block list of a MASK item (CSR), or all N_B blocks for a REPETITIVE item.
+struct TileList {
+    const uint16_t* idx;  // nullptr -> dense 0..n-1
+    int32_t n;
+    __device__ __forceinline__ int32_t at(int32_t j) const { return idx ? (int32_t)idx[j] : j; }
+};
+
+__device__ __forceinline__ TileList tile_list(const AttnArgs& a, const Item& it) {
+    TileList t;
+    if (it.kind) {
+        t.idx = nullptr;
+        t.n = a.g.NB;
+    } else {
+        const int32_t* rp = a.plan.blk_row_ptr + it.cell * (a.g.NB + 1);
+        const int32_t r0 = rp[it.idx], r1 = rp[it.idx + 1];
+        t.idx = a.plan.blk_idx + a.plan.blk_base[it.cell] + r0;
+        t.n = r1 - r0;
+    }
+    return t;
+}
+
+__device__ __forceinline__ int32_t anchor_row(int32_t H, int32_t k, int32_t m) {
+    return (int32_t)(((int64_t)(2 * m + 1) * H) / (2 * k));
+}
+
+template <int BK, int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    sparse_attn_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tq,
+                       const __grid_constant__ CUtensorMap tk,
+                       const __grid_constant__ CUtensorMap tv) {
+    using C = TileCfg<BK, D>;
+    using L = AttnSmem<BK, D>;
+    constexpr int S = L::kSlots;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    if ((smem_u32(smem) & 1023u) != 0u) __trap();  // SWIZZLE_128B atoms need 1 KiB alignment
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+    uint64_t* q_full = bars + 0;
+    uint64_t* q_empty = bars + 2;
+    uint64_t* kv_full = bars + 4;
+    uint64_t* kv_empty = bars + 4 + S;
+    uint64_t* s_full = bars + 4 + 2 * S;
+    uint64_t* p_full = bars + 6 + 2 * S;
+    uint64_t* o_full = bars + 8 + 2 * S;
+    uint64_t* o_empty = bars + 9 + 2 * S;
+    float* row_m = reinterpret_cast<float*>(smem + L::kRowOff);  // [2][128]
+    float* row_l = row_m + 256;                                   // [2][128]
+    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtrOff);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(q_full + i, 1);
+            mbar_init(q_empty + i, 1);
+            mbar_init(s_full + i, 1);
+            mbar_init(p_full + i, 4);
+        }
+        for (int i = 0; i < S; ++i) {
+            mbar_init(kv_full + i, 1);
+            mbar_init(kv_empty + i, 1);
+        }
+        mbar_init(o_full, 1);
+        mbar_init(o_empty, 8);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_ptr);
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tq);
+        tma_prefetch(&tk);
+        tma_prefetch(&tv);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_ptr;
+
+    const int32_t n_items = (*a.n_work) * a.batch;
+    const Geo& g = a.g;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------------ producer
+        const uint64_t pol_q = policy_evict_first();
+        const uint64_t pol_kv = policy_evict_last();
+        uint32_t ld = 0;  // K/V loads issued (ring position)
+        int32_t local = 0;
+        for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+            const Item it = decode_item(a, item);
+            const TileList tl = tile_list(a, it);
+            const int qb = local & 1;
+            uint8_t* qdst = smem + L::kQOff + qb * C::kQBytes;
+            mbar_wait(q_empty + qb, ((local >> 1) & 1) ^ 1);
+            if (it.kind == 0) {
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(q_full + qb, C::kBoxes * BK * 128);
+                    tma_tile<D>(qdst, C::kQBox, &tq, q_full + qb, it.h, it.idx * BK, it.b, pol_q);
+                }
+            } else {
+                // gather the anchor query rows of tile u: g = u*128 + row -> (f, m, j)
+                const int32_t kA = a.plan.anchor_k[it.cell];
+                const int32_t per_frame = kA * g.W;
+                const int32_t n_anchor = g.F * per_frame;
+                const __nv_bfloat16* qb_ptr = a.q + (int64_t)it.b * a.q_sb + (int64_t)it.h * a.q_sh;
+                constexpr int kChunks = D / 8;  // 16-byte chunks per row
+                for (int x = lane; x < 128 * kChunks; x += 32) {
+                    const int row = x / kChunks, ch = x % kChunks;
+                    const int32_t gi = it.idx * 128 + row;
+                    uint4 val = make_uint4(0u, 0u, 0u, 0u);
+                    if (gi < n_anchor) {
+                        const int32_t f = gi / per_frame;
+                        const int32_t m = (gi / g.W) % kA;
+                        const int32_t j = gi % g.W;
+                        const int64_t tok = (int64_t)f * g.H * g.W +
+                                            (int64_t)anchor_row(g.H, kA, m) * g.W + j;
+                        val = *reinterpret_cast<const uint4*>(qb_ptr + tok * a.q_sn + ch * 8);
+                    }
+                    *reinterpret_cast<uint4*>(qdst + (ch >> 3) * C::kQBox +
+                                              sw128_offset(row, ch & 7)) = val;
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(q_full + qb);
+            }
+            // K/V tiles in MMA consumption order: K0, (K1, V0), (K2, V1), ..., V_{n-1}
+            for (int32_t step = 0; step <= tl.n; ++step) {
+                for (int kv = 0; kv < 2; ++kv) {
+                    int32_t j;
+                    if (kv == 0) { if (step >= tl.n) continue; j = step; }
+                    else { if (step == 0) continue; j = step - 1; }
+                    const uint32_t slot = ld % S, ph = (ld / S) & 1;
+                    ++ld;
+                    mbar_wait(kv_empty + slot, ph ^ 1);
+                    if (lane == 0) {
+                        uint8_t* dst = smem + L::kKVOff + slot * C::kKVBytes;
+                        mbar_arrive_expect_tx(kv_full + slot, C::kKVBytes);
+                        tma_tile<D>(dst, C::kKBox, kv == 0 ? &tk : &tv, kv_full + slot, it.h,
+                                    tl.at(j) * BK, it.b, pol_kv);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            uint32_t cons = 0;           // K/V ring position consumed
+            uint32_t pcount[2] = {0, 0};  // p_full completions waited, per group
+            int32_t local = 0;
+            const uint32_t s_tmem[2] = {tmem, tmem + BK};
+            const uint32_t o_tmem[2] = {tmem + 2 * BK, tmem + 2 * BK + D};
+            const uint32_t q_base = smem_u32(smem + L::kQOff);
+            const uint32_t kv_base = smem_u32(smem + L::kKVOff);
+            for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+                const Item it = decode_item(a, item);
+                const TileList tl = tile_list(a, it);
+                const int qb = local & 1;
+                mbar_wait(q_full + qb, (local >> 1) & 1);
+                const uint32_t q_smem = q_base + qb * C::kQBytes;
+                auto do_pv = [&](int32_t t) {
+                    const int grp = t & 1;
+                    mbar_wait(p_full + grp, pcount[grp] & 1);
+                    ++pcount[grp];
+                    if (t == 0) mbar_wait(o_empty, (local & 1) ^ 1);  // epilogue of last item
+                    const uint32_t slot = cons % S, ph = (cons / S) & 1;
+                    ++cons;
+                    mbar_wait(kv_full + slot, ph);
+                    tc_fence_after();
+                    issue_pv<BK, D>(o_tmem[grp], s_tmem[grp], kv_base + slot * C::kKVBytes, t >= 2);
+                    mma_commit(kv_empty + slot);
+                };
+                if (tl.n == 0) {  // corrupt plan (empty MASK row): release Q, no output tiles
+                    mma_commit(q_empty + qb);
+                    mma_commit(o_full);
+                    continue;
+                }
+                for (int32_t j = 0; j < tl.n; ++j) {
+                    const int grp = j & 1;
+                    const uint32_t slot = cons % S, ph = (cons / S) & 1;
+                    ++cons;
+                    mbar_wait(kv_full + slot, ph);
+                    tc_fence_after();
+                    issue_qk<BK, D>(s_tmem[grp], q_smem, kv_base + slot * C::kKVBytes);
+                    mma_commit(s_full + grp);
+                    mma_commit(kv_empty + slot);
+                    if (j == tl.n - 1) mma_commit(q_empty + qb);
+                    if (j >= 1) do_pv(j - 1);
+                }
+                do_pv(tl.n - 1);
+                mma_commit(o_full);
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------------ softmax groups
+        const int grp = (warp - 4) >> 2;
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t s_col = grp * BK;
+        const uint32_t o_col = 2 * BK + grp * D;
+        const float sl2 = a.scale_log2;
+        uint32_t scount = 0;
+        int32_t local = 0;
+        for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+            const Item it = decode_item(a, item);
+            const TileList tl = tile_list(a, it);
+            float m_run = -INFINITY, l_run = 0.0f;
+            int32_t mine = 0;
+            for (int32_t j = grp; j < tl.n; j += 2, ++mine) {
+                mbar_wait(s_full + grp, scount & 1);
+                ++scount;
+                tc_fence_after();
+                float s[BK];
+#pragma unroll
+                for (int c = 0; c < BK; c += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(lane_addr + s_col + c, r);
+                    tmem_ld_wait(r);
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) s[c + x] = __uint_as_float(r[x]);
+                }
+                const int32_t cblk = tl.at(j);
+                const int32_t valid = g.N - cblk * BK;  // keys of this tile that exist (ragged)
+                if (valid < BK) {
+#pragma unroll
+                    for (int x = 0; x < BK; ++x)
+                        if (x >= valid) s[x] = -INFINITY;
+                }
+                float mx = s[0];
+#pragma unroll
+                for (int x = 1; x < BK; ++x) mx = fmaxf(mx, s[x]);
+                const float m_new = fmaxf(m_run, mx * sl2);
+                float alpha = 1.0f;
+                bool rescale = false;
+                if (mine == 0) {
+                    m_run = m_new;
+                } else if (m_new > m_run + kRescaleThreshold) {
+                    alpha = ex2_approx(m_run - m_new);
+                    l_run *= alpha;
+                    m_run = m_new;
+                    rescale = true;
+                }
+                float lsum = 0.0f;
+#pragma unroll
+                for (int c = 0; c < BK; c += 32) {  // P overwrites the first BK/2 columns of S
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int x = 0; x < 32; x += 2) {
+                        const float p0 = ex2_approx(fmaf(s[c + x], sl2, -m_run));
+                        const float p1 = ex2_approx(fmaf(s[c + x + 1], sl2, -m_run));
+                        lsum += p0 + p1;
+                        pk[x / 2] = pack_bf16(p0, p1);
+                    }
+                    tmem_st16(lane_addr + s_col + c / 2, pk);
+                }
+                l_run += lsum;
+                if (rescale) {
+#pragma unroll
+                    for (int c = 0; c < D; c += 32) {
+                        uint32_t r[32];
+                        tmem_ld32(lane_addr + o_col + c, r);
+                        tmem_ld_wait(r);
+#pragma unroll
+                        for (int x = 0; x < 32; ++x)
+                            r[x] = __float_as_uint(__uint_as_float(r[x]) * alpha);
+                        tmem_st32(lane_addr + o_col + c, r);
+                    }
+                }
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(p_full + grp);
+            }
+            // -------------------------------------------------------------- epilogue
+            mbar_wait(o_full, local & 1);
+            tc_fence_after();
+            row_m[grp * 128 + row] = m_run;
+            row_l[grp * 128 + row] = l_run;
+            named_bar_sync(1, 256);
+            const bool has0 = tl.n >= 1, has1 = tl.n >= 2;
+            const float m0 = row_m[row], m1 = row_m[128 + row];
+            const float l0 = row_l[row], l1 = row_l[128 + row];
+            const float M = has1 ? fmaxf(m0, m1) : m0;
+            const float a0 = has0 ? ex2_approx(m0 - M) : 0.0f;
+            const float a1 = has1 ? ex2_approx(m1 - M) : 0.0f;
+            const float Lsum = l0 * a0 + l1 * a1;
+            const float inv = 1.0f / Lsum;
+            const float f0 = a0 * inv, f1 = a1 * inv;
+            // output rows of this thread
+            int64_t tok0 = -1;
+            int32_t n_dst = 0, dst_stride_rows = 0;
+            if (it.kind == 0) {
+                const int64_t t = (int64_t)it.idx * BK + row;
+                if (row < BK && t < g.N) { tok0 = t; n_dst = 1; }
+            } else {
+                const int32_t kA = a.plan.anchor_k[it.cell];
+                const int32_t per_frame = kA * g.W;
+                const int32_t gi = it.idx * 128 + row;
+                if (gi < g.F * per_frame) {
+                    const int32_t f = gi / per_frame, m = (gi / g.W) % kA, jj = gi % g.W;
+                    const int32_t am = anchor_row(g.H, kA, m);
+                    const int32_t lo = m == 0 ? 0 : (anchor_row(g.H, kA, m - 1) + am) / 2 + 1;
+                    const int32_t hi =
+                        m == kA - 1 ? g.H : (am + anchor_row(g.H, kA, m + 1)) / 2 + 1;
+                    tok0 = (int64_t)f * g.H * g.W + (int64_t)lo * g.W + jj;
+                    n_dst = hi - lo;
+                    dst_stride_rows = g.W;
+                }
+            }
+            __nv_bfloat16* obase = a.o + (int64_t)it.b * a.o_sb + (int64_t)it.h * a.o_sh;
+#pragma unroll
+            for (int c = 0; c < D / 2; c += 32) {
+                const int col = grp * (D / 2) + c;
+                uint32_t r0[32], r1[32];
+                tmem_ld32(lane_addr + 2 * BK + col, r0);
+                if (has1) tmem_ld32(lane_addr + 2 * BK + D + col, r1);
+                tmem_ld_wait(r0);
+                if (has1) tmem_ld_wait(r1);
+                uint32_t packed[16];
+#pragma unroll
+                for (int x = 0; x < 32; x += 2) {
+                    float v0 = __uint_as_float(r0[x]) * f0;
+                    float v1 = __uint_as_float(r0[x + 1]) * f0;
+                    if (has1) {
+                        v0 = fmaf(__uint_as_float(r1[x]), f1, v0);
+                        v1 = fmaf(__uint_as_float(r1[x + 1]), f1, v1);
+                    }
+                    packed[x / 2] = pack_bf16(v0, v1);
+                }
+                for (int32_t dI = 0; dI < n_dst; ++dI) {
+                    uint4* dst = reinterpret_cast<uint4*>(
+                        obase + (tok0 + (int64_t)dI * dst_stride_rows) * a.o_sn + col);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v)
+                        dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2],
+                                            packed[4 * v + 3]);
+                }
+            }
+            if (grp == 0 && a.lse_out != nullptr) {
+                const float lse = (M + __log2f(Lsum)) * 0.69314718055994531f;
+                float* lb = a.lse_out + ((int64_t)it.b * a.n_heads + it.h) * (int64_t)g.N;
+                for (int32_t dI = 0; dI < n_dst; ++dI) lb[tok0 + (int64_t)dI * dst_stride_rows] = lse;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(o_empty);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+template <int BK, int D>
+cudaError_t launch_t(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                     const CUtensorMap& tv, int grid, cudaStream_t s) {
+    auto kern = sparse_attn_kernel<BK, D>;
+    const int smem = AttnSmem<BK, D>::kAlloc;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kThreads, smem, s>>>(a, tq, tk, tv);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_attn(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
+                        const CUtensorMap& tk, const CUtensorMap& tv, int grid, cudaStream_t s) {
+    if (a.g.B == 128 && head_dim == 128) return launch_t<128, 128>(a, tq, tk, tv, grid, s);
+    if (a.g.B == 128 && head_dim == 64) return launch_t<128, 64>(a, tq, tk, tv, grid, s);
+    if (a.g.B == 64 && head_dim == 128) return launch_t<64, 128>(a, tq, tk, tv, grid, s);
+    if (a.g.B == 64 && head_dim == 64) return launch_t<64, 64>(a, tq, tk, tv, grid, s);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace csa

@@ -1,0 +1,102 @@
+// csa_internal.cuh -- shared declarations of the CUDA side (kernels <-> C ABI layer).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include "../../include/csa.h"
+
+namespace csa {
+
+constexpr int kMaxBlocks = 2047;     // N_B limit (11-bit cost field of the work-list sort key)
+constexpr int kMaxWorkItems = 32768;  // single-CTA shared-memory sort of one launch's items
+constexpr int kAnchorTile = 128;      // gathered anchor-query rows per REPETITIVE work item
+
+struct Geo {
+    int32_t F, H, W, B;
+    int32_t N;   // F*H*W
+    int32_t NB;  // ceil(N/B)
+    int32_t W32; // ceil(NB/32) mask words per row
+};
+
+inline Geo make_geo(const csa_layout_t& L) {
+    Geo g;
+    g.F = L.frames;
+    g.H = L.rows;
+    g.W = L.cols;
+    g.B = L.block;
+    g.N = L.frames * L.rows * L.cols;
+    g.NB = (g.N + g.B - 1) / g.B;
+    g.W32 = (g.NB + 31) / 32;
+    return g;
+}
+
+// Plan pointers passed by value to kernels.
+struct PlanDev {
+    uint8_t* kind;
+    int32_t* anchor_k;
+    uint32_t* mask_bits;
+    int64_t* blk_base;
+    int32_t* blk_row_ptr;
+    uint16_t* blk_idx;
+    int64_t* ivl_base;
+    int32_t* ivl_row_ptr;
+    uint16_t* ivl;
+    int64_t* kept_area;
+    int64_t blk_capacity;
+    int64_t ivl_capacity;
+};
+
+inline PlanDev to_dev(const csa_plan_t& p) {
+    return PlanDev{p.kind,        p.anchor_k, p.mask_bits, p.blk_base,  p.blk_row_ptr, p.blk_idx,
+                   p.ivl_base,    p.ivl_row_ptr, p.ivl,    p.kept_area, p.blk_capacity,
+                   p.ivl_capacity};
+}
+
+// Launchers implemented in the .cu files; each returns a cudaError_t of the launch.
+cudaError_t launch_plan_count(const Geo& g, int64_t n_cells, const uint16_t* counts,
+                              int32_t min_count, const double* sim, double gamma, int32_t anchor_k,
+                              const PlanDev& p, cudaStream_t s);
+cudaError_t launch_plan_fill(const Geo& g, int64_t n_cells, const PlanDev& p, cudaStream_t s);
+cudaError_t launch_work_list(const Geo& g, const PlanDev& p, int64_t cell_base, int32_t n_heads,
+                             int32_t order, uint32_t* out, int32_t capacity, int32_t* n_work,
+                             cudaStream_t s);
+cudaError_t launch_validate(const Geo& g, int64_t n_cells, const PlanDev& p, uint32_t* flag,
+                            cudaStream_t s);
+
+struct CalibArgs {
+    Geo g;
+    int32_t n_heads;
+    float scale_log2;  // softmax_scale * log2(e)
+    const float* lse_in;
+    double eps;
+    uint16_t* keep_count;
+    float* energy_out;
+    float* lse_out;
+};
+cudaError_t launch_calib(const CalibArgs& a, int head_dim, const CUtensorMap& tq,
+                         const CUtensorMap& tk, int num_sms, cudaStream_t s);
+
+struct AttnArgs {
+    Geo g;
+    int32_t batch;
+    int32_t n_heads;
+    float scale_log2;
+    // q (for anchor-row gathers) and o: raw pointers + element strides
+    const __nv_bfloat16* q;
+    __nv_bfloat16* o;
+    int64_t q_sb, q_sn, q_sh;
+    int64_t o_sb, o_sn, o_sh;
+    float* lse_out;
+    PlanDev plan;
+    int64_t cell_base;
+    const uint32_t* work_list;
+    const int32_t* n_work;
+};
+cudaError_t launch_attn(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
+                        const CUtensorMap& tk, const CUtensorMap& tv, int grid,
+                        cudaStream_t s);
+
+}  // namespace csa

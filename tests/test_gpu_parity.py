@@ -1,0 +1,310 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on identical seeded
+inputs.  Bars:
+  * plan / mask / block-list / interval / work-list outputs: bit-exact;
+  * keep-count increments: bit-exact against the oracle's selection run on the GPU's own fp32 E;
+  * E: |dE| <= 5e-5 (fp32 exp2 path vs fp64), row sums 1 +- 1e-4;
+  * attention (bf16 I/O, fp32 accumulation): max |dO| <= 2e-2, mean |dO| <= 2e-3 (north star);
+    lse |d| <= 1e-3.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2603_05503_b200 import inputs
+from paper_2603_05503_b200.inputs import CONFIGS, Layout, qkv
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS, MEAN_ABS = 2e-2, 2e-3
+
+
+@pytest.fixture(scope="module")
+def csa():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_2603_05503_b200 import _build
+
+    _build.build()
+    from paper_2603_05503_b200 import csa as m
+
+    return m
+
+
+def head64(t, b, h):
+    return t[b, :, h].double().cpu().numpy()
+
+
+def u16_zeros(n):
+    return torch.zeros(n, dtype=torch.int16, device="cuda").view(torch.uint16)
+
+
+def u16_np(t):
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def u16_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint16).reshape(-1).view(np.int16)).cuda().view(torch.uint16)
+
+
+def unpack_bits(words, nb):
+    w = words.view(np.uint32) if words.dtype != np.uint32 else words
+    bits = np.unpackbits(w.view(np.uint8), bitorder="little")
+    return bits.reshape(-1, ((nb + 31) // 32) * 32)[:, :nb]
+
+
+def check_plan_against_oracle(csa, lay, counts_np, min_count, sim=None, gamma=0.87, anchor_k=5):
+    dev = torch.device("cuda")
+    cells = counts_np.shape[0]
+    counts = u16_dev(counts_np)
+    simt = None if sim is None else torch.tensor(sim, dtype=torch.float64, device=dev)
+    plan = csa.compile_plan(lay, counts, min_count, similarity=simt, gamma=gamma, anchor_k=anchor_k)
+    csa.validate_plan(plan)
+    nb = lay.NB
+    kind = plan.kind.cpu().numpy()
+    bits = unpack_bits(plan.mask_bits.cpu().numpy(), nb).reshape(cells, nb, nb)
+    brp = plan.blk_row_ptr.cpu().numpy().reshape(cells, nb + 1)
+    irp = plan.ivl_row_ptr.cpu().numpy().reshape(cells, nb + 1)
+    bb = plan.blk_base.cpu().numpy()
+    ib = plan.ivl_base.cpu().numpy()
+    bidx = u16_np(plan.blk_idx)
+    ivl = u16_np(plan.ivl)
+    area = plan.kept_area.cpu().numpy()
+    for c in range(cells):
+        ref = oracle.compile_cell(counts_np[c], lay.N, lay.B, lay.F, lay.H, lay.W, min_count,
+                                  similarity=None if sim is None else sim[c], gamma=gamma,
+                                  anchor_k=anchor_k)
+        assert kind[c] == ref["kind"]
+        assert area[c] == ref["kept_area"]
+        assert np.array_equal(brp[c], ref["blk_row_ptr"])
+        assert np.array_equal(irp[c], ref["ivl_row_ptr"])
+        if ref["kind"] == 0:
+            assert np.array_equal(bits[c], ref["mask"])
+            assert np.array_equal(bidx[bb[c]:bb[c + 1]], ref["blk_idx"])
+            assert np.array_equal(ivl[2 * ib[c]:2 * ib[c + 1]].reshape(-1, 2), ref["ivl"])
+        else:
+            assert not bits[c].any() and bb[c + 1] == bb[c]
+    return plan
+
+
+# ---------------------------------------------------------------- a6 plan compiler
+@pytest.mark.parametrize("lay", [Layout(2, 5, 25, 64), Layout(4, 8, 8, 64), Layout(21, 30, 52, 128),
+                                 Layout(3, 7, 100, 128)])
+def test_plan_compile_bit_exact(csa, lay):
+    nb = lay.NB
+    counts = inputs.random_counts(nb, 5, 64, seed=nb)
+    counts[1] = 0                                   # every row repaired -> argmax (c = 0)
+    counts[2] = 64                                  # all ones
+    counts[3] = 0
+    counts[3][:, ::2] = 40                          # alternating: worst-case intervals
+    check_plan_against_oracle(csa, lay, counts, 32)
+    sim = [0.5, 0.87, 0.8700001, 1.0, 0.0]          # s == gamma stays MASK (strict, Q8)
+    check_plan_against_oracle(csa, lay, counts, 32, sim=sim, anchor_k=min(5, lay.H))
+
+
+def test_plan_compile_wan720_synthetic(csa):
+    cfg = CONFIGS["wan720"]
+    counts = inputs.synthetic_counts(cfg.layout, 4, cfg.sparsity, 64, seed=3)
+    check_plan_against_oracle(csa, cfg.layout, counts, 32)
+
+
+def test_work_list_bit_exact(csa):
+    lay = Layout(21, 30, 52, 128)
+    counts = inputs.random_counts(lay.NB, 6, 8, seed=5)
+    sim = [0.0, 0.95, 0.0, 0.0, 0.99, 0.0]
+    plan = check_plan_against_oracle(csa, lay, counts, 4, sim=sim, anchor_k=5)
+    rp = plan.blk_row_ptr.cpu().numpy().reshape(6, lay.NB + 1)
+    nnz = np.diff(rp, axis=1)
+    kinds = plan.kind.cpu().numpy()
+    ak = plan.anchor_k.cpu().numpy()
+    for base, nh in ((0, 6), (1, 4)):
+        wl = csa.build_work_list(plan, base, nh, order=0)
+        got = wl.items.cpu().numpy().view(np.uint32)[: int(wl.n_work.item())]
+        ref = oracle.work_list(lay.N, lay.B, lay.F, lay.W, kinds[base:base + nh], ak[base:base + nh],
+                               nnz[base:base + nh])
+        assert np.array_equal(got, ref)
+        nat = csa.build_work_list(plan, base, nh, order=1)
+        gotn = nat.items.cpu().numpy().view(np.uint32)[: int(nat.n_work.item())]
+        key = lambda c: ((int(c) >> 20) & 0x7FF, int(c) & 0xFFFFF)
+        assert list(gotn) == sorted(ref.tolist(), key=key)
+
+
+# ---------------------------------------------------------------- a7/a8 attention
+def run_attention(csa, lay, q, k, v, masks=None, rep=None, anchor_k=2, order=0, lse=False):
+    """masks: [H, NB, NB] uint8 for MASK heads; rep: list of REPETITIVE head indices."""
+    heads = q.shape[2]
+    nb = lay.NB
+    if masks is None:
+        masks = np.ones((heads, nb, nb), np.uint8)
+    counts = masks.astype(np.uint16)
+    sim = None
+    if rep:
+        sim = torch.tensor([1.0 if h in rep else 0.0 for h in range(heads)], dtype=torch.float64,
+                           device="cuda")
+    ct = u16_dev(counts)
+    plan = csa.compile_plan(lay, ct, 1, similarity=sim, gamma=0.87, anchor_k=anchor_k)
+    work = csa.build_work_list(plan, 0, heads, order=order)
+    lse_t = torch.empty(q.shape[0] * heads * lay.N, dtype=torch.float32, device="cuda") if lse else None
+    out = csa.sparse_attn_fwd(q, k, v, plan, work, lse_out=lse_t)
+    torch.cuda.synchronize()
+    return out, lse_t, plan
+
+
+def oracle_head(lay, q, k, v, b, h, mask=None, rep_k=None, rows=None):
+    scale = 1.0 / np.sqrt(q.shape[3])
+    qh, kh, vh = head64(q, b, h), head64(k, b, h), head64(v, b, h)
+    if rep_k:
+        return oracle.anchor_attention_rows(lay.F, lay.H, lay.W, qh, kh, vh, scale, rep_k, rows)
+    return oracle.masked_attention_rows(qh, kh, vh, scale, lay.B, mask, rows)
+
+
+def assert_close(got, ref, what=""):
+    err = np.abs(got - ref)
+    assert err.max() <= MAX_ABS and err.mean() <= MEAN_ABS, f"{what} max {err.max()} mean {err.mean()}"
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny_ragged"])
+def test_attention_tiny_masks(csa, name):
+    cfg = CONFIGS[name]
+    lay = cfg.layout
+    q, k, v = qkv(1, lay.N, 1, cfg.d, seed=0, device="cuda")
+    nb = lay.NB
+    cases = {"hand": inputs.TINY_HAND_MASK, "ones": np.ones((nb, nb), np.uint8),
+             "identity": np.eye(nb, dtype=np.uint8),
+             "last_col": np.eye(nb, dtype=np.uint8)[[nb - 1] * nb]}
+    for cname, m in cases.items():
+        out, lse, _ = run_attention(csa, lay, q, k, v, masks=m[None], lse=True)
+        ref, ref_lse = oracle_head(lay, q, k, v, 0, 0, mask=m)
+        assert_close(out[0, :, 0].double().cpu().numpy(), ref, cname)
+        assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 1e-3, cname
+
+
+def test_attention_tiny_repetitive(csa):
+    cfg = CONFIGS["tiny"]
+    lay = cfg.layout
+    q, k, v = qkv(1, lay.N, 2, cfg.d, seed=4, device="cuda")
+    for kA in (1, 2, 5, lay.H):
+        out, _, _ = run_attention(csa, lay, q, k, v, rep=[1], anchor_k=kA)
+        ref, _ = oracle_head(lay, q, k, v, 0, 1, rep_k=kA)
+        o = out[0, :, 1].double().cpu().numpy()
+        assert_close(o, ref, f"k={kA}")
+        # broadcast rows are bitwise copies of their anchor row
+        anchors = oracle.anchor_rows(lay.H, kA)
+        o3 = out[0, :, 1].view(lay.F, lay.H, lay.W, -1)
+        for i in range(lay.H):
+            a = anchors[oracle.nearest_anchor(lay.H, kA, i)]
+            assert torch.equal(o3[:, i], o3[:, a])
+        ref0, _ = oracle_head(lay, q, k, v, 0, 0, mask=np.ones((lay.NB, lay.NB), np.uint8))
+        assert_close(out[0, :, 0].double().cpu().numpy(), ref0, "dense head")
+
+
+def test_attention_batch2_shares_plan_and_is_deterministic(csa):
+    lay = Layout(2, 5, 25, 64)
+    q, k, v = qkv(2, lay.N, 3, 64, seed=7, device="cuda")
+    rng = np.random.default_rng(1)
+    masks = (rng.random((3, lay.NB, lay.NB)) < 0.5).astype(np.uint8)
+    masks[:, np.arange(lay.NB), np.arange(lay.NB)] = 1
+    out, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[2], anchor_k=2)
+    out2, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[2], anchor_k=2, order=1)
+    assert torch.equal(out, out2)  # LPT vs natural order: per-item arithmetic is schedule-free
+    for b in range(2):
+        for h in range(3):
+            ref, _ = oracle_head(lay, q, k, v, b, h, mask=masks[h], rep_k=2 if h == 2 else None)
+            assert_close(out[b, :, h].double().cpu().numpy(), ref, f"b{b} h{h}")
+        single, _, _ = run_attention(csa, lay, q[b:b + 1].contiguous(), k[b:b + 1].contiguous(),
+                                     v[b:b + 1].contiguous(), masks=masks, rep=[2], anchor_k=2)
+        assert torch.equal(single[0], out[b])
+
+
+def sample_units(lay, heads, n, seed):
+    rng = np.random.default_rng(seed)
+    units = {(0, lay.NB - 1), (heads - 1, 0)}
+    while len(units) < n:
+        units.add((int(rng.integers(heads)), int(rng.integers(lay.NB))))
+    return sorted(units)
+
+
+@pytest.mark.parametrize("name", ["wan480", "wan720"])
+def test_attention_full_size_sampled(csa, name):
+    """BASELINE configs at full size, bench launch configuration; oracle on sampled (h, r)."""
+    cfg = CONFIGS[name]
+    lay = cfg.layout
+    q, k, v = qkv(1, lay.N, cfg.heads, cfg.d, seed=11, device="cuda")
+    masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity, seed=0)
+    rep = [3, 17, 29, 38]
+    out, lse, plan = run_attention(csa, lay, q, k, v, masks=masks, rep=rep, anchor_k=5, lse=True)
+    lse = lse.view(cfg.heads, lay.N).cpu().numpy()
+    errs = []
+    for h, r in sample_units(lay, cfg.heads, 10, seed=2):
+        rows = (r * lay.B, min((r + 1) * lay.B, lay.N))
+        ref, ref_lse = oracle_head(lay, q, k, v, 0, h, mask=masks[h],
+                                   rep_k=5 if h in rep else None, rows=rows)
+        got = out[0, rows[0]:rows[1], h].double().cpu().numpy()
+        assert_close(got, ref, f"h{h} r{r}")
+        assert np.abs(lse[h, rows[0]:rows[1]] - ref_lse).max() <= 1e-3
+        errs.append(np.abs(got - ref).max())
+    assert torch.isfinite(out).all()
+
+
+# ---------------------------------------------------------------- a2-a5 calibration
+@pytest.mark.parametrize("lay,heads,d", [(Layout(2, 5, 25, 64), 2, 64), (Layout(4, 8, 8, 64), 1, 64),
+                                         (Layout(2, 9, 40, 128), 2, 128)])
+def test_calibration_against_oracle(csa, lay, heads, d):
+    q, k, _ = inputs.structured_qk(lay, heads, d, head_seed=1, prompt_seed=2, alpha=1.0,
+                                   device="cuda")
+    nb = lay.NB
+    eps = 0.9
+    counts = u16_zeros(heads * nb * nb)
+    counts_np = np.zeros((heads, nb, nb), np.uint16)
+    energy = torch.empty(heads * nb * nb, dtype=torch.float32, device="cuda")
+    lse_out = torch.empty(heads * lay.N, dtype=torch.float32, device="cuda")
+    scale = 1.0 / np.sqrt(d)
+    for prompt in range(3):  # accumulate over prompts: integer counts exact
+        q, k, _ = inputs.structured_qk(lay, heads, d, 1, prompt, alpha=1.0, device="cuda")
+        csa.calib_accumulate(lay, q, k, eps, counts, energy_out=energy, lse_out=lse_out)
+        torch.cuda.synchronize()
+        E = energy.view(heads, nb, nb).double().cpu().numpy()
+        lg = lse_out.view(heads, lay.N).double().cpu().numpy()
+        for h in range(heads):
+            qh, kh = head64(q, 0, h), head64(k, 0, h)
+            ref_lse = oracle.row_lse(qh, kh, scale)
+            assert np.abs(lg[h] - ref_lse).max() <= 1e-3
+            E_ref = oracle.block_energy(qh, kh, scale, lay.B)
+            assert np.abs(E[h] - E_ref).max() <= 5e-5
+            assert np.abs(E[h].sum(1) - 1).max() <= 1e-4
+            for r in range(nb):
+                oracle.accumulate(oracle.select(E[h, r], eps), counts_np[h, r])
+        assert np.array_equal(u16_np(counts).reshape(heads, nb, nb), counts_np)
+    # LSE supplied from outside (the dense run's statistic) gives the same decisions on this E
+    counts2 = u16_zeros(heads * nb * nb)
+    csa.calib_accumulate(lay, q, k, eps, counts2, lse_in=lse_out, energy_out=energy)
+    torch.cuda.synchronize()
+    E2 = energy.view(heads, nb, nb).double().cpu().numpy()
+    c2 = u16_np(counts2).reshape(heads, nb, nb)
+    for h in range(heads):
+        for r in range(nb):
+            assert np.array_equal(oracle.select(E2[h, r], eps), c2[h, r])
+
+
+def test_calibration_wan480_sampled(csa):
+    cfg = CONFIGS["wan480"]
+    lay = cfg.layout
+    heads = 4
+    q, k, _ = inputs.structured_qk(lay, heads, cfg.d, 5, 0, alpha=[0.8, 1.0, 1.2, 1.5],
+                                   repetitive=(2,), device="cuda")
+    nb = lay.NB
+    counts = u16_zeros(heads * nb * nb)
+    energy = torch.empty(heads * nb * nb, dtype=torch.float32, device="cuda")
+    eps = oracle.epsilon(25, 50, oracle.A_of_N(lay.N), 0.99, 16)
+    csa.calib_accumulate(lay, q, k, eps, counts, energy_out=energy)
+    torch.cuda.synchronize()
+    E = energy.view(heads, nb, nb).double().cpu().numpy()
+    cnt = u16_np(counts).reshape(heads, nb, nb)
+    scale = 1.0 / np.sqrt(cfg.d)
+    for h in range(heads):
+        for r in range(nb):  # bit-exact selection on the GPU's own E, every row
+            assert np.array_equal(oracle.select(E[h, r], eps), cnt[h, r])
+    for h, r in ((0, 0), (3, nb - 1)):
+        qh, kh = head64(q, 0, h), head64(k, 0, h)
+        E_ref = oracle.block_energy(qh, kh, scale, lay.B, block_rows=(r, r + 1))
+        assert np.abs(E[h, r] - E_ref[0]).max() <= 5e-5
