@@ -1,6 +1,5 @@
 #!/bin/bash
 # One gpurun round trip: build, smoke, GPU parity tests (each bounded by its own timeout).
-set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
@@ -8,4 +7,5 @@ timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 echo "smoke exit $?" >> gpurun_out/smoke.log
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
-tail -5 gpurun_out/smoke.log gpurun_out/pytest_gpu.log
+tail -n 3 gpurun_out/smoke.log
+tail -n 5 gpurun_out/pytest_gpu.log
