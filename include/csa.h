@@ -152,7 +152,9 @@ CSA_API csa_status_t csa_compile_plan(csa_layout_t L, int64_t n_cells, const uin
  * cell_base + h.  MASK head: items (h, r), r < N_B, cost = kept blocks of row r; REPETITIVE
  * head: items (h, u), u < ceil(F*k*W/128) anchor-query tiles, cost = N_B.
  * order 0: longest-first, ties (h asc, kind asc, index asc) -- a total order (unique output);
- * order 1: natural (h asc, index asc).
+ * order 1: natural (h asc, index asc);
+ * order 2: head-major, longest-first within a head (h asc, cost desc, index asc) -- the L2-local
+ *          order the dynamic scheduler of csa_sparse_attn_fwd is built for (default).
  * Encoding: kind<<31 | h<<20 | (r or u).  work_list: uint32 [capacity]; n_work: device int32.
  * Requires n_heads <= 2048 and at most 32768 items. */
 CSA_API csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan, int64_t cell_base,
@@ -173,7 +175,10 @@ CSA_API csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan,
  *   lse_out     optional fp32 [batch][n_heads][N], natural log over the kept keys
  *   work_list   items from csa_build_work_list; n_work device int32 (count)
  *   max_work    host upper bound of *n_work (sizes the persistent grid)
- * Workspace: csa_workspace_size(CSA_WS_ATTN, ...) bytes. */
+ * Workspace: csa_workspace_size(CSA_WS_ATTN, ...) bytes of device memory holding the dynamic
+ * scheduler's counters; it must be zero-filled before its first use and is left zero-filled when
+ * the launch completes (so one buffer serves every launch on one stream).  NULL -> static
+ * round-robin assignment of work items to CTAs. */
 CSA_API csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
                                  int32_t head_dim, float softmax_scale, csa_tensor_t q,
                                  csa_tensor_t k, csa_tensor_t v, csa_tensor_t o, float* lse_out,

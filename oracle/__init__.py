@@ -79,7 +79,8 @@ def lib():
         L.csao_compile_cell.argtypes = [_c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _p, _c_i32, _c_i32,
                                         _c_dbl, _c_dbl, _c_i32, _p, _p, _p, _p, _p, _p, _p]
         L.csao_work_list.restype = _c_i64
-        L.csao_work_list.argtypes = [_c_i32, _c_i64, _c_i32, _c_i32, _c_i32, _p, _p, _p, _p, _c_i64]
+        L.csao_work_list.argtypes = [_c_i32, _c_i64, _c_i32, _c_i32, _c_i32, _p, _p, _p, _c_i32, _p,
+                                     _c_i64]
     return _lib
 
 
@@ -237,8 +238,10 @@ def compile_cell(count, n: int, block: int, F: int, H: int, W: int, min_count_: 
     }
 
 
-def work_list(n: int, block: int, F: int, W: int, kinds, anchor_k, row_nnz) -> np.ndarray:
-    """LPT work list of one launch (scheduling artefact)."""
+def work_list(n: int, block: int, F: int, W: int, kinds, anchor_k, row_nnz, order: int = 0
+              ) -> np.ndarray:
+    """Work list of one launch (scheduling artefact): order 0 longest-first,
+    1 natural, 2 head-major longest-first within a head."""
     kinds = np.ascontiguousarray(np.asarray(kinds, dtype=np.uint8))
     ak = np.ascontiguousarray(np.asarray(anchor_k, dtype=np.int32))
     nnz = np.ascontiguousarray(np.asarray(row_nnz, dtype=np.int32))
@@ -246,7 +249,7 @@ def work_list(n: int, block: int, F: int, W: int, kinds, anchor_k, row_nnz) -> n
     cap = int(kinds.size * max(nb, (F * int(ak.max(initial=1)) * W + 127) // 128) + 1)
     out = np.zeros(cap, np.uint32)
     cnt = lib().csao_work_list(kinds.size, n, block, F, W, _ptr(kinds), _ptr(ak), _ptr(nnz),
-                               _ptr(out), cap)
+                               order, _ptr(out), cap)
     if cnt < 0:
         raise ValueError("work_list: capacity")
     return out[:cnt].copy()

@@ -352,14 +352,18 @@ int csao_compile_cell(int64_t n, int32_t b, int32_t F, int32_t H, int32_t W,
 /* artefact of DESIGN.md; its order is a total order so the output is unique).                 */
 /*   MASK head h: items (h, r) for r < N_B, cost = nnz of row r;                                */
 /*   REPETITIVE head h: items (h, u) for u < ceil(F*k*W/128), cost = N_B.                        */
-/* Sorted by (cost desc, h asc, kind asc, r-or-u asc); encoded kind<<31 | h<<20 | (r or u).      */
+/* order 0: (cost desc, h asc, kind asc, r-or-u asc); order 1: (h asc, r-or-u asc);             */
+/* order 2: (h asc, cost desc, r-or-u asc).  Encoded kind<<31 | h<<20 | (r or u).               */
 /* row_nnz: [n_heads * N_B] (ignored for REPETITIVE heads).  Returns item count, -1 on error.   */
 /* ------------------------------------------------------------------------------------------ */
 typedef struct { int64_t cost; uint32_t code; } orc_item;
+static int g_order; /* qsort has no context argument; single-threaded use */
 static int cmp_item(const void* a, const void* b) {
     const orc_item* x = (const orc_item*)a;
     const orc_item* y = (const orc_item*)b;
-    if (x->cost != y->cost) return x->cost > y->cost ? -1 : 1;
+    const uint32_t hx = (x->code >> 20) & 0x7FF, hy = (y->code >> 20) & 0x7FF;
+    if (g_order != 0 && hx != hy) return hx < hy ? -1 : 1;
+    if (g_order != 1 && x->cost != y->cost) return x->cost > y->cost ? -1 : 1;
     /* h, kind, index are laid out so that code order == (h asc, kind asc, idx asc) */
     const uint32_t kx = ((x->code >> 20) & 0x7FF) << 21 | (x->code >> 31) << 20 | (x->code & 0xFFFFF);
     const uint32_t ky = ((y->code >> 20) & 0x7FF) << 21 | (y->code >> 31) << 20 | (y->code & 0xFFFFF);
@@ -368,7 +372,7 @@ static int cmp_item(const void* a, const void* b) {
 
 int64_t csao_work_list(int32_t n_heads, int64_t n, int32_t b, int32_t F, int32_t W,
                        const uint8_t* kinds, const int32_t* anchor_k, const int32_t* row_nnz,
-                       uint32_t* out, int64_t capacity) {
+                       int32_t order, uint32_t* out, int64_t capacity) {
     const int64_t nb = csao_num_blocks(n, b);
     int64_t total = 0;
     for (int32_t h = 0; h < n_heads; ++h)
@@ -393,6 +397,7 @@ int64_t csao_work_list(int32_t n_heads, int64_t n, int32_t b, int32_t F, int32_t
             }
         }
     }
+    g_order = order;
     qsort(it, (size_t)total, sizeof(orc_item), cmp_item);
     for (int64_t y = 0; y < total; ++y) out[y] = it[y].code;
     free(it);

@@ -242,8 +242,9 @@ class WorkList:
     max_work: int
 
 
-def build_work_list(plan: Plan, cell_base: int, n_heads: int, order: int = 0,
+def build_work_list(plan: Plan, cell_base: int, n_heads: int, order: int = 2,
                     stream=None) -> WorkList:
+    """csa_build_work_list; order 2 (head-major, longest row first) is the L2-local default."""
     cap = plan.items(cell_base, n_heads)
     items = torch.empty(max(cap, 1), dtype=torch.int32, device=plan.kind.device)
     n_work = torch.empty(1, dtype=torch.int32, device=plan.kind.device)
@@ -258,8 +259,9 @@ def build_work_list(plan: Plan, cell_base: int, n_heads: int, order: int = 0,
 def sparse_attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: Plan,
                     work: WorkList, cell_base: int = 0, out: torch.Tensor | None = None,
                     lse_out: torch.Tensor | None = None, scale: float | None = None,
-                    stream=None) -> torch.Tensor:
-    """csa_sparse_attn_fwd on q/k/v [batch, N, heads, d] (bf16, CUDA)."""
+                    stream=None, dynamic: bool = True) -> torch.Tensor:
+    """csa_sparse_attn_fwd on q/k/v [batch, N, heads, d] (bf16, CUDA).  dynamic=False uses the
+    static round-robin item assignment (no scheduler workspace)."""
     b, n, heads, d = q.shape
     assert n == plan.lay.N and k.shape == q.shape and v.shape == q.shape
     if out is None:
@@ -269,11 +271,25 @@ def sparse_attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: Pla
         assert lse_out.numel() == b * heads * n
     sc = default_scale(d) if scale is None else scale
     s = plan.struct()
+    ws = _sched_workspace(q.device) if dynamic else None
     _check(lib().csa_sparse_attn_fwd(_layout(plan.lay), b, heads, d, sc, _tensor(q), _tensor(k),
                                      _tensor(v), _tensor(out), _ptr(lse_out), ctypes.byref(s),
                                      cell_base, _ptr(work.items), _ptr(work.n_work), work.max_work,
-                                     None, 0, _stream(stream)), "csa_sparse_attn_fwd")
+                                     _ptr(ws), 0 if ws is None else ws.numel(), _stream(stream)),
+           "csa_sparse_attn_fwd")
     return out
+
+
+_SCHED_WS: dict = {}
+
+
+def _sched_workspace(device) -> torch.Tensor:
+    """Zero-filled dynamic-scheduler workspace (left zero-filled by every launch, csa.h)."""
+    key = torch.device(device).index
+    if key not in _SCHED_WS:
+        n = lib().csa_workspace_size(3, _LayoutT(1, 1, 1, 128), 1, 128)
+        _SCHED_WS[key] = torch.zeros(n, dtype=torch.uint8, device=device)
+    return _SCHED_WS[key]
 
 
 def version() -> str:

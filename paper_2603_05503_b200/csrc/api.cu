@@ -134,11 +134,10 @@ const char* csa_last_error(void) { return g_err.c_str(); }
 const char* csa_version(void) { return "csa-b200 0.1 (sm_100a)"; }
 
 size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_t head_dim) {
-    (void)which;
     (void)L;
     (void)n_heads;
     (void)head_dim;
-    return 0;  // every kernel of this version is workspace-free
+    return which == CSA_WS_ATTN ? 256 : 0;  // attention: dynamic-scheduler counters
 }
 
 csa_status_t csa_calib_accumulate(csa_layout_t L, int32_t n_heads, int32_t head_dim,
@@ -208,7 +207,7 @@ csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan, int64_t
     csa_status_t st = check_layout(L, 0, n_heads);
     if (st != CSA_OK) return st;
     if (n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "n_heads must be >= 1");
-    if (order != 0 && order != 1) return fail(CSA_ERR_INVALID_ARGUMENT, "order must be 0 or 1");
+    if (order < 0 || order > 2) return fail(CSA_ERR_INVALID_ARGUMENT, "order must be 0, 1 or 2");
     if (!plan_ptrs_ok(plan, false) || !work_list || !n_work)
         return fail(CSA_ERR_INVALID_ARGUMENT, "null buffer");
     if (cell_base < 0 || cell_base + n_heads > plan->n_cells)
@@ -228,10 +227,10 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
                                  const uint32_t* work_list, const int32_t* n_work,
                                  int32_t max_work, void* workspace, size_t workspace_bytes,
                                  csa_stream_t stream) {
-    (void)workspace;
-    (void)workspace_bytes;
     csa_status_t st = check_layout(L, head_dim, n_heads);
     if (st != CSA_OK) return st;
+    if (workspace != nullptr && (workspace_bytes < 8 || reinterpret_cast<uintptr_t>(workspace) % 8))
+        return fail(CSA_ERR_INVALID_ARGUMENT, "attention workspace: >= 8 bytes, 8-byte aligned");
     if (batch < 1 || n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "batch/n_heads < 1");
     if (!(softmax_scale > 0.0f)) return fail(CSA_ERR_INVALID_ARGUMENT, "softmax_scale <= 0");
     if (!plan_ptrs_ok(plan, true) || !work_list || !n_work)
@@ -270,6 +269,7 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
     a.cell_base = cell_base;
     a.work_list = work_list;
     a.n_work = n_work;
+    a.sched = static_cast<uint32_t*>(workspace);
     const int64_t items = (int64_t)max_work * batch;
     const int grid = (int)(items < di.sms ? items : di.sms);
     cudaError_t e = csa::launch_attn(a, head_dim, tq, tk, tv, grid, (cudaStream_t)stream);

@@ -8,16 +8,19 @@
 //   REPETITIVE cells: only the k anchor spatial rows of every frame are
 //     computed, densely against all N keys; row (f,i,j) receives row (f, a(i), j) (Q9, Q10).
 //
-// Design (DESIGN.md "Attention kernel"): persistent, one CTA per SM, 12 warps.
-//   warp 0      producer: Q tile (TMA, or an in-warp gather of anchor rows), then the kept K/V
-//               tiles of the item's block list through a FIFO ring of smem slots (TMA, SW128).
+// Design (DESIGN.md section 5): persistent, one CTA per SM, 12 warps.
+//   warp 0      scheduler + producer: claims items (dynamic, head-major work list) and publishes
+//               them through a 4-deep shared-memory ring; loads the Q tile (TMA, or an in-warp
+//               gather of anchor rows), then the kept K/V tiles of the item's block list through
+//               a FIFO ring of smem slots in MMA consumption order K0, K1, V0, K2, V1, ...
 //   warp 1      MMA issuer (one thread): S_j = Q K_j^T into S[j&1] (TMEM), then
 //               O[(j-1)&1] += P_{j-1} V_{j-1} with P read from TMEM (TS-MMA).
 //   warp 2      TMEM allocator (512 columns: S0 S1 O0 O1).
 //   warps 4-7   softmax group 0: even tiles of the item's list   } each keeps its own (m, l, O);
 //   warps 8-11  softmax group 1: odd tiles                          } merged in the epilogue.
 // One thread owns one query row (= one TMEM lane).  Lazy rescale: O is rescaled only when the
-// running max grows by more than 2^8.
+// running max grows by more than 2^8.  Packed f32x2 FMA/ADD; a fixed fraction of the exp2 are
+// evaluated by a degree-3 polynomial on the FMA pipe to offload the MUFU unit.
 #include <cstdint>
 
 #include "csa_internal.cuh"
@@ -28,6 +31,8 @@ namespace {
 
 constexpr int kThreads = 384;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr int kItemSlots = 4;
+constexpr int kEmuEvery = 8;  // every kEmuEvery-th element pair uses the polynomial exp2
 
 template <int BK, int D>
 struct AttnSmem {
@@ -36,10 +41,12 @@ struct AttnSmem {
     static constexpr int kQOff = 0;
     static constexpr int kKVOff = 2 * C::kQBytes;
     static constexpr int kBarOff = kKVOff + kSlots * C::kKVBytes;
-    // barriers: q_full[2] q_empty[2] kv_full[S] kv_empty[S] s_full[2] p_full[2] o_full o_empty
-    static constexpr int kNumBars = 4 + 2 * kSlots + 4 + 2;
+    // q_full[2] q_empty[2] kv_full[S] kv_empty[S] s_full[2] p_full[2] o_full o_empty
+    // item_full[4] item_empty[4]
+    static constexpr int kNumBars = 4 + 2 * kSlots + 4 + 2 + 2 * kItemSlots;
     static constexpr int kRowOff = kBarOff + kNumBars * 8;           // m[2][128], l[2][128]
-    static constexpr int kTmemPtrOff = kRowOff + 4 * 128 * 4;
+    static constexpr int kItemOff = kRowOff + 4 * 128 * 4;           // int32 [kItemSlots]
+    static constexpr int kTmemPtrOff = kItemOff + kItemSlots * 4;
     static constexpr int kBytes = kTmemPtrOff + 16;
     static constexpr int kAlloc = kBytes;  // base is 1 KiB aligned (__align__ on the extern)
     static_assert(kAlloc <= 232448, "smem");
@@ -87,6 +94,69 @@ __device__ __forceinline__ int32_t anchor_row(int32_t H, int32_t k, int32_t m) {
     return (int32_t)(((int64_t)(2 * m + 1) * H) / (2 * k));
 }
 
+// ------------------------------------------------------------------------ packed fp32 helpers
+__device__ __forceinline__ uint64_t pk2(uint32_t lo, uint32_t hi) {
+    return (uint64_t)lo | ((uint64_t)hi << 32);
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2_rm(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rm.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ float lo_f(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+    return pk2(__float_as_uint(lo), __float_as_uint(hi));
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
+// 2^x for a pair of x <= 8 on the FMA pipe: x = n + f, 2^f by a degree-3 minimax polynomial
+// (max rel. error 8.6e-5, far below the bf16 rounding of P), exponent added as integer.
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
+    const float x0 = fmaxf(lo_f(x), -127.0f), x1 = fmaxf(hi_f(x), -127.0f);
+    const uint64_t xc = f2(x0, x1);
+    const uint64_t kRound = f2(12582912.0f, 12582912.0f);  // 2^23 + 2^22
+    const uint64_t rnd = fadd2_rm(xc, kRound);               // floor(x) in the low mantissa bits
+    const uint64_t frac = fsub2(xc, fsub2(rnd, kRound));     // in [0, 1)
+    uint64_t p = f2(0.077066176f, 0.077066176f);
+    p = ffma2(p, frac, f2(0.22764593f, 0.22764593f));
+    p = ffma2(p, frac, f2(0.6951166f, 0.6951166f));
+    p = ffma2(p, frac, f2(1.0f, 1.0f));
+    const uint32_t e0 = (uint32_t)rnd << 23, e1 = (uint32_t)(rnd >> 32) << 23;
+    return pk2((uint32_t)p + e0, (uint32_t)(p >> 32) + e1);
+}
+
+__device__ __forceinline__ void set_maxnreg_dec56() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+}
+__device__ __forceinline__ void set_maxnreg_inc224() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
+}
+
 template <int BK, int D>
 __global__ void __launch_bounds__(kThreads, 1)
     sparse_attn_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tq,
@@ -106,8 +176,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* p_full = bars + 6 + 2 * S;
     uint64_t* o_full = bars + 8 + 2 * S;
     uint64_t* o_empty = bars + 9 + 2 * S;
+    uint64_t* item_full = bars + 10 + 2 * S;
+    uint64_t* item_empty = item_full + kItemSlots;
     float* row_m = reinterpret_cast<float*>(smem + L::kRowOff);  // [2][128]
     float* row_l = row_m + 256;                                   // [2][128]
+    volatile int32_t* item_slot = reinterpret_cast<int32_t*>(smem + L::kItemOff);
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtrOff);
 
     const uint32_t warp = warp_id(), lane = lane_id();
@@ -124,6 +197,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_init(o_full, 1);
         mbar_init(o_empty, 8);
+        for (int i = 0; i < kItemSlots; ++i) {
+            mbar_init(item_full + i, 1);
+            mbar_init(item_empty + i, 9);  // MMA thread + 8 softmax warps
+        }
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<512>(tmem_ptr);
@@ -140,13 +217,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int32_t n_items = (*a.n_work) * a.batch;
     const Geo& g = a.g;
 
+    // consumer side of the item ring
+    auto next_item = [&](int32_t local, bool is_warp_consumer) -> int32_t {
+        const int s = local % kItemSlots;
+        mbar_wait(item_full + s, (local / kItemSlots) & 1);
+        const int32_t idx = item_slot[s];
+        if (is_warp_consumer) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(item_empty + s);
+        } else {
+            mbar_arrive(item_empty + s);
+        }
+        return idx;
+    };
+
+    if (warp < 4) {
+    set_maxnreg_dec56();  // producer / MMA / allocator warpgroup hands registers to softmax
     if (warp == 0) {
-        // ------------------------------------------------------------------ producer
+        // ------------------------------------------------------------ scheduler + producer
         const uint64_t pol_q = policy_evict_first();
         const uint64_t pol_kv = policy_evict_last();
         uint32_t ld = 0;  // K/V loads issued (ring position)
-        int32_t local = 0;
-        for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+        for (int32_t local = 0;; ++local) {
+            const int s = local % kItemSlots;
+            mbar_wait(item_empty + s, ((local / kItemSlots) & 1) ^ 1);
+            int32_t item = 0;
+            if (lane == 0) {
+                item = a.sched ? (int32_t)atomicAdd(a.sched, 1u)
+                               : (int32_t)blockIdx.x + local * (int32_t)gridDim.x;
+                if (item >= n_items) item = -1;
+                item_slot[s] = item;
+                mbar_arrive(item_full + s);
+            }
+            item = __shfl_sync(0xffffffffu, item, 0);
+            if (item < 0) break;
             const Item it = decode_item(a, item);
             const TileList tl = tile_list(a, it);
             const int qb = local & 1;
@@ -162,7 +266,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int32_t kA = a.plan.anchor_k[it.cell];
                 const int32_t per_frame = kA * g.W;
                 const int32_t n_anchor = g.F * per_frame;
-                const __nv_bfloat16* qb_ptr = a.q + (int64_t)it.b * a.q_sb + (int64_t)it.h * a.q_sh;
+                const __nv_bfloat16* qb_ptr =
+                    a.q + (int64_t)it.b * a.q_sb + (int64_t)it.h * a.q_sh;
                 constexpr int kChunks = D / 8;  // 16-byte chunks per row
                 for (int x = lane; x < 128 * kChunks; x += 32) {
                     const int row = x / kChunks, ch = x % kChunks;
@@ -184,15 +289,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0) mbar_arrive(q_full + qb);
             }
             // K/V tiles in MMA consumption order: K0, (K1, V0), (K2, V1), ..., V_{n-1}
-            for (int32_t step = 0; step <= tl.n; ++step) {
-                for (int kv = 0; kv < 2; ++kv) {
-                    int32_t j;
-                    if (kv == 0) { if (step >= tl.n) continue; j = step; }
-                    else { if (step == 0) continue; j = step - 1; }
-                    const uint32_t slot = ld % S, ph = (ld / S) & 1;
-                    ++ld;
-                    mbar_wait(kv_empty + slot, ph ^ 1);
-                    if (lane == 0) {
+            if (lane == 0) {
+                for (int32_t step = 0; step <= tl.n; ++step) {
+                    for (int kv = 0; kv < 2; ++kv) {
+                        int32_t j;
+                        if (kv == 0) {
+                            if (step >= tl.n) continue;
+                            j = step;
+                        } else {
+                            if (step == 0) continue;
+                            j = step - 1;
+                        }
+                        const uint32_t slot = ld % S, ph = (ld / S) & 1;
+                        ++ld;
+                        mbar_wait(kv_empty + slot, ph ^ 1);
                         uint8_t* dst = smem + L::kKVOff + slot * C::kKVBytes;
                         mbar_arrive_expect_tx(kv_full + slot, C::kKVBytes);
                         tma_tile<D>(dst, C::kKBox, kv == 0 ? &tk : &tv, kv_full + slot, it.h,
@@ -205,19 +315,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         // ------------------------------------------------------------------ MMA issuer
         if (lane == 0) {
-            uint32_t cons = 0;           // K/V ring position consumed
+            uint32_t cons = 0;            // K/V ring position consumed
             uint32_t pcount[2] = {0, 0};  // p_full completions waited, per group
-            int32_t local = 0;
-            const uint32_t s_tmem[2] = {tmem, tmem + BK};
-            const uint32_t o_tmem[2] = {tmem + 2 * BK, tmem + 2 * BK + D};
             const uint32_t q_base = smem_u32(smem + L::kQOff);
             const uint32_t kv_base = smem_u32(smem + L::kKVOff);
-            for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+            for (int32_t local = 0;; ++local) {
+                const int32_t item = next_item(local, false);
+                if (item < 0) break;
                 const Item it = decode_item(a, item);
                 const TileList tl = tile_list(a, it);
                 const int qb = local & 1;
                 mbar_wait(q_full + qb, (local >> 1) & 1);
                 const uint32_t q_smem = q_base + qb * C::kQBytes;
+                if (tl.n == 0) {  // corrupt plan (empty MASK row): release Q, no tiles
+                    mma_commit(q_empty + qb);
+                    mma_commit(o_full);
+                    continue;
+                }
                 auto do_pv = [&](int32_t t) {
                     const int grp = t & 1;
                     mbar_wait(p_full + grp, pcount[grp] & 1);
@@ -227,21 +341,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ++cons;
                     mbar_wait(kv_full + slot, ph);
                     tc_fence_after();
-                    issue_pv<BK, D>(o_tmem[grp], s_tmem[grp], kv_base + slot * C::kKVBytes, t >= 2);
+                    issue_pv<BK, D>(tmem + 2 * BK + grp * D, tmem + grp * BK,
+                                    kv_base + slot * C::kKVBytes, t >= 2);
                     mma_commit(kv_empty + slot);
                 };
-                if (tl.n == 0) {  // corrupt plan (empty MASK row): release Q, no output tiles
-                    mma_commit(q_empty + qb);
-                    mma_commit(o_full);
-                    continue;
-                }
                 for (int32_t j = 0; j < tl.n; ++j) {
                     const int grp = j & 1;
                     const uint32_t slot = cons % S, ph = (cons / S) & 1;
                     ++cons;
                     mbar_wait(kv_full + slot, ph);
                     tc_fence_after();
-                    issue_qk<BK, D>(s_tmem[grp], q_smem, kv_base + slot * C::kKVBytes);
+                    issue_qk<BK, D>(tmem + grp * BK, q_smem, kv_base + slot * C::kKVBytes);
                     mma_commit(s_full + grp);
                     mma_commit(kv_empty + slot);
                     if (j == tl.n - 1) mma_commit(q_empty + qb);
@@ -252,7 +362,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         __syncwarp();
-    } else if (warp >= 4) {
+    }
+    } else {
+        set_maxnreg_inc224();
         // ------------------------------------------------------------------ softmax groups
         const int grp = (warp - 4) >> 2;
         const int quarter = warp & 3;
@@ -261,36 +373,43 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t s_col = grp * BK;
         const uint32_t o_col = 2 * BK + grp * D;
         const float sl2 = a.scale_log2;
+        const uint64_t sl2x2 = f2(sl2, sl2);
+        const int32_t tail_valid = g.N - (g.NB - 1) * BK;  // keys in the last (ragged) block
         uint32_t scount = 0;
-        int32_t local = 0;
-        for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+        for (int32_t local = 0;; ++local) {
+            const int32_t item = next_item(local, true);
+            if (item < 0) break;
             const Item it = decode_item(a, item);
             const TileList tl = tile_list(a, it);
+            // only the last listed tile can be the ragged block N_B - 1
+            const bool last_ragged = tail_valid < BK && tl.n > 0 && tl.at(tl.n - 1) == g.NB - 1;
             float m_run = -INFINITY, l_run = 0.0f;
             int32_t mine = 0;
             for (int32_t j = grp; j < tl.n; j += 2, ++mine) {
                 mbar_wait(s_full + grp, scount & 1);
                 ++scount;
                 tc_fence_after();
-                float s[BK];
+                uint32_t r[BK / 32][32];
 #pragma unroll
-                for (int c = 0; c < BK; c += 32) {
-                    uint32_t r[32];
-                    tmem_ld32(lane_addr + s_col + c, r);
-                    tmem_ld_wait(r);
+                for (int c = 0; c < BK / 32; ++c) tmem_ld32(lane_addr + s_col + c * 32, r[c]);
 #pragma unroll
-                    for (int x = 0; x < 32; ++x) s[c + x] = __uint_as_float(r[x]);
+                for (int c = 0; c < BK / 32; ++c) tmem_ld_wait(r[c]);
+                if (last_ragged && j == tl.n - 1) {
+#pragma unroll
+                    for (int c = 0; c < BK / 32; ++c)
+#pragma unroll
+                        for (int x = 0; x < 32; ++x)
+                            if (c * 32 + x >= tail_valid) r[c][x] = 0xff800000u;  // -inf
                 }
-                const int32_t cblk = tl.at(j);
-                const int32_t valid = g.N - cblk * BK;  // keys of this tile that exist (ragged)
-                if (valid < BK) {
+                float mx = __uint_as_float(r[0][0]);
 #pragma unroll
-                    for (int x = 0; x < BK; ++x)
-                        if (x >= valid) s[x] = -INFINITY;
-                }
-                float mx = s[0];
+                for (int c = 0; c < BK / 32; ++c)
 #pragma unroll
-                for (int x = 1; x < BK; ++x) mx = fmaxf(mx, s[x]);
+                    for (int x = (c == 0 ? 1 : 0); x + 1 < 32; x += 2)
+                        mx = fmax3(mx, __uint_as_float(r[c][x]), __uint_as_float(r[c][x + 1]));
+#pragma unroll
+                for (int c = 1; c < BK / 32; ++c) mx = fmaxf(mx, __uint_as_float(r[c][31]));
+                mx = fmaxf(mx, __uint_as_float(r[0][31]));
                 const float m_new = fmaxf(m_run, mx * sl2);
                 float alpha = 1.0f;
                 bool rescale = false;
@@ -302,30 +421,41 @@ __global__ void __launch_bounds__(kThreads, 1)
                     m_run = m_new;
                     rescale = true;
                 }
-                float lsum = 0.0f;
+                const uint64_t negm = f2(-m_run, -m_run);
+                uint64_t acc = 0;  // packed (sum_even, sum_odd)
 #pragma unroll
-                for (int c = 0; c < BK; c += 32) {  // P overwrites the first BK/2 columns of S
+                for (int c = 0; c < BK / 32; ++c) {  // P overwrites the first BK/2 columns of S
                     uint32_t pk[16];
 #pragma unroll
                     for (int x = 0; x < 32; x += 2) {
-                        const float p0 = ex2_approx(fmaf(s[c + x], sl2, -m_run));
-                        const float p1 = ex2_approx(fmaf(s[c + x + 1], sl2, -m_run));
-                        lsum += p0 + p1;
-                        pk[x / 2] = pack_bf16(p0, p1);
+                        const uint64_t sx = pk2(r[c][x], r[c][x + 1]);
+                        const uint64_t t = ffma2(sx, sl2x2, negm);
+                        uint64_t p;
+                        if (((c * 16 + x / 2) % kEmuEvery) == kEmuEvery - 1) {
+                            p = exp2_poly2(t);
+                        } else {
+                            p = f2(ex2_approx(lo_f(t)), ex2_approx(hi_f(t)));
+                        }
+                        acc = fadd2(acc, p);
+                        pk[x / 2] = pack_bf16(lo_f(p), hi_f(p));
                     }
-                    tmem_st16(lane_addr + s_col + c / 2, pk);
+                    tmem_st16(lane_addr + s_col + c * 16, pk);
                 }
-                l_run += lsum;
+                l_run += lo_f(acc) + hi_f(acc);
                 if (rescale) {
+                    const uint64_t al2 = f2(alpha, alpha);
 #pragma unroll
                     for (int c = 0; c < D; c += 32) {
-                        uint32_t r[32];
-                        tmem_ld32(lane_addr + o_col + c, r);
-                        tmem_ld_wait(r);
+                        uint32_t o[32];
+                        tmem_ld32(lane_addr + o_col + c, o);
+                        tmem_ld_wait(o);
 #pragma unroll
-                        for (int x = 0; x < 32; ++x)
-                            r[x] = __float_as_uint(__uint_as_float(r[x]) * alpha);
-                        tmem_st32(lane_addr + o_col + c, r);
+                        for (int x = 0; x < 32; x += 2) {
+                            const uint64_t v = fmul2(pk2(o[x], o[x + 1]), al2);
+                            o[x] = (uint32_t)v;
+                            o[x + 1] = (uint32_t)(v >> 32);
+                        }
+                        tmem_st32(lane_addr + o_col + c, o);
                     }
                 }
                 tmem_st_wait();
@@ -353,7 +483,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             int32_t n_dst = 0, dst_stride_rows = 0;
             if (it.kind == 0) {
                 const int64_t t = (int64_t)it.idx * BK + row;
-                if (row < BK && t < g.N) { tok0 = t; n_dst = 1; }
+                if (row < BK && t < g.N) {
+                    tok0 = t;
+                    n_dst = 1;
+                }
             } else {
                 const int32_t kA = a.plan.anchor_k[it.cell];
                 const int32_t per_frame = kA * g.W;
@@ -370,6 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             __nv_bfloat16* obase = a.o + (int64_t)it.b * a.o_sb + (int64_t)it.h * a.o_sh;
+            const uint64_t f0x2 = f2(f0, f0), f1x2 = f2(f1, f1);
 #pragma unroll
             for (int c = 0; c < D / 2; c += 32) {
                 const int col = grp * (D / 2) + c;
@@ -381,13 +515,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t packed[16];
 #pragma unroll
                 for (int x = 0; x < 32; x += 2) {
-                    float v0 = __uint_as_float(r0[x]) * f0;
-                    float v1 = __uint_as_float(r0[x + 1]) * f0;
-                    if (has1) {
-                        v0 = fmaf(__uint_as_float(r1[x]), f1, v0);
-                        v1 = fmaf(__uint_as_float(r1[x + 1]), f1, v1);
-                    }
-                    packed[x / 2] = pack_bf16(v0, v1);
+                    uint64_t v = fmul2(pk2(r0[x], r0[x + 1]), f0x2);
+                    if (has1) v = ffma2(pk2(r1[x], r1[x + 1]), f1x2, v);
+                    packed[x / 2] = pack_bf16(lo_f(v), hi_f(v));
                 }
                 for (int32_t dI = 0; dI < n_dst; ++dI) {
                     uint4* dst = reinterpret_cast<uint4*>(
@@ -401,7 +531,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (grp == 0 && a.lse_out != nullptr) {
                 const float lse = (M + __log2f(Lsum)) * 0.69314718055994531f;
                 float* lb = a.lse_out + ((int64_t)it.b * a.n_heads + it.h) * (int64_t)g.N;
-                for (int32_t dI = 0; dI < n_dst; ++dI) lb[tok0 + (int64_t)dI * dst_stride_rows] = lse;
+                for (int32_t dI = 0; dI < n_dst; ++dI)
+                    lb[tok0 + (int64_t)dI * dst_stride_rows] = lse;
             }
             tc_fence_before();
             __syncwarp();
@@ -413,6 +544,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<512>(tmem);
+    }
+    // self-resetting dynamic scheduler: the last CTA to finish zeroes the counters
+    if (threadIdx.x == 0 && a.sched != nullptr) {
+        __threadfence();
+        if (atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
+            atomicExch(a.sched, 0u);
+            atomicExch(a.sched + 1, 0u);
+        }
     }
 }
 

@@ -94,6 +94,7 @@ struct AttnArgs {
     int64_t cell_base;
     const uint32_t* work_list;
     const int32_t* n_work;
+    uint32_t* sched;  // [2] dynamic-scheduler counters (zero on entry and on exit) or nullptr
 };
 cudaError_t launch_attn(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
                         const CUtensorMap& tk, const CUtensorMap& tv, int grid,

@@ -294,6 +294,72 @@ __global__ void __launch_bounds__(1024)
     if (threadIdx.x == 0) *n_work = total;
 }
 
+// Order 2 (head-major, longest-first within a head): one CTA per head sorts its own segment.
+//   key = (2047 - cost) << 11 | index     (cost, index <= 2047)
+__global__ void __launch_bounds__(256)
+    work_list_head_kernel(Geo g, PlanDev p, int64_t cell_base, int32_t n_heads,
+                          uint32_t* __restrict__ out, int32_t capacity, int32_t* __restrict__ n_work) {
+    __shared__ uint32_t keys[2048];
+    __shared__ int32_t s_off, s_cnt, s_total;
+    const int h = blockIdx.x;
+    auto items_of = [&](int hh) -> int32_t {
+        const int64_t cell = cell_base + hh;
+        return p.kind[cell] ? (int32_t)(((int64_t)g.F * p.anchor_k[cell] * g.W + kAnchorTile - 1) /
+                                        kAnchorTile)
+                            : g.NB;
+    };
+    if (threadIdx.x == 0) {
+        int32_t off = 0, tot = 0;
+        for (int hh = 0; hh < n_heads; ++hh) {
+            const int32_t c = items_of(hh);
+            if (hh < h) off += c;
+            tot += c;
+        }
+        s_off = off;
+        s_cnt = items_of(h);
+        s_total = tot;
+    }
+    __syncthreads();
+    const int32_t cnt = s_cnt, off = s_off, total = s_total;
+    if (total > capacity || cnt > 2048) {
+        if (h == 0 && threadIdx.x == 0) *n_work = -1;
+        return;
+    }
+    const int64_t cell = cell_base + h;
+    const bool rep = p.kind[cell] != 0;
+    int32_t pow2 = 1;
+    while (pow2 < cnt) pow2 <<= 1;
+    for (int32_t x = threadIdx.x; x < pow2; x += blockDim.x) {
+        uint32_t key = 0xffffffffu;
+        if (x < cnt) {
+            int32_t cost = g.NB;
+            if (!rep) {
+                const int32_t* rp = p.blk_row_ptr + cell * (g.NB + 1);
+                cost = rp[x + 1] - rp[x];
+            }
+            key = ((uint32_t)(2047 - cost) << 11) | (uint32_t)x;
+        }
+        keys[x] = key;
+    }
+    __syncthreads();
+    for (int32_t k = 2; k <= pow2; k <<= 1) {
+        for (int32_t j = k >> 1; j > 0; j >>= 1) {
+            for (int32_t x = threadIdx.x; x < pow2; x += blockDim.x) {
+                const int32_t y = x ^ j;
+                if (y > x) {
+                    const uint32_t a = keys[x], b = keys[y];
+                    const bool up = (x & k) == 0;
+                    if ((a > b) == up) { keys[x] = b; keys[y] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int32_t x = threadIdx.x; x < cnt; x += blockDim.x)
+        out[off + x] = ((rep ? 1u : 0u) << 31) | ((uint32_t)h << 20) | (keys[x] & 0x7FFu);
+    if (h == 0 && threadIdx.x == 0) *n_work = total;
+}
+
 // --------------------------------------------------------------------------------- validate
 __global__ void plan_validate_kernel(Geo g, int64_t n_cells, PlanDev p, uint32_t* flag) {
     const int64_t total = n_cells * g.NB;
@@ -371,6 +437,11 @@ cudaError_t launch_plan_fill(const Geo& g, int64_t n_cells, const PlanDev& p, cu
 cudaError_t launch_work_list(const Geo& g, const PlanDev& p, int64_t cell_base, int32_t n_heads,
                              int32_t order, uint32_t* out, int32_t capacity, int32_t* n_work,
                              cudaStream_t s) {
+    if (order == 2) {
+        work_list_head_kernel<<<n_heads, 256, 0, s>>>(g, p, cell_base, n_heads, out, capacity,
+                                                     n_work);
+        return cudaGetLastError();
+    }
     const size_t smem = sizeof(uint32_t) * kMaxWorkItems;
     cudaError_t e =
         cudaFuncSetAttribute(work_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

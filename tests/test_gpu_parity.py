@@ -123,14 +123,16 @@ def test_work_list_bit_exact(csa):
         ref = oracle.work_list(lay.N, lay.B, lay.F, lay.W, kinds[base:base + nh], ak[base:base + nh],
                                nnz[base:base + nh])
         assert np.array_equal(got, ref)
-        nat = csa.build_work_list(plan, base, nh, order=1)
-        gotn = nat.items.cpu().numpy().view(np.uint32)[: int(nat.n_work.item())]
-        key = lambda c: ((int(c) >> 20) & 0x7FF, int(c) & 0xFFFFF)
-        assert list(gotn) == sorted(ref.tolist(), key=key)
+        for order in (1, 2):
+            wl = csa.build_work_list(plan, base, nh, order=order)
+            got = wl.items.cpu().numpy().view(np.uint32)[: int(wl.n_work.item())]
+            ref = oracle.work_list(lay.N, lay.B, lay.F, lay.W, kinds[base:base + nh],
+                                   ak[base:base + nh], nnz[base:base + nh], order=order)
+            assert np.array_equal(got, ref), order
 
 
 # ---------------------------------------------------------------- a7/a8 attention
-def run_attention(csa, lay, q, k, v, masks=None, rep=None, anchor_k=2, order=0, lse=False):
+def run_attention(csa, lay, q, k, v, masks=None, rep=None, anchor_k=2, order=2, lse=False):
     """masks: [H, NB, NB] uint8 for MASK heads; rep: list of REPETITIVE head indices."""
     heads = q.shape[2]
     nb = lay.NB
@@ -204,9 +206,14 @@ def test_attention_batch2_shares_plan_and_is_deterministic(csa):
     rng = np.random.default_rng(1)
     masks = (rng.random((3, lay.NB, lay.NB)) < 0.5).astype(np.uint8)
     masks[:, np.arange(lay.NB), np.arange(lay.NB)] = 1
-    out, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[2], anchor_k=2)
-    out2, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[2], anchor_k=2, order=1)
-    assert torch.equal(out, out2)  # LPT vs natural order: per-item arithmetic is schedule-free
+    out, _, plan = run_attention(csa, lay, q, k, v, masks=masks, rep=[2], anchor_k=2)
+    for order in (0, 1):
+        out2, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[2], anchor_k=2, order=order)
+        assert torch.equal(out, out2)  # item order never changes per-item arithmetic
+    static = csa.sparse_attn_fwd(q, k, v, plan, csa.build_work_list(plan, 0, 3), dynamic=False)
+    assert torch.equal(out, static)  # dynamic vs static scheduling
+    again, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[2], anchor_k=2)
+    assert torch.equal(out, again)  # run-to-run determinism (scheduler counters self-reset)
     for b in range(2):
         for h in range(3):
             ref, _ = oracle_head(lay, q, k, v, b, h, mask=masks[h], rep_k=2 if h == 2 else None)
