@@ -275,7 +275,7 @@ def main():
     sim = torch.tensor([1.0 if h in rep else 0.0 for h in my_heads], dtype=torch.float64, device=dev)
     t0 = time.perf_counter()
     plan = csa.compile_plan(lay, counts, 32, similarity=sim, gamma=0.87, anchor_k=5)
-    work = csa.build_work_list(plan, 0, hp, order=0)
+    work = csa.build_work_list(plan, 0, hp)  # head-major, longest row first (order 2)
     torch.cuda.synchronize()
     flop_rank, _ = flops_of(lay, masks, rep, my_heads, d, B)
     flop_all, area_all = flops_of(lay, masks, rep, range(H), d, B)

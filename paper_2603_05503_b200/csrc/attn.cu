@@ -32,7 +32,7 @@ namespace {
 constexpr int kThreads = 384;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kItemSlots = 4;
-constexpr int kEmuEvery = 8;  // every kEmuEvery-th element pair uses the polynomial exp2
+constexpr int kEmuEvery = 4;  // every kEmuEvery-th element pair uses the polynomial exp2
 
 template <int BK, int D>
 struct AttnSmem {
@@ -401,15 +401,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int x = 0; x < 32; ++x)
                             if (c * 32 + x >= tail_valid) r[c][x] = 0xff800000u;  // -inf
                 }
-                float mx = __uint_as_float(r[0][0]);
+                // row max: 8 independent FMNMX3 chains (short dependency depth), then combine
+                constexpr int kPer = BK / 8;  // elements per chain (even)
+                float mc[8];
 #pragma unroll
-                for (int c = 0; c < BK / 32; ++c)
+                for (int q8 = 0; q8 < 8; ++q8) {
+#define SV(e) __uint_as_float(r[(e) >> 5][(e) & 31])
+                    mc[q8] = SV(q8);
 #pragma unroll
-                    for (int x = (c == 0 ? 1 : 0); x + 1 < 32; x += 2)
-                        mx = fmax3(mx, __uint_as_float(r[c][x]), __uint_as_float(r[c][x + 1]));
-#pragma unroll
-                for (int c = 1; c < BK / 32; ++c) mx = fmaxf(mx, __uint_as_float(r[c][31]));
-                mx = fmaxf(mx, __uint_as_float(r[0][31]));
+                    for (int t = 1; t + 1 < kPer; t += 2)
+                        mc[q8] = fmax3(mc[q8], SV(q8 + 8 * t), SV(q8 + 8 * (t + 1)));
+                    mc[q8] = fmaxf(mc[q8], SV(q8 + 8 * (kPer - 1)));
+#undef SV
+                }
+                const float mx = fmaxf(fmax3(mc[0], mc[1], mc[2]),
+                                       fmaxf(fmax3(mc[3], mc[4], mc[5]), fmaxf(mc[6], mc[7])));
                 const float m_new = fmaxf(m_run, mx * sl2);
                 float alpha = 1.0f;
                 bool rescale = false;
@@ -422,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     rescale = true;
                 }
                 const uint64_t negm = f2(-m_run, -m_run);
-                uint64_t acc = 0;  // packed (sum_even, sum_odd)
+                uint64_t acc[4] = {0, 0, 0, 0};  // 4 packed partial sums (8 independent chains)
 #pragma unroll
                 for (int c = 0; c < BK / 32; ++c) {  // P overwrites the first BK/2 columns of S
                     uint32_t pk[16];
@@ -436,12 +442,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         } else {
                             p = f2(ex2_approx(lo_f(t)), ex2_approx(hi_f(t)));
                         }
-                        acc = fadd2(acc, p);
+                        acc[(x / 2) & 3] = fadd2(acc[(x / 2) & 3], p);
                         pk[x / 2] = pack_bf16(lo_f(p), hi_f(p));
                     }
                     tmem_st16(lane_addr + s_col + c * 16, pk);
                 }
-                l_run += lo_f(acc) + hi_f(acc);
+                const uint64_t acc2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+                l_run += lo_f(acc2) + hi_f(acc2);
                 if (rescale) {
                     const uint64_t al2 = f2(alpha, alpha);
 #pragma unroll
