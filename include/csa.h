@@ -199,6 +199,10 @@ CSA_API csa_status_t csa_validate_plan(const csa_plan_t* plan, csa_layout_t L, i
 /* Thread-local detail of the last error returned on this thread ("" if none). */
 CSA_API const char* csa_last_error(void);
 
+/* Debug only: device buffer of 4*1024*8 uint64 receiving clock64() stamps of CTA 0's attention
+ * pipeline events (softmax groups, S and P.V issue); NULL switches tracing off. */
+CSA_API csa_status_t csa_debug_trace(void* buf);
+
 /* Library version string. */
 CSA_API const char* csa_version(void);
 

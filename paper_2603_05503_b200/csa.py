@@ -52,7 +52,7 @@ class _PlanT(ctypes.Structure):
 
 EXPORTS = ["csa_calib_accumulate", "csa_compile_plan", "csa_build_work_list",
            "csa_sparse_attn_fwd", "csa_workspace_size", "csa_validate_plan", "csa_last_error",
-           "csa_version"]
+           "csa_version", "csa_debug_trace"]
 
 _lib = None
 
@@ -84,6 +84,8 @@ def lib() -> ctypes.CDLL:
     L.csa_sparse_attn_fwd.argtypes = [_LayoutT, i32, i32, i32, ctypes.c_float, _TensorT, _TensorT,
                                       _TensorT, _TensorT, vp, ctypes.POINTER(_PlanT), i64, vp, vp,
                                       i32, vp, ctypes.c_size_t, vp]
+    L.csa_debug_trace.restype = st
+    L.csa_debug_trace.argtypes = [vp]
     L.csa_validate_plan.restype = st
     L.csa_validate_plan.argtypes = [ctypes.POINTER(_PlanT), _LayoutT, i64, vp]
     _lib = L

@@ -133,6 +133,12 @@ const char* csa_last_error(void) { return g_err.c_str(); }
 
 const char* csa_version(void) { return "csa-b200 0.1 (sm_100a)"; }
 
+csa_status_t csa_debug_trace(void* buf) {
+    cudaError_t e = csa::set_attn_trace(buf);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyToSymbol");
+    return ok();
+}
+
 size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_t head_dim) {
     (void)L;
     (void)n_heads;

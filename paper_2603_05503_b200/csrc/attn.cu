@@ -150,6 +150,14 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
     return pk2((uint32_t)p + e0, (uint32_t)(p >> 32) + e1);
 }
 
+// Debug timeline (csa_debug_trace): clock64 stamps of CTA 0's pipeline events; nullptr = off.
+__device__ unsigned long long* g_trace;
+#define CSA_TRACE(slot, k, e)                                                             \
+    do {                                                                                  \
+        if (g_trace != nullptr && blockIdx.x == 0 && (k) < 1024)                          \
+            g_trace[((slot) * 1024 + (k)) * 8 + (e)] = clock64();                         \
+    } while (0)
+
 __device__ __forceinline__ void set_maxnreg_dec56() {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
 }
@@ -317,6 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             uint32_t cons = 0;            // K/V ring position consumed
             uint32_t pcount[2] = {0, 0};  // p_full completions waited, per group
+            int32_t ntr_s = 0, ntr_pv = 0;  // trace counters (debug timeline only)
             const uint32_t q_base = smem_u32(smem + L::kQOff);
             const uint32_t kv_base = smem_u32(smem + L::kKVOff);
             for (int32_t local = 0;; ++local) {
@@ -334,8 +343,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 auto do_pv = [&](int32_t t) {
                     const int grp = t & 1;
+                    CSA_TRACE(3, ntr_pv, 0);
                     mbar_wait(p_full + grp, pcount[grp] & 1);
                     ++pcount[grp];
+                    CSA_TRACE(3, ntr_pv, 1);
+                    ++ntr_pv;
                     if (t == 0) mbar_wait(o_empty, (local & 1) ^ 1);  // epilogue of last item
                     const uint32_t slot = cons % S, ph = (cons / S) & 1;
                     ++cons;
@@ -351,7 +363,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ++cons;
                     mbar_wait(kv_full + slot, ph);
                     tc_fence_after();
+                    CSA_TRACE(2, ntr_s, 0);
                     issue_qk<BK, D>(tmem + grp * BK, q_smem, kv_base + slot * C::kKVBytes);
+                    ++ntr_s;
                     mma_commit(s_full + grp);
                     mma_commit(kv_empty + slot);
                     if (j == tl.n - 1) mma_commit(q_empty + qb);
@@ -388,12 +402,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int32_t j = grp; j < tl.n; j += 2, ++mine) {
                 mbar_wait(s_full + grp, scount & 1);
                 ++scount;
+                const bool tr = (quarter == 0 && lane == 0);
+                if (tr) CSA_TRACE(grp, scount - 1, 0);
                 tc_fence_after();
                 uint32_t r[BK / 32][32];
 #pragma unroll
                 for (int c = 0; c < BK / 32; ++c) tmem_ld32(lane_addr + s_col + c * 32, r[c]);
 #pragma unroll
                 for (int c = 0; c < BK / 32; ++c) tmem_ld_wait(r[c]);
+                if (tr) CSA_TRACE(grp, scount - 1, 1);
                 if (last_ragged && j == tl.n - 1) {
 #pragma unroll
                     for (int c = 0; c < BK / 32; ++c)
@@ -417,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float mx = fmaxf(fmax3(mc[0], mc[1], mc[2]),
                                        fmaxf(fmax3(mc[3], mc[4], mc[5]), fmaxf(mc[6], mc[7])));
                 const float m_new = fmaxf(m_run, mx * sl2);
+                if (tr) CSA_TRACE(grp, scount - 1, 2);
                 float alpha = 1.0f;
                 bool rescale = false;
                 if (mine == 0) {
@@ -449,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 const uint64_t acc2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
                 l_run += lo_f(acc2) + hi_f(acc2);
+                if (tr) CSA_TRACE(grp, scount - 1, 3);
                 if (rescale) {
                     const uint64_t al2 = f2(alpha, alpha);
 #pragma unroll
@@ -468,6 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
+                if (tr) CSA_TRACE(grp, scount - 1, 4);
                 if (lane == 0) mbar_arrive(p_full + grp);
             }
             // -------------------------------------------------------------- epilogue
@@ -574,6 +594,11 @@ cudaError_t launch_t(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap
 }
 
 }  // namespace
+
+cudaError_t set_attn_trace(void* buf) {
+    unsigned long long* p = static_cast<unsigned long long*>(buf);
+    return cudaMemcpyToSymbol(g_trace, &p, sizeof(p));
+}
 
 cudaError_t launch_attn(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
                         const CUtensorMap& tk, const CUtensorMap& tv, int grid, cudaStream_t s) {
