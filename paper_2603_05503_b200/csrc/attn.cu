@@ -9,18 +9,19 @@
 //     computed, densely against all N keys; row (f,i,j) receives row (f, a(i), j) (Q9, Q10).
 //
 // Design: persistent, one CTA per SM, 12 warps.
-//   warp 0      scheduler + producer: claims items (dynamic, head-major work list) and publishes
-//               them through a 4-deep shared-memory ring; loads the Q tile (TMA, or an in-warp
-//               gather of anchor rows), then the kept K/V tiles of the item's block list through
-//               a FIFO ring of smem slots in MMA consumption order K0, K1, V0, K2, V1, ...
-//   warp 1      MMA issuer (one thread): S_j = Q K_j^T into S[j&1] (TMEM), then
-//               O[(j-1)&1] += P_{j-1} V_{j-1} with P read from TMEM (TS-MMA).
+//   warp 0      scheduler + producer: claims items (dynamic, head-major work list) through a
+//               4-deep shared-memory item ring; loads the Q tile (TMA, or an in-warp gather of
+//               anchor rows), then the kept K/V tiles of the item's block list through a FIFO ring
+//               of smem slots in MMA consumption order K0 K1 K2 V0 K3 V1 ... V_{n-1}.
+//   warp 1      MMA issuer (one thread): S_j = Q K_j^T into TMEM S[j&1]; as soon as group j&1 has
+//               read S_j it issues S_{j+2}; then O[j&1] += P_j V_j with P from shared memory.
 //   warp 2      TMEM allocator (512 columns: S0 S1 O0 O1).
 //   warps 4-7   softmax group 0: even tiles of the item's list   } each keeps its own (m, l, O);
 //   warps 8-11  softmax group 1: odd tiles                          } merged in the epilogue.
-// One thread owns one query row (= one TMEM lane).  Lazy rescale: O is rescaled only when the
-// running max grows by more than 2^8.  Packed f32x2 FMA/ADD; a fixed fraction of the exp2 are
-// evaluated by a degree-3 polynomial on the FMA pipe to offload the MUFU unit.
+// One thread owns one query row (= one TMEM lane).  exp2 is taken against the running max
+// speculatively; a tile whose max exceeds it by more than 2^8 is redone with the new max and O is
+// rescaled (lazy rescale).  Packed f32x2 FMA/ADD; a fixed fraction of the exp2 are evaluated by a
+// degree-3 polynomial on the FMA pipe to offload the MUFU unit.
 #include <cstdint>
 
 #include "csa_internal.cuh"
@@ -32,23 +33,27 @@ namespace {
 constexpr int kThreads = 384;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kItemSlots = 4;
-constexpr int kEmuEvery = 4;  // every kEmuEvery-th element pair uses the polynomial exp2
+constexpr int kEmuMask = 3;                // element pairs p with (p & 7) >= 5 -> polynomial exp2
 
 template <int BK, int D>
 struct AttnSmem {
     using C = TileCfg<BK, D>;
-    static constexpr int kSlots = (BK == 128 && D == 128) ? 5 : 8;
+    static constexpr int kPBytes = C::kQBox * (BK / 64);  // 128 rows x BK keys bf16
     static constexpr int kQOff = 0;
-    static constexpr int kKVOff = 2 * C::kQBytes;
+    static constexpr int kPOff = C::kQBytes;
+    static constexpr int kKVOff = kPOff + 2 * kPBytes;
+    static constexpr int kBudget = 224 * 1024 - kKVOff;
+    static constexpr int kSlots = kBudget / C::kKVBytes > 8 ? 8 : kBudget / C::kKVBytes;
     static constexpr int kBarOff = kKVOff + kSlots * C::kKVBytes;
-    // q_full[2] q_empty[2] kv_full[S] kv_empty[S] s_full[2] p_full[2] o_full o_empty
-    // item_full[4] item_empty[4]
-    static constexpr int kNumBars = 4 + 2 * kSlots + 4 + 2 + 2 * kItemSlots;
+    // q_full q_empty kv_full[S] kv_empty[S] s_full[2] s_free[2] p_full[2] p_empty[2] o_full
+    // o_empty item_full[4] item_empty[4]
+    static constexpr int kNumBars = 2 + 2 * kSlots + 8 + 2 + 2 * kItemSlots;
     static constexpr int kRowOff = kBarOff + kNumBars * 8;           // m[2][128], l[2][128]
     static constexpr int kItemOff = kRowOff + 4 * 128 * 4;           // int32 [kItemSlots]
     static constexpr int kTmemPtrOff = kItemOff + kItemSlots * 4;
     static constexpr int kBytes = kTmemPtrOff + 16;
     static constexpr int kAlloc = kBytes;  // base is 1 KiB aligned (__align__ on the extern)
+    static_assert(kSlots >= 3, "K/V ring too shallow");
     static_assert(kAlloc <= 232448, "smem");
 };
 
@@ -134,7 +139,7 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
     return d;
 }
 
-// 2^x for a pair of x <= 8 on the FMA pipe: x = n + f, 2^f by a degree-3 minimax polynomial
+// 2^x for a pair of x <= 127 on the FMA pipe: x = n + f, 2^f by a degree-3 minimax polynomial
 // (max rel. error 8.6e-5, far below the bf16 rounding of P), exponent added as integer.
 __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
     const float x0 = fmaxf(lo_f(x), -127.0f), x1 = fmaxf(hi_f(x), -127.0f);
@@ -148,6 +153,13 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
     p = ffma2(p, frac, f2(1.0f, 1.0f));
     const uint32_t e0 = (uint32_t)rnd << 23, e1 = (uint32_t)(rnd >> 32) << 23;
     return pk2((uint32_t)p + e0, (uint32_t)(p >> 32) + e1);
+}
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                             uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+                 "r"(d)
+                 : "memory");
 }
 
 // Debug timeline (csa_debug_trace): clock64 stamps of CTA 0's pipeline events; nullptr = off.
@@ -165,6 +177,59 @@ __device__ __forceinline__ void set_maxnreg_inc224() {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
 }
 
+// exp2(s * sl2 - m) for one 128-element row tile held in registers; P (bf16) written to the
+// K-major SW128 smem tile; returns the row sum.  `row` selects the swizzle phase.
+template <int BK>
+__device__ __forceinline__ float exp_row_to_smem(const uint32_t (&r)[BK / 32][32], float sl2,
+                                                 float m, uint32_t p_row_addr, uint32_t row) {
+    const uint64_t sl2x2 = f2(sl2, sl2);
+    const uint64_t negm = f2(-m, -m);
+    uint64_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < BK / 32; ++c) {
+#pragma unroll
+        for (int h8 = 0; h8 < 4; ++h8) {  // 8 keys = one 16-byte chunk of P
+            uint32_t w[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int x = h8 * 8 + q * 2;
+                const uint64_t t = ffma2(pk2(r[c][x], r[c][x + 1]), sl2x2, negm);
+                uint64_t p;
+                if (((x / 2) & 7) >= 8 - kEmuMask) {
+                    p = exp2_poly2(t);
+                } else {
+                    p = f2(ex2_approx(lo_f(t)), ex2_approx(hi_f(t)));
+                }
+                acc[q] = fadd2(acc[q], p);
+                w[q] = pack_bf16(lo_f(p), hi_f(p));
+            }
+            const uint32_t chunk = (uint32_t)(c * 4 + h8);  // 16-byte chunk index along keys
+            const uint32_t addr = p_row_addr + (chunk >> 3) * (128u * 128u) +
+                                  (((chunk & 7u) ^ (row & 7u)) << 4);
+            st_shared_v4(addr, w[0], w[1], w[2], w[3]);
+        }
+    }
+    const uint64_t s2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+    return lo_f(s2) + hi_f(s2);
+}
+
+template <int BK>
+__device__ __forceinline__ float row_max(const uint32_t (&r)[BK / 32][32]) {
+    constexpr int kPer = BK / 8;  // elements per chain (even)
+    float mc[8];
+#pragma unroll
+    for (int q8 = 0; q8 < 8; ++q8) {
+#define SV(e) __uint_as_float(r[(e) >> 5][(e) & 31])
+        mc[q8] = SV(q8);
+#pragma unroll
+        for (int t = 1; t + 1 < kPer; t += 2)
+            mc[q8] = fmax3(mc[q8], SV(q8 + 8 * t), SV(q8 + 8 * (t + 1)));
+        mc[q8] = fmaxf(mc[q8], SV(q8 + 8 * (kPer - 1)));
+#undef SV
+    }
+    return fmaxf(fmax3(mc[0], mc[1], mc[2]), fmaxf(fmax3(mc[3], mc[4], mc[5]), fmaxf(mc[6], mc[7])));
+}
+
 template <int BK, int D>
 __global__ void __launch_bounds__(kThreads, 1)
     sparse_attn_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tq,
@@ -177,14 +242,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if ((smem_u32(smem) & 1023u) != 0u) __trap();  // SWIZZLE_128B atoms need 1 KiB alignment
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
     uint64_t* q_full = bars + 0;
-    uint64_t* q_empty = bars + 2;
-    uint64_t* kv_full = bars + 4;
-    uint64_t* kv_empty = bars + 4 + S;
-    uint64_t* s_full = bars + 4 + 2 * S;
-    uint64_t* p_full = bars + 6 + 2 * S;
-    uint64_t* o_full = bars + 8 + 2 * S;
-    uint64_t* o_empty = bars + 9 + 2 * S;
-    uint64_t* item_full = bars + 10 + 2 * S;
+    uint64_t* q_empty = bars + 1;
+    uint64_t* kv_full = bars + 2;
+    uint64_t* kv_empty = bars + 2 + S;
+    uint64_t* s_full = bars + 2 + 2 * S;
+    uint64_t* s_free = s_full + 2;
+    uint64_t* p_full = s_full + 4;
+    uint64_t* p_empty = s_full + 6;
+    uint64_t* o_full = s_full + 8;
+    uint64_t* o_empty = s_full + 9;
+    uint64_t* item_full = s_full + 10;
     uint64_t* item_empty = item_full + kItemSlots;
     float* row_m = reinterpret_cast<float*>(smem + L::kRowOff);  // [2][128]
     float* row_l = row_m + 256;                                   // [2][128]
@@ -193,11 +260,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const uint32_t warp = warp_id(), lane = lane_id();
     if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(q_full + i, 1);
-            mbar_init(q_empty + i, 1);
             mbar_init(s_full + i, 1);
+            mbar_init(s_free + i, 4);
             mbar_init(p_full + i, 4);
+            mbar_init(p_empty + i, 1);
         }
         for (int i = 0; i < S; ++i) {
             mbar_init(kv_full + i, 1);
@@ -240,143 +309,143 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
 
     if (warp < 4) {
-    set_maxnreg_dec56();  // producer / MMA / allocator warpgroup hands registers to softmax
-    if (warp == 0) {
-        // ------------------------------------------------------------ scheduler + producer
-        const uint64_t pol_q = policy_evict_first();
-        const uint64_t pol_kv = policy_evict_last();
-        uint32_t ld = 0;  // K/V loads issued (ring position)
-        for (int32_t local = 0;; ++local) {
-            const int s = local % kItemSlots;
-            mbar_wait(item_empty + s, ((local / kItemSlots) & 1) ^ 1);
-            int32_t item = 0;
-            if (lane == 0) {
-                item = a.sched ? (int32_t)atomicAdd(a.sched, 1u)
-                               : (int32_t)blockIdx.x + local * (int32_t)gridDim.x;
-                if (item >= n_items) item = -1;
-                item_slot[s] = item;
-                mbar_arrive(item_full + s);
-            }
-            item = __shfl_sync(0xffffffffu, item, 0);
-            if (item < 0) break;
-            const Item it = decode_item(a, item);
-            const TileList tl = tile_list(a, it);
-            const int qb = local & 1;
-            uint8_t* qdst = smem + L::kQOff + qb * C::kQBytes;
-            mbar_wait(q_empty + qb, ((local >> 1) & 1) ^ 1);
-            if (it.kind == 0) {
+        set_maxnreg_dec56();  // producer / MMA / allocator warpgroup hands registers to softmax
+        if (warp == 0) {
+            // -------------------------------------------------------- scheduler + producer
+            const uint64_t pol_q = policy_evict_first();
+            const uint64_t pol_kv = policy_evict_last();
+            uint32_t ld = 0;  // K/V loads issued (ring position)
+            uint8_t* qdst = smem + L::kQOff;
+            for (int32_t local = 0;; ++local) {
+                const int s = local % kItemSlots;
+                mbar_wait(item_empty + s, ((local / kItemSlots) & 1) ^ 1);
+                int32_t item = 0;
                 if (lane == 0) {
-                    mbar_arrive_expect_tx(q_full + qb, C::kBoxes * BK * 128);
-                    tma_tile<D>(qdst, C::kQBox, &tq, q_full + qb, it.h, it.idx * BK, it.b, pol_q);
+                    item = a.sched ? (int32_t)atomicAdd(a.sched, 1u)
+                                   : (int32_t)blockIdx.x + local * (int32_t)gridDim.x;
+                    if (item >= n_items) item = -1;
+                    item_slot[s] = item;
+                    mbar_arrive(item_full + s);
                 }
-            } else {
-                // gather the anchor query rows of tile u: g = u*128 + row -> (f, m, j)
-                const int32_t kA = a.plan.anchor_k[it.cell];
-                const int32_t per_frame = kA * g.W;
-                const int32_t n_anchor = g.F * per_frame;
-                const __nv_bfloat16* qb_ptr =
-                    a.q + (int64_t)it.b * a.q_sb + (int64_t)it.h * a.q_sh;
-                constexpr int kChunks = D / 8;  // 16-byte chunks per row
-                for (int x = lane; x < 128 * kChunks; x += 32) {
-                    const int row = x / kChunks, ch = x % kChunks;
-                    const int32_t gi = it.idx * 128 + row;
-                    uint4 val = make_uint4(0u, 0u, 0u, 0u);
-                    if (gi < n_anchor) {
-                        const int32_t f = gi / per_frame;
-                        const int32_t m = (gi / g.W) % kA;
-                        const int32_t j = gi % g.W;
-                        const int64_t tok = (int64_t)f * g.H * g.W +
-                                            (int64_t)anchor_row(g.H, kA, m) * g.W + j;
-                        val = *reinterpret_cast<const uint4*>(qb_ptr + tok * a.q_sn + ch * 8);
+                item = __shfl_sync(0xffffffffu, item, 0);
+                if (item < 0) break;
+                const Item it = decode_item(a, item);
+                const TileList tl = tile_list(a, it);
+                mbar_wait(q_empty, (local & 1) ^ 1);
+                if (it.kind == 0) {
+                    if (lane == 0) {
+                        mbar_arrive_expect_tx(q_full, C::kBoxes * BK * 128);
+                        tma_tile<D>(qdst, C::kQBox, &tq, q_full, it.h, it.idx * BK, it.b, pol_q);
                     }
-                    *reinterpret_cast<uint4*>(qdst + (ch >> 3) * C::kQBox +
-                                              sw128_offset(row, ch & 7)) = val;
-                }
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(q_full + qb);
-            }
-            // K/V tiles in MMA consumption order: K0, (K1, V0), (K2, V1), ..., V_{n-1}
-            if (lane == 0) {
-                for (int32_t step = 0; step <= tl.n; ++step) {
-                    for (int kv = 0; kv < 2; ++kv) {
-                        int32_t j;
-                        if (kv == 0) {
-                            if (step >= tl.n) continue;
-                            j = step;
-                        } else {
-                            if (step == 0) continue;
-                            j = step - 1;
+                } else {
+                    // gather the anchor query rows of tile u: g = u*128 + row -> (f, m, j)
+                    const int32_t kA = a.plan.anchor_k[it.cell];
+                    const int32_t per_frame = kA * g.W;
+                    const int32_t n_anchor = g.F * per_frame;
+                    const __nv_bfloat16* qb_ptr =
+                        a.q + (int64_t)it.b * a.q_sb + (int64_t)it.h * a.q_sh;
+                    constexpr int kChunks = D / 8;  // 16-byte chunks per row
+                    for (int x = lane; x < 128 * kChunks; x += 32) {
+                        const int row = x / kChunks, ch = x % kChunks;
+                        const int32_t gi = it.idx * 128 + row;
+                        uint4 val = make_uint4(0u, 0u, 0u, 0u);
+                        if (gi < n_anchor) {
+                            const int32_t f = gi / per_frame;
+                            const int32_t m = (gi / g.W) % kA;
+                            const int32_t j = gi % g.W;
+                            const int64_t tok = (int64_t)f * g.H * g.W +
+                                                (int64_t)anchor_row(g.H, kA, m) * g.W + j;
+                            val = *reinterpret_cast<const uint4*>(qb_ptr + tok * a.q_sn + ch * 8);
                         }
+                        *reinterpret_cast<uint4*>(qdst + (ch >> 3) * C::kQBox +
+                                                  sw128_offset(row, ch & 7)) = val;
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(q_full);
+                }
+                // K/V tiles in MMA consumption order: K0 K1, then per j: K_{j+2} (if any), V_j
+                if (lane == 0) {
+                    auto load = [&](const CUtensorMap* map, int32_t j) {
                         const uint32_t slot = ld % S, ph = (ld / S) & 1;
                         ++ld;
                         mbar_wait(kv_empty + slot, ph ^ 1);
-                        uint8_t* dst = smem + L::kKVOff + slot * C::kKVBytes;
                         mbar_arrive_expect_tx(kv_full + slot, C::kKVBytes);
-                        tma_tile<D>(dst, C::kKBox, kv == 0 ? &tk : &tv, kv_full + slot, it.h,
-                                    tl.at(j) * BK, it.b, pol_kv);
+                        tma_tile<D>(smem + L::kKVOff + slot * C::kKVBytes, C::kKBox, map,
+                                    kv_full + slot, it.h, tl.at(j) * BK, it.b, pol_kv);
+                    };
+                    for (int32_t j = 0; j < tl.n && j < 2; ++j) load(&tk, j);
+                    for (int32_t j = 0; j < tl.n; ++j) {
+                        if (j + 2 < tl.n) load(&tk, j + 2);
+                        load(&tv, j);
                     }
+                }
+                __syncwarp();
+            }
+        } else if (warp == 1) {
+            // ---------------------------------------------------------------- MMA issuer
+            if (lane == 0) {
+                uint32_t cons = 0;                // K/V ring position consumed
+                uint32_t s_issued[2] = {0, 0};    // S MMAs issued per buffer
+                uint32_t pv_issued[2] = {0, 0};   // P.V MMAs issued per buffer
+                int32_t ntr_s = 0, ntr_pv = 0;    // trace counters (debug timeline only)
+                const uint32_t q_smem = smem_u32(smem + L::kQOff);
+                const uint32_t p_base = smem_u32(smem + L::kPOff);
+                const uint32_t kv_base = smem_u32(smem + L::kKVOff);
+                for (int32_t local = 0;; ++local) {
+                    const int32_t item = next_item(local, false);
+                    if (item < 0) break;
+                    const Item it = decode_item(a, item);
+                    const TileList tl = tile_list(a, it);
+                    const int32_t n = tl.n;
+                    mbar_wait(q_full, local & 1);
+                    if (n == 0) {  // corrupt plan (empty MASK row): release Q, no tiles
+                        mma_commit(q_empty);
+                        mma_commit(o_full);
+                        continue;
+                    }
+                    auto issue_s = [&](int32_t j) {
+                        const int grp = j & 1;
+                        if (s_issued[grp] > 0) mbar_wait(s_free + grp, (s_issued[grp] - 1) & 1);
+                        const uint32_t slot = cons % S, ph = (cons / S) & 1;
+                        ++cons;
+                        mbar_wait(kv_full + slot, ph);
+                        tc_fence_after();
+                        CSA_TRACE(2, ntr_s, 0);
+                        issue_qk<BK, D>(tmem + grp * BK, q_smem, kv_base + slot * C::kKVBytes);
+                        ++ntr_s;
+                        ++s_issued[grp];
+                        mma_commit(s_full + grp);
+                        mma_commit(kv_empty + slot);
+                        if (j == n - 1) mma_commit(q_empty);
+                    };
+                    auto issue_pv = [&](int32_t j) {
+                        const int grp = j & 1;
+                        CSA_TRACE(3, ntr_pv, 0);
+                        mbar_wait(p_full + grp, pv_issued[grp] & 1);
+                        CSA_TRACE(3, ntr_pv, 1);
+                        ++ntr_pv;
+                        if (j == 0) mbar_wait(o_empty, (local & 1) ^ 1);  // epilogue of last item
+                        const uint32_t slot = cons % S, ph = (cons / S) & 1;
+                        ++cons;
+                        mbar_wait(kv_full + slot, ph);
+                        tc_fence_after();
+                        issue_pv_ss<BK, D>(tmem + 2 * BK + grp * D, p_base + grp * L::kPBytes,
+                                           kv_base + slot * C::kKVBytes, j >= 2);
+                        ++pv_issued[grp];
+                        mma_commit(kv_empty + slot);
+                        mma_commit(p_empty + grp);
+                    };
+                    for (int32_t j = 0; j < n && j < 2; ++j) issue_s(j);
+                    for (int32_t j = 0; j < n; ++j) {
+                        if (j + 2 < n) issue_s(j + 2);
+                        issue_pv(j);
+                    }
+                    mma_commit(o_full);
                 }
             }
             __syncwarp();
         }
-    } else if (warp == 1) {
-        // ------------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            uint32_t cons = 0;            // K/V ring position consumed
-            uint32_t pcount[2] = {0, 0};  // p_full completions waited, per group
-            int32_t ntr_s = 0, ntr_pv = 0;  // trace counters (debug timeline only)
-            const uint32_t q_base = smem_u32(smem + L::kQOff);
-            const uint32_t kv_base = smem_u32(smem + L::kKVOff);
-            for (int32_t local = 0;; ++local) {
-                const int32_t item = next_item(local, false);
-                if (item < 0) break;
-                const Item it = decode_item(a, item);
-                const TileList tl = tile_list(a, it);
-                const int qb = local & 1;
-                mbar_wait(q_full + qb, (local >> 1) & 1);
-                const uint32_t q_smem = q_base + qb * C::kQBytes;
-                if (tl.n == 0) {  // corrupt plan (empty MASK row): release Q, no tiles
-                    mma_commit(q_empty + qb);
-                    mma_commit(o_full);
-                    continue;
-                }
-                auto do_pv = [&](int32_t t) {
-                    const int grp = t & 1;
-                    CSA_TRACE(3, ntr_pv, 0);
-                    mbar_wait(p_full + grp, pcount[grp] & 1);
-                    ++pcount[grp];
-                    CSA_TRACE(3, ntr_pv, 1);
-                    ++ntr_pv;
-                    if (t == 0) mbar_wait(o_empty, (local & 1) ^ 1);  // epilogue of last item
-                    const uint32_t slot = cons % S, ph = (cons / S) & 1;
-                    ++cons;
-                    mbar_wait(kv_full + slot, ph);
-                    tc_fence_after();
-                    issue_pv<BK, D>(tmem + 2 * BK + grp * D, tmem + grp * BK,
-                                    kv_base + slot * C::kKVBytes, t >= 2);
-                    mma_commit(kv_empty + slot);
-                };
-                for (int32_t j = 0; j < tl.n; ++j) {
-                    const int grp = j & 1;
-                    const uint32_t slot = cons % S, ph = (cons / S) & 1;
-                    ++cons;
-                    mbar_wait(kv_full + slot, ph);
-                    tc_fence_after();
-                    CSA_TRACE(2, ntr_s, 0);
-                    issue_qk<BK, D>(tmem + grp * BK, q_smem, kv_base + slot * C::kKVBytes);
-                    ++ntr_s;
-                    mma_commit(s_full + grp);
-                    mma_commit(kv_empty + slot);
-                    if (j == tl.n - 1) mma_commit(q_empty + qb);
-                    if (j >= 1) do_pv(j - 1);
-                }
-                do_pv(tl.n - 1);
-                mma_commit(o_full);
-            }
-        }
-        __syncwarp();
-    }
     } else {
         set_maxnreg_inc224();
         // ------------------------------------------------------------------ softmax groups
@@ -386,10 +455,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
         const uint32_t s_col = grp * BK;
         const uint32_t o_col = 2 * BK + grp * D;
+        const uint32_t p_row_addr = smem_u32(smem + L::kPOff + grp * L::kPBytes) + row * 128u;
         const float sl2 = a.scale_log2;
-        const uint64_t sl2x2 = f2(sl2, sl2);
         const int32_t tail_valid = g.N - (g.NB - 1) * BK;  // keys in the last (ragged) block
-        uint32_t scount = 0;
+        uint32_t scount = 0;  // S tiles consumed by this group (s_full phases)
+        uint32_t pcount = 0;  // P tiles produced by this group (p_empty phases)
         for (int32_t local = 0;; ++local) {
             const int32_t item = next_item(local, true);
             if (item < 0) break;
@@ -410,6 +480,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int c = 0; c < BK / 32; ++c) tmem_ld32(lane_addr + s_col + c * 32, r[c]);
 #pragma unroll
                 for (int c = 0; c < BK / 32; ++c) tmem_ld_wait(r[c]);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(s_free + grp);  // S[grp] may be overwritten now
                 if (tr) CSA_TRACE(grp, scount - 1, 1);
                 if (last_ragged && j == tl.n - 1) {
 #pragma unroll
@@ -418,73 +491,44 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int x = 0; x < 32; ++x)
                             if (c * 32 + x >= tail_valid) r[c][x] = 0xff800000u;  // -inf
                 }
-                // row max: 8 independent FMNMX3 chains (short dependency depth), then combine
-                constexpr int kPer = BK / 8;  // elements per chain (even)
-                float mc[8];
-#pragma unroll
-                for (int q8 = 0; q8 < 8; ++q8) {
-#define SV(e) __uint_as_float(r[(e) >> 5][(e) & 31])
-                    mc[q8] = SV(q8);
-#pragma unroll
-                    for (int t = 1; t + 1 < kPer; t += 2)
-                        mc[q8] = fmax3(mc[q8], SV(q8 + 8 * t), SV(q8 + 8 * (t + 1)));
-                    mc[q8] = fmaxf(mc[q8], SV(q8 + 8 * (kPer - 1)));
-#undef SV
-                }
-                const float mx = fmaxf(fmax3(mc[0], mc[1], mc[2]),
-                                       fmaxf(fmax3(mc[3], mc[4], mc[5]), fmaxf(mc[6], mc[7])));
-                const float m_new = fmaxf(m_run, mx * sl2);
-                if (tr) CSA_TRACE(grp, scount - 1, 2);
-                float alpha = 1.0f;
-                bool rescale = false;
+                // P[grp] smem may be rewritten once the previous P.V from it has completed
+                if (pcount > 0) mbar_wait(p_empty + grp, (pcount - 1) & 1);
+                ++pcount;
+                float lsum;
                 if (mine == 0) {
-                    m_run = m_new;
-                } else if (m_new > m_run + kRescaleThreshold) {
-                    alpha = ex2_approx(m_run - m_new);
-                    l_run *= alpha;
-                    m_run = m_new;
-                    rescale = true;
-                }
-                const uint64_t negm = f2(-m_run, -m_run);
-                uint64_t acc[4] = {0, 0, 0, 0};  // 4 packed partial sums (8 independent chains)
+                    m_run = row_max<BK>(r) * sl2;
+                    if (tr) CSA_TRACE(grp, scount - 1, 2);
+                    lsum = exp_row_to_smem<BK>(r, sl2, m_run, p_row_addr, (uint32_t)row);
+                } else {
+                    // speculative: exponentiate against the running max, check the tile max after
+                    lsum = exp_row_to_smem<BK>(r, sl2, m_run, p_row_addr, (uint32_t)row);
+                    const float m_tile = row_max<BK>(r) * sl2;
+                    if (tr) CSA_TRACE(grp, scount - 1, 2);
+                    if (m_tile > m_run + kRescaleThreshold) {  // rare: redo with the new max
+                        const float alpha = ex2_approx(m_run - m_tile);
+                        l_run *= alpha;
+                        m_run = m_tile;
+                        lsum = exp_row_to_smem<BK>(r, sl2, m_run, p_row_addr, (uint32_t)row);
+                        const uint64_t al2 = f2(alpha, alpha);
 #pragma unroll
-                for (int c = 0; c < BK / 32; ++c) {  // P overwrites the first BK/2 columns of S
-                    uint32_t pk[16];
+                        for (int c = 0; c < D; c += 32) {
+                            uint32_t o[32];
+                            tmem_ld32(lane_addr + o_col + c, o);
+                            tmem_ld_wait(o);
 #pragma unroll
-                    for (int x = 0; x < 32; x += 2) {
-                        const uint64_t sx = pk2(r[c][x], r[c][x + 1]);
-                        const uint64_t t = ffma2(sx, sl2x2, negm);
-                        uint64_t p;
-                        if (((c * 16 + x / 2) % kEmuEvery) == kEmuEvery - 1) {
-                            p = exp2_poly2(t);
-                        } else {
-                            p = f2(ex2_approx(lo_f(t)), ex2_approx(hi_f(t)));
+                            for (int x = 0; x < 32; x += 2) {
+                                const uint64_t v = fmul2(pk2(o[x], o[x + 1]), al2);
+                                o[x] = (uint32_t)v;
+                                o[x + 1] = (uint32_t)(v >> 32);
+                            }
+                            tmem_st32(lane_addr + o_col + c, o);
                         }
-                        acc[(x / 2) & 3] = fadd2(acc[(x / 2) & 3], p);
-                        pk[x / 2] = pack_bf16(lo_f(p), hi_f(p));
+                        tmem_st_wait();
                     }
-                    tmem_st16(lane_addr + s_col + c * 16, pk);
                 }
-                const uint64_t acc2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-                l_run += lo_f(acc2) + hi_f(acc2);
+                l_run += lsum;
                 if (tr) CSA_TRACE(grp, scount - 1, 3);
-                if (rescale) {
-                    const uint64_t al2 = f2(alpha, alpha);
-#pragma unroll
-                    for (int c = 0; c < D; c += 32) {
-                        uint32_t o[32];
-                        tmem_ld32(lane_addr + o_col + c, o);
-                        tmem_ld_wait(o);
-#pragma unroll
-                        for (int x = 0; x < 32; x += 2) {
-                            const uint64_t v = fmul2(pk2(o[x], o[x + 1]), al2);
-                            o[x] = (uint32_t)v;
-                            o[x + 1] = (uint32_t)(v >> 32);
-                        }
-                        tmem_st32(lane_addr + o_col + c, o);
-                    }
-                }
-                tmem_st_wait();
+                fence_proxy_async_smem();  // P (generic-proxy stores) -> visible to the MMA
                 tc_fence_before();
                 __syncwarp();
                 if (tr) CSA_TRACE(grp, scount - 1, 4);

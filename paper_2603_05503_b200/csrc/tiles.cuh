@@ -51,6 +51,20 @@ __device__ __forceinline__ void issue_pv(uint32_t o_tmem, uint32_t p_tmem, uint3
     }
 }
 
+// O[tmem] (+)= P[smem] . V with P a 128 x BK bf16 tile staged K-major in SW128 boxes of
+// [128 rows][64 keys] (written by the softmax threads), V MN-major (BK/16 MMAs of K = 16).
+template <int BK, int D>
+__device__ __forceinline__ void issue_pv_ss(uint32_t o_tmem, uint32_t p_smem, uint32_t v_smem,
+                                            bool accumulate) {
+    using C = TileCfg<BK, D>;
+#pragma unroll
+    for (int kk = 0; kk < BK / 16; ++kk) {
+        const uint64_t a = umma_desc_sw128(p_smem + (kk >> 2) * C::kQBox + (kk & 3) * 32, 16, 1024);
+        const uint64_t b = umma_desc_sw128(v_smem + kk * 16 * 128, C::kKBox, 1024);
+        mma_ss(o_tmem, a, b, C::kIdescPV, (accumulate || kk > 0) ? 1u : 0u);
+    }
+}
+
 // TMA-load one [rows][D] tile of a [batch, N, heads, D] tensor (4-D map: d, h, n, b).
 template <int D>
 __device__ __forceinline__ void tma_tile(uint8_t* dst, int box_bytes, const CUtensorMap* map,
