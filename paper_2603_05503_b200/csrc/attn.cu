@@ -13,15 +13,17 @@
 //               4-deep shared-memory item ring; loads the Q tile (TMA, or an in-warp gather of
 //               anchor rows), then the kept K/V tiles of the item's block list through a FIFO ring
 //               of smem slots in MMA consumption order K0 K1 K2 V0 K3 V1 ... V_{n-1}.
-//   warp 1      MMA issuer (one thread): S_j = Q K_j^T into TMEM S[j&1]; as soon as group j&1 has
-//               read S_j it issues S_{j+2}; then O[j&1] += P_j V_j with P from shared memory.
-//   warp 2      TMEM allocator (512 columns: S0 S1 O0 O1).
-//   warps 4-7   softmax group 0: even tiles of the item's list   } each keeps its own (m, l, O);
-//   warps 8-11  softmax group 1: odd tiles                          } merged in the epilogue.
-// One thread owns one query row (= one TMEM lane).  exp2 is taken against the running max
-// speculatively; a tile whose max exceeds it by more than 2^8 is redone with the new max and O is
-// rescaled (lazy rescale).  Packed f32x2 FMA/ADD; a fixed fraction of the exp2 are evaluated by a
-// degree-3 polynomial on the FMA pipe to offload the MUFU unit.
+//   warp 1      MMA issuer (one thread): S_j = Q K_j^T into TMEM S[j&1]; S_{j+2} is issued as
+//               soon as the softmax warps have read S_j; O += P_j V_j with P_j read from TMEM
+//               buffer P[j&1] (TS-MMA).  TMEM: S0 S1 | P0 P1 | O  (2BK + BK + D <= 512 columns).
+//   warp 2      TMEM allocator.
+//   warps 4-11  softmax: one query row (TMEM lane) per thread; warps 4-7 take the first half of
+//               the tile's key columns, warps 8-11 the second half.  exp2 is taken against the
+//               running max speculatively; the two halves agree on the tile max through shared
+//               memory once per tile and, in the rare case it exceeds the running max by more
+//               than 2^8, redo the tile with the new max and rescale O (lazy rescale).
+// Packed f32x2 FMA/ADD; a fixed fraction of the exp2 are evaluated by a degree-3 polynomial on
+// the FMA pipe to offload the MUFU unit.
 #include <cstdint>
 
 #include "csa_internal.cuh"
@@ -33,28 +35,31 @@ namespace {
 constexpr int kThreads = 384;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kItemSlots = 4;
-constexpr int kEmuMask = 3;                // element pairs p with (p & 7) >= 5 -> polynomial exp2
+constexpr int kEmuPerOctet = 3;            // element pairs p with (p & 7) >= 8 - this -> poly exp2
 
 template <int BK, int D>
 struct AttnSmem {
     using C = TileCfg<BK, D>;
-    static constexpr int kPBytes = C::kQBox * (BK / 64);  // 128 rows x BK keys bf16
     static constexpr int kQOff = 0;
-    static constexpr int kPOff = C::kQBytes;
-    static constexpr int kKVOff = kPOff + 2 * kPBytes;
+    static constexpr int kKVOff = 2 * C::kQBytes;
     static constexpr int kBudget = 224 * 1024 - kKVOff;
     static constexpr int kSlots = kBudget / C::kKVBytes > 8 ? 8 : kBudget / C::kKVBytes;
     static constexpr int kBarOff = kKVOff + kSlots * C::kKVBytes;
-    // q_full q_empty kv_full[S] kv_empty[S] s_full[2] s_free[2] p_full[2] p_empty[2] o_full
-    // o_empty item_full[4] item_empty[4]
-    static constexpr int kNumBars = 2 + 2 * kSlots + 8 + 2 + 2 * kItemSlots;
-    static constexpr int kRowOff = kBarOff + kNumBars * 8;           // m[2][128], l[2][128]
-    static constexpr int kItemOff = kRowOff + 4 * 128 * 4;           // int32 [kItemSlots]
+    // q_full[2] q_empty[2] kv_full[S] kv_empty[S] s_full[2] s_free[2] p_full[2] p_empty[2]
+    // o_full o_empty item_full[4] item_empty[4]
+    static constexpr int kNumBars = 4 + 2 * kSlots + 8 + 2 + 2 * kItemSlots;
+    static constexpr int kRowOff = kBarOff + kNumBars * 8;  // hmax[parity][half][128]
+    static constexpr int kItemOff = kRowOff + 4 * 128 * 4;  // int32 [kItemSlots]
     static constexpr int kTmemPtrOff = kItemOff + kItemSlots * 4;
     static constexpr int kBytes = kTmemPtrOff + 16;
     static constexpr int kAlloc = kBytes;  // base is 1 KiB aligned (__align__ on the extern)
-    static_assert(kSlots >= 3, "K/V ring too shallow");
+    static_assert(kSlots >= 4, "K/V ring too shallow");
     static_assert(kAlloc <= 232448, "smem");
+    // TMEM columns
+    static constexpr uint32_t kS = 0;           // S0 at 0, S1 at BK
+    static constexpr uint32_t kP = 2 * BK;      // P0 at 2BK, P1 at 2BK + BK/2
+    static constexpr uint32_t kO = 3 * BK;      // O: D columns
+    static_assert(3 * BK + D <= 512, "TMEM");
 };
 
 struct Item {
@@ -155,13 +160,6 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
     return pk2((uint32_t)p + e0, (uint32_t)(p >> 32) + e1);
 }
 
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
-                                             uint32_t d) {
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
-                 "r"(d)
-                 : "memory");
-}
-
 // Debug timeline (csa_debug_trace): clock64 stamps of CTA 0's pipeline events; nullptr = off.
 __device__ unsigned long long* g_trace;
 #define CSA_TRACE(slot, k, e)                                                             \
@@ -177,57 +175,69 @@ __device__ __forceinline__ void set_maxnreg_inc224() {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
 }
 
-// exp2(s * sl2 - m) for one 128-element row tile held in registers; P (bf16) written to the
-// K-major SW128 smem tile; returns the row sum.  `row` selects the swizzle phase.
-template <int BK>
-__device__ __forceinline__ float exp_row_to_smem(const uint32_t (&r)[BK / 32][32], float sl2,
-                                                 float m, uint32_t p_row_addr, uint32_t row) {
+// Half-row tile: HC = BK/2 columns per thread.  exp2(s*sl2 - m) -> packed bf16 pk[HC/2], returns
+// the sum of the fp32 values.
+template <int HC>
+__device__ __forceinline__ float exp_half(const uint32_t (&r)[HC], float sl2, float m,
+                                          uint32_t (&pk)[HC / 2]) {
     const uint64_t sl2x2 = f2(sl2, sl2);
     const uint64_t negm = f2(-m, -m);
     uint64_t acc[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int c = 0; c < BK / 32; ++c) {
-#pragma unroll
-        for (int h8 = 0; h8 < 4; ++h8) {  // 8 keys = one 16-byte chunk of P
-            uint32_t w[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int x = h8 * 8 + q * 2;
-                const uint64_t t = ffma2(pk2(r[c][x], r[c][x + 1]), sl2x2, negm);
-                uint64_t p;
-                if (((x / 2) & 7) >= 8 - kEmuMask) {
-                    p = exp2_poly2(t);
-                } else {
-                    p = f2(ex2_approx(lo_f(t)), ex2_approx(hi_f(t)));
-                }
-                acc[q] = fadd2(acc[q], p);
-                w[q] = pack_bf16(lo_f(p), hi_f(p));
-            }
-            const uint32_t chunk = (uint32_t)(c * 4 + h8);  // 16-byte chunk index along keys
-            const uint32_t addr = p_row_addr + (chunk >> 3) * (128u * 128u) +
-                                  (((chunk & 7u) ^ (row & 7u)) << 4);
-            st_shared_v4(addr, w[0], w[1], w[2], w[3]);
+    for (int x = 0; x < HC; x += 2) {
+        const uint64_t t = ffma2(pk2(r[x], r[x + 1]), sl2x2, negm);
+        uint64_t p;
+        if (((x / 2) & 7) >= 8 - kEmuPerOctet) {
+            p = exp2_poly2(t);
+        } else {
+            p = f2(ex2_approx(lo_f(t)), ex2_approx(hi_f(t)));
         }
+        acc[(x / 2) & 3] = fadd2(acc[(x / 2) & 3], p);
+        pk[x / 2] = pack_bf16(lo_f(p), hi_f(p));
     }
     const uint64_t s2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
     return lo_f(s2) + hi_f(s2);
 }
 
-template <int BK>
-__device__ __forceinline__ float row_max(const uint32_t (&r)[BK / 32][32]) {
-    constexpr int kPer = BK / 8;  // elements per chain (even)
+template <int HC>
+__device__ __forceinline__ float max_half(const uint32_t (&r)[HC]) {
+    constexpr int kPer = HC / 8;  // elements per chain (even)
     float mc[8];
 #pragma unroll
     for (int q8 = 0; q8 < 8; ++q8) {
-#define SV(e) __uint_as_float(r[(e) >> 5][(e) & 31])
-        mc[q8] = SV(q8);
+        mc[q8] = __uint_as_float(r[q8]);
 #pragma unroll
         for (int t = 1; t + 1 < kPer; t += 2)
-            mc[q8] = fmax3(mc[q8], SV(q8 + 8 * t), SV(q8 + 8 * (t + 1)));
-        mc[q8] = fmaxf(mc[q8], SV(q8 + 8 * (kPer - 1)));
-#undef SV
+            mc[q8] = fmax3(mc[q8], __uint_as_float(r[q8 + 8 * t]), __uint_as_float(r[q8 + 8 * (t + 1)]));
+        if (kPer % 2 == 0) mc[q8] = fmaxf(mc[q8], __uint_as_float(r[q8 + 8 * (kPer - 1)]));
     }
     return fmaxf(fmax3(mc[0], mc[1], mc[2]), fmaxf(fmax3(mc[3], mc[4], mc[5]), fmaxf(mc[6], mc[7])));
+}
+
+template <int HC>
+__device__ __forceinline__ void tmem_load_half(uint32_t addr, uint32_t (&r)[HC]) {
+    static_assert(HC == 32 || HC == 64, "half tile");
+    if constexpr (HC == 64) {
+        uint32_t(&a0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[0]);
+        uint32_t(&a1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[32]);
+        tmem_ld32(addr, a0);
+        tmem_ld32(addr + 32, a1);
+        tmem_ld_wait(a0);
+        tmem_ld_wait(a1);
+    } else {
+        uint32_t(&a0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[0]);
+        tmem_ld32(addr, a0);
+        tmem_ld_wait(a0);
+    }
+}
+
+template <int HC>
+__device__ __forceinline__ void tmem_store_p(uint32_t addr, const uint32_t (&pk)[HC / 2]) {
+    if constexpr (HC == 64) {
+        tmem_st32(addr, pk);
+    } else {
+        tmem_st16(addr, pk);
+    }
 }
 
 template <int BK, int D>
@@ -238,14 +248,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     using C = TileCfg<BK, D>;
     using L = AttnSmem<BK, D>;
     constexpr int S = L::kSlots;
+    constexpr int HC = BK / 2;  // columns per softmax thread
     extern __shared__ __align__(1024) uint8_t smem[];
     if ((smem_u32(smem) & 1023u) != 0u) __trap();  // SWIZZLE_128B atoms need 1 KiB alignment
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
     uint64_t* q_full = bars + 0;
-    uint64_t* q_empty = bars + 1;
-    uint64_t* kv_full = bars + 2;
-    uint64_t* kv_empty = bars + 2 + S;
-    uint64_t* s_full = bars + 2 + 2 * S;
+    uint64_t* q_empty = bars + 2;
+    uint64_t* kv_full = bars + 4;
+    uint64_t* kv_empty = bars + 4 + S;
+    uint64_t* s_full = bars + 4 + 2 * S;
     uint64_t* s_free = s_full + 2;
     uint64_t* p_full = s_full + 4;
     uint64_t* p_empty = s_full + 6;
@@ -253,19 +264,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* o_empty = s_full + 9;
     uint64_t* item_full = s_full + 10;
     uint64_t* item_empty = item_full + kItemSlots;
-    float* row_m = reinterpret_cast<float*>(smem + L::kRowOff);  // [2][128]
-    float* row_l = row_m + 256;                                   // [2][128]
+    float* hmax = reinterpret_cast<float*>(smem + L::kRowOff);  // [parity][half][128]
     volatile int32_t* item_slot = reinterpret_cast<int32_t*>(smem + L::kItemOff);
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtrOff);
 
     const uint32_t warp = warp_id(), lane = lane_id();
     if (threadIdx.x == 0) {
-        mbar_init(q_full, 1);
-        mbar_init(q_empty, 1);
         for (int i = 0; i < 2; ++i) {
+            mbar_init(q_full + i, 1);
+            mbar_init(q_empty + i, 1);
             mbar_init(s_full + i, 1);
-            mbar_init(s_free + i, 4);
-            mbar_init(p_full + i, 4);
+            mbar_init(s_free + i, 8);
+            mbar_init(p_full + i, 8);
             mbar_init(p_empty + i, 1);
         }
         for (int i = 0; i < S; ++i) {
@@ -315,7 +325,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol_q = policy_evict_first();
             const uint64_t pol_kv = policy_evict_last();
             uint32_t ld = 0;  // K/V loads issued (ring position)
-            uint8_t* qdst = smem + L::kQOff;
             for (int32_t local = 0;; ++local) {
                 const int s = local % kItemSlots;
                 mbar_wait(item_empty + s, ((local / kItemSlots) & 1) ^ 1);
@@ -331,11 +340,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (item < 0) break;
                 const Item it = decode_item(a, item);
                 const TileList tl = tile_list(a, it);
-                mbar_wait(q_empty, (local & 1) ^ 1);
+                const int qb = local & 1;
+                uint8_t* qdst = smem + L::kQOff + qb * C::kQBytes;
+                mbar_wait(q_empty + qb, ((local >> 1) & 1) ^ 1);
                 if (it.kind == 0) {
                     if (lane == 0) {
-                        mbar_arrive_expect_tx(q_full, C::kBoxes * BK * 128);
-                        tma_tile<D>(qdst, C::kQBox, &tq, q_full, it.h, it.idx * BK, it.b, pol_q);
+                        mbar_arrive_expect_tx(q_full + qb, C::kBoxes * BK * 128);
+                        tma_tile<D>(qdst, C::kQBox, &tq, q_full + qb, it.h, it.idx * BK, it.b,
+                                    pol_q);
                     }
                 } else {
                     // gather the anchor query rows of tile u: g = u*128 + row -> (f, m, j)
@@ -362,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(q_full);
+                    if (lane == 0) mbar_arrive(q_full + qb);
                 }
                 // K/V tiles in MMA consumption order: K0 K1, then per j: K_{j+2} (if any), V_j
                 if (lane == 0) {
@@ -385,12 +397,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else if (warp == 1) {
             // ---------------------------------------------------------------- MMA issuer
             if (lane == 0) {
-                uint32_t cons = 0;                // K/V ring position consumed
-                uint32_t s_issued[2] = {0, 0};    // S MMAs issued per buffer
-                uint32_t pv_issued[2] = {0, 0};   // P.V MMAs issued per buffer
-                int32_t ntr_s = 0, ntr_pv = 0;    // trace counters (debug timeline only)
-                const uint32_t q_smem = smem_u32(smem + L::kQOff);
-                const uint32_t p_base = smem_u32(smem + L::kPOff);
+                uint32_t cons = 0;   // K/V ring position consumed
+                uint32_t gbase = 0;  // tiles of earlier items: tile j of this item is global
+                                     // tile gbase + j, buffer (gbase + j) & 1, use (..) >> 1
+                int32_t ntr_s = 0, ntr_pv = 0;  // trace counters (debug timeline only)
+                const uint32_t q_base = smem_u32(smem + L::kQOff);
                 const uint32_t kv_base = smem_u32(smem + L::kKVOff);
                 for (int32_t local = 0;; ++local) {
                     const int32_t item = next_item(local, false);
@@ -398,31 +409,35 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const Item it = decode_item(a, item);
                     const TileList tl = tile_list(a, it);
                     const int32_t n = tl.n;
-                    mbar_wait(q_full, local & 1);
+                    const int qb = local & 1;
+                    mbar_wait(q_full + qb, (local >> 1) & 1);
+                    const uint32_t q_smem = q_base + qb * C::kQBytes;
                     if (n == 0) {  // corrupt plan (empty MASK row): release Q, no tiles
-                        mma_commit(q_empty);
+                        mma_commit(q_empty + qb);
                         mma_commit(o_full);
                         continue;
                     }
-                    auto issue_s = [&](int32_t j) {
-                        const int grp = j & 1;
-                        if (s_issued[grp] > 0) mbar_wait(s_free + grp, (s_issued[grp] - 1) & 1);
+                    auto do_s = [&](int32_t j) {
+                        const uint32_t gj = gbase + (uint32_t)j;
+                        const int b = gj & 1;
+                        const uint32_t use = gj >> 1;
+                        if (use > 0) mbar_wait(s_free + b, (use - 1) & 1);
                         const uint32_t slot = cons % S, ph = (cons / S) & 1;
                         ++cons;
                         mbar_wait(kv_full + slot, ph);
                         tc_fence_after();
                         CSA_TRACE(2, ntr_s, 0);
-                        issue_qk<BK, D>(tmem + grp * BK, q_smem, kv_base + slot * C::kKVBytes);
                         ++ntr_s;
-                        ++s_issued[grp];
-                        mma_commit(s_full + grp);
+                        issue_qk<BK, D>(tmem + L::kS + b * BK, q_smem, kv_base + slot * C::kKVBytes);
+                        mma_commit(s_full + b);
                         mma_commit(kv_empty + slot);
-                        if (j == n - 1) mma_commit(q_empty);
+                        if (j == n - 1) mma_commit(q_empty + qb);
                     };
-                    auto issue_pv = [&](int32_t j) {
-                        const int grp = j & 1;
+                    auto do_pv = [&](int32_t j) {
+                        const uint32_t gj = gbase + (uint32_t)j;
+                        const int b = gj & 1;
                         CSA_TRACE(3, ntr_pv, 0);
-                        mbar_wait(p_full + grp, pv_issued[grp] & 1);
+                        mbar_wait(p_full + b, (gj >> 1) & 1);
                         CSA_TRACE(3, ntr_pv, 1);
                         ++ntr_pv;
                         if (j == 0) mbar_wait(o_empty, (local & 1) ^ 1);  // epilogue of last item
@@ -430,36 +445,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ++cons;
                         mbar_wait(kv_full + slot, ph);
                         tc_fence_after();
-                        issue_pv_ss<BK, D>(tmem + 2 * BK + grp * D, p_base + grp * L::kPBytes,
-                                           kv_base + slot * C::kKVBytes, j >= 2);
-                        ++pv_issued[grp];
+                        issue_pv<BK, D>(tmem + L::kO, tmem + L::kP + b * (BK / 2),
+                                        kv_base + slot * C::kKVBytes, j > 0);
                         mma_commit(kv_empty + slot);
-                        mma_commit(p_empty + grp);
+                        mma_commit(p_empty + b);
                     };
-                    for (int32_t j = 0; j < n && j < 2; ++j) issue_s(j);
+                    for (int32_t j = 0; j < n && j < 2; ++j) do_s(j);
                     for (int32_t j = 0; j < n; ++j) {
-                        if (j + 2 < n) issue_s(j + 2);
-                        issue_pv(j);
+                        if (j + 2 < n) do_s(j + 2);
+                        do_pv(j);
                     }
                     mma_commit(o_full);
+                    gbase += (uint32_t)n;
                 }
             }
             __syncwarp();
         }
     } else {
         set_maxnreg_inc224();
-        // ------------------------------------------------------------------ softmax groups
-        const int grp = (warp - 4) >> 2;
+        // ------------------------------------------------------------------ softmax warps
+        const int half = (warp - 4) >> 2;  // key-column half of every tile
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
-        const uint32_t s_col = grp * BK;
-        const uint32_t o_col = 2 * BK + grp * D;
-        const uint32_t p_row_addr = smem_u32(smem + L::kPOff + grp * L::kPBytes) + row * 128u;
         const float sl2 = a.scale_log2;
         const int32_t tail_valid = g.N - (g.NB - 1) * BK;  // keys in the last (ragged) block
-        uint32_t scount = 0;  // S tiles consumed by this group (s_full phases)
-        uint32_t pcount = 0;  // P tiles produced by this group (p_empty phases)
+        uint32_t tcount = 0;  // tiles processed (s_full / p phases, hmax parity)
         for (int32_t local = 0;; ++local) {
             const int32_t item = next_item(local, true);
             if (item < 0) break;
@@ -468,87 +479,88 @@ __global__ void __launch_bounds__(kThreads, 1)
             // only the last listed tile can be the ragged block N_B - 1
             const bool last_ragged = tail_valid < BK && tl.n > 0 && tl.at(tl.n - 1) == g.NB - 1;
             float m_run = -INFINITY, l_run = 0.0f;
-            int32_t mine = 0;
-            for (int32_t j = grp; j < tl.n; j += 2, ++mine) {
-                mbar_wait(s_full + grp, scount & 1);
-                ++scount;
+            for (int32_t j = 0; j < tl.n; ++j, ++tcount) {
+                const int b = tcount & 1;          // S / P buffer of this (global) tile
+                const uint32_t use = tcount >> 1;  // earlier uses of buffer b
+                mbar_wait(s_full + b, use & 1);
                 const bool tr = (quarter == 0 && lane == 0);
-                if (tr) CSA_TRACE(grp, scount - 1, 0);
+                if (tr) CSA_TRACE(half, tcount, 0);
                 tc_fence_after();
-                uint32_t r[BK / 32][32];
-#pragma unroll
-                for (int c = 0; c < BK / 32; ++c) tmem_ld32(lane_addr + s_col + c * 32, r[c]);
-#pragma unroll
-                for (int c = 0; c < BK / 32; ++c) tmem_ld_wait(r[c]);
+                uint32_t r[HC];
+                tmem_load_half<HC>(lane_addr + L::kS + b * BK + half * HC, r);
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(s_free + grp);  // S[grp] may be overwritten now
-                if (tr) CSA_TRACE(grp, scount - 1, 1);
+                if (lane == 0) mbar_arrive(s_free + b);  // S[b] may be overwritten now
+                if (tr) CSA_TRACE(half, tcount, 1);
                 if (last_ragged && j == tl.n - 1) {
 #pragma unroll
-                    for (int c = 0; c < BK / 32; ++c)
-#pragma unroll
-                        for (int x = 0; x < 32; ++x)
-                            if (c * 32 + x >= tail_valid) r[c][x] = 0xff800000u;  // -inf
+                    for (int x = 0; x < HC; ++x)
+                        if (half * HC + x >= tail_valid) r[x] = 0xff800000u;  // -inf
                 }
-                // P[grp] smem may be rewritten once the previous P.V from it has completed
-                if (pcount > 0) mbar_wait(p_empty + grp, (pcount - 1) & 1);
-                ++pcount;
+                float* hm = hmax + (tcount & 1) * 256;
+                uint32_t pk[HC / 2];
                 float lsum;
-                if (mine == 0) {
-                    m_run = row_max<BK>(r) * sl2;
-                    if (tr) CSA_TRACE(grp, scount - 1, 2);
-                    lsum = exp_row_to_smem<BK>(r, sl2, m_run, p_row_addr, (uint32_t)row);
+                bool redo = false;
+                float m_tile;
+                if (j == 0) {
+                    // first tile: agree on the tile max before exponentiating
+                    hm[half * 128 + row] = max_half<HC>(r);
+                    named_bar_sync(1, 256);
+                    m_tile = fmaxf(hm[row], hm[128 + row]) * sl2;
+                    m_run = m_tile;
+                    lsum = exp_half<HC>(r, sl2, m_run, pk);
                 } else {
-                    // speculative: exponentiate against the running max, check the tile max after
-                    lsum = exp_row_to_smem<BK>(r, sl2, m_run, p_row_addr, (uint32_t)row);
-                    const float m_tile = row_max<BK>(r) * sl2;
-                    if (tr) CSA_TRACE(grp, scount - 1, 2);
-                    if (m_tile > m_run + kRescaleThreshold) {  // rare: redo with the new max
-                        const float alpha = ex2_approx(m_run - m_tile);
-                        l_run *= alpha;
-                        m_run = m_tile;
-                        lsum = exp_row_to_smem<BK>(r, sl2, m_run, p_row_addr, (uint32_t)row);
-                        const uint64_t al2 = f2(alpha, alpha);
+                    // speculative: exponentiate against the running max, then agree on the max
+                    lsum = exp_half<HC>(r, sl2, m_run, pk);
+                    hm[half * 128 + row] = max_half<HC>(r);
+                    named_bar_sync(1, 256);
+                    m_tile = fmaxf(hm[row], hm[128 + row]) * sl2;
+                    redo = m_tile > m_run + kRescaleThreshold;  // same decision in both halves
+                }
+                if (tr) CSA_TRACE(half, tcount, 2);
+                // P[b] and O may be written once the P.V that last read P[b] has completed
+                if (use > 0) mbar_wait(p_empty + b, (use - 1) & 1);
+                if (redo) {  // rare: new max -> rescale O (after every earlier P.V) and redo P
+                    mbar_wait(p_empty + (b ^ 1), ((tcount - 1) >> 1) & 1);  // P.V of tile j-1
+                    tc_fence_after();
+                    const float alpha = ex2_approx(m_run - m_tile);
+                    l_run *= alpha;
+                    m_run = m_tile;
+                    lsum = exp_half<HC>(r, sl2, m_run, pk);
+                    const uint64_t al2 = f2(alpha, alpha);
 #pragma unroll
-                        for (int c = 0; c < D; c += 32) {
-                            uint32_t o[32];
-                            tmem_ld32(lane_addr + o_col + c, o);
-                            tmem_ld_wait(o);
+                    for (int c = 0; c < D / 2; c += 32) {
+                        uint32_t o[32];
+                        const uint32_t oa = lane_addr + L::kO + half * (D / 2) + c;
+                        tmem_ld32(oa, o);
+                        tmem_ld_wait(o);
 #pragma unroll
-                            for (int x = 0; x < 32; x += 2) {
-                                const uint64_t v = fmul2(pk2(o[x], o[x + 1]), al2);
-                                o[x] = (uint32_t)v;
-                                o[x + 1] = (uint32_t)(v >> 32);
-                            }
-                            tmem_st32(lane_addr + o_col + c, o);
+                        for (int x = 0; x < 32; x += 2) {
+                            const uint64_t v = fmul2(pk2(o[x], o[x + 1]), al2);
+                            o[x] = (uint32_t)v;
+                            o[x + 1] = (uint32_t)(v >> 32);
                         }
-                        tmem_st_wait();
+                        tmem_st32(oa, o);
                     }
                 }
                 l_run += lsum;
-                if (tr) CSA_TRACE(grp, scount - 1, 3);
-                fence_proxy_async_smem();  // P (generic-proxy stores) -> visible to the MMA
+                tmem_store_p<HC>(lane_addr + L::kP + b * (BK / 2) + half * (HC / 2), pk);
+                tmem_st_wait();
+                if (tr) CSA_TRACE(half, tcount, 3);
                 tc_fence_before();
                 __syncwarp();
-                if (tr) CSA_TRACE(grp, scount - 1, 4);
-                if (lane == 0) mbar_arrive(p_full + grp);
+                if (lane == 0) mbar_arrive(p_full + b);
+                if (tr) CSA_TRACE(half, tcount, 4);
             }
             // -------------------------------------------------------------- epilogue
             mbar_wait(o_full, local & 1);
             tc_fence_after();
-            row_m[grp * 128 + row] = m_run;
-            row_l[grp * 128 + row] = l_run;
+            // row sums of the two halves; uses the hmax slot the last tile did not use
+            float* row_l = hmax + (tcount & 1) * 256;
+            row_l[half * 128 + row] = l_run;
             named_bar_sync(1, 256);
-            const bool has0 = tl.n >= 1, has1 = tl.n >= 2;
-            const float m0 = row_m[row], m1 = row_m[128 + row];
-            const float l0 = row_l[row], l1 = row_l[128 + row];
-            const float M = has1 ? fmaxf(m0, m1) : m0;
-            const float a0 = has0 ? ex2_approx(m0 - M) : 0.0f;
-            const float a1 = has1 ? ex2_approx(m1 - M) : 0.0f;
-            const float Lsum = l0 * a0 + l1 * a1;
-            const float inv = 1.0f / Lsum;
-            const float f0 = a0 * inv, f1 = a1 * inv;
+            const float inv = 1.0f / (row_l[row] + row_l[128 + row]);
+            const float Lsum = row_l[row] + row_l[128 + row];
             // output rows of this thread
             int64_t tok0 = -1;
             int32_t n_dst = 0, dst_stride_rows = 0;
@@ -574,20 +586,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             __nv_bfloat16* obase = a.o + (int64_t)it.b * a.o_sb + (int64_t)it.h * a.o_sh;
-            const uint64_t f0x2 = f2(f0, f0), f1x2 = f2(f1, f1);
+            const uint64_t inv2 = f2(inv, inv);
 #pragma unroll
             for (int c = 0; c < D / 2; c += 32) {
-                const int col = grp * (D / 2) + c;
-                uint32_t r0[32], r1[32];
-                tmem_ld32(lane_addr + 2 * BK + col, r0);
-                if (has1) tmem_ld32(lane_addr + 2 * BK + D + col, r1);
+                const int col = half * (D / 2) + c;
+                uint32_t r0[32];
+                tmem_ld32(lane_addr + L::kO + col, r0);
                 tmem_ld_wait(r0);
-                if (has1) tmem_ld_wait(r1);
                 uint32_t packed[16];
 #pragma unroll
                 for (int x = 0; x < 32; x += 2) {
-                    uint64_t v = fmul2(pk2(r0[x], r0[x + 1]), f0x2);
-                    if (has1) v = ffma2(pk2(r1[x], r1[x + 1]), f1x2, v);
+                    const uint64_t v = fmul2(pk2(r0[x], r0[x + 1]), inv2);
                     packed[x / 2] = pack_bf16(lo_f(v), hi_f(v));
                 }
                 for (int32_t dI = 0; dI < n_dst; ++dI) {
@@ -599,14 +608,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                                             packed[4 * v + 3]);
                 }
             }
-            if (grp == 0 && a.lse_out != nullptr) {
-                const float lse = (M + __log2f(Lsum)) * 0.69314718055994531f;
+            if (half == 0 && a.lse_out != nullptr) {
+                const float lse = (m_run + __log2f(Lsum)) * 0.69314718055994531f;
                 float* lb = a.lse_out + ((int64_t)it.b * a.n_heads + it.h) * (int64_t)g.N;
                 for (int32_t dI = 0; dI < n_dst; ++dI)
                     lb[tok0 + (int64_t)dI * dst_stride_rows] = lse;
             }
             tc_fence_before();
-            __syncwarp();
+            named_bar_sync(1, 256);  // row_l reused by the next item's epilogue
             if (lane == 0) mbar_arrive(o_empty);
         }
     }

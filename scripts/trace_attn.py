@@ -32,13 +32,13 @@ for g in (0, 1):
     a = t[g]
     ok = (a[:, 4] > 0)
     a = a[ok][20:400]
-    print(f"group {g}: tiles {ok.sum()}  ld {np.median(a[:,1]-a[:,0]):.0f}  max {np.median(a[:,2]-a[:,1]):.0f}"
-          f"  exp {np.median(a[:,3]-a[:,2]):.0f}  st {np.median(a[:,4]-a[:,3]):.0f}"
+    print(f"half {g}: tiles {ok.sum()}  ld {np.median(a[:,1]-a[:,0]):.0f}  exp+max+bar {np.median(a[:,2]-a[:,1]):.0f}"
+          f"  pwait+st {np.median(a[:,3]-a[:,2]):.0f}  arrive {np.median(a[:,4]-a[:,3]):.0f}"
           f"  busy {np.median(a[:,4]-a[:,0]):.0f}  period {np.median(np.diff(a[:,0])):.0f}")
 s = t[2][t[2][:, 0] > 0][20:400, 0]
 pv = t[3][t[3][:, 1] > 0][20:400]
 print(f"S issue period {np.median(np.diff(s)):.0f}; PV p_full wait {np.median(pv[:,1]-pv[:,0]):.0f}"
       f"  PV period {np.median(np.diff(pv[:,1])):.0f}")
-for j in range(40, 48):
+for j in range(80, 88):
     print(j, [int(x - t0) for x in t[0, j, :5]], [int(x - t0) for x in t[1, j, :5]],
-          int(t[2, 2 * j, 0] - t0), int(t[3, 2 * j, 1] - t0))
+          "S", int(t[2, j, 0] - t0), "PVp", int(t[3, j, 0] - t0), int(t[3, j, 1] - t0))
