@@ -201,7 +201,7 @@ CSA_API const char* csa_last_error(void);
 
 /* Debug only: device buffer of 4*1024*8 uint64 receiving clock64() stamps of CTA 0's attention
  * pipeline events (softmax groups, S and P.V issue); NULL switches tracing off. */
-CSA_API csa_status_t csa_debug_trace(void* buf);
+CSA_API csa_status_t csa_debug_trace(void* buf, int32_t mode);
 
 /* Library version string. */
 CSA_API const char* csa_version(void);

@@ -85,7 +85,7 @@ def lib() -> ctypes.CDLL:
                                       _TensorT, _TensorT, vp, ctypes.POINTER(_PlanT), i64, vp, vp,
                                       i32, vp, ctypes.c_size_t, vp]
     L.csa_debug_trace.restype = st
-    L.csa_debug_trace.argtypes = [vp]
+    L.csa_debug_trace.argtypes = [vp, i32]
     L.csa_validate_plan.restype = st
     L.csa_validate_plan.argtypes = [ctypes.POINTER(_PlanT), _LayoutT, i64, vp]
     _lib = L

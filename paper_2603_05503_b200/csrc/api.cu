@@ -133,8 +133,8 @@ const char* csa_last_error(void) { return g_err.c_str(); }
 
 const char* csa_version(void) { return "csa-b200 0.1 (sm_100a)"; }
 
-csa_status_t csa_debug_trace(void* buf) {
-    cudaError_t e = csa::set_attn_trace(buf);
+csa_status_t csa_debug_trace(void* buf, int32_t mode) {
+    cudaError_t e = csa::set_attn_trace(buf, mode);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyToSymbol");
     return ok();
 }

@@ -162,6 +162,7 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
 
 // Debug timeline (csa_debug_trace): clock64 stamps of CTA 0's pipeline events; nullptr = off.
 __device__ unsigned long long* g_trace;
+__device__ int g_debug_mode;  // 0 normal; 1 skip the softmax arithmetic (pipeline measurement)
 #define CSA_TRACE(slot, k, e)                                                             \
     do {                                                                                  \
         if (g_trace != nullptr && blockIdx.x == 0 && (k) < 1024)                          \
@@ -485,6 +486,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(s_full + b, use & 1);
                 const bool tr = (quarter == 0 && lane == 0);
                 if (tr) CSA_TRACE(half, tcount, 0);
+                if (g_debug_mode == 1) {  // debug: pipeline without softmax work
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(s_free + b);
+                        mbar_arrive(p_full + b);
+                    }
+                    continue;
+                }
                 tc_fence_after();
                 uint32_t r[HC];
                 tmem_load_half<HC>(lane_addr + L::kS + b * BK + half * HC, r);
@@ -648,9 +658,11 @@ cudaError_t launch_t(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap
 
 }  // namespace
 
-cudaError_t set_attn_trace(void* buf) {
+cudaError_t set_attn_trace(void* buf, int mode) {
     unsigned long long* p = static_cast<unsigned long long*>(buf);
-    return cudaMemcpyToSymbol(g_trace, &p, sizeof(p));
+    cudaError_t e = cudaMemcpyToSymbol(g_trace, &p, sizeof(p));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyToSymbol(g_debug_mode, &mode, sizeof(mode));
 }
 
 cudaError_t launch_attn(const AttnArgs& a, int head_dim, const CUtensorMap& tq,

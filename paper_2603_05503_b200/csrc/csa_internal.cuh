@@ -96,7 +96,7 @@ struct AttnArgs {
     const int32_t* n_work;
     uint32_t* sched;  // [2] dynamic-scheduler counters (zero on entry and on exit) or nullptr
 };
-cudaError_t set_attn_trace(void* buf);
+cudaError_t set_attn_trace(void* buf, int mode);
 cudaError_t launch_attn(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
                         const CUtensorMap& tk, const CUtensorMap& tv, int grid,
                         cudaStream_t s);

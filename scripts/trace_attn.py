@@ -20,10 +20,10 @@ work = csa.build_work_list(plan, 0, cfg.heads)
 q, k, v = inputs.qkv(1, lay.N, cfg.heads, cfg.d, seed=11, device="cuda")
 out = csa.sparse_attn_fwd(q, k, v, plan, work)
 buf = torch.zeros(4 * 1024 * 8, dtype=torch.int64, device="cuda")
-csa.lib().csa_debug_trace(ctypes.c_void_p(buf.data_ptr()))
+csa.lib().csa_debug_trace(ctypes.c_void_p(buf.data_ptr()), int(os.environ.get("CSA_DEBUG_MODE", "0")))
 csa.sparse_attn_fwd(q, k, v, plan, work, out=out)
 torch.cuda.synchronize()
-csa.lib().csa_debug_trace(None)
+csa.lib().csa_debug_trace(None, 0)
 t = buf.view(4, 1024, 8).cpu().numpy().astype(np.int64)
 os.makedirs("gpurun_out", exist_ok=True)
 np.save("gpurun_out/trace.npy", t)
