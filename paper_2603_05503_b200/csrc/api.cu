@@ -2,6 +2,7 @@
 // No allocation, no host synchronisation (except csa_validate_plan), thread-local error text.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -277,7 +278,11 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
     a.n_work = n_work;
     a.sched = static_cast<uint32_t*>(workspace);
     const int64_t items = (int64_t)max_work * batch;
-    const int grid = (int)(items < di.sms ? items : di.sms);
+    int grid = (int)(items < di.sms ? items : di.sms);
+    if (const char* dbg = std::getenv("CSA_DEBUG_GRID")) {  // debug: fewer persistent CTAs
+        const int want = std::atoi(dbg);
+        if (want > 0 && want < grid) grid = want;
+    }
     cudaError_t e = csa::launch_attn(a, head_dim, tq, tk, tv, grid, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "attention launch");
     return ok();

@@ -429,7 +429,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tc_fence_after();
                         CSA_TRACE(2, ntr_s, 0);
                         ++ntr_s;
-                        issue_qk<BK, D>(tmem + L::kS + b * BK, q_smem, kv_base + slot * C::kKVBytes);
+                        issue_qk<BK, D>(tmem + L::kS + b * BK, q_smem,
+                                        kv_base + slot * C::kKVBytes,
+                                        (g_debug_mode == 7 || g_debug_mode == 8) ? 1 : D / 16);
                         mma_commit(s_full + b);
                         mma_commit(kv_empty + slot);
                         if (j == n - 1) mma_commit(q_empty + qb);
@@ -447,7 +449,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mbar_wait(kv_full + slot, ph);
                         tc_fence_after();
                         issue_pv<BK, D>(tmem + L::kO, tmem + L::kP + b * (BK / 2),
-                                        kv_base + slot * C::kKVBytes, j > 0);
+                                        kv_base + slot * C::kKVBytes, j > 0,
+                                        (g_debug_mode == 6 || g_debug_mode == 8) ? 1 : BK / 16);
                         mma_commit(kv_empty + slot);
                         mma_commit(p_empty + b);
                     };
@@ -486,13 +489,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(s_full + b, use & 1);
                 const bool tr = (quarter == 0 && lane == 0);
                 if (tr) CSA_TRACE(half, tcount, 0);
-                if (g_debug_mode == 1) {  // debug: pipeline without softmax work
+                if (g_debug_mode != 0) {  // debug: pipeline without softmax work
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) {
-                        mbar_arrive(s_free + b);
-                        mbar_arrive(p_full + b);
-                    }
+                    if (lane == 0) mbar_arrive(s_free + b);
+                    if (use > 0) mbar_wait(p_empty + b, (use - 1) & 1);  // no phase overrun
+                    if (lane == 0) mbar_arrive(p_full + b);
                     continue;
                 }
                 tc_fence_after();

@@ -28,10 +28,12 @@ struct TileCfg {
 
 // S[tmem] = Q . K^T over head_dim (D/16 MMAs of K = 16).
 template <int BK, int D>
-__device__ __forceinline__ void issue_qk(uint32_t s_tmem, uint32_t q_smem, uint32_t k_smem) {
+__device__ __forceinline__ void issue_qk(uint32_t s_tmem, uint32_t q_smem, uint32_t k_smem,
+                                         int nsteps = D / 16) {
     using C = TileCfg<BK, D>;
 #pragma unroll
     for (int kk = 0; kk < D / 16; ++kk) {
+        if (kk >= nsteps) break;  // debug measurements only (truncated contraction)
         const uint32_t off = (kk & 3) * 32;  // 16 bf16 = 32 B inside a 128-B box row
         const uint64_t a = umma_desc_sw128(q_smem + (kk >> 2) * C::kQBox + off, 16, 1024);
         const uint64_t b = umma_desc_sw128(k_smem + (kk >> 2) * C::kKBox + off, 16, 1024);
@@ -42,10 +44,11 @@ __device__ __forceinline__ void issue_qk(uint32_t s_tmem, uint32_t q_smem, uint3
 // O[tmem] (+)= P[tmem] . V over the BK keys of the tile (BK/16 MMAs of K = 16).
 template <int BK, int D>
 __device__ __forceinline__ void issue_pv(uint32_t o_tmem, uint32_t p_tmem, uint32_t v_smem,
-                                         bool accumulate) {
+                                         bool accumulate, int nsteps = BK / 16) {
     using C = TileCfg<BK, D>;
 #pragma unroll
     for (int kk = 0; kk < BK / 16; ++kk) {
+        if (kk >= nsteps) break;  // debug measurements only (truncated contraction)
         const uint64_t b = umma_desc_sw128(v_smem + kk * 16 * 128, C::kKBox, 1024);
         mma_ts(o_tmem, p_tmem + kk * 8, b, C::kIdescPV, (accumulate || kk > 0) ? 1u : 0u);
     }

@@ -20,7 +20,8 @@ q, k, v = inputs.qkv(1, lay.N, cfg.heads, cfg.d, seed=11, device="cuda")
 out = torch.empty_like(q)
 sizes = np.array([lay.block_size(c) for c in range(lay.NB)], np.int64)
 flop = 4.0 * cfg.d * float(np.einsum("hrc,r,c->", masks.astype(np.int64), sizes, sizes))
-for mode in (0, 1, 0):
+modes = [int(x) for x in os.environ.get("MODES", "0,1,2,3,4").split(",")]
+for mode in modes:
     csa.lib().csa_debug_trace(None, mode)
     for _ in range(3):
         csa.sparse_attn_fwd(q, k, v, plan, work, out=out)
