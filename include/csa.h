@@ -154,8 +154,11 @@ CSA_API csa_status_t csa_compile_plan(csa_layout_t L, int64_t n_cells, const uin
  * order 0: longest-first, ties (h asc, kind asc, index asc) -- a total order (unique output);
  * order 1: natural (h asc, index asc);
  * order 2: head-major, longest-first within a head (h asc, cost desc, index asc) -- the L2-local
- *          order the dynamic scheduler of csa_sparse_attn_fwd is built for (default).
- * Encoding: kind<<31 | h<<20 | (r or u).  work_list: uint32 [capacity]; n_work: device int32.
+ *          order the dynamic scheduler of csa_sparse_attn_fwd is built for;
+ * order 3: PAIR items for the CTA-pair kernel (block 128, head_dim 128): item (h, p) stands for
+ *          rows (2p, 2p+1) of a MASK head or anchor tiles (2p, 2p+1) of a REPETITIVE head,
+ *          p < ceil(units/2), cost = sum of the members' costs; head-major, cost desc, p asc.
+ * Encoding: kind<<31 | h<<20 | (r, u or p).  work_list: uint32 [capacity]; n_work: device int32.
  * Requires n_heads <= 2048 and at most 32768 items. */
 CSA_API csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan, int64_t cell_base,
                                  int32_t n_heads, int32_t order, uint32_t* work_list,
@@ -175,17 +178,20 @@ CSA_API csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan,
  *   lse_out     optional fp32 [batch][n_heads][N], natural log over the kept keys
  *   work_list   items from csa_build_work_list; n_work device int32 (count)
  *   max_work    host upper bound of *n_work (sizes the persistent grid)
+ *   pair_items  0: single items (orders 0-2), one CTA per item;  1: pair items (order 3), two
+ *               CTAs of a cluster per item (cta_group::2 MMAs, each CTA loads half of every K/V
+ *               tile); requires block 128 and head_dim 128.  Results are identical per row.
  * Workspace: csa_workspace_size(CSA_WS_ATTN, ...) bytes of device memory holding the dynamic
  * scheduler's counters; it must be zero-filled before its first use and is left zero-filled when
  * the launch completes (so one buffer serves every launch on one stream).  NULL -> static
- * round-robin assignment of work items to CTAs. */
+ * round-robin assignment of work items to CTAs (pair items are always assigned statically). */
 CSA_API csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
                                  int32_t head_dim, float softmax_scale, csa_tensor_t q,
                                  csa_tensor_t k, csa_tensor_t v, csa_tensor_t o, float* lse_out,
                                  const csa_plan_t* plan, int64_t cell_base,
                                  const uint32_t* work_list, const int32_t* n_work,
-                                 int32_t max_work, void* workspace, size_t workspace_bytes,
-                                 csa_stream_t stream);
+                                 int32_t max_work, int32_t pair_items, void* workspace,
+                                 size_t workspace_bytes, csa_stream_t stream);
 
 /* Workspace bytes for `which` (CSA_WS_*). */
 CSA_API size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_t head_dim);

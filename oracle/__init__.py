@@ -241,7 +241,7 @@ def compile_cell(count, n: int, block: int, F: int, H: int, W: int, min_count_: 
 def work_list(n: int, block: int, F: int, W: int, kinds, anchor_k, row_nnz, order: int = 0
               ) -> np.ndarray:
     """Work list of one launch (scheduling artefact): order 0 longest-first,
-    1 natural, 2 head-major longest-first within a head."""
+    1 natural, 2 head-major longest-first within a head, 3 the same over pair items (2p, 2p+1)."""
     kinds = np.ascontiguousarray(np.asarray(kinds, dtype=np.uint8))
     ak = np.ascontiguousarray(np.asarray(anchor_k, dtype=np.int32))
     nnz = np.ascontiguousarray(np.asarray(row_nnz, dtype=np.int32))

@@ -354,6 +354,7 @@ int csao_compile_cell(int64_t n, int32_t b, int32_t F, int32_t H, int32_t W,
 /*   REPETITIVE head h: items (h, u) for u < ceil(F*k*W/128), cost = N_B.                        */
 /* order 0: (cost desc, h asc, kind asc, r-or-u asc); order 1: (h asc, r-or-u asc);             */
 /* order 2: (h asc, cost desc, r-or-u asc).  Encoded kind<<31 | h<<20 | (r or u).               */
+/* order 3: pair items p (members 2p, 2p+1), cost = members' sum, sorted as order 2.            */
 /* row_nnz: [n_heads * N_B] (ignored for REPETITIVE heads).  Returns item count, -1 on error.   */
 /* ------------------------------------------------------------------------------------------ */
 typedef struct { int64_t cost; uint32_t code; } orc_item;
@@ -374,14 +375,29 @@ int64_t csao_work_list(int32_t n_heads, int64_t n, int32_t b, int32_t F, int32_t
                        const uint8_t* kinds, const int32_t* anchor_k, const int32_t* row_nnz,
                        int32_t order, uint32_t* out, int64_t capacity) {
     const int64_t nb = csao_num_blocks(n, b);
+    const int pairs = (order == 3);
     int64_t total = 0;
-    for (int32_t h = 0; h < n_heads; ++h)
-        total += kinds[h] ? ((int64_t)F * anchor_k[h] * W + 127) / 128 : nb;
+    for (int32_t h = 0; h < n_heads; ++h) {
+        const int64_t units = kinds[h] ? ((int64_t)F * anchor_k[h] * W + 127) / 128 : nb;
+        total += pairs ? (units + 1) / 2 : units;
+    }
     if (total > capacity) return -1;
     orc_item* it = (orc_item*)malloc(sizeof(orc_item) * (size_t)(total ? total : 1));
     if (!it) return -1;
     int64_t x = 0;
-    for (int32_t h = 0; h < n_heads; ++h) {
+    for (int32_t h = 0; h < n_heads && pairs; ++h) {
+        /* order 3: item p = members 2p, 2p+1; cost = sum of the existing members' costs */
+        const int64_t units = kinds[h] ? ((int64_t)F * anchor_k[h] * W + 127) / 128 : nb;
+        for (int64_t p = 0; 2 * p < units; ++p) {
+            int64_t cost = 0;
+            for (int64_t u = 2 * p; u < 2 * p + 2 && u < units; ++u)
+                cost += kinds[h] ? nb : row_nnz[(int64_t)h * nb + u];
+            it[x].cost = cost;
+            it[x].code = ((kinds[h] ? 1u : 0u) << 31) | ((uint32_t)h << 20) | (uint32_t)p;
+            ++x;
+        }
+    }
+    for (int32_t h = 0; h < n_heads && !pairs; ++h) {
         if (kinds[h]) {
             const int64_t nu = ((int64_t)F * anchor_k[h] * W + 127) / 128;
             for (int64_t u = 0; u < nu; ++u) {

@@ -83,7 +83,7 @@ def lib() -> ctypes.CDLL:
     L.csa_sparse_attn_fwd.restype = st
     L.csa_sparse_attn_fwd.argtypes = [_LayoutT, i32, i32, i32, ctypes.c_float, _TensorT, _TensorT,
                                       _TensorT, _TensorT, vp, ctypes.POINTER(_PlanT), i64, vp, vp,
-                                      i32, vp, ctypes.c_size_t, vp]
+                                      i32, i32, vp, ctypes.c_size_t, vp]
     L.csa_debug_trace.restype = st
     L.csa_debug_trace.argtypes = [vp, i32]
     L.csa_validate_plan.restype = st
@@ -178,15 +178,16 @@ class Plan:
             self.kind, self.anchor_k, self.mask_bits, self.blk_base, self.blk_row_ptr,
             self.blk_idx, self.ivl_base, self.ivl_row_ptr, self.ivl, self.kept_area))
 
-    def items(self, cell_base: int, n_heads: int) -> int:
+    def items(self, cell_base: int, n_heads: int, pairs: bool = False) -> int:
         """Work items of one launch (host-side count used to size the persistent grid)."""
         tot = 0
         for h in range(n_heads):
             c = cell_base + h
             if self.kind_host[c]:
-                tot += (self.lay.F * self.anchor_k_host[c] * self.lay.W + 127) // 128
+                units = (self.lay.F * self.anchor_k_host[c] * self.lay.W + 127) // 128
             else:
-                tot += self.lay.NB
+                units = self.lay.NB
+            tot += (units + 1) // 2 if pairs else units
         return tot
 
 
@@ -242,19 +243,26 @@ class WorkList:
     items: torch.Tensor   # uint32 codes (stored as int32)
     n_work: torch.Tensor  # device int32 [1]
     max_work: int
+    pairs: bool = False   # order 3: items are (row 2p, row 2p+1) pairs for the CTA-pair kernel
+
+
+def default_order(lay: Layout, d: int) -> int:
+    """Pair items (CTA-pair kernel) where supported (block 128, head_dim 128), else order 2."""
+    return 3 if (lay.B == 128 and d == 128) else 2
 
 
 def build_work_list(plan: Plan, cell_base: int, n_heads: int, order: int = 2,
                     stream=None) -> WorkList:
-    """csa_build_work_list; order 2 (head-major, longest row first) is the L2-local default."""
-    cap = plan.items(cell_base, n_heads)
+    """csa_build_work_list.  order 2: head-major, longest row first (one CTA per item);
+    order 3: pair items for the CTA-pair kernel (block 128, head_dim 128)."""
+    cap = plan.items(cell_base, n_heads, pairs=(order == 3))
     items = torch.empty(max(cap, 1), dtype=torch.int32, device=plan.kind.device)
     n_work = torch.empty(1, dtype=torch.int32, device=plan.kind.device)
     s = plan.struct()
     _check(lib().csa_build_work_list(_layout(plan.lay), ctypes.byref(s), cell_base, n_heads, order,
                                      _ptr(items), cap, _ptr(n_work), None, 0, _stream(stream)),
            "csa_build_work_list")
-    return WorkList(items, n_work, cap)
+    return WorkList(items, n_work, cap, pairs=(order == 3))
 
 
 # ------------------------------------------------------------------------------- attention
@@ -277,7 +285,8 @@ def sparse_attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: Pla
     _check(lib().csa_sparse_attn_fwd(_layout(plan.lay), b, heads, d, sc, _tensor(q), _tensor(k),
                                      _tensor(v), _tensor(out), _ptr(lse_out), ctypes.byref(s),
                                      cell_base, _ptr(work.items), _ptr(work.n_work), work.max_work,
-                                     _ptr(ws), 0 if ws is None else ws.numel(), _stream(stream)),
+                                     1 if work.pairs else 0, _ptr(ws),
+                                     0 if ws is None else ws.numel(), _stream(stream)),
            "csa_sparse_attn_fwd")
     return out
 

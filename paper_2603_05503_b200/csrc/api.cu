@@ -136,6 +136,7 @@ const char* csa_version(void) { return "csa-b200 0.1 (sm_100a)"; }
 
 csa_status_t csa_debug_trace(void* buf, int32_t mode) {
     cudaError_t e = csa::set_attn_trace(buf, mode);
+    if (e == cudaSuccess) e = csa::set_attn2_trace(buf, mode);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyToSymbol");
     return ok();
 }
@@ -214,7 +215,7 @@ csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan, int64_t
     csa_status_t st = check_layout(L, 0, n_heads);
     if (st != CSA_OK) return st;
     if (n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "n_heads must be >= 1");
-    if (order < 0 || order > 2) return fail(CSA_ERR_INVALID_ARGUMENT, "order must be 0, 1 or 2");
+    if (order < 0 || order > 3) return fail(CSA_ERR_INVALID_ARGUMENT, "order must be 0..3");
     if (!plan_ptrs_ok(plan, false) || !work_list || !n_work)
         return fail(CSA_ERR_INVALID_ARGUMENT, "null buffer");
     if (cell_base < 0 || cell_base + n_heads > plan->n_cells)
@@ -232,10 +233,12 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
                                  csa_tensor_t k, csa_tensor_t v, csa_tensor_t o, float* lse_out,
                                  const csa_plan_t* plan, int64_t cell_base,
                                  const uint32_t* work_list, const int32_t* n_work,
-                                 int32_t max_work, void* workspace, size_t workspace_bytes,
-                                 csa_stream_t stream) {
+                                 int32_t max_work, int32_t pair_items, void* workspace,
+                                 size_t workspace_bytes, csa_stream_t stream) {
     csa_status_t st = check_layout(L, head_dim, n_heads);
     if (st != CSA_OK) return st;
+    if (pair_items && (L.block != 128 || head_dim != 128))
+        return fail(CSA_ERR_UNSUPPORTED, "pair work items need block 128 and head_dim 128");
     if (workspace != nullptr && (workspace_bytes < 8 || reinterpret_cast<uintptr_t>(workspace) % 8))
         return fail(CSA_ERR_INVALID_ARGUMENT, "attention workspace: >= 8 bytes, 8-byte aligned");
     if (batch < 1 || n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "batch/n_heads < 1");
@@ -277,13 +280,22 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
     a.work_list = work_list;
     a.n_work = n_work;
     a.sched = static_cast<uint32_t*>(workspace);
-    const int64_t items = (int64_t)max_work * batch;
+    const int64_t items = (int64_t)max_work * batch * (pair_items ? 2 : 1);
     int grid = (int)(items < di.sms ? items : di.sms);
     if (const char* dbg = std::getenv("CSA_DEBUG_GRID")) {  // debug: fewer persistent CTAs
         const int want = std::atoi(dbg);
         if (want > 0 && want < grid) grid = want;
     }
-    cudaError_t e = csa::launch_attn(a, head_dim, tq, tk, tv, grid, (cudaStream_t)stream);
+    cudaError_t e;
+    if (pair_items) {
+        CUtensorMap tk_half;  // K halves: 64-key boxes (each CTA of a pair loads one half)
+        if ((st = make_map(&tk_half, k, batch, g.N, n_heads, head_dim, g.B / 2, "k")) != CSA_OK)
+            return st;
+        a.sched = nullptr;  // the pair kernel assigns pair items statically per cluster
+        e = csa::launch_attn_pair(a, head_dim, tq, tk_half, tv, grid, (cudaStream_t)stream);
+    } else {
+        e = csa::launch_attn(a, head_dim, tq, tk, tv, grid, (cudaStream_t)stream);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "attention launch");
     return ok();
 }

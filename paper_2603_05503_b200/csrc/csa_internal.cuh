@@ -100,5 +100,10 @@ cudaError_t set_attn_trace(void* buf, int mode);
 cudaError_t launch_attn(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
                         const CUtensorMap& tk, const CUtensorMap& tv, int grid,
                         cudaStream_t s);
+cudaError_t set_attn2_trace(void* buf, int mode);
+// CTA-pair kernel (block 128, head_dim 128): work items are pairs of rows / anchor tiles.
+cudaError_t launch_attn_pair(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
+                             const CUtensorMap& tk_half, const CUtensorMap& tv, int grid,
+                             cudaStream_t s);
 
 }  // namespace csa

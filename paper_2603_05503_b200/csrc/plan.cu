@@ -295,18 +295,24 @@ __global__ void __launch_bounds__(1024)
 }
 
 // Order 2 (head-major, longest-first within a head): one CTA per head sorts its own segment.
-//   key = (2047 - cost) << 11 | index     (cost, index <= 2047)
+//   key = (4095 - cost) << 11 | index     (cost <= 4094, index <= 2047)
+// Order 3 (pairs): item p of a head stands for rows (2p, 2p+1) [or anchor tiles (2p, 2p+1)];
+//   cost = sum of the members' costs (the pair kernel walks the union of their lists).
 __global__ void __launch_bounds__(256)
-    work_list_head_kernel(Geo g, PlanDev p, int64_t cell_base, int32_t n_heads,
+    work_list_head_kernel(Geo g, PlanDev p, int64_t cell_base, int32_t n_heads, int32_t pairs,
                           uint32_t* __restrict__ out, int32_t capacity, int32_t* __restrict__ n_work) {
     __shared__ uint32_t keys[2048];
     __shared__ int32_t s_off, s_cnt, s_total;
     const int h = blockIdx.x;
-    auto items_of = [&](int hh) -> int32_t {
+    auto units_of = [&](int hh) -> int32_t {  // rows (MASK) or anchor tiles (REPETITIVE)
         const int64_t cell = cell_base + hh;
         return p.kind[cell] ? (int32_t)(((int64_t)g.F * p.anchor_k[cell] * g.W + kAnchorTile - 1) /
                                         kAnchorTile)
                             : g.NB;
+    };
+    auto items_of = [&](int hh) -> int32_t {
+        const int32_t u = units_of(hh);
+        return pairs ? (u + 1) / 2 : u;
     };
     if (threadIdx.x == 0) {
         int32_t off = 0, tot = 0;
@@ -332,12 +338,15 @@ __global__ void __launch_bounds__(256)
     for (int32_t x = threadIdx.x; x < pow2; x += blockDim.x) {
         uint32_t key = 0xffffffffu;
         if (x < cnt) {
-            int32_t cost = g.NB;
-            if (!rep) {
+            const int32_t units = units_of(h);
+            auto unit_cost = [&](int32_t u) -> int32_t {
+                if (u >= units) return 0;
+                if (rep) return g.NB;
                 const int32_t* rp = p.blk_row_ptr + cell * (g.NB + 1);
-                cost = rp[x + 1] - rp[x];
-            }
-            key = ((uint32_t)(2047 - cost) << 11) | (uint32_t)x;
+                return rp[u + 1] - rp[u];
+            };
+            const int32_t cost = pairs ? unit_cost(2 * x) + unit_cost(2 * x + 1) : unit_cost(x);
+            key = ((uint32_t)(4095 - cost) << 11) | (uint32_t)x;
         }
         keys[x] = key;
     }
@@ -437,9 +446,9 @@ cudaError_t launch_plan_fill(const Geo& g, int64_t n_cells, const PlanDev& p, cu
 cudaError_t launch_work_list(const Geo& g, const PlanDev& p, int64_t cell_base, int32_t n_heads,
                              int32_t order, uint32_t* out, int32_t capacity, int32_t* n_work,
                              cudaStream_t s) {
-    if (order == 2) {
-        work_list_head_kernel<<<n_heads, 256, 0, s>>>(g, p, cell_base, n_heads, out, capacity,
-                                                     n_work);
+    if (order == 2 || order == 3) {
+        work_list_head_kernel<<<n_heads, 256, 0, s>>>(g, p, cell_base, n_heads, order == 3 ? 1 : 0,
+                                                     out, capacity, n_work);
         return cudaGetLastError();
     }
     const size_t smem = sizeof(uint32_t) * kMaxWorkItems;
