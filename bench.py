@@ -275,7 +275,8 @@ def main():
     sim = torch.tensor([1.0 if h in rep else 0.0 for h in my_heads], dtype=torch.float64, device=dev)
     t0 = time.perf_counter()
     plan = csa.compile_plan(lay, counts, 32, similarity=sim, gamma=0.87, anchor_k=5)
-    work = csa.build_work_list(plan, 0, hp)  # head-major, longest row first (order 2)
+    # pair items for the CTA-pair kernel (block 128, d 128), else head-major single items
+    work = csa.build_work_list(plan, 0, hp, order=csa.default_order(lay, d))
     torch.cuda.synchronize()
     flop_rank, _ = flops_of(lay, masks, rep, my_heads, d, B)
     flop_all, area_all = flops_of(lay, masks, rep, range(H), d, B)
@@ -357,7 +358,7 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
     H, d, B = cfg.heads, cfg.d, args.batch
     ones = torch.full((H * lay.NB * lay.NB,), 64, dtype=torch.int16, device=dev).view(torch.uint16)
     plan1 = csa.compile_plan(lay, ones, 32)
-    work1 = csa.build_work_list(plan1, 0, H)
+    work1 = csa.build_work_list(plan1, 0, H, order=csa.default_order(lay, d))
     t_dense, _ = time_loop(lambda: csa.sparse_attn_fwd(q, k, v, plan1, work1, out=out),
                            max(2, args.steps // 3), 2, stream)
     t_dense /= max(2, args.steps // 3)

@@ -302,10 +302,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                         const uint32_t gj = gbase + (uint32_t)j;
                         const int b = gj & 1;
                         const uint32_t use = gj >> 1;
+                        CSA_TRACE(2, gj, 0);
                         if (use > 0) mbar_wait_cluster(s_free + b, (use - 1) & 1);
+                        CSA_TRACE(2, gj, 1);
                         const uint32_t slot = cons % S, ph = (cons / S) & 1;
                         ++cons;
                         mbar_wait_cluster(kv_full + slot, ph);
+                        CSA_TRACE(2, gj, 2);
                         tc_fence_after();
                         const uint32_t k_smem = kv_base + slot * L::kSlotBytes;
 #pragma unroll
@@ -317,6 +320,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                                 umma_desc_sw128(k_smem + (kk >> 2) * L::kKHalfBox + off, 16, 1024);
                             mma_ss_pair(tmem + L::kS + b * BK, ad, bd, L::kIdescQK, kk > 0);
                         }
+                        CSA_TRACE(2, gj, 3);
                         mma_commit_pair(s_full + b);
                         mma_commit_pair(kv_empty + slot);
                         if (j == n - 1) mma_commit_pair(q_empty + qb);
@@ -324,11 +328,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     auto do_pv = [&](int32_t j) {
                         const uint32_t gj = gbase + (uint32_t)j;
                         const int b = gj & 1;
+                        CSA_TRACE(3, gj, 0);
                         mbar_wait_cluster(p_full + b, (gj >> 1) & 1);
+                        CSA_TRACE(3, gj, 1);
                         if (j == 0) mbar_wait_cluster(o_empty, (local & 1) ^ 1);
                         const uint32_t slot = cons % S, ph = (cons / S) & 1;
                         ++cons;
                         mbar_wait_cluster(kv_full + slot, ph);
+                        CSA_TRACE(3, gj, 2);
                         tc_fence_after();
                         const uint32_t v_smem = kv_base + slot * L::kSlotBytes;
 #pragma unroll
@@ -338,6 +345,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                                         L::kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
                         }
                         mma_commit_pair(kv_empty + slot);
+                        CSA_TRACE(3, gj, 3);
                         mma_commit_pair(p_empty + b);
                     };
                     for (int32_t j = 0; j < n && j < 2; ++j) do_s(j);
@@ -380,6 +388,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 const int b = tcount & 1;
                 const uint32_t use = tcount >> 1;
                 mbar_wait(s_full + b, use & 1);
+                const bool tr = (quarter == 0 && lane == 0);
+                if (tr) CSA_TRACE(half, tcount, 0);
                 tc_fence_after();
                 uint32_t pk[HC / 2];
                 float lsum = 0.0f;
@@ -449,6 +459,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(lf_pful[b]);
+                if (tr) CSA_TRACE(half, tcount, 4);
             }
             // -------------------------------------------------------------- epilogue
             mbar_wait(o_full, local & 1);

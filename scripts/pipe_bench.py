@@ -15,7 +15,7 @@ lay = cfg.layout
 masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity or 0.69, seed=0)
 cnt = torch.from_numpy((masks.astype(np.uint16) * np.uint16(64)).reshape(-1).view(np.int16)).cuda()
 plan = csa.compile_plan(lay, cnt.view(torch.uint16), 32)
-work = csa.build_work_list(plan, 0, cfg.heads)
+work = csa.build_work_list(plan, 0, cfg.heads, order=int(os.environ.get("ORDER", "3")))
 q, k, v = inputs.qkv(1, lay.N, cfg.heads, cfg.d, seed=11, device="cuda")
 out = torch.empty_like(q)
 sizes = np.array([lay.block_size(c) for c in range(lay.NB)], np.int64)
