@@ -245,6 +245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                                                   sw128_offset(row, ch & 7)) = val;
                     }
                     fence_proxy_async_smem();
+                    fence_cluster();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(lead(q_full + qb));
                 }
@@ -291,7 +292,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     const PairItem it = decode_pair(a, item);
                     const int32_t n = union_size(member_list(a, it, 0), member_list(a, it, 1));
                     const int qb = local & 1;
-                    mbar_wait_cluster(q_full + qb, (local >> 1) & 1);
+                    mbar_wait(q_full + qb, (local >> 1) & 1);
                     const uint32_t q_smem = q_base + qb * L::kQBytes;
                     if (n == 0) {
                         mma_commit_pair(q_empty + qb);
@@ -303,11 +304,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                         const int b = gj & 1;
                         const uint32_t use = gj >> 1;
                         CSA_TRACE(2, gj, 0);
-                        if (use > 0) mbar_wait_cluster(s_free + b, (use - 1) & 1);
+                        if (use > 0) mbar_wait(s_free + b, (use - 1) & 1);
                         CSA_TRACE(2, gj, 1);
                         const uint32_t slot = cons % S, ph = (cons / S) & 1;
                         ++cons;
-                        mbar_wait_cluster(kv_full + slot, ph);
+                        mbar_wait(kv_full + slot, ph);
                         CSA_TRACE(2, gj, 2);
                         tc_fence_after();
                         const uint32_t k_smem = kv_base + slot * L::kSlotBytes;
@@ -329,12 +330,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                         const uint32_t gj = gbase + (uint32_t)j;
                         const int b = gj & 1;
                         CSA_TRACE(3, gj, 0);
-                        mbar_wait_cluster(p_full + b, (gj >> 1) & 1);
+                        mbar_wait(p_full + b, (gj >> 1) & 1);
                         CSA_TRACE(3, gj, 1);
-                        if (j == 0) mbar_wait_cluster(o_empty, (local & 1) ^ 1);
+                        if (j == 0) mbar_wait(o_empty, (local & 1) ^ 1);
                         const uint32_t slot = cons % S, ph = (cons / S) & 1;
                         ++cons;
-                        mbar_wait_cluster(kv_full + slot, ph);
+                        mbar_wait(kv_full + slot, ph);
                         CSA_TRACE(3, gj, 2);
                         tc_fence_after();
                         const uint32_t v_smem = kv_base + slot * L::kSlotBytes;
