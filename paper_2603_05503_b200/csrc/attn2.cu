@@ -139,6 +139,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     using L = PairSmem<D>;
     constexpr int BK = 128;
     constexpr int S = L::kSlots;
+    constexpr int SK = S / 2, SV = S - SK;  // K-half ring slots, V-half ring slots
     constexpr int HC = BK / 2;
     extern __shared__ __align__(1024) uint8_t smem[];
     if ((smem_u32(smem) & 1023u) != 0u) __trap();
@@ -199,7 +200,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             // ------------------------------------------------------------------- producer
             const uint64_t pol_q = policy_evict_first();
             const uint64_t pol_kv = policy_evict_last();
-            uint32_t ld = 0;
+            uint32_t ldk = 0, ldv = 0;  // loads issued into the K ring / the V ring
             int32_t local = 0;
             for (int32_t item = cl; item < n_items; item += ncl, ++local) {
                 const PairItem it = decode_pair(a, item);
@@ -257,8 +258,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     auto load = [&](bool is_k) {
                         bool in0, in1;
                         const int32_t c = is_k ? ik.next(in0, in1) : iv.next(in0, in1);
-                        const uint32_t slot = ld % S, ph = (ld / S) & 1;
-                        ++ld;
+                        uint32_t slot, ph;
+                        if (is_k) {
+                            slot = ldk % SK;
+                            ph = (ldk / SK) & 1;
+                            ++ldk;
+                        } else {
+                            slot = SK + ldv % SV;
+                            ph = (ldv / SV) & 1;
+                            ++ldv;
+                        }
                         mbar_wait(kv_empty + slot, ph ^ 1);
                         uint8_t* dst = smem + L::kKVOff + slot * L::kSlotBytes;
                         const uint32_t fb = lead(kv_full + slot);
@@ -281,8 +290,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 }
                 __syncwarp();
             }
-        } else if (warp == 1 && rank == 0) {
-            // ------------------------------------------------------- MMA issuer (leader)
+        } else if ((warp == 1 || warp == 3) && rank == 0) {
+            // ------------------------------------------- MMA issuers (leader CTA): warp 1 issues
+            // every S = Q K^T, warp 3 every O += P V, each in order from its own ring of K or V
+            // halves, so neither stream's waits stall the other (tcgen05.commit tracks the
+            // issuing thread's own MMAs).
+            const bool s_issuer = (warp == 1);
             if (lane == 0) {
                 uint32_t cons = 0, gbase = 0;
                 int32_t local = 0;
@@ -292,69 +305,64 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     const PairItem it = decode_pair(a, item);
                     const int32_t n = union_size(member_list(a, it, 0), member_list(a, it, 1));
                     const int qb = local & 1;
-                    mbar_wait(q_full + qb, (local >> 1) & 1);
-                    const uint32_t q_smem = q_base + qb * L::kQBytes;
-                    if (n == 0) {
-                        mma_commit_pair(q_empty + qb);
+                    if (s_issuer) {
+                        mbar_wait(q_full + qb, (local >> 1) & 1);
+                        const uint32_t q_smem = q_base + qb * L::kQBytes;
+                        if (n == 0) mma_commit_pair(q_empty + qb);
+                        for (int32_t j = 0; j < n; ++j) {
+                            const uint32_t gj = gbase + (uint32_t)j;
+                            const int b = gj & 1;
+                            const uint32_t use = gj >> 1;
+                            CSA_TRACE(2, gj, 0);
+                            if (use > 0) mbar_wait(s_free + b, (use - 1) & 1);
+                            CSA_TRACE(2, gj, 1);
+                            const uint32_t slot = cons % SK, ph = (cons / SK) & 1;
+                            ++cons;
+                            mbar_wait(kv_full + slot, ph);
+                            CSA_TRACE(2, gj, 2);
+                            tc_fence_after();
+                            const uint32_t k_smem = kv_base + slot * L::kSlotBytes;
+#pragma unroll
+                            for (int kk = 0; kk < D / 16; ++kk) {
+                                const uint32_t off = (kk & 3) * 32;
+                                const uint64_t ad =
+                                    umma_desc_sw128(q_smem + (kk >> 2) * L::kQBox + off, 16, 1024);
+                                const uint64_t bd = umma_desc_sw128(
+                                    k_smem + (kk >> 2) * L::kKHalfBox + off, 16, 1024);
+                                mma_ss_pair(tmem + L::kS + b * BK, ad, bd, L::kIdescQK, kk > 0);
+                            }
+                            CSA_TRACE(2, gj, 3);
+                            mma_commit_pair(s_full + b);
+                            mma_commit_pair(kv_empty + slot);
+                            if (j == n - 1) mma_commit_pair(q_empty + qb);
+                        }
+                    } else {
+                        for (int32_t j = 0; j < n; ++j) {
+                            const uint32_t gj = gbase + (uint32_t)j;
+                            const int b = gj & 1;
+                            CSA_TRACE(3, gj, 0);
+                            mbar_wait(p_full + b, (gj >> 1) & 1);
+                            CSA_TRACE(3, gj, 1);
+                            if (j == 0) mbar_wait(o_empty, (local & 1) ^ 1);
+                            const uint32_t slot = SK + cons % SV, ph = (cons / SV) & 1;
+                            ++cons;
+                            mbar_wait(kv_full + slot, ph);
+                            CSA_TRACE(3, gj, 2);
+                            tc_fence_after();
+                            const uint32_t v_smem = kv_base + slot * L::kSlotBytes;
+#pragma unroll
+                            for (int kk = 0; kk < BK / 16; ++kk) {
+                                const uint64_t bd =
+                                    umma_desc_sw128(v_smem + kk * 16 * 128, 16384, 1024);
+                                mma_ts_pair(tmem + L::kO, tmem + L::kP + b * (BK / 2) + kk * 8, bd,
+                                            L::kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
+                            }
+                            CSA_TRACE(3, gj, 3);
+                            mma_commit_pair(kv_empty + slot);
+                            mma_commit_pair(p_empty + b);
+                        }
                         mma_commit_pair(o_full);
-                        continue;
                     }
-                    auto do_s = [&](int32_t j) {
-                        const uint32_t gj = gbase + (uint32_t)j;
-                        const int b = gj & 1;
-                        const uint32_t use = gj >> 1;
-                        CSA_TRACE(2, gj, 0);
-                        if (use > 0) mbar_wait(s_free + b, (use - 1) & 1);
-                        CSA_TRACE(2, gj, 1);
-                        const uint32_t slot = cons % S, ph = (cons / S) & 1;
-                        ++cons;
-                        mbar_wait(kv_full + slot, ph);
-                        CSA_TRACE(2, gj, 2);
-                        tc_fence_after();
-                        const uint32_t k_smem = kv_base + slot * L::kSlotBytes;
-#pragma unroll
-                        for (int kk = 0; kk < D / 16; ++kk) {
-                            const uint32_t off = (kk & 3) * 32;
-                            const uint64_t ad =
-                                umma_desc_sw128(q_smem + (kk >> 2) * L::kQBox + off, 16, 1024);
-                            const uint64_t bd =
-                                umma_desc_sw128(k_smem + (kk >> 2) * L::kKHalfBox + off, 16, 1024);
-                            mma_ss_pair(tmem + L::kS + b * BK, ad, bd, L::kIdescQK, kk > 0);
-                        }
-                        CSA_TRACE(2, gj, 3);
-                        mma_commit_pair(s_full + b);
-                        mma_commit_pair(kv_empty + slot);
-                        if (j == n - 1) mma_commit_pair(q_empty + qb);
-                    };
-                    auto do_pv = [&](int32_t j) {
-                        const uint32_t gj = gbase + (uint32_t)j;
-                        const int b = gj & 1;
-                        CSA_TRACE(3, gj, 0);
-                        mbar_wait(p_full + b, (gj >> 1) & 1);
-                        CSA_TRACE(3, gj, 1);
-                        if (j == 0) mbar_wait(o_empty, (local & 1) ^ 1);
-                        const uint32_t slot = cons % S, ph = (cons / S) & 1;
-                        ++cons;
-                        mbar_wait(kv_full + slot, ph);
-                        CSA_TRACE(3, gj, 2);
-                        tc_fence_after();
-                        const uint32_t v_smem = kv_base + slot * L::kSlotBytes;
-#pragma unroll
-                        for (int kk = 0; kk < BK / 16; ++kk) {
-                            const uint64_t bd = umma_desc_sw128(v_smem + kk * 16 * 128, 16384, 1024);
-                            mma_ts_pair(tmem + L::kO, tmem + L::kP + b * (BK / 2) + kk * 8, bd,
-                                        L::kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
-                        }
-                        mma_commit_pair(kv_empty + slot);
-                        CSA_TRACE(3, gj, 3);
-                        mma_commit_pair(p_empty + b);
-                    };
-                    for (int32_t j = 0; j < n && j < 2; ++j) do_s(j);
-                    for (int32_t j = 0; j < n; ++j) {
-                        if (j + 2 < n) do_s(j + 2);
-                        do_pv(j);
-                    }
-                    mma_commit_pair(o_full);
                     gbase += (uint32_t)n;
                 }
             }
