@@ -247,8 +247,11 @@ class WorkList:
 
 
 def default_order(lay: Layout, d: int) -> int:
-    """Pair items (CTA-pair kernel) where supported (block 128, head_dim 128), else order 2."""
-    return 3 if (lay.B == 128 and d == 128) else 2
+    """Work-list order of the production path: 2 (head-major single items, one CTA per query
+    block).  Order 3 selects the CTA-pair kernel (block 128, head_dim 128), bit-identical but
+    currently slower on B200; it stays opt-in."""
+    del lay, d
+    return 2
 
 
 def build_work_list(plan: Plan, cell_base: int, n_heads: int, order: int = 2,
