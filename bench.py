@@ -212,35 +212,6 @@ def cpu_oracle_sample(lay, cfg, masks, rep, q, k, v, seconds_target=12.0, anchor
                       f"threads, {wall:.1f} s wall; value = sampled kept FLOP / wall"}
 
 
-def ulysses_step_factory(q_loc, k_loc, v_loc, world, rank, heads, plan_run, stream):
-    """Sequence-sharded [1, N/P, H, d] -> all-to-all -> head-sharded [1, N, H/P, d], attention on
-    the rank's heads, all-to-all back.  (Plumbing through torch.distributed / NCCL.)"""
-    import torch.distributed as dist
-
-    _, n_loc, H, d = q_loc.shape
-    hp = H // world
-    n = n_loc * world
-
-    def pack(t):  # [1, n_loc, P, hp, d] -> [P, n_loc, hp, d] contiguous
-        return t.view(n_loc, world, hp, d).permute(1, 0, 2, 3).contiguous()
-
-    recv = [torch.empty((world, n_loc, hp, d), dtype=q_loc.dtype, device=q_loc.device)
-            for _ in range(3)]
-    o_recv = torch.empty((world, n_loc, hp, d), dtype=q_loc.dtype, device=q_loc.device)
-    out_loc = torch.empty_like(q_loc)
-
-    def step():
-        for src, dst in zip((q_loc, k_loc, v_loc), recv):
-            dist.all_to_all_single(dst, pack(src))
-        qh, kh, vh = (r.view(1, n, hp, d) for r in recv)
-        o = plan_run(qh, kh, vh)  # [1, n, hp, d] == [P_dst, n_loc, hp, d]
-        dist.all_to_all_single(o_recv, o.view(world, n_loc, hp, d))
-        out_loc.view(n_loc, world, hp, d).copy_(o_recv.permute(1, 0, 2, 3))
-        return out_loc
-
-    return step
-
-
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -291,14 +262,15 @@ def main():
         def step():
             return csa.sparse_attn_fwd(q, k, v, plan, work, out=out)
     else:
-        n_loc = lay.N // world
-        ql, kl, vl = (t[:, rank * n_loc:(rank + 1) * n_loc].contiguous() for t in (q, k, v))
+        from paper_2603_05503_b200 import ulysses
+
+        ql, kl, vl = (ulysses.sequence_shard(t, world, rank) for t in (q, k, v))
         del q, k, v
         q = k = v = None
 
         def run_heads(qh, kh, vh):
             return csa.sparse_attn_fwd(qh, kh, vh, plan, work, out=out)
-        step = ulysses_step_factory(ql, kl, vl, world, rank, H, run_heads, stream)
+        step = ulysses.make_layer_step(ql, kl, vl, world, run_heads)
 
     with ClockSampler(local) as clk:
         total_ms, per = time_loop(step, args.steps, args.warmup, stream)

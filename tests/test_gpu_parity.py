@@ -123,7 +123,7 @@ def test_work_list_bit_exact(csa):
         ref = oracle.work_list(lay.N, lay.B, lay.F, lay.W, kinds[base:base + nh], ak[base:base + nh],
                                nnz[base:base + nh])
         assert np.array_equal(got, ref)
-        for order in (1, 2):
+        for order in (1, 2, 3):
             wl = csa.build_work_list(plan, base, nh, order=order)
             got = wl.items.cpu().numpy().view(np.uint32)[: int(wl.n_work.item())]
             ref = oracle.work_list(lay.N, lay.B, lay.F, lay.W, kinds[base:base + nh],
@@ -315,3 +315,23 @@ def test_calibration_wan480_sampled(csa):
         qh, kh = head64(q, 0, h), head64(k, 0, h)
         E_ref = oracle.block_energy(qh, kh, scale, lay.B, block_rows=(r, r + 1))
         assert np.abs(E[h, r] - E_ref[0]).max() <= 5e-5
+
+
+# ---------------------------------------------------------------- CTA-pair kernel (order 3)
+@pytest.mark.parametrize("lay,heads", [(Layout(2, 9, 40, 128), 3), (Layout(21, 30, 52, 128), 6)])
+def test_pair_kernel_bitwise_equals_single_and_oracle(csa, lay, heads):
+    """The cta_group::2 kernel walks the union of two rows' lists; each row's arithmetic is
+    unchanged, so its output must equal the single-CTA kernel's bit for bit."""
+    rng = np.random.default_rng(heads)
+    masks = (rng.random((heads, lay.NB, lay.NB)) < 0.4).astype(np.uint8)
+    masks[:, np.arange(lay.NB), np.arange(lay.NB)] = 1
+    q, k, v = qkv(1, lay.N, heads, 128, seed=5, device="cuda")
+    rep = [heads - 1]
+    single, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=rep, anchor_k=5, order=2)
+    pair, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=rep, anchor_k=5, order=3)
+    assert torch.equal(single, pair)
+    for h, r in ((0, 0), (heads - 2, lay.NB - 1), (heads - 1, 1)):
+        rows = (r * 128, min((r + 1) * 128, lay.N))
+        ref, _ = oracle_head(lay, q, k, v, 0, h, mask=masks[h],
+                             rep_k=5 if h in rep else None, rows=rows)
+        assert_close(pair[0, rows[0]:rows[1], h].double().cpu().numpy(), ref, f"h{h} r{r}")

@@ -379,3 +379,29 @@ def test_work_list_is_sorted_permutation(orc):
     assert items == sorted(items)
     assert sorted((h, k, i) for _, h, k, i in items) == sorted(
         [(h, 0, r) for h in (0, 2, 3) for r in range(nb)] + [(1, 1, u) for u in range(nu)])
+
+
+def test_pair_work_list_covers_every_row_once(orc):
+    """Order 3: item p of a head stands for members (2p, 2p+1); cost = members' sum."""
+    rng = np.random.default_rng(8)
+    n, b, F, W = 250 * 3, 64, 2, 25        # N_B = 12 (even) -- and an odd case below
+    for n_, nb in ((n, 12), (250 * 3 - 64, 11)):
+        kinds = np.array([0, 1, 0], np.uint8)
+        ak = np.array([0, 3, 0], np.int32)
+        nnz = rng.integers(1, nb + 1, size=(3, nb)).astype(np.int32)
+        wl = orc.work_list(n_, b, F, W, kinds, ak, nnz, order=3)
+        nu = (F * 3 * W + 127) // 128
+        assert wl.size == 2 * ((nb + 1) // 2) + (nu + 1) // 2
+        covered = []
+        prev = None
+        for code in wl:
+            kind, h, p = int(code) >> 31, (int(code) >> 20) & 0x7FF, int(code) & 0xFFFFF
+            units = nu if kind else nb
+            members = [u for u in (2 * p, 2 * p + 1) if u < units]
+            cost = nb * len(members) if kind else int(sum(nnz[h, u] for u in members))
+            key = (h, -cost, p)
+            assert prev is None or key > prev        # head-major, cost desc, p asc
+            prev = key
+            covered += [(h, u) for u in members]
+        expect = [(h, u) for h in (0, 2) for u in range(nb)] + [(1, u) for u in range(nu)]
+        assert sorted(covered) == sorted(expect)

@@ -1,0 +1,59 @@
+"""Multi-process (world size 2, gloo, CPU) tests of the head-sharded exchange used by the
+multi-GPU path: sequence-sharded -> head-sharded -> back is the identity, each rank receives
+exactly its heads' full-sequence tensors, and a head-local operation commutes with the exchange
+(so per-head results cannot depend on the number of ranks)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2603_05503_b200 import ulysses
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, batch, results):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(3)
+        n, h, d = 12, 4, 8
+        x = torch.randn((batch, n, h, d), generator=g)       # identical on every rank
+        x_loc = ulysses.sequence_shard(x, world, rank)
+        xh = ulysses.scatter_heads(x_loc, world)
+        h0, h1 = ulysses.head_range(h, world, rank)
+        ok_scatter = torch.equal(xh, x[:, :, h0:h1])
+        back = ulysses.gather_heads(xh, world)
+        ok_roundtrip = torch.equal(back, x_loc)
+        # a head-local op (per-head scaling by the head index) commutes with the exchange
+        scale = torch.arange(h0, h1, dtype=x.dtype).view(1, 1, -1, 1) + 1
+        step = ulysses.make_layer_step(x_loc, x_loc, x_loc, world, lambda q, k, v: q * scale)
+        y_loc = step()
+        ref = (x * (torch.arange(h, dtype=x.dtype).view(1, 1, -1, 1) + 1))
+        ok_layer = torch.equal(y_loc, ulysses.sequence_shard(ref, world, rank))
+        results[rank] = (ok_scatter, ok_roundtrip, ok_layer)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("batch", [1, 2])
+def test_ulysses_exchange_gloo_world2(batch):
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker, args=(2, _free_port(), batch, results), nprocs=2, join=True)
+    assert dict(results) == {0: (True, True, True), 1: (True, True, True)}
+
+
+def test_head_range_and_shard_checks():
+    assert ulysses.head_range(40, 8, 3) == (15, 20)
+    with pytest.raises(ValueError):
+        ulysses.head_range(40, 3, 0)
+    with pytest.raises(ValueError):
+        ulysses.sequence_shard(torch.zeros(1, 10, 2, 2), 3, 0)
