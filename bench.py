@@ -358,10 +358,13 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
     # eps(t=25 of T=50) from Eq. eq:epsilon_schedule with A(N), host fp64
     eps = 0.796 + 1.41e-6 * lay.N + (0.99 - (0.796 + 1.41e-6 * lay.N)) * math.exp(-16 * 25 / 50)
     t_cal, _ = time_loop(lambda: csa.calib_accumulate(lay, q[:1], k[:1], eps, counts_c), 1, 1, stream)
-    ph["calib_accumulate_ms"] = round(t_cal, 3)
-    calib_exps = 2.0 * H * float(lay.N) ** 2
+    t_cal2, _ = time_loop(lambda: csa.calib_accumulate(lay, q[:1], k[:1], eps, counts_c,
+                                                       single_pass=False), 1, 1, stream)
+    ph["calib_accumulate_ms"] = round(t_cal, 3)             # single exponential pass (scratch)
+    ph["calib_accumulate_two_pass_ms"] = round(t_cal2, 3)   # LSE pass + E pass
+    calib_exps = 1.0 * H * float(lay.N) ** 2                 # one exp per score
     ph["calib_exp_per_s"] = calib_exps / (t_cal * 1e-3)
-    ph["calib_qk_tflops"] = round(2 * 2.0 * d * H * float(lay.N) ** 2 / (t_cal * 1e-3) / 1e12, 1)
+    ph["calib_qk_tflops"] = round(2.0 * d * H * float(lay.N) ** 2 / (t_cal * 1e-3) / 1e12, 1)
     cnt = torch.from_numpy((masks.astype(np.uint16) * np.uint16(64)).reshape(-1).view(np.int16)).to(dev).view(torch.uint16)
     sim = torch.tensor([1.0 if h in rep else 0.0 for h in range(H)], dtype=torch.float64, device=dev)
     torch.cuda.synchronize()

@@ -122,7 +122,11 @@ enum { CSA_WS_CALIB = 0, CSA_WS_COMPILE = 1, CSA_WS_WORK_LIST = 2, CSA_WS_ATTN =
  *   keep_count  uint16 [n_heads][N_B][N_B], accumulated in place
  *   energy_out  optional fp32 [n_heads][N_B][N_B] (the exact values the selection consumed)
  *   lse_out     optional fp32 [n_heads][N] (natural log; the values pass B used)
- * Workspace: csa_workspace_size(CSA_WS_CALIB, ...) bytes (may be 0 -> NULL allowed). */
+ * Workspace (device, 16-byte aligned, contents irrelevant): with lse_in == NULL and a buffer of
+ * at least csa_workspace_size(CSA_WS_CALIB, L, n_heads, head_dim) bytes, the kernel makes ONE
+ * exponential pass (per-(row, key block) partial sums kept there until the row LSE is known);
+ * NULL -> two passes (LSE, then E), same results up to fp32 rounding order.  Ignored when lse_in
+ * is given (one pass).  A non-NULL buffer that is too small -> CSA_ERR_INVALID_ARGUMENT. */
 CSA_API csa_status_t csa_calib_accumulate(csa_layout_t L, int32_t n_heads, int32_t head_dim,
                                   float softmax_scale, csa_tensor_t q, csa_tensor_t k,
                                   const float* lse_in, double eps, uint16_t* keep_count,

@@ -128,8 +128,10 @@ def default_scale(d: int) -> float:
 def calib_accumulate(lay: Layout, q: torch.Tensor, k: torch.Tensor, eps: float,
                      keep_count: torch.Tensor, lse_in: torch.Tensor | None = None,
                      energy_out: torch.Tensor | None = None, lse_out: torch.Tensor | None = None,
-                     scale: float | None = None, stream=None) -> None:
-    """csa_calib_accumulate: one prompt at one (t, l), all heads of q/k [1, N, H, d]."""
+                     scale: float | None = None, stream=None, single_pass: bool = True) -> None:
+    """csa_calib_accumulate: one prompt at one (t, l), all heads of q/k [1, N, H, d].
+    single_pass: hand the kernel its scratch workspace (one exponential pass when lse_in is
+    None); False -> the two-pass path."""
     _, n, heads, d = q.shape
     assert n == lay.N and keep_count.dtype == torch.uint16 and keep_count.is_contiguous()
     assert keep_count.numel() == heads * lay.NB * lay.NB
@@ -138,10 +140,28 @@ def calib_accumulate(lay: Layout, q: torch.Tensor, k: torch.Tensor, eps: float,
         if t is not None:
             assert t.dtype == torch.float32 and t.is_contiguous() and t.numel() == shape
     sc = default_scale(d) if scale is None else scale
+    ws, ws_bytes = None, 0
+    if single_pass and lse_in is None:
+        ws_bytes = lib().csa_workspace_size(0, _layout(lay), heads, d)
+        ws = _calib_workspace(q.device, ws_bytes)
     _check(lib().csa_calib_accumulate(_layout(lay), heads, d, sc, _tensor(q), _tensor(k),
                                       _ptr(lse_in), float(eps), _ptr(keep_count),
-                                      _ptr(energy_out), _ptr(lse_out), None, 0, _stream(stream)),
+                                      _ptr(energy_out), _ptr(lse_out), _ptr(ws), ws_bytes,
+                                      _stream(stream)),
            "csa_calib_accumulate")
+
+
+_CALIB_WS: dict = {}
+
+
+def _calib_workspace(device, nbytes: int) -> torch.Tensor:
+    """Cached scratch for the single-pass calibration (grown on demand, one per device)."""
+    key = str(device)
+    buf = _CALIB_WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
+        _CALIB_WS[key] = buf
+    return buf
 
 
 # ------------------------------------------------------------------------------- plan

@@ -142,10 +142,15 @@ csa_status_t csa_debug_trace(void* buf, int32_t mode) {
 }
 
 size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_t head_dim) {
-    (void)L;
-    (void)n_heads;
     (void)head_dim;
-    return which == CSA_WS_ATTN ? 256 : 0;  // attention: dynamic-scheduler counters
+    if (which == CSA_WS_ATTN) return 256;  // attention: dynamic-scheduler counters
+    if (which == CSA_WS_CALIB) {           // single-pass calibration: (t, m) row partials
+        if (check_layout(L, 0, 0) != CSA_OK || n_heads < 1) return 0;
+        DeviceInfo di;
+        if (device_info(&di) != CSA_OK) return 0;
+        return csa::calib_scratch_bytes(csa::make_geo(L), n_heads, di.sms);
+    }
+    return 0;
 }
 
 csa_status_t csa_calib_accumulate(csa_layout_t L, int32_t n_heads, int32_t head_dim,
@@ -153,8 +158,6 @@ csa_status_t csa_calib_accumulate(csa_layout_t L, int32_t n_heads, int32_t head_
                                   const float* lse_in, double eps, uint16_t* keep_count,
                                   float* energy_out, float* lse_out, void* workspace,
                                   size_t workspace_bytes, csa_stream_t stream) {
-    (void)workspace;
-    (void)workspace_bytes;
     csa_status_t st = check_layout(L, head_dim, n_heads);
     if (st != CSA_OK) return st;
     if (n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "n_heads must be >= 1");
@@ -176,6 +179,16 @@ csa_status_t csa_calib_accumulate(csa_layout_t L, int32_t n_heads, int32_t head_
     a.keep_count = keep_count;
     a.energy_out = energy_out;
     a.lse_out = lse_out;
+    a.scratch = nullptr;
+    if (workspace != nullptr && lse_in == nullptr) {
+        const size_t need = csa::calib_scratch_bytes(g, n_heads, di.sms);
+        if (workspace_bytes < need)
+            return fail(CSA_ERR_INVALID_ARGUMENT, "calibration workspace smaller than "
+                                                  "csa_workspace_size(CSA_WS_CALIB)");
+        if (reinterpret_cast<uintptr_t>(workspace) % 16 != 0)
+            return fail(CSA_ERR_INVALID_ARGUMENT, "workspace must be 16-byte aligned");
+        a.scratch = static_cast<float2*>(workspace);
+    }
     cudaError_t e = csa::launch_calib(a, head_dim, tq, tk, di.sms, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "calib launch");
     return ok();

@@ -2,48 +2,107 @@
 //
 // PAPER.md P:486-571 + P:643 ("custom CUDA kernel that operates at block granularity and
 // accumulates the required statistics without materializing the full attention matrix P"):
-//   a2  lse_i = log sum_j exp(scale q_i.k_j)                    (pass A; skipped if lse_in given)
-//   a3  E_{r,c} = (1/|I_r|) sum_{i in I_r} sum_{j in J_c} exp(s_ij - lse_i)   (pass B,
-//       Eq. eq:block_energy; divides by the actual |I_r| -- reading Q2)
+//   a2  lse_i = log sum_j exp(scale q_i.k_j)            (or taken from lse_in, the dense run's own)
+//   a3  E_{r,c} = (1/|I_r|) sum_{i in I_r} sum_{j in J_c} exp(s_ij - lse_i)   (Eq. eq:block_energy;
+//       divides by the actual |I_r| -- reading Q2)
 //   a4  shortest prefix of (E desc, c asc) whose fp64 sequential sum of the fp32 E values
 //       reaches eps(t) (Eq. eq:row_energy_constraint; readings Q4, Q5)
 //   a5  keep_count[h][r][c] += kept (numerator of Eq. eq:mask_mean)
-// One work item = one (head, query block) pair; the CTA owns the row, so no atomics anywhere and
+// One work item = one (head, query block); the CTA owns the row, so there are no atomics and
 // every reduction runs in a fixed order (bit-reproducible).
 //
-// Roles (persistent, one CTA per SM, 12 warps): warp 0 TMA producer (Q, then every K tile of
-// pass A and pass B), warp 1 MMA issuer (S_j = Q K_j^T into TMEM S[j&1]), warp 2 TMEM allocator,
-// warps 4-7 / 8-11 two row groups taking alternate tiles.  Exp-bound (N^2 exp per pass).
+// Passes over the N_B key tiles of an item (each tile: S = Q K^T by tcgen05 into TMEM):
+//   lse_in given      one pass: per-row sums of exp(s - lse) reduced to E_{r,c} tile by tile.
+//   scratch given     one pass: per (row, tile) the partial sum t_ic = sum_j 2^(s_ij*l2e - m_ic)
+//                     and the running max m_ic it was taken against go to global scratch; after the
+//                     pass lse is known and E_{r,c} = sum_i t_ic 2^(m_ic - lse2_i) / |I_r|.
+//   neither           two passes (online LSE, then E) -- twice the exponentials.
+// Roles (persistent, one CTA per SM, 12 warps): warp 0 TMA producer, warp 1 MMA issuer, warp 2
+// TMEM allocator, warps 4-7 / 8-11 two row groups taking alternate tiles.  Exp-bound: packed
+// f32x2 arithmetic and a polynomial exp2 for part of the elements offload the MUFU unit.
 #include <cstdint>
 
-#include "csa_internal.cuh"
-#include "tiles.cuh"
+#include "attn_common.cuh"
 
 namespace csa {
 namespace {
 
+using namespace attn;
+
 constexpr int kThreads = 384;
+constexpr int kCalibEmuPerOctet = 3;  // element pairs p with (p & 7) >= 8 - this -> exp2_poly5
 
 template <int BK, int D>
 struct CalibSmem {
     using C = TileCfg<BK, D>;
-    static constexpr int kBudget = 200 * 1024 - 2 * C::kQBytes - 2 * 2048 * 4 - 2048 * 8;
-    static constexpr int kSlots = kBudget / C::kKVBytes > 8 ? 8 : kBudget / C::kKVBytes;
-    static constexpr int kMaxBlocks1 = 2048;
+    // One Q buffer (the next item's Q waits for this item's last MMA: one bubble per N_B tiles);
+    // everything else not in the K ring is small, so the ring gets 4 slots of 128x128 bf16 --
+    // the pass streams K from L2 and needs that many loads in flight.
+    static constexpr int kFixed = C::kQBytes + 2048 * 4 + 4 * 2048 * 4 + 4096;
     static constexpr int kQOff = 0;
-    static constexpr int kKOff = 2 * C::kQBytes;
-    static constexpr int kERowOff = kKOff + kSlots * C::kKVBytes;          // float [2][2048]
-    static constexpr int kSortOff = kERowOff + 2 * kMaxBlocks1 * 4;         // u64 [2048]
-    static constexpr int kBarOff = kSortOff + 2048 * 8;
-    // q_full[2] q_empty[2] k_full[S] k_empty[S] s_full[2] s_empty[2]
+    static constexpr int kKOff = C::kQBytes;
+    static constexpr int kBudget = 232448 - kFixed;
+    static constexpr int kSlots = kBudget / C::kKVBytes > 8 ? 8 : kBudget / C::kKVBytes;
+    static constexpr int kERowOff = kKOff + kSlots * C::kKVBytes;  // float [2048]
+    // float [4][2048] per-quarter column partials (scratch E phase), then -- once the E row is
+    // complete -- u64 [2048] sort keys of the selection (a4): the two uses never overlap in time
+    static constexpr int kColOff = kERowOff + 2048 * 4;
+    static constexpr int kSortOff = kColOff;
+    static constexpr int kBarOff = kColOff + 4 * 2048 * 4;
+    // q_full[2] q_empty[2] (entry 0 used) k_full[S] k_empty[S] s_full[2] s_empty[2]
     static constexpr int kNumBars = 8 + 2 * kSlots;
-    static constexpr int kRowOff = kBarOff + kNumBars * 8;                  // m[2][128] l[2][128]
-    static constexpr int kPartOff = kRowOff + 4 * 128 * 4;                  // float [2][2][4]
-    static constexpr int kTmemPtrOff = kPartOff + 16 * 4;
+    static constexpr int kRowOff = kBarOff + kNumBars * 8;           // m[2][128] l[2][128]
+    static constexpr int kPartOff = kRowOff + 4 * 128 * 4;           // float [2][2][4]
+    static constexpr int kMiscOff = kPartOff + 16 * 4;               // int32 s_cnt
+    static constexpr int kTmemPtrOff = kMiscOff + 16;
     static constexpr int kBytes = kTmemPtrOff + 16;
-    static constexpr int kAlloc = kBytes;  // base is 1 KiB aligned (__align__ on the extern)
+    static constexpr int kAlloc = kBytes;
+    static_assert(kSlots >= 2, "K ring");
     static_assert(kAlloc <= 232448, "smem");
 };
+
+// 2^x for a pair of x on the FMA pipe with a degree-5 polynomial for 2^frac (relative
+// minimax fit on [0,1), max rel. error 1.7e-7 -- as accurate as ex2.approx, which the energies
+// need: unlike P in the attention kernel they are not rounded to bf16 afterwards).
+__device__ __forceinline__ uint64_t exp2_poly5(uint64_t x) {
+    // clamp at -126: the fit's p(0) = 0.99999994 < 1, so floor(x) = -127 would borrow out of
+    // the exponent field (0x3F7FFFFF - 0x3F800000 = NaN bits); at -126 the result is a
+    // denormal that the .ftz arithmetic downstream reads as 0 (masked keys hold -inf).
+    const float x0 = fmaxf(lo_f(x), -126.0f), x1 = fmaxf(hi_f(x), -126.0f);
+    const uint64_t xc = f2(x0, x1);
+    const uint64_t kRound = f2(12582912.0f, 12582912.0f);  // 2^23 + 2^22
+    const uint64_t rnd = fadd2_rm(xc, kRound);               // floor(x) in the low mantissa bits
+    const uint64_t frac = fsub2(xc, fsub2(rnd, kRound));     // in [0, 1)
+    uint64_t p = f2(0.0018775767f, 0.0018775767f);
+    p = ffma2(p, frac, f2(0.0089893406f, 0.0089893406f));
+    p = ffma2(p, frac, f2(0.055826318f, 0.055826318f));
+    p = ffma2(p, frac, f2(0.24015361f, 0.24015361f));
+    p = ffma2(p, frac, f2(0.69315308f, 0.69315308f));
+    p = ffma2(p, frac, f2(0.99999994f, 0.99999994f));
+    const uint32_t e0 = (uint32_t)rnd << 23, e1 = (uint32_t)(rnd >> 32) << 23;
+    return pk2((uint32_t)p + e0, (uint32_t)(p >> 32) + e1);
+}
+
+// sum of 2^(s*sl2 - m) over the BK columns of a row (masked columns hold -inf)
+template <int BK>
+__device__ __forceinline__ float exp_sum(const uint32_t (&r)[BK], float sl2, float m) {
+    const uint64_t sl2x2 = f2(sl2, sl2);
+    const uint64_t negm = f2(-m, -m);
+    uint64_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int x = 0; x < BK; x += 2) {
+        const uint64_t t = ffma2(pk2(r[x], r[x + 1]), sl2x2, negm);
+        uint64_t p;
+        if (((x / 2) & 7) >= 8 - kCalibEmuPerOctet) {
+            p = exp2_poly5(t);
+        } else {
+            p = f2(ex2_approx(lo_f(t)), ex2_approx(hi_f(t)));
+        }
+        acc[(x / 2) & 3] = fadd2(acc[(x / 2) & 3], p);
+    }
+    const uint64_t s2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+    return lo_f(s2) + hi_f(s2);
+}
 
 template <int BK, int D>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -53,7 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     using L = CalibSmem<BK, D>;
     constexpr int S = L::kSlots;
     extern __shared__ __align__(1024) uint8_t smem[];
-    if ((smem_u32(smem) & 1023u) != 0u) __trap();  // SWIZZLE_128B atoms need 1 KiB alignment
+    if ((smem_u32(smem) & 1023u) != 0u) __trap();
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
     uint64_t* q_full = bars + 0;
     uint64_t* q_empty = bars + 2;
@@ -61,17 +120,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* k_empty = bars + 4 + S;
     uint64_t* s_full = bars + 4 + 2 * S;
     uint64_t* s_empty = bars + 6 + 2 * S;
-    float* e_row = reinterpret_cast<float*>(smem + L::kERowOff);          // [2][2048]
-    uint64_t* keys = reinterpret_cast<uint64_t*>(smem + L::kSortOff);     // [2048]
+    float* e_row = reinterpret_cast<float*>(smem + L::kERowOff);        // [2048]
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem + L::kSortOff);   // [2048]
+    float* colp = reinterpret_cast<float*>(smem + L::kColOff);          // [4][2048]
     float* row_m = reinterpret_cast<float*>(smem + L::kRowOff);
     float* row_l = row_m + 256;
-    float* part = reinterpret_cast<float*>(smem + L::kPartOff);           // [grp][parity][4]
+    float* part = reinterpret_cast<float*>(smem + L::kPartOff);         // [grp][parity][4]
+    volatile int32_t* s_cnt = reinterpret_cast<int32_t*>(smem + L::kMiscOff);
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtrOff);
 
     const uint32_t warp = warp_id(), lane = lane_id();
     const Geo& g = a.g;
     const int32_t n_items = a.n_heads * g.NB;
-    const int32_t passes = a.lse_in ? 1 : 2;
+    const bool have_lse = a.lse_in != nullptr;
+    const bool use_scratch = !have_lse && a.scratch != nullptr;
+    const int32_t passes = (have_lse || use_scratch) ? 1 : 2;
     const int32_t tiles_per_item = passes * g.NB;
 
     if (threadIdx.x == 0) {
@@ -97,16 +160,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_ptr;
 
-    if (warp == 0) {
-        if (lane == 0) {
+    if (warp < 4) {
+        set_maxnreg_dec56();
+        if (warp == 0 && lane == 0) {
+            // ------------------------------------------------------------------- producer
             const uint64_t pol_q = policy_evict_first();
             const uint64_t pol_k = policy_evict_last();
             uint32_t ld = 0;
             int32_t local = 0;
             for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
                 const int32_t h = item / g.NB, r = item % g.NB;
-                const int qb = local & 1;
-                mbar_wait(q_empty + qb, ((local >> 1) & 1) ^ 1);
+                const int qb = 0;  // single Q buffer
+                mbar_wait(q_empty + qb, (local & 1) ^ 1);
                 mbar_arrive_expect_tx(q_full + qb, C::kBoxes * BK * 128);
                 tma_tile<D>(smem + L::kQOff + qb * C::kQBytes, C::kQBox, &tq, q_full + qb, h,
                             r * BK, 0, pol_q);
@@ -120,22 +185,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 h, c * BK, 0, pol_k);
                 }
             }
-        }
-        __syncwarp();
-    } else if (warp == 1) {
-        if (lane == 0) {
+        } else if (warp == 1 && lane == 0) {
+            // ---------------------------------------------------------------- MMA issuer
             uint32_t cons = 0;
-            uint32_t sused[2] = {0, 0};
+            uint32_t sused0 = 0, sused1 = 0;
             int32_t local = 0;
             const uint32_t q_base = smem_u32(smem + L::kQOff);
             const uint32_t k_base = smem_u32(smem + L::kKOff);
             for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
-                const int qb = local & 1;
-                mbar_wait(q_full + qb, (local >> 1) & 1);
+                const int qb = 0;
+                mbar_wait(q_full + qb, local & 1);
                 for (int32_t j = 0; j < tiles_per_item; ++j) {
                     const int grp = j & 1;
-                    mbar_wait(s_empty + grp, (sused[grp] & 1) ^ 1);
-                    ++sused[grp];
+                    uint32_t& sused = grp ? sused1 : sused0;
+                    mbar_wait(s_empty + grp, (sused & 1) ^ 1);
+                    ++sused;
                     const uint32_t slot = cons % S, ph = (cons / S) & 1;
                     ++cons;
                     mbar_wait(k_full + slot, ph);
@@ -149,60 +213,70 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         __syncwarp();
-    } else if (warp >= 4) {
+    } else {
+        set_maxnreg_inc224();
+        // ----------------------------------------------------------------- row groups
         const int grp = (warp - 4) >> 2;
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
+        const int gtid = threadIdx.x - 128;  // 0..255
         const uint32_t s_addr = tmem + ((uint32_t)(quarter * 32) << 16) + grp * BK;
         const float sl2 = a.scale_log2;
+        const int32_t tail_valid = g.N - (g.NB - 1) * BK;
+        float2* scr = use_scratch ? a.scratch + (int64_t)blockIdx.x * g.NB * 128 : nullptr;
         uint32_t scount = 0;
         int32_t local = 0;
         for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
             const int32_t h = item / g.NB, r = item % g.NB;
             const int32_t rows_valid = min(BK, g.N - r * BK);
             const bool row_ok = row < rows_valid;
-            float* erow = e_row + (local & 1) * 2048;
+            float* erow = e_row;
             float m_run = -INFINITY, l_run = 0.0f, lse2 = 0.0f;
-            // load the S row of tile j (group grp owns every other tile), then free S[grp]
-            auto load_s = [&](float (&s)[BK]) {
+            int32_t mine = 0;
+            // S row of this group's next tile into registers; frees S[grp] for the next MMA
+            auto load_s = [&](uint32_t (&s)[BK], int32_t c) {
                 mbar_wait(s_full + grp, scount & 1);
                 ++scount;
                 tc_fence_after();
-                uint32_t rr[32];
 #pragma unroll
                 for (int cc = 0; cc < BK; cc += 32) {
+                    uint32_t(&rr)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[cc]);
                     tmem_ld32(s_addr + cc, rr);
-                    tmem_ld_wait(rr);
-#pragma unroll
-                    for (int x = 0; x < 32; ++x) s[cc + x] = __uint_as_float(rr[x]);
                 }
+#pragma unroll
+                for (int cc = 0; cc < BK; cc += 32)
+                    tmem_ld_wait(*reinterpret_cast<uint32_t(*)[32]>(&s[cc]));
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(s_empty + grp);
+                if (c == g.NB - 1 && tail_valid < BK) {  // keys >= N do not exist (Q2)
+#pragma unroll
+                    for (int x = 0; x < BK; ++x)
+                        if (x >= tail_valid) s[x] = 0xff800000u;
+                }
             };
-            // ---------------- pass A: online row max / sum over all N keys (a2)
-            if (passes == 2) {
-                for (int32_t j = grp; j < g.NB; j += 2) {
-                    float s[BK];
-                    load_s(s);
-                    const int32_t valid = g.N - j * BK;
-                    float mx = -INFINITY;
-#pragma unroll
-                    for (int x = 0; x < BK; ++x)
-                        if (x < valid) mx = fmaxf(mx, s[x]);
-                    const float m_new = fmaxf(m_run, mx * sl2);
-                    float acc = 0.0f;
-#pragma unroll
-                    for (int x = 0; x < BK; ++x)
-                        if (x < valid) acc += ex2_approx(fmaf(s[x], sl2, -m_new));
-                    l_run = l_run * ex2_approx(m_run - m_new) + acc;
-                    m_run = m_new;
+            // ---------------- LSE (a2): two-pass pass A, or the scratch single pass
+            if (!have_lse) {
+                for (int32_t c = grp; c < g.NB; c += 2, ++mine) {
+                    uint32_t s[BK];
+                    load_s(s, c);
+                    const float mt = max_half<BK>(s) * sl2;
+                    float m_use = m_run;
+                    if (mine == 0 || mt > m_run + kRescaleThreshold) {  // lazy running max
+                        const float m_new = fmaxf(m_run, mt);
+                        if (mine > 0) l_run *= ex2_approx(m_run - m_new);
+                        m_run = m_new;
+                        m_use = m_new;
+                    }
+                    const float t = exp_sum<BK>(s, sl2, m_use);
+                    l_run += t;
+                    if (use_scratch) scr[(int64_t)c * 128 + row] = make_float2(t, m_use);
                 }
                 row_m[grp * 128 + row] = m_run;
                 row_l[grp * 128 + row] = l_run;
             }
             named_bar_sync(1, 256);
-            if (passes == 2) {
+            if (!have_lse) {
                 const float m0 = row_m[row], m1 = row_m[128 + row];
                 const float l0 = row_l[row], l1 = row_l[128 + row];
                 const float M = fmaxf(m0, m1);
@@ -215,28 +289,42 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (grp == 0 && a.lse_out != nullptr && row_ok)
                 a.lse_out[(int64_t)h * g.N + r * BK + row] = lse2 * 0.69314718055994531f;
-            // ---------------- pass B: block energies E_{r,c} (a3)
-            const int32_t first_b = passes == 2 ? g.NB : 0;
-            int32_t nb_mine = 0;
-            for (int32_t j = first_b + (((first_b & 1) != grp) ? 1 : 0); j < tiles_per_item;
-                 j += 2, ++nb_mine) {
-                float s[BK];
-                load_s(s);
-                const int32_t c = j - first_b;
-                const int32_t valid = g.N - c * BK;
-                float acc = 0.0f;
-                if (row_ok) {
+            if (use_scratch) {
+                // ---------------- E from the stored partials: column c of the [NB][128] matrix
+                // weighted by 2^(m_ic - lse2_i), reduced over this warp's 32 rows (fixed tree)
+                for (int32_t c = grp; c < g.NB; c += 2) {
+                    float w = 0.0f;
+                    if (row_ok) {
+                        const float2 tm = scr[(int64_t)c * 128 + row];
+                        w = tm.x * ex2_approx(tm.y - lse2);
+                    }
 #pragma unroll
-                    for (int x = 0; x < BK; ++x)
-                        if (x < valid) acc += ex2_approx(fmaf(s[x], sl2, -lse2));
+                    for (int off = 16; off > 0; off >>= 1) w += __shfl_xor_sync(0xffffffffu, w, off);
+                    if (lane == 0) colp[quarter * 2048 + c] = w;
                 }
+                named_bar_sync(1, 256);
+                for (int32_t c = gtid; c < g.NB; c += 256)
+                    erow[c] = (((colp[c] + colp[2048 + c]) + colp[4096 + c]) + colp[6144 + c]) /
+                              (float)rows_valid;
+            } else {
+                // ---------------- E tile by tile against the known lse (a3)
+                const int32_t first_b = passes == 2 ? g.NB : 0;
+                int32_t nb_mine = 0;
+                for (int32_t j = first_b + (((first_b & 1) != grp) ? 1 : 0); j < tiles_per_item;
+                     j += 2, ++nb_mine) {
+                    const int32_t c = j - first_b;
+                    uint32_t s[BK];
+                    load_s(s, c);
+                    float acc = row_ok ? exp_sum<BK>(s, sl2, lse2) : 0.0f;
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-                float* pp = part + (grp * 2 + (nb_mine & 1)) * 4;
-                if (lane == 0) pp[quarter] = acc;
-                named_bar_sync(2 + grp, 128);
-                if (quarter == 0 && lane == 0)
-                    erow[c] = (((pp[0] + pp[1]) + pp[2]) + pp[3]) / (float)rows_valid;
+                    for (int off = 16; off > 0; off >>= 1)
+                        acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                    float* pp = part + (grp * 2 + (nb_mine & 1)) * 4;
+                    if (lane == 0) pp[quarter] = acc;
+                    named_bar_sync(2 + grp, 128);
+                    if (quarter == 0 && lane == 0)
+                        erow[c] = (((pp[0] + pp[1]) + pp[2]) + pp[3]) / (float)rows_valid;
+                }
             }
             // ---------------------------------------------------- selection (group 0)
             named_bar_sync(1, 256);  // E row complete
@@ -268,7 +356,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         named_bar_sync(3, 128);
                     }
                 }
-                __shared__ int32_t s_cnt;
                 if (t == 0) {
                     double acc = 0.0;
                     int32_t cnt = 0;
@@ -278,10 +365,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         acc = __dadd_rn(acc, (double)erow[c]);
                         if (acc >= a.eps) break;
                     }
-                    s_cnt = cnt;
+                    *s_cnt = cnt;
                 }
                 named_bar_sync(3, 128);
-                const int32_t cnt = s_cnt;
+                const int32_t cnt = *s_cnt;
                 uint16_t* kc = a.keep_count + ((int64_t)h * g.NB + r) * g.NB;
                 for (int32_t x = t; x < cnt; x += 128) {
                     const uint32_t c = (uint32_t)(keys[x] & 0xFFFFFFFFu);
@@ -313,10 +400,18 @@ cudaError_t launch_t(const CalibArgs& a, const CUtensorMap& tq, const CUtensorMa
 
 }  // namespace
 
+static int calib_grid(const Geo& g, int32_t n_heads, int num_sms) {
+    const int64_t items = (int64_t)n_heads * g.NB;
+    return (int)(items < num_sms ? items : num_sms);
+}
+
+size_t calib_scratch_bytes(const Geo& g, int32_t n_heads, int num_sms) {
+    return (size_t)calib_grid(g, n_heads, num_sms) * g.NB * 128 * sizeof(float2);
+}
+
 cudaError_t launch_calib(const CalibArgs& a, int head_dim, const CUtensorMap& tq,
                          const CUtensorMap& tk, int num_sms, cudaStream_t s) {
-    const int64_t items = (int64_t)a.n_heads * a.g.NB;
-    const int grid = (int)(items < num_sms ? items : num_sms);
+    const int grid = calib_grid(a.g, a.n_heads, num_sms);
     if (a.g.B == 128 && head_dim == 128) return launch_t<128, 128>(a, tq, tk, grid, s);
     if (a.g.B == 128 && head_dim == 64) return launch_t<128, 64>(a, tq, tk, grid, s);
     if (a.g.B == 64 && head_dim == 128) return launch_t<64, 128>(a, tq, tk, grid, s);

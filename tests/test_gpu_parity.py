@@ -256,7 +256,8 @@ def test_attention_full_size_sampled(csa, name):
 # ---------------------------------------------------------------- a2-a5 calibration
 @pytest.mark.parametrize("lay,heads,d", [(Layout(2, 5, 25, 64), 2, 64), (Layout(4, 8, 8, 64), 1, 64),
                                          (Layout(2, 9, 40, 128), 2, 128)])
-def test_calibration_against_oracle(csa, lay, heads, d):
+@pytest.mark.parametrize("single_pass", [True, False])
+def test_calibration_against_oracle(csa, lay, heads, d, single_pass):
     q, k, _ = inputs.structured_qk(lay, heads, d, head_seed=1, prompt_seed=2, alpha=1.0,
                                    device="cuda")
     nb = lay.NB
@@ -268,7 +269,8 @@ def test_calibration_against_oracle(csa, lay, heads, d):
     scale = 1.0 / np.sqrt(d)
     for prompt in range(3):  # accumulate over prompts: integer counts exact
         q, k, _ = inputs.structured_qk(lay, heads, d, 1, prompt, alpha=1.0, device="cuda")
-        csa.calib_accumulate(lay, q, k, eps, counts, energy_out=energy, lse_out=lse_out)
+        csa.calib_accumulate(lay, q, k, eps, counts, energy_out=energy, lse_out=lse_out,
+                             single_pass=single_pass)
         torch.cuda.synchronize()
         E = energy.view(heads, nb, nb).double().cpu().numpy()
         lg = lse_out.view(heads, lay.N).double().cpu().numpy()
@@ -319,9 +321,11 @@ def test_calibration_wan480_sampled(csa):
 
 # ---------------------------------------------------------------- CTA-pair kernel (order 3)
 @pytest.mark.parametrize("lay,heads", [(Layout(2, 9, 40, 128), 3), (Layout(21, 30, 52, 128), 6)])
-def test_pair_kernel_bitwise_equals_single_and_oracle(csa, lay, heads):
-    """The cta_group::2 kernel walks the union of two rows' lists; each row's arithmetic is
-    unchanged, so its output must equal the single-CTA kernel's bit for bit."""
+def test_pair_kernel_matches_single_and_oracle(csa, lay, heads):
+    """The cta_group::2 kernel walks the union of two rows' lists (P = 0 for the other row's
+    keys).  Its softmax offloads a different share of exponentials to the polynomial than the
+    production kernel, so the two agree to bf16 rounding, not bit for bit; both meet the oracle
+    tolerance."""
     rng = np.random.default_rng(heads)
     masks = (rng.random((heads, lay.NB, lay.NB)) < 0.4).astype(np.uint8)
     masks[:, np.arange(lay.NB), np.arange(lay.NB)] = 1
@@ -329,9 +333,10 @@ def test_pair_kernel_bitwise_equals_single_and_oracle(csa, lay, heads):
     rep = [heads - 1]
     single, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=rep, anchor_k=5, order=2)
     pair, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=rep, anchor_k=5, order=3)
-    assert torch.equal(single, pair)
+    assert (single.float() - pair.float()).abs().max().item() <= 8e-3
     for h, r in ((0, 0), (heads - 2, lay.NB - 1), (heads - 1, 1)):
         rows = (r * 128, min((r + 1) * 128, lay.N))
         ref, _ = oracle_head(lay, q, k, v, 0, h, mask=masks[h],
                              rep_k=5 if h in rep else None, rows=rows)
         assert_close(pair[0, rows[0]:rows[1], h].double().cpu().numpy(), ref, f"h{h} r{r}")
+        assert_close(single[0, rows[0]:rows[1], h].double().cpu().numpy(), ref, f"h{h} r{r}")
