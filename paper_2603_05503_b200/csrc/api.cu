@@ -137,6 +137,7 @@ const char* csa_version(void) { return "csa-b200 0.1 (sm_100a)"; }
 csa_status_t csa_debug_trace(void* buf, int32_t mode) {
     cudaError_t e = csa::set_attn_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_attn2_trace(buf, mode);
+    if (e == cudaSuccess) e = csa::set_calib_trace(buf, mode);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyToSymbol");
     return ok();
 }

@@ -29,30 +29,37 @@ namespace {
 
 using namespace attn;
 
+static __device__ unsigned long long* g_trace;  // csa_debug_trace (CTA 0, first item)
+static __device__ int g_debug_mode;  // csa_debug_trace mode: 11 skip softmax math, 12 also skip ld
+
 constexpr int kThreads = 384;
 constexpr int kCalibEmuPerOctet = 3;  // element pairs p with (p & 7) >= 8 - this -> exp2_poly5
 
 template <int BK, int D>
 struct CalibSmem {
     using C = TileCfg<BK, D>;
+    // BK = 128: Q lives in TMEM (tcgen05.cp from the TMA'd tile) and S = Q K^T runs as a TS
+    // MMA reading only K from shared memory -- measured 74 vs 107 cycles per 128x128x16
+    // dispatch for the SS form (scripts/mma_bench.cu); S is then single-buffered per group
+    // (TMEM: S[2] 256 + Q 64 columns).  BK = 64 (M = 64) keeps the SS form, S double-buffered.
+    static constexpr bool kQT = BK == 128;
+    static constexpr int kSBufs = kQT ? 1 : 2;
+    static constexpr uint32_t kQCol = 2 * kSBufs * BK;
     // One Q buffer (the next item's Q waits for this item's last MMA: one bubble per N_B tiles);
     // everything else not in the K ring is small, so the ring gets 4 slots of 128x128 bf16 --
     // the pass streams K from L2 and needs that many loads in flight.
-    static constexpr int kFixed = C::kQBytes + 2048 * 4 + 4 * 2048 * 4 + 4096;
+    static constexpr int kFixed = C::kQBytes + 2048 * 4 + 2048 * 8 + 4096;
     static constexpr int kQOff = 0;
     static constexpr int kKOff = C::kQBytes;
     static constexpr int kBudget = 232448 - kFixed;
     static constexpr int kSlots = kBudget / C::kKVBytes > 8 ? 8 : kBudget / C::kKVBytes;
     static constexpr int kERowOff = kKOff + kSlots * C::kKVBytes;  // float [2048]
-    // float [4][2048] per-quarter column partials (scratch E phase), then -- once the E row is
-    // complete -- u64 [2048] sort keys of the selection (a4): the two uses never overlap in time
-    static constexpr int kColOff = kERowOff + 2048 * 4;
-    static constexpr int kSortOff = kColOff;
-    static constexpr int kBarOff = kColOff + 4 * 2048 * 4;
-    // q_full[2] q_empty[2] (entry 0 used) k_full[S] k_empty[S] s_full[2] s_empty[2]
-    static constexpr int kNumBars = 8 + 2 * kSlots;
-    static constexpr int kRowOff = kBarOff + kNumBars * 8;           // m[2][128] l[2][128]
-    static constexpr int kPartOff = kRowOff + 4 * 128 * 4;           // float [2][2][4]
+    static constexpr int kSortOff = kERowOff + 2048 * 4;              // u64 [2048] (a4 sort)
+    static constexpr int kBarOff = kSortOff + 2048 * 8;
+    // q_full[2] q_empty[2] (entry 0 used) k_full[S] k_empty[S] s_full[2][2] s_empty[2][2]
+    static constexpr int kNumBars = 12 + 2 * kSlots;
+    static constexpr int kRowOff = kBarOff + kNumBars * 8;  // m[2][128] l[2][128] lse2[128]
+    static constexpr int kPartOff = kRowOff + 5 * 128 * 4;           // float [2][2][4]
     static constexpr int kMiscOff = kPartOff + 16 * 4;               // int32 s_cnt
     static constexpr int kTmemPtrOff = kMiscOff + 16;
     static constexpr int kBytes = kTmemPtrOff + 16;
@@ -118,13 +125,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* q_empty = bars + 2;
     uint64_t* k_full = bars + 4;
     uint64_t* k_empty = bars + 4 + S;
-    uint64_t* s_full = bars + 4 + 2 * S;
-    uint64_t* s_empty = bars + 6 + 2 * S;
+    uint64_t* s_full = bars + 4 + 2 * S;   // [grp][buf]
+    uint64_t* s_empty = bars + 8 + 2 * S;  // [grp][buf]
     float* e_row = reinterpret_cast<float*>(smem + L::kERowOff);        // [2048]
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem + L::kSortOff);   // [2048]
-    float* colp = reinterpret_cast<float*>(smem + L::kColOff);          // [4][2048]
     float* row_m = reinterpret_cast<float*>(smem + L::kRowOff);
     float* row_l = row_m + 256;
+    float* row_lse2 = row_m + 512;
     float* part = reinterpret_cast<float*>(smem + L::kPartOff);         // [grp][parity][4]
     volatile int32_t* s_cnt = reinterpret_cast<int32_t*>(smem + L::kMiscOff);
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtrOff);
@@ -136,11 +143,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool use_scratch = !have_lse && a.scratch != nullptr;
     const int32_t passes = (have_lse || use_scratch) ? 1 : 2;
     const int32_t tiles_per_item = passes * g.NB;
+    const int dbg = g_debug_mode;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(q_full + i, 1);
             mbar_init(q_empty + i, 1);
+        }
+        for (int i = 0; i < 4; ++i) {
             mbar_init(s_full + i, 1);
             mbar_init(s_empty + i, 4);
         }
@@ -150,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc<256>(tmem_ptr);
+    if (warp == 2) tmem_alloc<512>(tmem_ptr);  // S[grp][buf] fp32, then Q (kQT)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tq);
         tma_prefetch(&tk);
@@ -162,8 +172,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp < 4) {
         set_maxnreg_dec56();
-        if (warp == 0 && lane == 0) {
+        if (warp == 0) {
             // ------------------------------------------------------------------- producer
+            // (whole warp in the loop, one elected lane issues -- see the MMA issuer below)
             const uint64_t pol_q = policy_evict_first();
             const uint64_t pol_k = policy_evict_last();
             uint32_t ld = 0;
@@ -172,21 +183,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int32_t h = item / g.NB, r = item % g.NB;
                 const int qb = 0;  // single Q buffer
                 mbar_wait(q_empty + qb, (local & 1) ^ 1);
-                mbar_arrive_expect_tx(q_full + qb, C::kBoxes * BK * 128);
-                tma_tile<D>(smem + L::kQOff + qb * C::kQBytes, C::kQBox, &tq, q_full + qb, h,
-                            r * BK, 0, pol_q);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(q_full + qb, C::kBoxes * BK * 128);
+                    tma_tile<D>(smem + L::kQOff + qb * C::kQBytes, C::kQBox, &tq, q_full + qb, h,
+                                r * BK, 0, pol_q);
+                }
+                __syncwarp();
                 for (int32_t j = 0; j < tiles_per_item; ++j) {
                     const int32_t c = j % g.NB;
                     const uint32_t slot = ld % S, ph = (ld / S) & 1;
                     ++ld;
+                    if (local == 0 && lane == 0) CSA_TRACE(3, j, 0);
                     mbar_wait(k_empty + slot, ph ^ 1);
-                    mbar_arrive_expect_tx(k_full + slot, C::kKVBytes);
-                    tma_tile<D>(smem + L::kKOff + slot * C::kKVBytes, C::kKBox, &tk, k_full + slot,
-                                h, c * BK, 0, pol_k);
+                    if (local == 0 && lane == 0) CSA_TRACE(3, j, 1);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(k_full + slot, C::kKVBytes);
+                        tma_tile<D>(smem + L::kKOff + slot * C::kKVBytes, C::kKBox, &tk,
+                                    k_full + slot, h, c * BK, 0, pol_k);
+                    }
+                    __syncwarp();
                 }
             }
-        } else if (warp == 1 && lane == 0) {
+        } else if (warp == 1) {
             // ---------------------------------------------------------------- MMA issuer
+            // The whole warp runs the loop (warp-uniform values stay in uniform registers);
+            // one elected lane issues.  A single-lane branch makes ptxas wrap every
+            // tcgen05.mma in an ELECT / R2UR.BROADCAST / BRA.U.ANY loop (~16 instructions of
+            // dependent latency each), which capped the issue rate below the tensor pipe's.
             uint32_t cons = 0;
             uint32_t sused0 = 0, sused1 = 0;
             int32_t local = 0;
@@ -195,20 +218,55 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
                 const int qb = 0;
                 mbar_wait(q_full + qb, local & 1);
+                if constexpr (L::kQT) {
+                    // Q tile -> TMEM columns [kQCol, kQCol + D/2): one 128x256b copy per K = 16
+                    // slice.  In-order with the MMAs: the previous item's MMAs have read the old
+                    // Q before this copy lands; the smem buffer is free once the copy is done.
+                    tc_fence_after();
+                    if (elect_one()) {
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk)
+                            tmem_cp_128x256b(tmem + L::kQCol + kk * 8,
+                                             umma_desc_sw128(q_base + qb * C::kQBytes +
+                                                                 (kk >> 2) * C::kQBox + (kk & 3) * 32,
+                                                             16, 1024));
+                        mma_commit(q_empty + qb);
+                    }
+                    __syncwarp();
+                }
                 for (int32_t j = 0; j < tiles_per_item; ++j) {
+                    // tile j -> group j & 1 (S single- or double-buffered per group)
                     const int grp = j & 1;
                     uint32_t& sused = grp ? sused1 : sused0;
-                    mbar_wait(s_empty + grp, (sused & 1) ^ 1);
+                    const uint32_t sb = grp * L::kSBufs + (sused % L::kSBufs);
+                    if (local == 0 && lane == 0) CSA_TRACE(2, j, 0);
+                    mbar_wait(s_empty + sb, ((sused / L::kSBufs) & 1) ^ 1);
+                    if (local == 0 && lane == 0) CSA_TRACE(2, j, 1);
                     ++sused;
                     const uint32_t slot = cons % S, ph = (cons / S) & 1;
                     ++cons;
                     mbar_wait(k_full + slot, ph);
+                    if (local == 0 && lane == 0) CSA_TRACE(2, j, 2);
                     tc_fence_after();
-                    issue_qk<BK, D>(tmem + grp * BK, q_base + qb * C::kQBytes,
-                                    k_base + slot * C::kKVBytes);
-                    mma_commit(s_full + grp);
-                    mma_commit(k_empty + slot);
-                    if (j == tiles_per_item - 1) mma_commit(q_empty + qb);
+                    if (elect_one()) {
+                        if constexpr (L::kQT) {
+#pragma unroll
+                            for (int kk = 0; kk < D / 16; ++kk) {
+                                const uint64_t b = umma_desc_sw128(
+                                    k_base + slot * C::kKVBytes + (kk >> 2) * C::kKBox +
+                                        (kk & 3) * 32, 16, 1024);
+                                mma_ts(tmem + sb * BK, tmem + L::kQCol + kk * 8, b, C::kIdescQK,
+                                       kk > 0 ? 1u : 0u);
+                            }
+                        } else {
+                            issue_qk<BK, D>(tmem + sb * BK, q_base + qb * C::kQBytes,
+                                            k_base + slot * C::kKVBytes);
+                        }
+                        mma_commit(s_full + sb);
+                        mma_commit(k_empty + slot);
+                        if (!L::kQT && j == tiles_per_item - 1) mma_commit(q_empty + qb);
+                    }
+                    __syncwarp();
                 }
             }
         }
@@ -220,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const int gtid = threadIdx.x - 128;  // 0..255
-        const uint32_t s_addr = tmem + ((uint32_t)(quarter * 32) << 16) + grp * BK;
+        const uint32_t s_lane = tmem + ((uint32_t)(quarter * 32) << 16);
         const float sl2 = a.scale_log2;
         const int32_t tail_valid = g.N - (g.NB - 1) * BK;
         float2* scr = use_scratch ? a.scratch + (int64_t)blockIdx.x * g.NB * 128 : nullptr;
@@ -235,9 +293,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             int32_t mine = 0;
             // S row of this group's next tile into registers; frees S[grp] for the next MMA
             auto load_s = [&](uint32_t (&s)[BK], int32_t c) {
-                mbar_wait(s_full + grp, scount & 1);
+                const uint32_t sb = grp * L::kSBufs + (scount % L::kSBufs);
+                const bool tr = local == 0 && (warp & 3) == 0 && lane == 0;
+                if (tr) CSA_TRACE(grp, c, 0);
+                mbar_wait(s_full + sb, (scount / L::kSBufs) & 1);
+                if (tr) CSA_TRACE(grp, c, 1);
                 ++scount;
                 tc_fence_after();
+                const uint32_t s_addr = s_lane + sb * BK;
 #pragma unroll
                 for (int cc = 0; cc < BK; cc += 32) {
                     uint32_t(&rr)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[cc]);
@@ -248,7 +311,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_ld_wait(*reinterpret_cast<uint32_t(*)[32]>(&s[cc]));
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(s_empty + grp);
+                if (lane == 0) mbar_arrive(s_empty + sb);
+                if (tr) CSA_TRACE(grp, c, 2);
                 if (c == g.NB - 1 && tail_valid < BK) {  // keys >= N do not exist (Q2)
 #pragma unroll
                     for (int x = 0; x < BK; ++x)
@@ -260,6 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int32_t c = grp; c < g.NB; c += 2, ++mine) {
                     uint32_t s[BK];
                     load_s(s, c);
+                    if (dbg >= 11) continue;  // debug: pipeline without the softmax math
                     const float mt = max_half<BK>(s) * sl2;
                     float m_use = m_run;
                     if (mine == 0 || mt > m_run + kRescaleThreshold) {  // lazy running max
@@ -271,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float t = exp_sum<BK>(s, sl2, m_use);
                     l_run += t;
                     if (use_scratch) scr[(int64_t)c * 128 + row] = make_float2(t, m_use);
+                    if (local == 0 && (warp & 3) == 0 && lane == 0) CSA_TRACE(grp, c, 3);
                 }
                 row_m[grp * 128 + row] = m_run;
                 row_l[grp * 128 + row] = l_run;
@@ -291,21 +357,46 @@ __global__ void __launch_bounds__(kThreads, 1)
                 a.lse_out[(int64_t)h * g.N + r * BK + row] = lse2 * 0.69314718055994531f;
             if (use_scratch) {
                 // ---------------- E from the stored partials: column c of the [NB][128] matrix
-                // weighted by 2^(m_ic - lse2_i), reduced over this warp's 32 rows (fixed tree)
-                for (int32_t c = grp; c < g.NB; c += 2) {
-                    float w = 0.0f;
-                    if (row_ok) {
-                        const float2 tm = scr[(int64_t)c * 128 + row];
-                        w = tm.x * ex2_approx(tm.y - lse2);
+                // weighted by 2^(m_ic - lse2_i) and summed over the valid rows.  Warp w (of 8)
+                // takes columns c = w mod 8, four at a time; lane l holds rows l, l+32, l+64,
+                // l+96 (coalesced 256 B loads, 16 in flight), then a fixed butterfly.
+                if (grp == 0) row_lse2[row] = lse2;
+                named_bar_sync(1, 256);
+                const int w8 = gtid >> 5;
+                float lr[4];
+                bool okr[4];
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    okr[q4] = lane + 32 * q4 < rows_valid;
+                    lr[q4] = okr[q4] ? row_lse2[lane + 32 * q4] : 0.0f;  // no NaN from dead rows
+                }
+                for (int32_t c0 = w8; c0 < g.NB; c0 += 32) {
+                    float v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int32_t c = c0 + 8 * u;
+                        float2 tm[4];
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4)
+                            tm[q4] = (c < g.NB && okr[q4])
+                                         ? scr[(int64_t)c * 128 + lane + 32 * q4]
+                                         : make_float2(0.0f, 0.0f);
+                        float acc = 0.0f;
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4)
+                            acc = fmaf(tm[q4].x, ex2_approx(tm[q4].y - lr[q4]), acc);
+                        v[u] = acc;
                     }
 #pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) w += __shfl_xor_sync(0xffffffffu, w, off);
-                    if (lane == 0) colp[quarter * 2048 + c] = w;
+                    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) v[u] += __shfl_xor_sync(0xffffffffu, v[u], off);
+                    if (lane == 0) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (c0 + 8 * u < g.NB) erow[c0 + 8 * u] = v[u] / (float)rows_valid;
+                    }
                 }
-                named_bar_sync(1, 256);
-                for (int32_t c = gtid; c < g.NB; c += 256)
-                    erow[c] = (((colp[c] + colp[2048 + c]) + colp[4096 + c]) + colp[6144 + c]) /
-                              (float)rows_valid;
             } else {
                 // ---------------- E tile by tile against the known lse (a3)
                 const int32_t first_b = passes == 2 ? g.NB : 0;
@@ -383,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<256>(tmem);
+        tmem_dealloc<512>(tmem);
     }
 }
 
@@ -407,6 +498,13 @@ static int calib_grid(const Geo& g, int32_t n_heads, int num_sms) {
 
 size_t calib_scratch_bytes(const Geo& g, int32_t n_heads, int num_sms) {
     return (size_t)calib_grid(g, n_heads, num_sms) * g.NB * 128 * sizeof(float2);
+}
+
+cudaError_t set_calib_trace(void* buf, int mode) {
+    unsigned long long* p = static_cast<unsigned long long*>(buf);
+    cudaError_t e = cudaMemcpyToSymbol(g_trace, &p, sizeof(p));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyToSymbol(g_debug_mode, &mode, sizeof(mode));
 }
 
 cudaError_t launch_calib(const CalibArgs& a, int head_dim, const CUtensorMap& tq,

@@ -78,6 +78,7 @@ struct CalibArgs {
     float2* scratch;  // [grid][N_B][128] (t, m) partials; nullptr -> two passes (or lse_in)
 };
 size_t calib_scratch_bytes(const Geo& g, int32_t n_heads, int num_sms);
+cudaError_t set_calib_trace(void* buf, int mode);
 cudaError_t launch_calib(const CalibArgs& a, int head_dim, const CUtensorMap& tq,
                          const CUtensorMap& tk, int num_sms, cudaStream_t s);
 

@@ -128,6 +128,13 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Copy 128 rows x 256 bits (16 bf16 per row) from shared memory, described like an MMA operand
+// (smem matrix descriptor), into TMEM lanes 0..127, 8 columns from taddr.  Executes in issue
+// order with this thread's tcgen05.mma, so an MMA issued after it may read the copy as its A
+// operand (the K = 16 slice of a K-major tile lands exactly where a TS MMA expects it).
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
 // Arrive on an mbarrier once every previously issued tcgen05 op of this thread has completed.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile(

@@ -1,6 +1,11 @@
 """Debug: calibration LSE / E errors vs the oracle for the single-pass, two-pass and lse_in modes."""
+import os
+import sys
+
 import numpy as np
 import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import oracle
 from paper_2603_05503_b200 import csa, inputs
