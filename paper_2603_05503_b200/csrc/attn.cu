@@ -288,80 +288,93 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(q_full + qb);
             }
-            // K/V tiles in MMA consumption order: K0, (K1, V0), (K2, V1), ..., V_{n-1}
-            if (lane == 0) {
-                for (int32_t step = 0; step <= tl.n; ++step) {
-                    for (int kv = 0; kv < 2; ++kv) {
-                        int32_t j;
-                        if (kv == 0) {
-                            if (step >= tl.n) continue;
-                            j = step;
-                        } else {
-                            if (step == 0) continue;
-                            j = step - 1;
-                        }
-                        const uint32_t slot = ld % S, ph = (ld / S) & 1;
-                        ++ld;
-                        mbar_wait(kv_empty + slot, ph ^ 1);
+            // K/V tiles in MMA consumption order: K0, (K1, V0), (K2, V1), ..., V_{n-1}.  The
+            // whole warp walks the list (warp-uniform values live in uniform registers); one
+            // elected lane issues -- a lane-0-only loop makes ptxas wrap each TMA in an
+            // ELECT / R2UR / BRA.U.ANY loop.
+            for (int32_t step = 0; step <= tl.n; ++step) {
+                for (int kv = 0; kv < 2; ++kv) {
+                    int32_t j;
+                    if (kv == 0) {
+                        if (step >= tl.n) continue;
+                        j = step;
+                    } else {
+                        if (step == 0) continue;
+                        j = step - 1;
+                    }
+                    const uint32_t slot = ld % S, ph = (ld / S) & 1;
+                    ++ld;
+                    const int32_t c = tl.at(j);
+                    mbar_wait(kv_empty + slot, ph ^ 1);
+                    if (elect_one()) {
                         uint8_t* dst = smem + L::kKVOff + slot * C::kKVBytes;
                         mbar_arrive_expect_tx(kv_full + slot, C::kKVBytes);
                         tma_tile<D>(dst, C::kKBox, kv == 0 ? &tk : &tv, kv_full + slot, it.h,
-                                    tl.at(j) * BK, it.b, pol_kv);
+                                    c * BK, it.b, pol_kv);
                     }
+                    __syncwarp();
                 }
             }
-            __syncwarp();
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            uint32_t cons = 0;            // K/V ring position consumed
-            uint32_t pcount[2] = {0, 0};  // p_full completions waited, per group
-            const uint32_t q_base = smem_u32(smem + L::kQOff);
-            const uint32_t kv_base = smem_u32(smem + L::kKVOff);
-            for (int32_t local = 0;; ++local) {
-                const int32_t item = next_item(local, false);
-                if (item < 0) break;
-                const Item it = decode_item(a, item);
-                const TileList tl = tile_list(a, it);
-                const int qb = local & 1;
-                mbar_wait(q_full + qb, (local >> 1) & 1);
-                const uint32_t q_smem = q_base + qb * C::kQBytes;
-                if (tl.n == 0) {  // corrupt plan (empty MASK row): release Q, no tiles
+        // Whole warp in the loop, one elected lane issues (see the producer above): the
+        // lane-0-only form cost ~16 dependent instructions per tcgen05.mma.
+        uint32_t cons = 0;            // K/V ring position consumed
+        uint32_t pcount[2] = {0, 0};  // p_full completions waited, per group
+        const uint32_t q_base = smem_u32(smem + L::kQOff);
+        const uint32_t kv_base = smem_u32(smem + L::kKVOff);
+        for (int32_t local = 0;; ++local) {
+            const int32_t item = next_item(local, true);
+            if (item < 0) break;
+            const Item it = decode_item(a, item);
+            const TileList tl = tile_list(a, it);
+            const int qb = local & 1;
+            mbar_wait(q_full + qb, (local >> 1) & 1);
+            const uint32_t q_smem = q_base + qb * C::kQBytes;
+            if (tl.n == 0) {  // corrupt plan (empty MASK row): release Q, no tiles
+                if (elect_one()) {
                     mma_commit(q_empty + qb);
                     mma_commit(o_full);
-                    continue;
                 }
-                auto do_pv = [&](int32_t t) {
-                    const int grp = t & 1;
-                    mbar_wait(p_full + grp, pcount[grp] & 1);
-                    ++pcount[grp];
-                    if (t == 0) mbar_wait(o_empty, (local & 1) ^ 1);  // epilogue of last item
-                    const uint32_t slot = cons % S, ph = (cons / S) & 1;
-                    ++cons;
-                    mbar_wait(kv_full + slot, ph);
-                    tc_fence_after();
+                __syncwarp();
+                continue;
+            }
+            auto do_pv = [&](int32_t t) {
+                const int grp = t & 1;
+                mbar_wait(p_full + grp, pcount[grp] & 1);
+                ++pcount[grp];
+                if (t == 0) mbar_wait(o_empty, (local & 1) ^ 1);  // epilogue of last item
+                const uint32_t slot = cons % S, ph = (cons / S) & 1;
+                ++cons;
+                mbar_wait(kv_full + slot, ph);
+                tc_fence_after();
+                if (elect_one()) {
                     issue_pv<BK, D>(tmem + 2 * BK + grp * D, tmem + grp * BK,
                                     kv_base + slot * C::kKVBytes, t >= 2);
                     mma_commit(kv_empty + slot);
-                };
-                for (int32_t j = 0; j < tl.n; ++j) {
-                    const int grp = j & 1;
-                    const uint32_t slot = cons % S, ph = (cons / S) & 1;
-                    ++cons;
-                    mbar_wait(kv_full + slot, ph);
-                    tc_fence_after();
+                }
+                __syncwarp();
+            };
+            for (int32_t j = 0; j < tl.n; ++j) {
+                const int grp = j & 1;
+                const uint32_t slot = cons % S, ph = (cons / S) & 1;
+                ++cons;
+                mbar_wait(kv_full + slot, ph);
+                tc_fence_after();
+                if (elect_one()) {
                     issue_qk<BK, D>(tmem + grp * BK, q_smem, kv_base + slot * C::kKVBytes);
                     mma_commit(s_full + grp);
                     mma_commit(kv_empty + slot);
                     if (j == tl.n - 1) mma_commit(q_empty + qb);
-                    if (j >= 1) do_pv(j - 1);
                 }
-                do_pv(tl.n - 1);
-                mma_commit(o_full);
+                __syncwarp();
+                if (j >= 1) do_pv(j - 1);
             }
+            do_pv(tl.n - 1);
+            if (elect_one()) mma_commit(o_full);
+            __syncwarp();
         }
-        __syncwarp();
     }
     } else {
         set_maxnreg_inc224();
