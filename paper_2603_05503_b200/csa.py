@@ -17,7 +17,7 @@ import torch
 from .inputs import Layout
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcsa.so")
+LIB_PATH = os.environ.get("CSA_LIB") or os.path.join(_HERE, "libcsa.so")  # CSA_LIB: A/B builds
 
 CSA_OK = 0
 _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "UNSUPPORTED", 3: "CORRUPT_PLAN", 4: "CUDA",

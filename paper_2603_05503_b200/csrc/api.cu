@@ -137,6 +137,7 @@ const char* csa_version(void) { return "csa-b200 0.1 (sm_100a)"; }
 csa_status_t csa_debug_trace(void* buf, int32_t mode) {
     cudaError_t e = csa::set_attn_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_attn2_trace(buf, mode);
+    if (e == cudaSuccess) e = csa::set_attn3_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_calib_trace(buf, mode);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyToSymbol");
     return ok();
@@ -307,6 +308,10 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
             return st;
         a.sched = nullptr;  // the pair kernel assigns pair items statically per cluster
         e = csa::launch_attn_pair(a, head_dim, tq, tk_half, tv, grid, (cudaStream_t)stream);
+    } else if (g.B == 128 && head_dim == 128 && std::getenv("CSA_ATTN_QTMEM")) {
+        // experimental: Q resident in TMEM, column-split softmax (attn3.cu); measured slower
+        // than attn.cu at Wan 720p, kept for A/B measurements
+        e = csa::launch_attn_q_tmem(a, tq, tk, tv, grid, (cudaStream_t)stream);
     } else {
         e = csa::launch_attn(a, head_dim, tq, tk, tv, grid, (cudaStream_t)stream);
     }

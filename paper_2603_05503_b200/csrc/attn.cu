@@ -22,6 +22,7 @@
 // running max grows by more than 2^8.  Packed f32x2 FMA/ADD; a fixed fraction of the exp2 are
 // evaluated by a degree-3 polynomial on the FMA pipe to offload the MUFU unit.
 #include <cstdint>
+#include <cstdlib>
 
 #include "csa_internal.cuh"
 #include "tiles.cuh"
@@ -30,9 +31,22 @@ namespace csa {
 namespace {
 
 constexpr int kThreads = 384;
+static __device__ unsigned long long* g_trace;  // csa_debug_trace: CTA 0's first item timeline
+#ifdef CSA_ENABLE_TRACE  // trace builds only (see attn_common.cuh)
+#define ATRACE(slot, k, e)                                                                  \
+    do {                                                                                    \
+        if (g_trace != nullptr && blockIdx.x == 0 && local == 0 && (k) < 1024)              \
+            g_trace[((slot) * 1024 + (k)) * 8 + (e)] = clock64();                           \
+    } while (0)
+#else
+#define ATRACE(slot, k, e) \
+    do {                   \
+    } while (0)
+#endif
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kItemSlots = 4;
-constexpr int kEmuEvery = 4;  // every kEmuEvery-th element pair uses the polynomial exp2
+constexpr int kEmuEvery = 0;  // every kEmuEvery-th element pair uses the polynomial exp2 (0:
+                               // none -- measured fastest: the softmax is issue-bound, not MUFU-bound)
 
 template <int BK, int D>
 struct AttnSmem {
@@ -157,7 +171,7 @@ __device__ __forceinline__ void set_maxnreg_inc224() {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
 }
 
-template <int BK, int D>
+template <int BK, int D, int kEmuE = kEmuEvery>
 __global__ void __launch_bounds__(kThreads, 1)
     sparse_attn_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tq,
                        const __grid_constant__ CUtensorMap tk,
@@ -342,7 +356,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             auto do_pv = [&](int32_t t) {
                 const int grp = t & 1;
+                if (lane == 0) ATRACE(2, t, 2);
                 mbar_wait(p_full + grp, pcount[grp] & 1);
+                if (lane == 0) ATRACE(2, t, 3);
                 ++pcount[grp];
                 if (t == 0) mbar_wait(o_empty, (local & 1) ^ 1);  // epilogue of last item
                 const uint32_t slot = cons % S, ph = (cons / S) & 1;
@@ -360,7 +376,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int grp = j & 1;
                 const uint32_t slot = cons % S, ph = (cons / S) & 1;
                 ++cons;
+                if (lane == 0) ATRACE(2, j, 0);
                 mbar_wait(kv_full + slot, ph);
+                if (lane == 0) ATRACE(2, j, 1);
                 tc_fence_after();
                 if (elect_one()) {
                     issue_qk<BK, D>(tmem + grp * BK, q_smem, kv_base + slot * C::kKVBytes);
@@ -399,7 +417,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             float m_run = -INFINITY, l_run = 0.0f;
             int32_t mine = 0;
             for (int32_t j = grp; j < tl.n; j += 2, ++mine) {
+                const bool tr = quarter == 0 && lane == 0;
+                if (tr) ATRACE(grp, j, 0);
                 mbar_wait(s_full + grp, scount & 1);
+                if (tr) ATRACE(grp, j, 1);
                 ++scount;
                 tc_fence_after();
                 uint32_t r[BK / 32][32];
@@ -431,15 +452,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                                        fmaxf(fmax3(mc[3], mc[4], mc[5]), fmaxf(mc[6], mc[7])));
                 const float m_new = fmaxf(m_run, mx * sl2);
                 float alpha = 1.0f;
-                bool rescale = false;
+                bool need = false;
                 if (mine == 0) {
                     m_run = m_new;
                 } else if (m_new > m_run + kRescaleThreshold) {
                     alpha = ex2_approx(m_run - m_new);
                     l_run *= alpha;
                     m_run = m_new;
-                    rescale = true;
+                    need = true;
                 }
+                // tcgen05.ld/st are warp-collective (.sync.aligned): the O rescale below runs for
+                // the whole warp when any of its rows needs it (alpha = 1 for the others)
+                const bool rescale = __any_sync(0xffffffffu, need);
                 const uint64_t negm = f2(-m_run, -m_run);
                 uint64_t acc[4] = {0, 0, 0, 0};  // 4 packed partial sums (8 independent chains)
 #pragma unroll
@@ -450,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint64_t sx = pk2(r[c][x], r[c][x + 1]);
                         const uint64_t t = ffma2(sx, sl2x2, negm);
                         uint64_t p;
-                        if (((c * 16 + x / 2) % kEmuEvery) == kEmuEvery - 1) {
+                        if (kEmuE > 0 && ((c * 16 + x / 2) % (kEmuE > 0 ? kEmuE : 1)) == kEmuE - 1) {
                             p = exp2_poly2(t);
                         } else {
                             p = f2(ex2_approx(lo_f(t)), ex2_approx(hi_f(t)));
@@ -463,6 +487,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint64_t acc2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
                 l_run += lo_f(acc2) + hi_f(acc2);
                 if (rescale) {
+                    // O_grp holds only this group's earlier tiles; their P.V completed before
+                    // this tile's S (issued after it on the in-order tensor pipe) was ready
                     const uint64_t al2 = f2(alpha, alpha);
 #pragma unroll
                     for (int c = 0; c < D; c += 32) {
@@ -482,6 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(p_full + grp);
+                if (tr) ATRACE(grp, j, 2);
             }
             // -------------------------------------------------------------- epilogue
             mbar_wait(o_full, local & 1);
@@ -575,10 +602,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-template <int BK, int D>
+template <int BK, int D, int kEmuE = kEmuEvery>
 cudaError_t launch_t(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
                      const CUtensorMap& tv, int grid, cudaStream_t s) {
-    auto kern = sparse_attn_kernel<BK, D>;
+    auto kern = sparse_attn_kernel<BK, D, kEmuE>;
     const int smem = AttnSmem<BK, D>::kAlloc;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
@@ -588,16 +615,24 @@ cudaError_t launch_t(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap
 
 }  // namespace
 
-// This kernel carries no debug timeline (see attn2.cu for the pair kernel's).
 cudaError_t set_attn_trace(void* buf, int mode) {
-    (void)buf;
     (void)mode;
-    return cudaSuccess;
+    unsigned long long* p = static_cast<unsigned long long*>(buf);
+    return cudaMemcpyToSymbol(g_trace, &p, sizeof(p));
 }
 
 cudaError_t launch_attn(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
                         const CUtensorMap& tk, const CUtensorMap& tv, int grid, cudaStream_t s) {
-    if (a.g.B == 128 && head_dim == 128) return launch_t<128, 128>(a, tq, tk, tv, grid, s);
+    if (a.g.B == 128 && head_dim == 128) {
+        // debug A/B: CSA_EMU_EVERY = 0 (no polynomial exp2), 2, 3, 8 (default 4)
+        const char* ev = std::getenv("CSA_EMU_EVERY");
+        const int ee = ev ? std::atoi(ev) : kEmuEvery;
+        if (ee == 0) return launch_t<128, 128, 0>(a, tq, tk, tv, grid, s);
+        if (ee == 2) return launch_t<128, 128, 2>(a, tq, tk, tv, grid, s);
+        if (ee == 3) return launch_t<128, 128, 3>(a, tq, tk, tv, grid, s);
+        if (ee == 8) return launch_t<128, 128, 8>(a, tq, tk, tv, grid, s);
+        return launch_t<128, 128>(a, tq, tk, tv, grid, s);
+    }
     if (a.g.B == 128 && head_dim == 64) return launch_t<128, 64>(a, tq, tk, tv, grid, s);
     if (a.g.B == 64 && head_dim == 128) return launch_t<64, 128>(a, tq, tk, tv, grid, s);
     if (a.g.B == 64 && head_dim == 64) return launch_t<64, 64>(a, tq, tk, tv, grid, s);

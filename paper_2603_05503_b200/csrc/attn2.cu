@@ -250,7 +250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(lead(q_full + qb));
                 }
-                if (lane == 0) {
+                {  // whole warp walks the union (uniform values); one elected lane issues
                     const int32_t n = union_size(l0, l1);
                     UnionIter ik, iv;
                     ik.init(l0, l1);
@@ -269,18 +269,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                             ++ldv;
                         }
                         mbar_wait(kv_empty + slot, ph ^ 1);
-                        uint8_t* dst = smem + L::kKVOff + slot * L::kSlotBytes;
-                        const uint32_t fb = lead(kv_full + slot);
-                        mbar_arrive_expect_tx_cluster(fb, L::kSlotBytes);
-                        if (is_k) {  // keys 64*rank .. +63 of block c, all D columns
+                        if (elect_one()) {
+                            uint8_t* dst = smem + L::kKVOff + slot * L::kSlotBytes;
+                            const uint32_t fb = lead(kv_full + slot);
+                            mbar_arrive_expect_tx_cluster(fb, L::kSlotBytes);
+                            if (is_k) {  // keys 64*rank .. +63 of block c, all D columns
 #pragma unroll
-                            for (int x = 0; x < D / 64; ++x)
-                                tma_load_4d_pair(dst + x * L::kKHalfBox, &tk_half, fb, x * 64,
-                                                 it.h, c * BK + 64 * (int)rank, it.b, pol_kv);
-                        } else {     // all 128 keys of block c, columns 64*rank .. +63
-                            tma_load_4d_pair(dst, &tv, fb, 64 * (int)rank, it.h, c * BK, it.b,
-                                             pol_kv);
+                                for (int x = 0; x < D / 64; ++x)
+                                    tma_load_4d_pair(dst + x * L::kKHalfBox, &tk_half, fb, x * 64,
+                                                     it.h, c * BK + 64 * (int)rank, it.b, pol_kv);
+                            } else {     // all 128 keys of block c, columns 64*rank .. +63
+                                tma_load_4d_pair(dst, &tv, fb, 64 * (int)rank, it.h, c * BK,
+                                                 it.b, pol_kv);
+                            }
                         }
+                        __syncwarp();
                     };
                     for (int32_t j = 0; j < n && j < 2; ++j) load(true);
                     for (int32_t j = 0; j < n; ++j) {
@@ -296,7 +299,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             // halves, so neither stream's waits stall the other (tcgen05.commit tracks the
             // issuing thread's own MMAs).
             const bool s_issuer = (warp == 1);
-            if (lane == 0) {
+            {  // whole warp in the loop, one elected lane issues
                 uint32_t cons = 0, gbase = 0;
                 int32_t local = 0;
                 const uint32_t q_base = smem_u32(smem + L::kQOff);
@@ -308,60 +311,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     if (s_issuer) {
                         mbar_wait(q_full + qb, (local >> 1) & 1);
                         const uint32_t q_smem = q_base + qb * L::kQBytes;
-                        if (n == 0) mma_commit_pair(q_empty + qb);
+                        if (n == 0) {
+                            if (elect_one()) mma_commit_pair(q_empty + qb);
+                            __syncwarp();
+                        }
                         for (int32_t j = 0; j < n; ++j) {
                             const uint32_t gj = gbase + (uint32_t)j;
                             const int b = gj & 1;
                             const uint32_t use = gj >> 1;
-                            CSA_TRACE(2, gj, 0);
+                            if (lane == 0) CSA_TRACE(2, gj, 0);
                             if (use > 0) mbar_wait(s_free + b, (use - 1) & 1);
-                            CSA_TRACE(2, gj, 1);
+                            if (lane == 0) CSA_TRACE(2, gj, 1);
                             const uint32_t slot = cons % SK, ph = (cons / SK) & 1;
                             ++cons;
                             mbar_wait(kv_full + slot, ph);
-                            CSA_TRACE(2, gj, 2);
+                            if (lane == 0) CSA_TRACE(2, gj, 2);
                             tc_fence_after();
                             const uint32_t k_smem = kv_base + slot * L::kSlotBytes;
+                            if (elect_one()) {
 #pragma unroll
-                            for (int kk = 0; kk < D / 16; ++kk) {
-                                const uint32_t off = (kk & 3) * 32;
-                                const uint64_t ad =
-                                    umma_desc_sw128(q_smem + (kk >> 2) * L::kQBox + off, 16, 1024);
-                                const uint64_t bd = umma_desc_sw128(
-                                    k_smem + (kk >> 2) * L::kKHalfBox + off, 16, 1024);
-                                mma_ss_pair(tmem + L::kS + b * BK, ad, bd, L::kIdescQK, kk > 0);
+                                for (int kk = 0; kk < D / 16; ++kk) {
+                                    const uint32_t off = (kk & 3) * 32;
+                                    const uint64_t ad = umma_desc_sw128(
+                                        q_smem + (kk >> 2) * L::kQBox + off, 16, 1024);
+                                    const uint64_t bd = umma_desc_sw128(
+                                        k_smem + (kk >> 2) * L::kKHalfBox + off, 16, 1024);
+                                    mma_ss_pair(tmem + L::kS + b * BK, ad, bd, L::kIdescQK,
+                                                kk > 0);
+                                }
+                                mma_commit_pair(s_full + b);
+                                mma_commit_pair(kv_empty + slot);
+                                if (j == n - 1) mma_commit_pair(q_empty + qb);
                             }
-                            CSA_TRACE(2, gj, 3);
-                            mma_commit_pair(s_full + b);
-                            mma_commit_pair(kv_empty + slot);
-                            if (j == n - 1) mma_commit_pair(q_empty + qb);
+                            __syncwarp();
+                            if (lane == 0) CSA_TRACE(2, gj, 3);
                         }
                     } else {
                         for (int32_t j = 0; j < n; ++j) {
                             const uint32_t gj = gbase + (uint32_t)j;
                             const int b = gj & 1;
-                            CSA_TRACE(3, gj, 0);
+                            if (lane == 0) CSA_TRACE(3, gj, 0);
                             mbar_wait(p_full + b, (gj >> 1) & 1);
-                            CSA_TRACE(3, gj, 1);
+                            if (lane == 0) CSA_TRACE(3, gj, 1);
                             if (j == 0) mbar_wait(o_empty, (local & 1) ^ 1);
                             const uint32_t slot = SK + cons % SV, ph = (cons / SV) & 1;
                             ++cons;
                             mbar_wait(kv_full + slot, ph);
-                            CSA_TRACE(3, gj, 2);
+                            if (lane == 0) CSA_TRACE(3, gj, 2);
                             tc_fence_after();
                             const uint32_t v_smem = kv_base + slot * L::kSlotBytes;
+                            if (elect_one()) {
 #pragma unroll
-                            for (int kk = 0; kk < BK / 16; ++kk) {
-                                const uint64_t bd =
-                                    umma_desc_sw128(v_smem + kk * 16 * 128, 16384, 1024);
-                                mma_ts_pair(tmem + L::kO, tmem + L::kP + b * (BK / 2) + kk * 8, bd,
-                                            L::kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
+                                for (int kk = 0; kk < BK / 16; ++kk) {
+                                    const uint64_t bd =
+                                        umma_desc_sw128(v_smem + kk * 16 * 128, 16384, 1024);
+                                    mma_ts_pair(tmem + L::kO, tmem + L::kP + b * (BK / 2) + kk * 8,
+                                                bd, L::kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
+                                }
+                                mma_commit_pair(kv_empty + slot);
+                                mma_commit_pair(p_empty + b);
                             }
-                            CSA_TRACE(3, gj, 3);
-                            mma_commit_pair(kv_empty + slot);
-                            mma_commit_pair(p_empty + b);
+                            __syncwarp();
+                            if (lane == 0) CSA_TRACE(3, gj, 3);
                         }
-                        mma_commit_pair(o_full);
+                        if (elect_one()) mma_commit_pair(o_full);
+                        __syncwarp();
                     }
                     gbase += (uint32_t)n;
                 }
@@ -433,7 +447,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                         hm[half * 128 + row] = max_half<HC>(r);
                         named_bar_sync(1, 256);
                         m_tile = fmaxf(hm[row], hm[128 + row]) * sl2;
-                        redo = m_tile > m_run + kRescaleThreshold;
+                        // warp-uniform decision: the O rescale uses warp-collective tcgen05 ops
+                        const bool need = m_tile > m_run + kRescaleThreshold;
+                        redo = __any_sync(0xffffffffu, need);
+                        if (!need) m_tile = m_run;  // alpha = 1 for rows that need no rescale
                     }
                     ++mine;
                     if (redo) {

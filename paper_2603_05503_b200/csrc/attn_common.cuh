@@ -113,11 +113,19 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
 
 // Debug timeline (csa_debug_trace): clock64 stamps of CTA 0's pipeline events; nullptr = off.
 // Each translation unit defines its own `static __device__` g_trace / g_debug_mode (debug only).
+// Compiled in only for trace builds (CSA_TRACE_BUILD=1 python -m paper_2603_05503_b200._build
+// --force): the global load of g_trace in the hot loops costs several percent otherwise.
+#ifdef CSA_ENABLE_TRACE
 #define CSA_TRACE(slot, k, e)                                                             \
     do {                                                                                  \
         if (g_trace != nullptr && blockIdx.x == 0 && (k) < 1024)                          \
             g_trace[((slot) * 1024 + (k)) * 8 + (e)] = clock64();                         \
     } while (0)
+#else
+#define CSA_TRACE(slot, k, e) \
+    do {                      \
+    } while (0)
+#endif
 
 __device__ __forceinline__ void set_maxnreg_dec56() {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
@@ -128,7 +136,7 @@ __device__ __forceinline__ void set_maxnreg_inc224() {
 
 // Half-row tile: HC = BK/2 columns per thread.  exp2(s*sl2 - m) -> packed bf16 pk[HC/2], returns
 // the sum of the fp32 values.
-template <int HC>
+template <int HC, int kEmu = kEmuPerOctet>
 __device__ __forceinline__ float exp_half(const uint32_t (&r)[HC], float sl2, float m,
                                           uint32_t (&pk)[HC / 2]) {
     const uint64_t sl2x2 = f2(sl2, sl2);
@@ -138,7 +146,7 @@ __device__ __forceinline__ float exp_half(const uint32_t (&r)[HC], float sl2, fl
     for (int x = 0; x < HC; x += 2) {
         const uint64_t t = ffma2(pk2(r[x], r[x + 1]), sl2x2, negm);
         uint64_t p;
-        if (((x / 2) & 7) >= 8 - kEmuPerOctet) {
+        if (((x / 2) & 7) >= 8 - kEmu) {
             p = exp2_poly2(t);
         } else {
             p = f2(ex2_approx(lo_f(t)), ex2_approx(hi_f(t)));

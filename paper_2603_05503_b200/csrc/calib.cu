@@ -44,7 +44,7 @@ struct CalibSmem {
     // (TMEM: S[2] 256 + Q 64 columns).  BK = 64 (M = 64) keeps the SS form, S double-buffered.
     static constexpr bool kQT = BK == 128;
     static constexpr int kSBufs = kQT ? 1 : 2;
-    static constexpr uint32_t kQCol = 2 * kSBufs * BK;
+    static constexpr uint32_t kQCol = 2 * kSBufs * BK;  // used when kQT
     // One Q buffer (the next item's Q waits for this item's last MMA: one bubble per N_B tiles);
     // everything else not in the K ring is small, so the ring gets 4 slots of 128x128 bf16 --
     // the pass streams K from L2 and needs that many loads in flight.

@@ -104,6 +104,10 @@ cudaError_t launch_attn(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
                         const CUtensorMap& tk, const CUtensorMap& tv, int grid,
                         cudaStream_t s);
 cudaError_t set_attn2_trace(void* buf, int mode);
+cudaError_t set_attn3_trace(void* buf, int mode);
+// Block 128, head_dim 128, one CTA per query block with Q resident in TMEM (attn3.cu).
+cudaError_t launch_attn_q_tmem(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                               const CUtensorMap& tv, int grid, cudaStream_t s);
 // CTA-pair kernel (block 128, head_dim 128): work items are pairs of rows / anchor tiles.
 cudaError_t launch_attn_pair(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
                              const CUtensorMap& tk_half, const CUtensorMap& tv, int grid,

@@ -181,6 +181,33 @@ def test_attention_tiny_masks(csa, name):
         assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 1e-3, cname
 
 
+@pytest.mark.parametrize("variant", [{}, {"CSA_EMU_EVERY": "4"}, {"CSA_ATTN_QTMEM": "1"}])
+@pytest.mark.parametrize("jump", [3.0, 40.0])
+def test_attention_running_max_jumps(csa, variant, jump, monkeypatch):
+    """Key blocks whose scores grow block by block: later tiles exceed the running max (lazy
+    rescale / overflow-guard redo paths, including jumps far beyond 2^8); ragged last block.
+    Covers the production kernel, its polynomial-exp2 variant and the Q-in-TMEM kernel."""
+    for key, val in variant.items():
+        monkeypatch.setenv(key, val)
+    lay = Layout(2, 9, 40, 128)
+    heads, nb = 2, lay.NB
+    q, k, v = qkv(1, lay.N, heads, 128, seed=21, device="cuda")
+    gain = torch.ones(lay.N, device="cuda")
+    for c in range(nb):
+        gain[c * 128:(c + 1) * 128] = 1.0 + jump * c / nb
+    k = (k.float() * gain.view(1, -1, 1, 1)).to(torch.bfloat16)
+    rng = np.random.default_rng(5)
+    masks = (rng.random((heads, nb, nb)) < 0.6).astype(np.uint8)
+    masks[:, :, 0] = 1  # every row starts from the low-score block
+    masks[:, :, nb - 1] = 1  # and reaches the largest-score (ragged) block
+    out, lse, _ = run_attention(csa, lay, q, k, v, masks=masks, lse=True)
+    lse_np = lse.view(heads, lay.N).cpu().numpy()
+    for h in range(heads):
+        ref, ref_lse = oracle_head(lay, q, k, v, 0, h, mask=masks[h])
+        assert_close(out[0, :, h].double().cpu().numpy(), ref, f"{variant} jump {jump} h{h}")
+        assert np.abs(lse_np[h] - ref_lse).max() <= 1e-3 * max(1.0, np.abs(ref_lse).max())
+
+
 def test_attention_tiny_repetitive(csa):
     cfg = CONFIGS["tiny"]
     lay = cfg.layout
