@@ -308,9 +308,9 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
             return st;
         a.sched = nullptr;  // the pair kernel assigns pair items statically per cluster
         e = csa::launch_attn_pair(a, head_dim, tq, tk_half, tv, grid, (cudaStream_t)stream);
-    } else if (g.B == 128 && head_dim == 128 && std::getenv("CSA_ATTN_QTMEM")) {
-        // experimental: Q resident in TMEM, column-split softmax (attn3.cu); measured slower
-        // than attn.cu at Wan 720p, kept for A/B measurements
+    } else if (g.B == 128 && head_dim == 128 && !std::getenv("CSA_ATTN_V3")) {
+        // production shape: Q resident in TMEM, column-split softmax (attn3.cu); CSA_ATTN_V3
+        // selects the shared-memory-Q kernel (attn.cu, all other shapes) for A/B measurements
         e = csa::launch_attn_q_tmem(a, tq, tk, tv, grid, (cudaStream_t)stream);
     } else {
         e = csa::launch_attn(a, head_dim, tq, tk, tv, grid, (cudaStream_t)stream);

@@ -29,7 +29,7 @@ using namespace attn;
 
 constexpr int kThreads3 = 384;
 constexpr int kItemSlots3 = 4;
-constexpr int kEmu3 = 3;  // element pairs p with (p & 7) >= 8 - kEmu3 -> polynomial exp2
+constexpr int kEmu3 = 2;  // element pairs p with (p & 7) >= 8 - kEmu3 -> polynomial exp2 (A/B: 2 > 0, 3)
 static __device__ unsigned long long* g_trace;
 static __device__ int g_debug_mode;
 

@@ -181,12 +181,13 @@ def test_attention_tiny_masks(csa, name):
         assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 1e-3, cname
 
 
-@pytest.mark.parametrize("variant", [{}, {"CSA_EMU_EVERY": "4"}, {"CSA_ATTN_QTMEM": "1"}])
+@pytest.mark.parametrize("variant", [{}, {"CSA_ATTN_V3": "1"}, {"CSA_ATTN_V3": "1", "CSA_EMU_EVERY": "4"}])
 @pytest.mark.parametrize("jump", [3.0, 40.0])
 def test_attention_running_max_jumps(csa, variant, jump, monkeypatch):
     """Key blocks whose scores grow block by block: later tiles exceed the running max (lazy
     rescale / overflow-guard redo paths, including jumps far beyond 2^8); ragged last block.
-    Covers the production kernel, its polynomial-exp2 variant and the Q-in-TMEM kernel."""
+    Covers the production (Q-in-TMEM) kernel and the shared-memory-Q kernel with and without
+    its polynomial exp2."""
     for key, val in variant.items():
         monkeypatch.setenv(key, val)
     lay = Layout(2, 9, 40, 128)
