@@ -324,7 +324,9 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
                           "frac": round(achieved / pk["bf16_tflops"], 4), "traffic": traffic,
                           "peak_src": f"{pk['src']} bf16 burst",
                           "frac_of_sustained": round(achieved / pk["bf16_tflops_sustained"], 4),
-                          "kernel": "sparse_attn_kernel<128,128>",
+                          "kernel": ("sparse_attn_q_tmem_kernel (attn3.cu)"
+                                     if lay.B == 128 and cfg.d == 128 and not os.environ.get("CSA_ATTN_V3")
+                                     else f"sparse_attn_kernel<{lay.B},{cfg.d}> (attn.cu)"),
                           "algorithmic_flop_per_launch": flop_all}
     # ---- dense comparators: our kernel on an all-ones plan, and torch SDPA (cuDNN/flash)
     H, d, B = cfg.heads, cfg.d, args.batch

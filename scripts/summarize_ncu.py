@@ -1,9 +1,10 @@
 """Summarise an ncu --set full report and a launch-list CSV into profiles/ (committed evidence).
 
-usage: python scripts/summarize_ncu.py TAG CONFIG
-reads gpurun_out/prof_attn_TAG_CONFIG.ncu-rep and gpurun_out/launches_TAG_CONFIG.csv
-writes profiles/TAG_CONFIG_attn_ncu.txt, profiles/TAG_CONFIG_launches.csv,
-       profiles/ncu_CONFIG_attn.json (dram bytes per launch, read by bench.py as roofline.traffic)
+usage: python scripts/summarize_ncu.py TAG CONFIG [KIND]   (KIND: attn (default) or calib)
+reads gpurun_out/prof_KIND_TAG_CONFIG.ncu-rep and gpurun_out/launches_TAG_CONFIG.csv
+writes profiles/TAG_CONFIG_KIND_ncu.txt, profiles/TAG_CONFIG_launches.csv,
+       profiles/ncu_CONFIG_KIND.json (dram bytes per launch; bench.py reads the attn one as
+       roofline.traffic)
 """
 import csv
 import io
@@ -14,8 +15,9 @@ import subprocess
 import sys
 
 tag, cfg = sys.argv[1], sys.argv[2]
+kind = sys.argv[3] if len(sys.argv) > 3 else "attn"
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-rep = os.path.join(root, "gpurun_out", f"prof_attn_{tag}_{cfg}.ncu-rep")
+rep = os.path.join(root, "gpurun_out", f"prof_{kind}_{tag}_{cfg}.ncu-rep")
 out_dir = os.path.join(root, "profiles")
 os.makedirs(out_dir, exist_ok=True)
 
@@ -63,13 +65,13 @@ rb, ru = get("dram__bytes_read.sum")
 wb, wu = get("dram__bytes_write.sum")
 traffic = to_bytes(rb, ru) + to_bytes(wb, wu)
 lines.append(f"  dram bytes per launch (read + write)                                   {traffic:.4g} B")
-with open(os.path.join(out_dir, f"{tag}_{cfg}_attn_ncu.txt"), "w") as fh:
+with open(os.path.join(out_dir, f"{tag}_{cfg}_{kind}_ncu.txt"), "w") as fh:
     fh.write("\n".join(lines) + "\n")
-with open(os.path.join(out_dir, f"ncu_{cfg}_attn.json"), "w") as fh:
+with open(os.path.join(out_dir, f"ncu_{cfg}_{kind}.json"), "w") as fh:
     json.dump({"report": os.path.basename(rep), "dram_bytes_per_launch": traffic}, fh, indent=1)
 
 lc = os.path.join(root, "gpurun_out", f"launches_{tag}_{cfg}.csv")
-if os.path.exists(lc):
+if kind == "attn" and os.path.exists(lc):
     shutil.copy(lc, os.path.join(out_dir, f"{tag}_{cfg}_launches.csv"))
     txt = open(lc).read()
     body = txt[txt.index('"ID"'):] if '"ID"' in txt else txt
@@ -82,6 +84,6 @@ if os.path.exists(lc):
     share = [f"launch-list shares ({os.path.basename(lc)}, cold-cache serialised ncu times):"]
     for n, t in sorted(tot.items(), key=lambda x: -x[1]):
         share.append(f"  {t / 1e6:10.3f} ms  {100 * t / allt:5.1f}%  {n}")
-    with open(os.path.join(out_dir, f"{tag}_{cfg}_attn_ncu.txt"), "a") as fh:
+    with open(os.path.join(out_dir, f"{tag}_{cfg}_{kind}_ncu.txt"), "a") as fh:
         fh.write("\n".join(share) + "\n")
-print(open(os.path.join(out_dir, f"{tag}_{cfg}_attn_ncu.txt")).read())
+print(open(os.path.join(out_dir, f"{tag}_{cfg}_{kind}_ncu.txt")).read())
