@@ -113,13 +113,50 @@ def kept_area_host(masks: np.ndarray, lay: inputs.Layout) -> np.ndarray:
 
 
 def workload(cfg, args, heads_lo, heads_hi, rank_dev):
-    """Plan counts for this rank's heads: synthetic MASK heads (generator S at the config's
-    sparsity) and args.rep_heads REPETITIVE heads (k=5), spread over the head range."""
+    """Plan inputs for all heads: keep counts + min_count for the compiler (a6), the resulting
+    MASK-head masks (host, for FLOP accounting and the oracle sample), the REPETITIVE heads.
+
+    Configs with a BASELINE sparsity (Wan 480p / 720p): generator S masks at that sparsity,
+    counts = 64 * M, min_count 32.  Configs without one (Mochi, M4): the
+    calibration path itself -- |D| = 8 generator-G prompts through csa_calib_accumulate at
+    t = 32 of T = 64 (eps from Eq. eq:epsilon_schedule), rho = 0.5 -> min_count 4."""
     lay = cfg.layout
-    target = cfg.sparsity if cfg.sparsity is not None else 0.69
-    masks = inputs.synthetic_masks(lay, cfg.heads, target, seed=0)
     rep = set(np.linspace(0, cfg.heads - 1, args.rep_heads).astype(int).tolist()) if args.rep_heads else set()
-    return lay, masks, rep
+    if cfg.sparsity is not None:
+        masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity, seed=0)
+        counts = masks.astype(np.uint16) * np.uint16(64)
+        return lay, masks, rep, counts, 32, None
+    from paper_2603_05503_b200 import csa
+
+    n_prompts, t, T = 8, 32, 64
+    a_n = 0.796 + 1.41e-6 * lay.N                       # A(N), P:888-894
+    eps = a_n + (0.99 - a_n) * math.exp(-16.0 * t / T)  # Eq. eq:epsilon_schedule, C = 0.99, k = 16
+    alphas = np.linspace(0.8, 1.6, cfg.heads)           # peak-logit scale spread across heads
+    counts_t = torch.zeros(cfg.heads * lay.NB * lay.NB, dtype=torch.int16,
+                           device=rank_dev).view(torch.uint16)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for p in range(n_prompts):
+        qc, kc, _ = inputs.structured_qk(lay, cfg.heads, cfg.d, head_seed=1, prompt_seed=p,
+                                         alpha=alphas, repetitive=tuple(sorted(rep)),
+                                         device=rank_dev)
+        csa.calib_accumulate(lay, qc, kc, eps, counts_t)
+        del qc, kc
+    torch.cuda.synchronize()
+    calib_s = time.perf_counter() - t0
+    counts = counts_t.view(torch.int16).cpu().numpy().view(np.uint16).reshape(
+        cfg.heads, lay.NB, lay.NB)
+    min_count = math.ceil(0.5 * n_prompts)
+    masks = np.zeros((cfg.heads, lay.NB, lay.NB), np.uint8)
+    plan = csa.compile_plan(lay, counts_t, min_count)   # MASK view of every head, for accounting
+    bits = plan.mask_bits.cpu().numpy().view(np.uint32)
+    w32 = (lay.NB + 31) // 32
+    unpacked = np.unpackbits(bits.view(np.uint8), bitorder="little").reshape(
+        cfg.heads, lay.NB, w32 * 32)[:, :, :lay.NB]
+    masks[:] = unpacked
+    calib = {"prompts": n_prompts, "t": t, "T": T, "eps": round(eps, 6), "min_count": min_count,
+             "wall_s_incl_generator": round(calib_s, 3)}
+    return lay, masks, rep, counts, min_count, calib
 
 
 def flops_of(lay, masks, rep, heads, d, batch, anchor_k=5):
@@ -237,15 +274,15 @@ def main():
         raise SystemExit(f"heads {H} / tokens {lay.N} not divisible by {world}")
     hp = H // world
     h_lo, h_hi = rank * hp, (rank + 1) * hp
-    lay, masks, rep = workload(cfg, args, 0, H, dev)
+    lay, masks, rep, counts_all, min_count, calib = workload(cfg, args, 0, H, dev)
     my_heads = list(range(h_lo, h_hi))
 
     # ---- plan for this rank's heads (a6 through the C ABI), REPETITIVE via similarity > gamma
-    counts_np = (masks[h_lo:h_hi].astype(np.uint16) * np.uint16(64))
+    counts_np = np.ascontiguousarray(counts_all[h_lo:h_hi], dtype=np.uint16)
     counts = torch.from_numpy(counts_np.reshape(-1).view(np.int16)).to(dev).view(torch.uint16)
     sim = torch.tensor([1.0 if h in rep else 0.0 for h in my_heads], dtype=torch.float64, device=dev)
     t0 = time.perf_counter()
-    plan = csa.compile_plan(lay, counts, 32, similarity=sim, gamma=0.87, anchor_k=5)
+    plan = csa.compile_plan(lay, counts, min_count, similarity=sim, gamma=0.87, anchor_k=5)
     # pair items for the CTA-pair kernel (block 128, d 128), else head-major single items
     work = csa.build_work_list(plan, 0, hp, order=csa.default_order(lay, d))
     torch.cuda.synchronize()
@@ -286,7 +323,10 @@ def main():
         "metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (seeded N(0,1) bf16 Q/K/V; generator-S calibrated-like block masks)",
+        "data": ("synthetic (seeded N(0,1) bf16 Q/K/V; generator-S calibrated-like block masks)"
+                 if calib is None else
+                 "synthetic (seeded N(0,1) bf16 Q/K/V; plan calibrated by this repo's a2-a6 path "
+                 "on 8 generator-G prompts)"),
         "config": {"workload": f"{cfg.name} single attention layer",
                    "F_H_W": [lay.F, lay.H, lay.W], "tokens": lay.N, "heads": H, "head_dim": d,
                    "block": lay.B, "batch": B, "kept_fraction": round(kept_fraction, 4),
@@ -294,6 +334,7 @@ def main():
                    "anchor_k": 5, "parallelism": f"heads{world} (Ulysses a2a)" if world > 1 else "1 GPU",
                    "l2": "inputs 3x%.2f GB > 126 MB L2; no flush" % (B * lay.N * H * d * 2 / 1e9)},
         "gpu_launches": args.steps * 1,
+        **({"calibration": calib} if calib is not None else {}),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_extras:
@@ -367,6 +408,12 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
     calib_exps = 1.0 * H * float(lay.N) ** 2                 # one exp per score
     ph["calib_exp_per_s"] = calib_exps / (t_cal * 1e-3)
     ph["calib_qk_tflops"] = round(2.0 * d * H * float(lay.N) ** 2 / (t_cal * 1e-3) / 1e12, 1)
+    # exp roofline of a2-a3: MUFU ex2 = 16 / clk / SM at the SM clock sampled during
+    # the timed attention region (a quarter to 3/8 of the exps run on the FMA pipe instead)
+    sm_mhz = (result.get("clocks") or {}).get("sm_mhz") or 1965.0
+    mufu = 16.0 * torch.cuda.get_device_properties(dev).multi_processor_count * sm_mhz * 1e6
+    ph["calib_mufu_peak_exp_per_s"] = mufu
+    ph["calib_exp_frac_of_mufu"] = round(ph["calib_exp_per_s"] / mufu, 4)
     cnt = torch.from_numpy((masks.astype(np.uint16) * np.uint16(64)).reshape(-1).view(np.int16)).to(dev).view(torch.uint16)
     sim = torch.tensor([1.0 if h in rep else 0.0 for h in range(H)], dtype=torch.float64, device=dev)
     torch.cuda.synchronize()
@@ -405,8 +452,11 @@ def reference_arm(args, cfg, world, rank):
     if rank != 0:
         return
     lay = cfg.layout
-    masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity or 0.69, seed=0)
-    rep = set(np.linspace(0, cfg.heads - 1, args.rep_heads).astype(int).tolist()) if args.rep_heads else set()
+    if cfg.sparsity is None and torch.cuda.is_available():  # the calibrated plan of our arm
+        _, masks, rep, _, _, _ = workload(cfg, args, 0, cfg.heads, torch.device("cuda"))
+    else:
+        masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity or 0.69, seed=0)
+        rep = set(np.linspace(0, cfg.heads - 1, args.rep_heads).astype(int).tolist()) if args.rep_heads else set()
     q, k, v = inputs.qkv(1, lay.N, cfg.heads, cfg.d, seed=11, device="cpu")
     vals, t_steps = [], []
     for i in range(args.warmup + args.steps):
