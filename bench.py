@@ -337,6 +337,30 @@ def main():
         **({"calibration": calib} if calib is not None else {}),
         "clocks": clk.summary(),
     }
+    if world > 1:
+        # e2e at N GPUs through the public API: every step copies this rank's sequence shard of
+        # Q, K, V in from pinned host memory, runs the head-sharded layer (a2a, attention, a2a)
+        # and copies the rank's output shard back; max over ranks.  Bytes are whole-job totals.
+        hq, hk, hv = (t.cpu().pin_memory() for t in (ql, kl, vl))
+        dq, dk, dv = (torch.empty_like(t) for t in (ql, kl, vl))
+        step_e2e = ulysses.make_layer_step(dq, dk, dv, world, run_heads)
+        ho = torch.empty(ql.shape, dtype=ql.dtype).pin_memory()
+
+        def e2e_step():
+            dq.copy_(hq, non_blocking=True)
+            dk.copy_(hk, non_blocking=True)
+            dv.copy_(hv, non_blocking=True)
+            ho.copy_(step_e2e(), non_blocking=True)
+
+        n_e2e = max(2, args.steps // 3)
+        t_e2e, _ = time_loop(e2e_step, n_e2e, 1, stream)
+        te = torch.tensor([t_e2e / n_e2e], device=dev)
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(te.item())
+        result["e2e"] = {"value": round(flop_all / (t_e2e * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+                         "ms_per_step": round(t_e2e, 3),
+                         "h2d_bytes_per_step": 3 * ql.numel() * 2 * world,
+                         "d2h_bytes_per_step": ql.numel() * 2 * world}
     if rank == 0 and world == 1 and not args.no_extras:
         extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_all, dense_flop,
                kept_fraction, per, pk, stream, dev, csa)

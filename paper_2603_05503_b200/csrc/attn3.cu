@@ -19,6 +19,7 @@
 // rings), warp 1 S-issuer (Q copy + S = Q K^T), warp 3 PV-issuer (O += P V), warp 2 TMEM
 // allocator.  Issuers and producer run warp-uniform loops; one elected lane issues.
 #include <cstdint>
+#include <cstdlib>
 
 #include "attn_common.cuh"
 
@@ -27,30 +28,38 @@ namespace {
 
 using namespace attn;
 
-constexpr int kThreads3 = 384;
 constexpr int kItemSlots3 = 4;
+// P placement: true -> own 64-column TMEM buffer (S[b] is released as soon as the softmax has
+// loaded it, so S-MMAs never wait for a P.V; the softmax waits for the previous tile's P.V
+// before overwriting P); false -> P over S[b]'s first 64 columns (S[b] released by the P.V).
+constexpr bool kSeparateP = false;
 constexpr int kEmu3 = 2;  // element pairs p with (p & 7) >= 8 - kEmu3 -> polynomial exp2 (A/B: 2 > 0, 3)
 static __device__ unsigned long long* g_trace;
 static __device__ int g_debug_mode;
 
+// CG = softmax column groups (4 warps each): every tile is split over CG x 4 warps, group g
+// taking key columns g*128/CG ...; more groups = more warps per SM sub-partition to hide the
+// TMEM-load / exchange / P-store latencies of the per-tile softmax.
+template <int CG>
 struct Smem3 {
-
+    static constexpr int kThreads = 128 + 128 * CG;
     static constexpr int kBox = 128 * 128;      // [128 rows][64 cols] bf16, SWIZZLE_128B
     static constexpr int kTile = 2 * kBox;      // 128 x 128 bf16 (Q, K or V tile)
     static constexpr int kQOff = 0;             // single Q buffer (freed once copied to TMEM)
     static constexpr int kKOff = kTile;
-    static constexpr int kKSlots = 3, kVSlots = 3;
+    static constexpr int kKSlots = 3, kVSlots = CG == 2 ? 3 : 2;
     static constexpr int kVOff = kKOff + kKSlots * kTile;
     static constexpr int kBarOff = kVOff + kVSlots * kTile;
     // q_full q_empty | k_full[KS] k_empty[KS] | v_full[VS] v_empty[VS] | s_full[2] s_free[2] |
     // p_full p_empty | o_full o_empty | item_full[4] item_empty[4]
-    static constexpr int kNumBars = 2 + 2 * kKSlots + 2 * kVSlots + 4 + 2 + 2 + 2 * kItemSlots3 + 4;
-    static constexpr int kHmaxOff = kBarOff + kNumBars * 8;     // float [2 parity][2 half][128]
-    static constexpr int kItemOff = kHmaxOff + 4 * 128 * 4;     // int32 [kItemSlots3]
+    static constexpr int kNumBars =
+        2 + 2 * kKSlots + 2 * kVSlots + 4 + 2 + 2 + 2 * kItemSlots3 + 2 * CG;
+    static constexpr int kHmaxOff = kBarOff + kNumBars * 8;     // float [2 parity][CG][128]
+    static constexpr int kItemOff = kHmaxOff + 2 * CG * 128 * 4;  // int32 [kItemSlots3]
     static constexpr int kTmemPtrOff = kItemOff + kItemSlots3 * 4;
     static constexpr int kBytes = kTmemPtrOff + 16;
     static_assert(kBytes <= 232448, "smem");
-    static constexpr uint32_t kS = 0, kO = 256, kQ = 384;  // P aliases S[b] (columns 0-63)
+    static constexpr uint32_t kS = 0, kO = 256, kQ = 384, kP = 448;  // kP unused if P aliases S
     static constexpr uint32_t kIdescQK = umma_idesc_bf16(128, 128, 0, 0);
     static constexpr uint32_t kIdescPV = umma_idesc_bf16(128, 128, 0, 1);
 };
@@ -67,12 +76,13 @@ struct Smem3 {
     } while (0)
 #endif
 
-__global__ void __launch_bounds__(kThreads3, 1)
+template <int CG>
+__global__ void __launch_bounds__(Smem3<CG>::kThreads, 1)
     sparse_attn_q_tmem_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tq,
                               const __grid_constant__ CUtensorMap tk,
                               const __grid_constant__ CUtensorMap tv) {
-    using L = Smem3;
-    constexpr int BK = 128, D = 128, HC = 64;
+    using L = Smem3<CG>;
+    constexpr int BK = 128, D = 128, HC = 128 / CG;
     constexpr int KS = L::kKSlots, VS = L::kVSlots;
     extern __shared__ __align__(1024) uint8_t smem[];
     if ((smem_u32(smem) & 1023u) != 0u) __trap();
@@ -84,14 +94,14 @@ __global__ void __launch_bounds__(kThreads3, 1)
     uint64_t* v_full = k_empty + KS;
     uint64_t* v_empty = v_full + VS;
     uint64_t* s_full = v_empty + VS;
-    uint64_t* pv_done = s_full + 2;  // [b]: the P.V that read P from S[b] has completed
+    uint64_t* pv_done = s_full + 2;  // [b]: S[b] free (softmax loaded it / its P.V completed)
     uint64_t* p_full = pv_done + 2;
     uint64_t* p_empty = p_full + 1;
     uint64_t* o_full = p_empty + 1;
     uint64_t* o_empty = o_full + 1;
     uint64_t* item_full = o_empty + 1;
     uint64_t* item_empty = item_full + kItemSlots3;
-    uint64_t* hx_full = item_empty + kItemSlots3;  // [half][parity]: half posted its tile max
+    uint64_t* hx_full = item_empty + kItemSlots3;  // [group][parity]: group posted its tile max
     float* hmax = reinterpret_cast<float*>(smem + L::kHmaxOff);
     volatile int32_t* item_slot = reinterpret_cast<int32_t*>(smem + L::kItemOff);
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtrOff);
@@ -110,17 +120,17 @@ __global__ void __launch_bounds__(kThreads3, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(s_full + i, 1);
-            mbar_init(pv_done + i, 1);
+            mbar_init(pv_done + i, kSeparateP ? 4 * CG : 1);
         }
-        mbar_init(p_full, 8);
+        mbar_init(p_full, 4 * CG);
         mbar_init(p_empty, 1);
         mbar_init(o_full, 1);
-        mbar_init(o_empty, 8);
+        mbar_init(o_empty, 4 * CG);
         for (int i = 0; i < kItemSlots3; ++i) {
             mbar_init(item_full + i, 1);
-            mbar_init(hx_full + i, 4);  // kItemSlots3 == 4 == 2 halves x 2 parities, 4 warps each
-            mbar_init(item_empty + i, 10);  // S-issuer, PV-issuer, 8 softmax warps
+            mbar_init(item_empty + i, 2 + 4 * CG);  // S-issuer, PV-issuer, softmax warps
         }
+        for (int i = 0; i < 2 * CG; ++i) mbar_init(hx_full + i, 4);  // 4 warps per group
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<512>(tmem_ptr);
@@ -146,7 +156,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
     };
 
     if (warp < 4) {
-        set_maxnreg_dec56();
+        if constexpr (CG == 2) set_maxnreg_dec56();
         if (warp == 0) {
             // ------------------------------------------------------------ scheduler + producer
             const uint64_t pol_q = policy_evict_first();
@@ -267,7 +277,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
                 for (int32_t j = 0; j < tl.n; ++j, ++tcount) {
                     const uint32_t b = tcount & 1, use = tcount >> 1;
                     if (lane == 0) TRACE3(2, j, 0);
-                    // S[b] holds P of tile t-2 until that tile's P.V has completed
+                    // S[b] still holds tile t-2 (its S until loaded, or its P until its P.V ran)
                     mbar_wait(pv_done + b, (use & 1) ^ 1);
                     const uint32_t slot = cons % KS, ph = (cons / KS) & 1;
                     ++cons;
@@ -308,14 +318,14 @@ __global__ void __launch_bounds__(kThreads3, 1)
                     tc_fence_after();
                     if (elect_one()) {
                         const uint32_t vb = v_base + slot * L::kTile;
-                        const uint32_t pcol = L::kS + (tcount & 1) * BK;  // P aliases S[b]
+                        const uint32_t pcol = kSeparateP ? L::kP : L::kS + (tcount & 1) * BK;
 #pragma unroll
                         for (int kk = 0; kk < BK / 16; ++kk)
                             mma_ts(tmem + L::kO, tmem + pcol + kk * 8,
                                    umma_desc_sw128(vb + kk * 16 * 128, L::kBox, 1024),
                                    L::kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
                         mma_commit(p_empty);
-                        mma_commit(pv_done + (tcount & 1));
+                        if (!kSeparateP) mma_commit(pv_done + (tcount & 1));
                         mma_commit(v_empty + slot);
                     }
                     __syncwarp();
@@ -326,9 +336,10 @@ __global__ void __launch_bounds__(kThreads3, 1)
         }
         __syncwarp();
     } else {
-        set_maxnreg_inc224();
+        if constexpr (CG == 2) set_maxnreg_inc224();
         // ------------------------------------------------------------------------ softmax
-        const int half = (warp - 4) >> 2;   // key columns half*64 .. +63; O columns likewise
+        const int half = (warp - 4) >> 2;   // column group: key columns half*HC .. +HC-1 of
+                                            // every tile, O columns half*D/CG .. likewise
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
@@ -345,13 +356,18 @@ __global__ void __launch_bounds__(kThreads3, 1)
             float m_run = -INFINITY, l_run = 0.0f;
             for (int32_t j = 0; j < tl.n; ++j, ++tcount) {
                 const uint32_t b = tcount & 1;
-                const bool tr = quarter == 0 && lane == 0;
+                const bool tr = quarter == 0 && lane == 0 && half < 2;
                 if (tr) TRACE3(half, j, 0);
                 mbar_wait(s_full + b, (tcount >> 1) & 1);
                 if (tr) TRACE3(half, j, 1);
                 tc_fence_after();
                 uint32_t r[HC];
                 tmem_load_half<HC>(lane_addr + L::kS + b * BK + half * HC, r);
+                if constexpr (kSeparateP) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(pv_done + b);  // S[b] may be overwritten
+                }
                 if (tr) TRACE3(half, j, 3);
                 if (last_ragged && j == tl.n - 1) {
 #pragma unroll
@@ -366,27 +382,36 @@ __global__ void __launch_bounds__(kThreads3, 1)
                 // the running max, then waits for the other half's post (bar.sync on the other
                 // id).  Having passed that wait also proves the other half has loaded its S
                 // columns, so P may then overwrite S[b] (P aliases the first 64 columns).
-                float* hm = hmax + (tcount & 1) * 256;
+                float* hm = hmax + (tcount & 1) * (CG * 128);
                 hm[half * 128 + row] = dbg ? 0.0f : max_half<HC>(r);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(hx_full + half * 2 + (tcount & 1));
+                // wait for every other group's post of this tile; returns the row's tile max
+                auto exchange = [&]() -> float {
+#pragma unroll
+                    for (int g2 = 0; g2 < CG; ++g2)
+                        if (g2 != half)
+                            mbar_wait(hx_full + g2 * 2 + (tcount & 1), (tcount >> 1) & 1);
+                    float mx = hm[row];
+#pragma unroll
+                    for (int g2 = 1; g2 < CG; ++g2) mx = fmaxf(mx, hm[g2 * 128 + row]);
+                    return mx;
+                };
                 if (dbg) {
 #pragma unroll
                     for (int x = 0; x < HC / 2; ++x) pk[x] = 0u;
                     lsum = 0.0f;
-                    mbar_wait(hx_full + (half ^ 1) * 2 + (tcount & 1), (tcount >> 1) & 1);
+                    exchange();
                 } else if (j == 0) {
-                    mbar_wait(hx_full + (half ^ 1) * 2 + (tcount & 1), (tcount >> 1) & 1);
-                    m_run = fmaxf(hm[row], hm[128 + row]) * sl2;
+                    m_run = exchange() * sl2;
                     lsum = exp_half<HC, kEmu3>(r, sl2, m_run, pk);
                 } else {
                     // exponentials against the running max first (the common case); redo only
                     // when the tile max jumps by more than 2^8
                     lsum = exp_half<HC, kEmu3>(r, sl2, m_run, pk);
                     if (tr) TRACE3(half, j, 4);
-                    mbar_wait(hx_full + (half ^ 1) * 2 + (tcount & 1), (tcount >> 1) & 1);
+                    const float m_tile = exchange() * sl2;
                     if (tr) TRACE3(half, j, 5);
-                    const float m_tile = fmaxf(hm[row], hm[128 + row]) * sl2;
                     // warp-uniform decision: the O rescale uses warp-collective tcgen05.ld/st
                     const bool need = m_tile > m_run + kRescaleThreshold;
                     redo = __any_sync(0xffffffffu, need);
@@ -401,9 +426,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
                         tc_fence_after();
                         const uint64_t al2 = f2(alpha, alpha);
 #pragma unroll
-                        for (int cc = 0; cc < D / 2; cc += 32) {
+                        for (int cc = 0; cc < D / CG; cc += 32) {
                             uint32_t o[32];
-                            const uint32_t oa = lane_addr + L::kO + half * (D / 2) + cc;
+                            const uint32_t oa = lane_addr + L::kO + half * (D / CG) + cc;
                             tmem_ld32(oa, o);
                             tmem_ld_wait(o);
 #pragma unroll
@@ -417,8 +442,11 @@ __global__ void __launch_bounds__(kThreads3, 1)
                     }
                 }
                 l_run += lsum;
+                // one P buffer: the previous tile's P.V must have read it (redo already waited)
+                if (kSeparateP && tcount > 0 && !redo) mbar_wait(p_empty, (tcount - 1) & 1);
                 if (tr) TRACE3(half, j, 6);
-                tmem_store_p<HC>(lane_addr + L::kS + b * BK + half * (HC / 2), pk);
+                tmem_store_p<HC>(lane_addr + (kSeparateP ? L::kP : L::kS + b * BK) +
+                                     half * (HC / 2), pk);
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
@@ -430,10 +458,12 @@ __global__ void __launch_bounds__(kThreads3, 1)
             tc_fence_after();
             // the last tile's buffer: o_full implies both halves are past their reads of it,
             // and the next item's first tile uses the other one
-            float* row_l = hmax + ((tcount - 1) & 1) * 256;
+            float* row_l = hmax + ((tcount - 1) & 1) * (CG * 128);
             row_l[half * 128 + row] = l_run;
-            named_bar_sync(3, 256);
-            const float Lsum = row_l[row] + row_l[128 + row];
+            named_bar_sync(3, 128 * CG);
+            float Lsum = row_l[row];
+#pragma unroll
+            for (int g2 = 1; g2 < CG; ++g2) Lsum += row_l[g2 * 128 + row];
             const float inv = Lsum > 0.0f ? 1.0f / Lsum : 0.0f;
             int64_t tok0 = -1;
             int32_t n_dst = 0, dst_stride_rows = 0;
@@ -461,8 +491,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
             __nv_bfloat16* obase = a.o + (int64_t)it.b * a.o_sb + (int64_t)it.h * a.o_sh;
             const uint64_t inv2 = f2(inv, inv);
 #pragma unroll
-            for (int cc = 0; cc < D / 2; cc += 32) {
-                const int col = half * (D / 2) + cc;
+            for (int cc = 0; cc < D / CG; cc += 32) {
+                const int col = half * (D / CG) + cc;
                 uint32_t r0[32];
                 tmem_ld32(lane_addr + L::kO + col, r0);
                 tmem_ld_wait(r0);
@@ -517,15 +547,25 @@ cudaError_t set_attn3_trace(void* buf, int mode) {
     return cudaMemcpyToSymbol(g_debug_mode, &mode, sizeof(mode));
 }
 
+namespace {
+template <int CG>
+cudaError_t launch_cg(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                      const CUtensorMap& tv, int grid, cudaStream_t s) {
+    auto kern = sparse_attn_q_tmem_kernel<CG>;
+    const int smem = Smem3<CG>::kBytes;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, Smem3<CG>::kThreads, smem, s>>>(a, tq, tk, tv);
+    return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t launch_attn_q_tmem(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
                                const CUtensorMap& tv, int grid, cudaStream_t s) {
     if (a.g.B != 128) return cudaErrorInvalidValue;
-    auto kern = sparse_attn_q_tmem_kernel;
-    const int smem = Smem3::kBytes;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    kern<<<grid, kThreads3, smem, s>>>(a, tq, tk, tv);
-    return cudaGetLastError();
+    const char* cg = std::getenv("CSA_ATTN_CG");  // A/B: softmax column groups (2 or 4)
+    if (cg && std::atoi(cg) == 4) return launch_cg<4>(a, tq, tk, tv, grid, s);
+    return launch_cg<2>(a, tq, tk, tv, grid, s);
 }
 
 }  // namespace csa

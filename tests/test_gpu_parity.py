@@ -181,7 +181,8 @@ def test_attention_tiny_masks(csa, name):
         assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 1e-3, cname
 
 
-@pytest.mark.parametrize("variant", [{}, {"CSA_ATTN_V3": "1"}, {"CSA_ATTN_V3": "1", "CSA_EMU_EVERY": "4"}])
+@pytest.mark.parametrize("variant", [{}, {"CSA_ATTN_CG": "4"}, {"CSA_ATTN_V3": "1"},
+                                     {"CSA_ATTN_V3": "1", "CSA_EMU_EVERY": "4"}])
 @pytest.mark.parametrize("jump", [3.0, 40.0])
 def test_attention_running_max_jumps(csa, variant, jump, monkeypatch):
     """Key blocks whose scores grow block by block: later tiles exceed the running max (lazy
