@@ -64,6 +64,9 @@ def lib():
         L.csao_anchor_attention_rows.restype = ctypes.c_int
         L.csao_anchor_attention_rows.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _p, _p, _p,
                                                  _c_dbl, _c_i32, _c_i64, _c_i64, _p, _p]
+        L.csao_spatial_cos.restype = ctypes.c_int
+        L.csao_spatial_cos.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _p, _p, _c_dbl, _c_i32,
+                                       _c_i32, _c_i32, _p]
         L.csao_row_lse.restype = ctypes.c_int
         L.csao_row_lse.argtypes = [_c_i64, _c_i32, _p, _p, _c_dbl, _c_i64, _c_i64, _p]
         L.csao_block_energy_rows.restype = ctypes.c_int
@@ -158,6 +161,24 @@ def anchor_attention_rows(F, H, W, q, k, v, scale: float, kA: int, rows=None):
     if rc != 0:
         raise ValueError("csao_anchor_attention_rows: invalid argument")
     return out, lse
+
+
+def spatial_cos(F, H, W, q, k, scale: float, kA: int, f: int, i: int) -> float:
+    """cos(P^(f,i), P^(f,a(i))) of one prompt (readings Q23-Q25): flattened W x N
+    blocks of the dense map, query (f,i,j) paired with (f,a(i),j)."""
+    q, k = _f64(q), _f64(k)
+    n, d = q.shape
+    assert n == F * H * W
+    out = np.empty((1,), np.float64)
+    if lib().csao_spatial_cos(F, H, W, d, _ptr(q), _ptr(k), scale, kA, f, i, _ptr(out)) != 0:
+        raise ValueError("spatial_cos: invalid argument")
+    return float(out[0])
+
+
+def spatial_similarity(F, H, W, q, k, scale: float, kA: int) -> float:
+    """s of one prompt: mean of spatial_cos over every (f, i) (reading Q24)."""
+    return float(np.mean([spatial_cos(F, H, W, q, k, scale, kA, f, i)
+                          for f in range(F) for i in range(H)]))
 
 
 def row_lse(q, k, scale: float, rows=None) -> np.ndarray:

@@ -180,6 +180,58 @@ int csao_anchor_attention_rows(int32_t F, int32_t H, int32_t W, int32_t d, const
 }
 
 /* ------------------------------------------------------------------------------------------ */
+/* f1. Spatial similarity.  P:624-626: "We compute the cosine similarity between each P^(f,i)   */
+/* and its nearest anchor row, then average over f, i, and the input prompts to obtain s".      */
+/* P^(f,i) is the block of the dense map P (Eq. eq:p, all N keys) whose query rows are the W     */
+/* tokens (f,i,0..W-1) of spatial row i of frame f.  Readings (DESIGN.md */
+/* Q23-Q25): the cosine is that of the two W x N blocks flattened, pairing query (f,i,j) with    */
+/* (f,a(i),j); the average runs over every (f,i) including the anchor rows themselves (cos 1);   */
+/* a(i) is the nearest anchor of Q9.  This function returns cos for one (f,i) of one prompt.     */
+/* ------------------------------------------------------------------------------------------ */
+static int dense_prob_row(int64_t n, int32_t d, const double* qi, const double* k, double scale,
+                          double* p) {
+    double mx = -INFINITY;
+    for (int64_t j = 0; j < n; ++j) {
+        p[j] = dot_scaled(qi, k + j * d, d, scale);
+        if (p[j] > mx) mx = p[j];
+    }
+    double l = 0.0;
+    for (int64_t j = 0; j < n; ++j) l += exp(p[j] - mx);
+    const double lse = mx + log(l);
+    for (int64_t j = 0; j < n; ++j) p[j] = exp(p[j] - lse);
+    return ORC_OK;
+}
+
+int csao_spatial_cos(int32_t F, int32_t H, int32_t W, int32_t d, const double* q, const double* k,
+                     double scale, int32_t kA, int32_t f, int32_t i, double* cos_out) {
+    const int64_t n = (int64_t)F * H * W;
+    if (kA < 1 || kA > H || f < 0 || f >= F || i < 0 || i >= H) return ORC_EINVAL;
+    const int32_t m = csao_nearest_anchor(H, kA, i);
+    const int32_t a = (int32_t)(((int64_t)(2 * m + 1) * H) / (2 * kA));
+    double* pi = (double*)malloc(sizeof(double) * (size_t)n);
+    double* pa = (double*)malloc(sizeof(double) * (size_t)n);
+    if (!pi || !pa) {
+        free(pi);
+        free(pa);
+        return ORC_EINVAL;
+    }
+    double dot = 0.0, ni = 0.0, na = 0.0;
+    for (int32_t j = 0; j < W; ++j) {
+        dense_prob_row(n, d, q + csao_token_index(H, W, f, i, j) * d, k, scale, pi);
+        dense_prob_row(n, d, q + csao_token_index(H, W, f, a, j) * d, k, scale, pa);
+        for (int64_t t = 0; t < n; ++t) {
+            dot += pi[t] * pa[t];
+            ni += pi[t] * pi[t];
+            na += pa[t] * pa[t];
+        }
+    }
+    *cos_out = dot / (sqrt(ni) * sqrt(na));
+    free(pi);
+    free(pa);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------------------------ */
 /* a2. Row log-sum-exp over all N keys of the dense map P (Eq. eq:p), two-pass:       */
 /* lse_i = m_i + log sum_j exp(s_ij - m_i).  Rows [row_begin,row_end).                           */
 /* ------------------------------------------------------------------------------------------ */

@@ -405,3 +405,55 @@ def test_pair_work_list_covers_every_row_once(orc):
             covered += [(h, u) for u in members]
         expect = [(h, u) for h in (0, 2) for u in range(nb)] + [(1, u) for u in range(nu)]
         assert sorted(covered) == sorted(expect)
+
+
+# ---------------------------------------------------------------- f1: spatial similarity
+def _brute_spatial_cos(F, H, W, q, k, scale, kA, anchors_near):
+    """Materialised dense P (SciPy softmax), reshaped to [F, H, W, N]; Frobenius cosine of the
+    W x N blocks of row i and of its nearest anchor row (independent of the oracle)."""
+    p = scipy.special.softmax(scale * (q @ k.T), axis=1).reshape(F, H, W, -1)
+    out = np.empty((F, H))
+    for f in range(F):
+        for i in range(H):
+            a = anchors_near[i]
+            x, y = p[f, i].ravel(), p[f, a].ravel()
+            out[f, i] = x @ y / (np.linalg.norm(x) * np.linalg.norm(y))
+    return out
+
+
+def test_spatial_cos_equals_materialised_P(orc):
+    F, H, W, d = 2, 7, 5, 16
+    n = F * H * W
+    q, k, _ = _rand(n, d, 31)
+    for kA in (1, 3, 7):
+        a = orc.anchor_rows(H, kA)
+        near = [a[orc.nearest_anchor(H, kA, i)] for i in range(H)]
+        ref = _brute_spatial_cos(F, H, W, q, k, 0.3, kA, near)
+        got = np.array([[orc.spatial_cos(F, H, W, q, k, 0.3, kA, f, i) for i in range(H)]
+                        for f in range(F)])
+        assert np.max(np.abs(got - ref)) < 1e-12
+        # anchor rows are their own nearest anchor: cos = 1
+        for f in range(F):
+            for m in a:
+                assert abs(got[f, m] - 1.0) < 1e-14
+        assert abs(orc.spatial_similarity(F, H, W, q, k, 0.3, kA) - ref.mean()) < 1e-12
+
+
+def test_spatial_similarity_closed_forms(orc):
+    F, H, W, d = 2, 6, 4, 48
+    n = F * H * W
+    # k = H: every row is an anchor -> s = 1
+    q, k, _ = _rand(n, d, 32)
+    assert abs(orc.spatial_similarity(F, H, W, q, k, 0.5, H) - 1.0) < 1e-14
+    # queries independent of the spatial row (Obs. 4's ideal case) -> P^(f,i) = P^(f,a) -> s = 1
+    rng = np.random.default_rng(4)
+    base = rng.standard_normal((F, 1, W, d))
+    qr = np.broadcast_to(base, (F, H, W, d)).reshape(n, d)
+    for kA in (1, 2, 5):
+        assert abs(orc.spatial_similarity(F, H, W, qr, k, 0.5, kA) - 1.0) < 1e-13
+    # one-hot attention (query t attends to key t only): blocks of different rows are
+    # orthogonal -> cos = 0 except on the k anchor rows -> s = k/H
+    eye = 30.0 * np.eye(n, d)  # n = 48 <= d
+    for kA in (1, 2, 3, 6):
+        s = orc.spatial_similarity(F, H, W, eye, eye, 1.0, kA)
+        assert abs(s - kA / H) < 1e-12
