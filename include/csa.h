@@ -103,7 +103,8 @@ typedef struct {
 } csa_plan_t;
 
 /* Which workspace a call needs (csa_workspace_size). */
-enum { CSA_WS_CALIB = 0, CSA_WS_COMPILE = 1, CSA_WS_WORK_LIST = 2, CSA_WS_ATTN = 3 };
+enum { CSA_WS_CALIB = 0, CSA_WS_COMPILE = 1, CSA_WS_WORK_LIST = 2, CSA_WS_ATTN = 3,
+       CSA_WS_SIMILARITY = 4 };
 
 /* ------------------------------------------------------------------------------------------
  * csa_calib_accumulate -- one calibration prompt at one (t, l), all heads.
@@ -132,6 +133,28 @@ CSA_API csa_status_t csa_calib_accumulate(csa_layout_t L, int32_t n_heads, int32
                                   const float* lse_in, double eps, uint16_t* keep_count,
                                   float* energy_out, float* lse_out, void* workspace,
                                   size_t workspace_bytes, csa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * csa_spatial_similarity -- the repetitive-head statistic of one calibration prompt (f1),
+ * for every frame f and spatial row i, the cosine between P^(f,i) and P^(f,a(i)),
+ * where P^(f,i) are the rows of the dense map P = softmax(softmax_scale Q K^T) (all N keys,
+ * Eq. eq:p) of the W query tokens (f,i,0..W-1) and a(i) the nearest of the anchor rows
+ * floor((2m+1)H/(2k)) (tie -> lower).  Readings (Q23-Q25): Frobenius cosine of the two
+ * W x N blocks, query (f,i,j) paired with (f,a(i),j); the average runs over all (f,i).
+ *   q, k        bf16 [1, N, n_heads, head_dim] (batch index 0)
+ *   lse         fp32 [n_heads][N] natural-log row LSE of the same prompt (csa_calib_accumulate's
+ *               lse_out, or the dense forward's) -- required
+ *   sim_sum     fp64 [n_heads], accumulated in place: += sum over (f,i) of cos; after |D| prompts
+ *               s[h] = sim_sum[h] / (F * H * |D|) is the `similarity` of csa_compile_plan
+ *   cos_out     optional fp32 [n_heads][F*H] (this prompt's cos per (f,i))
+ * P is never materialised (one pass over the key tiles per (head, query block)); reductions run
+ * in a fixed order (bit-reproducible).  Workspace (required): csa_workspace_size(
+ * CSA_WS_SIMILARITY, L, n_heads, head_dim) bytes, 16-byte aligned, contents irrelevant. */
+CSA_API csa_status_t csa_spatial_similarity(csa_layout_t L, int32_t n_heads, int32_t head_dim,
+                                    float softmax_scale, csa_tensor_t q, csa_tensor_t k,
+                                    const float* lse, int32_t anchor_k, double* sim_sum,
+                                    float* cos_out, void* workspace, size_t workspace_bytes,
+                                    csa_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------
  * csa_compile_plan -- keep counts -> plan, for cells [0, n_cells).

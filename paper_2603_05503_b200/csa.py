@@ -52,7 +52,7 @@ class _PlanT(ctypes.Structure):
 
 EXPORTS = ["csa_calib_accumulate", "csa_compile_plan", "csa_build_work_list",
            "csa_sparse_attn_fwd", "csa_workspace_size", "csa_validate_plan", "csa_last_error",
-           "csa_version", "csa_debug_trace"]
+           "csa_version", "csa_debug_trace", "csa_spatial_similarity"]
 
 _lib = None
 
@@ -84,6 +84,9 @@ def lib() -> ctypes.CDLL:
     L.csa_sparse_attn_fwd.argtypes = [_LayoutT, i32, i32, i32, ctypes.c_float, _TensorT, _TensorT,
                                       _TensorT, _TensorT, vp, ctypes.POINTER(_PlanT), i64, vp, vp,
                                       i32, i32, vp, ctypes.c_size_t, vp]
+    L.csa_spatial_similarity.restype = st
+    L.csa_spatial_similarity.argtypes = [_LayoutT, i32, i32, ctypes.c_float, _TensorT, _TensorT,
+                                         vp, i32, vp, vp, vp, ctypes.c_size_t, vp]
     L.csa_debug_trace.restype = st
     L.csa_debug_trace.argtypes = [vp, i32]
     L.csa_validate_plan.restype = st
@@ -151,12 +154,33 @@ def calib_accumulate(lay: Layout, q: torch.Tensor, k: torch.Tensor, eps: float,
            "csa_calib_accumulate")
 
 
+def spatial_similarity(lay: Layout, q: torch.Tensor, k: torch.Tensor, lse: torch.Tensor,
+                       anchor_k: int, sim_sum: torch.Tensor, cos_out: torch.Tensor | None = None,
+                       scale: float | None = None, stream=None) -> None:
+    """csa_spatial_similarity (f1): sim_sum[h] += sum over (f, i) of
+    cos(P^(f,i), P^(f,a(i))) for one prompt; lse [heads * N] fp32 natural log (e.g. the
+    calibration pass's lse_out).  s[h] = sim_sum[h] / (F * H * prompts) feeds compile_plan."""
+    _, n, heads, d = q.shape
+    assert n == lay.N and lse.dtype == torch.float32 and lse.numel() == heads * n
+    assert sim_sum.dtype == torch.float64 and sim_sum.numel() == heads
+    if cos_out is not None:
+        assert cos_out.dtype == torch.float32 and cos_out.numel() == heads * lay.F * lay.H
+    sc = default_scale(d) if scale is None else scale
+    nbytes = lib().csa_workspace_size(4, _layout(lay), heads, d)
+    ws = _calib_workspace(q.device, nbytes, key="sim")
+    _check(lib().csa_spatial_similarity(_layout(lay), heads, d, sc, _tensor(q), _tensor(k),
+                                        _ptr(lse), int(anchor_k), _ptr(sim_sum), _ptr(cos_out),
+                                        _ptr(ws), nbytes, _stream(stream)),
+           "csa_spatial_similarity")
+
+
 _CALIB_WS: dict = {}
 
 
-def _calib_workspace(device, nbytes: int) -> torch.Tensor:
-    """Cached scratch for the single-pass calibration (grown on demand, one per device)."""
-    key = str(device)
+def _calib_workspace(device, nbytes: int, key: str = "calib") -> torch.Tensor:
+    """Cached scratch for the single-pass calibration / the similarity pass (grown on demand,
+    one per device and use)."""
+    key = f"{key}:{device}"
     buf = _CALIB_WS.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)

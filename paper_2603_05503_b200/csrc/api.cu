@@ -146,6 +146,10 @@ csa_status_t csa_debug_trace(void* buf, int32_t mode) {
 size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_t head_dim) {
     (void)head_dim;
     if (which == CSA_WS_ATTN) return 256;  // attention: dynamic-scheduler counters
+    if (which == CSA_WS_SIMILARITY) {     // per-token (dot, |p|^2, |p_a|^2) partials
+        if (check_layout(L, 0, 0) != CSA_OK || n_heads < 1) return 0;
+        return (size_t)n_heads * (size_t)L.frames * L.rows * L.cols * 3 * sizeof(float);
+    }
     if (which == CSA_WS_CALIB) {           // single-pass calibration: (t, m) row partials
         if (check_layout(L, 0, 0) != CSA_OK || n_heads < 1) return 0;
         DeviceInfo di;
@@ -193,6 +197,49 @@ csa_status_t csa_calib_accumulate(csa_layout_t L, int32_t n_heads, int32_t head_
     }
     cudaError_t e = csa::launch_calib(a, head_dim, tq, tk, di.sms, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "calib launch");
+    return ok();
+}
+
+csa_status_t csa_spatial_similarity(csa_layout_t L, int32_t n_heads, int32_t head_dim,
+                                    float softmax_scale, csa_tensor_t q, csa_tensor_t k,
+                                    const float* lse, int32_t anchor_k, double* sim_sum,
+                                    float* cos_out, void* workspace, size_t workspace_bytes,
+                                    csa_stream_t stream) {
+    csa_status_t st = check_layout(L, head_dim, n_heads);
+    if (st != CSA_OK) return st;
+    if (n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "n_heads must be >= 1");
+    if (!(softmax_scale > 0.0f)) return fail(CSA_ERR_INVALID_ARGUMENT, "softmax_scale <= 0");
+    if (anchor_k < 1 || anchor_k > L.rows)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "anchor_k %d outside [1, rows=%d]", anchor_k, L.rows);
+    if (!lse || !sim_sum) return fail(CSA_ERR_INVALID_ARGUMENT, "lse and sim_sum are required");
+    const size_t need = csa_workspace_size(CSA_WS_SIMILARITY, L, n_heads, head_dim);
+    if (!workspace || workspace_bytes < need)
+        return fail(CSA_ERR_INVALID_ARGUMENT,
+                    "workspace smaller than csa_workspace_size(CSA_WS_SIMILARITY) = %zu", need);
+    if (reinterpret_cast<uintptr_t>(workspace) % 16 != 0)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "workspace must be 16-byte aligned");
+    if (!q.ptr || (q.stride_n * 2) % 16 || (q.stride_h * 2) % 16)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "q: null or strides not 16-byte multiples");
+    DeviceInfo di;
+    if ((st = device_info(&di)) != CSA_OK) return st;
+    const csa::Geo g = csa::make_geo(L);
+    CUtensorMap tq, tk;
+    if ((st = make_map(&tq, q, 1, g.N, n_heads, head_dim, g.B, "q")) != CSA_OK) return st;
+    if ((st = make_map(&tk, k, 1, g.N, n_heads, head_dim, g.B, "k")) != CSA_OK) return st;
+    csa::SimArgs a;
+    a.g = g;
+    a.n_heads = n_heads;
+    a.scale_log2 = softmax_scale * 1.4426950408889634f;
+    a.q = static_cast<const __nv_bfloat16*>(q.ptr);
+    a.q_sn = q.stride_n;
+    a.q_sh = q.stride_h;
+    a.lse = lse;
+    a.anchor_k = anchor_k;
+    a.partials = static_cast<float*>(workspace);
+    a.sim_sum = sim_sum;
+    a.cos_out = cos_out;
+    cudaError_t e = csa::launch_similarity(a, head_dim, tq, tk, di.sms, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "similarity launch");
     return ok();
 }
 

@@ -82,6 +82,22 @@ cudaError_t set_calib_trace(void* buf, int mode);
 cudaError_t launch_calib(const CalibArgs& a, int head_dim, const CUtensorMap& tq,
                          const CUtensorMap& tk, int num_sms, cudaStream_t s);
 
+// f1 spatial similarity (sim.cu)
+struct SimArgs {
+    Geo g;
+    int32_t n_heads;
+    float scale_log2;
+    const __nv_bfloat16* q;  // batch 0, for the anchor-row gather
+    int64_t q_sn, q_sh;
+    const float* lse;        // [n_heads][N] natural log
+    int32_t anchor_k;
+    float* partials;         // workspace [n_heads][N][3]
+    double* sim_sum;         // [n_heads] += sum over (f, i) of cos
+    float* cos_out;          // optional [n_heads][F*H]
+};
+cudaError_t launch_similarity(const SimArgs& a, int head_dim, const CUtensorMap& tq,
+                              const CUtensorMap& tk, int num_sms, cudaStream_t s);
+
 struct AttnArgs {
     Geo g;
     int32_t batch;

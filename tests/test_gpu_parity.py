@@ -369,3 +369,71 @@ def test_pair_kernel_matches_single_and_oracle(csa, lay, heads):
                              rep_k=5 if h in rep else None, rows=rows)
         assert_close(pair[0, rows[0]:rows[1], h].double().cpu().numpy(), ref, f"h{h} r{r}")
         assert_close(single[0, rows[0]:rows[1], h].double().cpu().numpy(), ref, f"h{h} r{r}")
+
+
+# ---------------------------------------------------------------- f1 spatial similarity
+def _gpu_similarity(csa, lay, q, k, kA, reps=1):
+    heads = q.shape[2]
+    nb = lay.NB
+    lse = torch.empty(heads * lay.N, dtype=torch.float32, device="cuda")
+    counts = u16_zeros(heads * nb * nb)
+    csa.calib_accumulate(lay, q, k, 0.9, counts, lse_out=lse)   # the pass's own LSE
+    sim = torch.zeros(heads, dtype=torch.float64, device="cuda")
+    cos = torch.empty(heads * lay.F * lay.H, dtype=torch.float32, device="cuda")
+    for _ in range(reps):
+        csa.spatial_similarity(lay, q, k, lse, kA, sim, cos_out=cos)
+    torch.cuda.synchronize()
+    return sim.cpu().numpy(), cos.view(heads, lay.F, lay.H).double().cpu().numpy()
+
+
+@pytest.mark.parametrize("lay,heads,d", [(Layout(2, 5, 25, 64), 2, 64), (Layout(2, 9, 40, 128), 2, 128)])
+@pytest.mark.parametrize("kind", ["random", "structured"])
+def test_spatial_similarity_against_oracle(csa, lay, heads, d, kind):
+    if kind == "random":
+        q, k, _ = qkv(1, lay.N, heads, d, seed=41, device="cuda")
+    else:
+        q, k, _ = inputs.structured_qk(lay, heads, d, 3, 1, alpha=[0.9, 1.4], repetitive=(1,),
+                                       device="cuda")
+    scale = 1.0 / np.sqrt(d)
+    for kA in (1, 2, lay.H):
+        sim, cos = _gpu_similarity(csa, lay, q, k, kA)
+        for h in range(heads):
+            qh, kh = head64(q, 0, h), head64(k, 0, h)
+            ref = np.array([[oracle.spatial_cos(lay.F, lay.H, lay.W, qh, kh, scale, kA, f, i)
+                             for i in range(lay.H)] for f in range(lay.F)])
+            assert np.abs(cos[h] - ref).max() <= 2e-5, (kind, kA, h)
+            assert abs(sim[h] - cos[h].sum()) <= 1e-7 * lay.F * lay.H  # cos_out is fp32
+            assert abs(sim[h] / (lay.F * lay.H) - ref.mean()) <= 2e-5
+        if kA == lay.H:
+            assert np.abs(cos - 1.0).max() <= 1e-5  # every row is its own anchor
+
+
+def test_spatial_similarity_repetitive_structure_and_accumulation(csa):
+    lay = Layout(2, 9, 40, 128)
+    heads = 2
+    q, k, _ = qkv(1, lay.N, heads, 128, seed=43, device="cuda")
+    # queries independent of the spatial row: P^(f,i) = P^(f,a(i)) -> cos = 1 (Obs. 4)
+    q3 = q.view(1, lay.F, lay.H, lay.W, heads, 128)
+    qr = q3[:, :, :1].expand(-1, -1, lay.H, -1, -1, -1).reshape(1, lay.N, heads, 128).contiguous()
+    sim, cos = _gpu_similarity(csa, lay, qr, k, 3)
+    assert np.abs(cos - 1.0).max() <= 1e-5
+    # sim_sum accumulates across prompts; repeated runs are bitwise identical
+    s1, c1 = _gpu_similarity(csa, lay, q, k, 3, reps=1)
+    s2, c2 = _gpu_similarity(csa, lay, q, k, 3, reps=2)
+    assert np.array_equal(c1, c2)
+    assert np.array_equal(2 * s1, s2)
+
+
+def test_spatial_similarity_wan480_sampled(csa):
+    cfg = CONFIGS["wan480"]
+    lay = cfg.layout
+    heads = 2
+    q, k, _ = inputs.structured_qk(lay, heads, cfg.d, 5, 0, alpha=[1.0, 1.3], repetitive=(1,),
+                                   device="cuda")
+    sim, cos = _gpu_similarity(csa, lay, q, k, 5)
+    scale = 1.0 / np.sqrt(cfg.d)
+    for h, f, i in ((0, 0, 0), (0, 20, 29), (1, 7, 13), (1, 0, 3)):
+        qh, kh = head64(q, 0, h), head64(k, 0, h)
+        ref = oracle.spatial_cos(lay.F, lay.H, lay.W, qh, kh, scale, 5, f, i)
+        assert abs(cos[h, f, i] - ref) <= 2e-5, (h, f, i)
+    assert sim[1] / (lay.F * lay.H) > sim[0] / (lay.F * lay.H)  # the repetitive head scores higher
