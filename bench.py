@@ -136,14 +136,21 @@ def workload(cfg, args, heads_lo, heads_hi, rank_dev):
                            device=rank_dev).view(torch.uint16)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    lse = torch.empty(cfg.heads * lay.N, dtype=torch.float32, device=rank_dev)
+    sim_sum = torch.zeros(cfg.heads, dtype=torch.float64, device=rank_dev)
     for p in range(n_prompts):
         qc, kc, _ = inputs.structured_qk(lay, cfg.heads, cfg.d, head_seed=1, prompt_seed=p,
                                          alpha=alphas, repetitive=tuple(sorted(rep)),
                                          device=rank_dev)
-        csa.calib_accumulate(lay, qc, kc, eps, counts_t)
+        csa.calib_accumulate(lay, qc, kc, eps, counts_t, lse_out=lse)   # a2-a5
+        csa.spatial_similarity(lay, qc, kc, lse, 5, sim_sum)            # f1
         del qc, kc
     torch.cuda.synchronize()
     calib_s = time.perf_counter() - t0
+    s_head = (sim_sum / (lay.F * lay.H * n_prompts)).cpu().numpy()
+    # REPETITIVE where s > gamma = 0.87 (strict, Q8): the decision is the data's,
+    # not the generator's labels (which are only reported next to it)
+    detected = {h for h in range(cfg.heads) if s_head[h] > 0.87}
     counts = counts_t.view(torch.int16).cpu().numpy().view(np.uint16).reshape(
         cfg.heads, lay.NB, lay.NB)
     min_count = math.ceil(0.5 * n_prompts)
@@ -155,8 +162,11 @@ def workload(cfg, args, heads_lo, heads_hi, rank_dev):
         cfg.heads, lay.NB, w32 * 32)[:, :, :lay.NB]
     masks[:] = unpacked
     calib = {"prompts": n_prompts, "t": t, "T": T, "eps": round(eps, 6), "min_count": min_count,
-             "wall_s_incl_generator": round(calib_s, 3)}
-    return lay, masks, rep, counts, min_count, calib
+             "wall_s_incl_generator": round(calib_s, 3),
+             "similarity": [round(float(x), 4) for x in s_head], "gamma": 0.87,
+             "repetitive_detected": sorted(detected),
+             "repetitive_generated": sorted(rep)}
+    return lay, masks, detected, counts, min_count, calib
 
 
 def flops_of(lay, masks, rep, heads, d, batch, anchor_k=5):
@@ -280,7 +290,8 @@ def main():
     # ---- plan for this rank's heads (a6 through the C ABI), REPETITIVE via similarity > gamma
     counts_np = np.ascontiguousarray(counts_all[h_lo:h_hi], dtype=np.uint16)
     counts = torch.from_numpy(counts_np.reshape(-1).view(np.int16)).to(dev).view(torch.uint16)
-    sim = torch.tensor([1.0 if h in rep else 0.0 for h in my_heads], dtype=torch.float64, device=dev)
+    sim = torch.tensor([calib["similarity"][h] if calib is not None else (1.0 if h in rep else 0.0)
+                        for h in my_heads], dtype=torch.float64, device=dev)
     t0 = time.perf_counter()
     plan = csa.compile_plan(lay, counts, min_count, similarity=sim, gamma=0.87, anchor_k=5)
     # pair items for the CTA-pair kernel (block 128, d 128), else head-major single items
@@ -427,6 +438,12 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
     t_cal, _ = time_loop(lambda: csa.calib_accumulate(lay, q[:1], k[:1], eps, counts_c), 1, 1, stream)
     t_cal2, _ = time_loop(lambda: csa.calib_accumulate(lay, q[:1], k[:1], eps, counts_c,
                                                        single_pass=False), 1, 1, stream)
+    lse_c = torch.empty(H * lay.N, dtype=torch.float32, device=dev)
+    csa.calib_accumulate(lay, q[:1], k[:1], eps, counts_c, lse_out=lse_c)
+    sim_c = torch.zeros(H, dtype=torch.float64, device=dev)
+    t_sim, _ = time_loop(lambda: csa.spatial_similarity(lay, q[:1], k[:1], lse_c, 5, sim_c), 1, 1,
+                         stream)
+    ph["spatial_similarity_ms"] = round(t_sim, 3)          # f1: 2 exps per score
     ph["calib_accumulate_ms"] = round(t_cal, 3)             # single exponential pass (scratch)
     ph["calib_accumulate_two_pass_ms"] = round(t_cal2, 3)   # LSE pass + E pass
     calib_exps = 1.0 * H * float(lay.N) ** 2                 # one exp per score
