@@ -67,6 +67,14 @@ def lib():
         L.csao_spatial_cos.restype = ctypes.c_int
         L.csao_spatial_cos.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _p, _p, _c_dbl, _c_i32,
                                        _c_i32, _c_i32, _p]
+        L.csao_percentile_nearest_rank.restype = _c_i32
+        L.csao_percentile_nearest_rank.argtypes = [_c_i64, _p, _c_dbl]
+        L.csao_merge_row.restype = _c_i32
+        L.csao_merge_row.argtypes = [_c_i32, _p, _c_i32, _p]
+        L.csao_skipped_iou.restype = _c_dbl
+        L.csao_skipped_iou.argtypes = [_c_i64, _p, _p]
+        L.csao_cluster_timesteps.restype = _c_i32
+        L.csao_cluster_timesteps.argtypes = [_c_i32, _p, _c_dbl, _p]
         L.csao_row_lse.restype = ctypes.c_int
         L.csao_row_lse.argtypes = [_c_i64, _c_i32, _p, _p, _c_dbl, _c_i64, _c_i64, _p]
         L.csao_block_energy_rows.restype = ctypes.c_int
@@ -179,6 +187,41 @@ def spatial_similarity(F, H, W, q, k, scale: float, kA: int) -> float:
     """s of one prompt: mean of spatial_cos over every (f, i) (reading Q24)."""
     return float(np.mean([spatial_cos(F, H, W, q, k, scale, kA, f, i)
                           for f in range(F) for i in range(H)]))
+
+
+def percentile_nearest_rank(values, p: float) -> int:
+    """Nearest-rank p-th percentile (sorted ascending, element ceil(p/100 n)); reading Q26."""
+    v = np.ascontiguousarray(values, dtype=np.int32)
+    out = lib().csao_percentile_nearest_rank(v.size, _ptr(v), float(p))
+    if out < 0:
+        raise ValueError("percentile: need n > 0 and 0 < p <= 100")
+    return int(out)
+
+
+def merge_row(intervals, target: int):
+    """Greedy smallest-gap (leftmost) merging of one row's intervals until count <= target
+    (reading Q28).  Returns (merged [(s, e), ...], added blocks)."""
+    iv = np.ascontiguousarray(np.asarray(intervals, dtype=np.uint16).reshape(-1, 2))
+    added = np.zeros(1, np.int64)
+    n = lib().csao_merge_row(iv.shape[0], _ptr(iv), int(target), _ptr(added))
+    return [tuple(int(x) for x in iv[i]) for i in range(n)], int(added[0])
+
+
+def skipped_iou(kept1, kept2) -> float:
+    """|S1 & S2| / |S1 | S2| over skipped blocks (Eq. eq:timestep_iou); 1 if both empty."""
+    a = np.ascontiguousarray(kept1, dtype=np.uint8).ravel()
+    b = np.ascontiguousarray(kept2, dtype=np.uint8).ravel()
+    assert a.size == b.size
+    return float(lib().csao_skipped_iou(a.size, _ptr(a), _ptr(b)))
+
+
+def cluster_timesteps(iou, tau: float):
+    """Greedy cliques over timesteps (reading Q27).  Returns cluster ids [T]."""
+    m = np.ascontiguousarray(iou, dtype=np.float64)
+    T = m.shape[0]
+    out = np.empty(T, np.int32)
+    lib().csao_cluster_timesteps(T, _ptr(m), float(tau), _ptr(out))
+    return out
 
 
 def row_lse(q, k, scale: float, rows=None) -> np.ndarray:

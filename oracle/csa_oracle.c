@@ -400,6 +400,87 @@ int csao_compile_cell(int64_t n, int32_t b, int32_t F, int32_t H, int32_t W,
 }
 
 /* ------------------------------------------------------------------------------------------ */
+/* f2. Plan memory compaction (Table tab:skip_list_memory).             */
+/* Interval merging: "progressively merging nearby intervals, which intentionally      */
+/* marks a small number of additional blocks for computation"; the merge percentile p of the    */
+/* table sets the target row width.  Readings (Q26-Q28): target = nearest-rank p-th    */
+/* percentile of the per-row interval counts over all rows of the collection; a row above the   */
+/* target repeatedly merges the adjacent pair with the smallest gap (leftmost on ties), the gap */
+/* blocks becoming kept, until its count <= target.                                             */
+/* ------------------------------------------------------------------------------------------ */
+static int cmp_i32(const void* a, const void* b) {
+    const int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+    return (x > y) - (x < y);
+}
+
+/* nearest-rank percentile: sorted ascending, element ceil(p/100 * n) (1-based), p in (0,100] */
+int32_t csao_percentile_nearest_rank(int64_t n, const int32_t* values, double p) {
+    if (n <= 0 || !(p > 0.0) || p > 100.0) return -1;
+    int32_t* v = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+    if (!v) return -1;
+    memcpy(v, values, sizeof(int32_t) * (size_t)n);
+    qsort(v, (size_t)n, sizeof(int32_t), cmp_i32);
+    int64_t rank = (int64_t)ceil(p / 100.0 * (double)n);
+    if (rank < 1) rank = 1;
+    const int32_t out = v[rank - 1];
+    free(v);
+    return out;
+}
+
+/* ivl: [n][2] half-open (start, end), ascending, disjoint, non-adjacent; merged in place.
+ * Returns the new interval count; *added = blocks newly marked kept. */
+int32_t csao_merge_row(int32_t n, uint16_t* ivl, int32_t target, int64_t* added) {
+    *added = 0;
+    while (n > target && n > 1) {
+        int32_t best = 0;
+        int32_t best_gap = (int32_t)ivl[2] - (int32_t)ivl[1];
+        for (int32_t i = 1; i + 1 < n; ++i) {
+            const int32_t gap = (int32_t)ivl[2 * (i + 1)] - (int32_t)ivl[2 * i + 1];
+            if (gap < best_gap) { best = i; best_gap = gap; } /* strict: leftmost on ties */
+        }
+        *added += best_gap;
+        ivl[2 * best + 1] = ivl[2 * (best + 1) + 1];
+        for (int32_t i = best + 1; i + 1 < n; ++i) {
+            ivl[2 * i] = ivl[2 * (i + 1)];
+            ivl[2 * i + 1] = ivl[2 * (i + 1) + 1];
+        }
+        --n;
+    }
+    return n;
+}
+
+/* Timestep sharing: IoU of the skipped-block sets (Eq. eq:timestep_iou); greedy
+ * cliques: timesteps in ascending order, each joins the earliest-created cluster whose every
+ * member has IoU >= tau with it (Q27: the table caption's ">= tau"), else opens a new one; the
+ * cluster's shared mask is the OR of the members' kept-block masks. */
+double csao_skipped_iou(int64_t len, const uint8_t* kept1, const uint8_t* kept2) {
+    int64_t inter = 0, uni = 0;
+    for (int64_t x = 0; x < len; ++x) {
+        const int s1 = !kept1[x], s2 = !kept2[x];
+        inter += s1 & s2;
+        uni += s1 | s2;
+    }
+    return uni == 0 ? 1.0 : (double)inter / (double)uni;
+}
+
+/* iou: [T][T]; cluster_out[t] = index of t's cluster (clusters numbered by creation order).
+ * Returns the number of clusters. */
+int32_t csao_cluster_timesteps(int32_t T, const double* iou, double tau, int32_t* cluster_out) {
+    int32_t n_clusters = 0;
+    for (int32_t t = 0; t < T; ++t) {
+        int32_t joined = -1;
+        for (int32_t c = 0; c < n_clusters && joined < 0; ++c) {
+            int32_t ok = 1;
+            for (int32_t u = 0; u < t && ok; ++u)
+                if (cluster_out[u] == c && !(iou[t * T + u] >= tau)) ok = 0;
+            if (ok) joined = c;
+        }
+        cluster_out[t] = joined >= 0 ? joined : n_clusters++;
+    }
+    return n_clusters;
+}
+
+/* ------------------------------------------------------------------------------------------ */
 /* Work list for one launch over n_heads consecutive cells (not in the paper: the scheduling    */
 /* artefact of DESIGN.md; its order is a total order so the output is unique).                 */
 /*   MASK head h: items (h, r) for r < N_B, cost = nnz of row r;                                */

@@ -457,3 +457,90 @@ def test_spatial_similarity_closed_forms(orc):
     for kA in (1, 2, 3, 6):
         s = orc.spatial_similarity(F, H, W, eye, eye, 1.0, kA)
         assert abs(s - kA / H) < 1e-12
+
+
+# ---------------------------------------------------------------- f2: plan compaction
+def test_percentile_nearest_rank_textbook(orc):
+    v = [15, 20, 35, 40, 50]  # the standard nearest-rank example
+    assert [orc.percentile_nearest_rank(v, p) for p in (5, 30, 40, 50, 100)] == [15, 20, 20, 35, 50]
+    assert orc.percentile_nearest_rank(list(range(1, 11)), 90) == 9
+    assert orc.percentile_nearest_rank([7] * 3, 100) == 7
+
+
+def test_merge_row_worked_example_and_ties(orc):
+    assert orc.merge_row([(0, 2), (3, 4), (10, 12)], 2) == ([(0, 4), (10, 12)], 1)
+    assert orc.merge_row([(0, 1), (2, 3), (4, 5)], 2) == ([(0, 3), (4, 5)], 1)      # tie: leftmost
+    assert orc.merge_row([(0, 1), (5, 6)], 3) == ([(0, 1), (5, 6)], 0)              # within target
+    assert orc.merge_row([(0, 1), (5, 6), (9, 10)], 1) == ([(0, 10)], 7)
+
+
+def test_merge_row_is_optimal_against_subset_brute_force(orc):
+    """Merging two adjacent intervals removes exactly the gap between them, so reaching `target`
+    removes n - target gaps: the minimum total of added blocks is the sum of the n - target
+    smallest gaps (checked by enumerating every gap subset), and the result must decode to a
+    superset of the row with at most `target` intervals."""
+    rng = np.random.default_rng(8)
+    for _ in range(300):
+        nb = int(rng.integers(4, 40))
+        row = rng.random(nb) < rng.uniform(0.2, 0.7)
+        row[int(rng.integers(nb))] = True
+        ivl, c = [], 0
+        while c < nb:
+            if row[c]:
+                s = c
+                while c < nb and row[c]:
+                    c += 1
+                ivl.append((s, c))
+            else:
+                c += 1
+        n = len(ivl)
+        target = int(rng.integers(1, n + 1))
+        merged, added = orc.merge_row(ivl, target)
+        gaps = [ivl[i + 1][0] - ivl[i][1] for i in range(n - 1)]
+        best = min((sum(gaps[i] for i in sub) for sub in itertools.combinations(range(n - 1), n - target)),
+                   default=0)
+        assert added == best and len(merged) == min(n, max(target, 1))
+        kept = np.zeros(nb, bool)
+        for s_, e_ in merged:
+            kept[s_:e_] = True
+        assert kept[row].all() and kept.sum() == row.sum() + added
+
+
+def test_skipped_iou_and_timestep_clusters(orc):
+    # S:463: skipped {(0,1),(0,2)} vs {(0,2),(1,3)} over a 2x4 mask -> 1/3
+    k1 = np.ones((2, 4), np.uint8)
+    k2 = np.ones((2, 4), np.uint8)
+    k1[0, 1] = k1[0, 2] = 0
+    k2[0, 2] = k2[1, 3] = 0
+    assert orc.skipped_iou(k1, k2) == 1.0 / 3.0
+    assert orc.skipped_iou(k1, k1) == 1.0
+    assert orc.skipped_iou(np.ones(5), np.ones(5)) == 1.0  # nothing skipped
+    a, b = np.array([0, 1, 1]), np.array([1, 0, 1])
+    assert orc.skipped_iou(a, b) == 0.0
+    # S:479: {t0, t1} mutually >= tau; t2 >= tau with t1 only; t3 isolated
+    iou = np.eye(4)
+    iou[0, 1] = iou[1, 0] = 0.99
+    iou[1, 2] = iou[2, 1] = 0.99
+    iou[0, 2] = iou[2, 0] = 0.5
+    assert orc.cluster_timesteps(iou, 0.97).tolist() == [0, 0, 1, 2]
+    assert orc.cluster_timesteps(np.ones((5, 5)), 0.98).tolist() == [0] * 5
+    assert orc.cluster_timesteps(np.eye(4) * 0 + np.eye(4), 1.0).tolist() == [0, 1, 2, 3]
+
+
+def test_timestep_clusters_are_cliques_and_greedy(orc):
+    rng = np.random.default_rng(9)
+    for _ in range(200):
+        T = int(rng.integers(2, 12))
+        m = rng.random((T, T))
+        iou = (m + m.T) / 2
+        np.fill_diagonal(iou, 1.0)
+        tau = float(rng.uniform(0.3, 0.8))
+        cl = orc.cluster_timesteps(iou, tau)
+        for c in set(cl.tolist()):
+            mem = np.flatnonzero(cl == c)
+            assert all(iou[x, y] >= tau for x in mem for y in mem)
+        # greedy: t could not join any cluster created before its own
+        for t in range(T):
+            for c in range(cl[t]):
+                earlier = [u for u in range(t) if cl[u] == c]
+                assert not all(iou[t, u] >= tau for u in earlier)
