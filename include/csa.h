@@ -104,7 +104,7 @@ typedef struct {
 
 /* Which workspace a call needs (csa_workspace_size). */
 enum { CSA_WS_CALIB = 0, CSA_WS_COMPILE = 1, CSA_WS_WORK_LIST = 2, CSA_WS_ATTN = 3,
-       CSA_WS_SIMILARITY = 4 };
+       CSA_WS_SIMILARITY = 4, CSA_WS_MERGE = 5 };
 
 /* ------------------------------------------------------------------------------------------
  * csa_calib_accumulate -- one calibration prompt at one (t, l), all heads.
@@ -173,6 +173,40 @@ CSA_API csa_status_t csa_compile_plan(csa_layout_t L, int64_t n_cells, const uin
                               int32_t min_count, const double* similarity, double gamma,
                               int32_t anchor_k, int32_t phase, const csa_plan_t* plan,
                               void* workspace, size_t workspace_bytes, csa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * csa_merge_intervals -- interval merging of a compiled plan (f2, Table
+ * tab:skip_list_memory "Merge %").  target = nearest-rank `percentile`-th percentile (0 < p <=
+ * 100) of the per-row interval counts over every row of the MASK cells [0, n_cells) (DESIGN.md
+ * Q26); every row with more intervals fills its (count - target) smallest gaps, ties -> leftmost
+ * (= repeated smallest-gap merging, Q28): the gap blocks' keep_count entries are set to
+ * min_count, so csa_compile_plan on the same counts yields the merged plan (kept set superset of
+ * the original, at most max(target, 1) intervals per row).  REPETITIVE cells are skipped.
+ *   plan        compiled from keep_count with this min_count (read only)
+ *   keep_count  uint16 [n_cells][N_B][N_B], updated in place
+ *   target_out  device int32 (the width reached);  added_out device uint64, += blocks added
+ * Workspace: csa_workspace_size(CSA_WS_MERGE, ...) bytes (device, 4-byte aligned). */
+CSA_API csa_status_t csa_merge_intervals(csa_layout_t L, int64_t n_cells, const csa_plan_t* plan,
+                                 double percentile, int32_t min_count, uint16_t* keep_count,
+                                 int32_t* target_out, unsigned long long* added_out,
+                                 void* workspace, size_t workspace_bytes, csa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * csa_share_timesteps -- timestep mask sharing (f2, Eq. eq:timestep_iou).  Cells
+ * are (t, g) = t * n_groups + g for t < n_steps (g e.g. = l * n_heads + h).  Per group: the IoU
+ * of the compiled masks' skipped-block sets for every pair (t1, t2) (1 when both are empty),
+ * greedy cliques over t ascending -- t joins the earliest-created clique whose every member has
+ * IoU >= tau with it (Q27), else opens one -- and the OR of each clique's kept masks written to
+ * every member's keep_count as min_count * M_shared, so csa_compile_plan gives all members one
+ * identical mask.  REPETITIVE cells: IoU -1 with everything, singleton cliques, counts untouched.
+ *   plan         compiled from keep_count with this min_count (read only)
+ *   keep_count   uint16 [n_steps * n_groups][N_B][N_B], updated in place
+ *   cluster_out  device int32 [n_groups][n_steps] clique index (creation order)
+ *   iou_out      device fp64 [n_groups][n_steps][n_steps] (required; also the scratch) */
+CSA_API csa_status_t csa_share_timesteps(csa_layout_t L, int32_t n_groups, int32_t n_steps,
+                                 const csa_plan_t* plan, double tau, int32_t min_count,
+                                 uint16_t* keep_count, int32_t* cluster_out, double* iou_out,
+                                 csa_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------
  * csa_build_work_list -- items of one attention launch over heads [0, n_heads) whose cells are

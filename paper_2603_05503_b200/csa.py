@@ -52,7 +52,8 @@ class _PlanT(ctypes.Structure):
 
 EXPORTS = ["csa_calib_accumulate", "csa_compile_plan", "csa_build_work_list",
            "csa_sparse_attn_fwd", "csa_workspace_size", "csa_validate_plan", "csa_last_error",
-           "csa_version", "csa_debug_trace", "csa_spatial_similarity"]
+           "csa_version", "csa_debug_trace", "csa_spatial_similarity", "csa_merge_intervals",
+           "csa_share_timesteps"]
 
 _lib = None
 
@@ -87,6 +88,12 @@ def lib() -> ctypes.CDLL:
     L.csa_spatial_similarity.restype = st
     L.csa_spatial_similarity.argtypes = [_LayoutT, i32, i32, ctypes.c_float, _TensorT, _TensorT,
                                          vp, i32, vp, vp, vp, ctypes.c_size_t, vp]
+    L.csa_merge_intervals.restype = st
+    L.csa_merge_intervals.argtypes = [_LayoutT, i64, ctypes.POINTER(_PlanT), ctypes.c_double, i32,
+                                      vp, vp, vp, vp, ctypes.c_size_t, vp]
+    L.csa_share_timesteps.restype = st
+    L.csa_share_timesteps.argtypes = [_LayoutT, i32, i32, ctypes.POINTER(_PlanT), ctypes.c_double,
+                                      i32, vp, vp, vp, vp]
     L.csa_debug_trace.restype = st
     L.csa_debug_trace.argtypes = [vp, i32]
     L.csa_validate_plan.restype = st
@@ -273,6 +280,42 @@ def compile_plan(lay: Layout, keep_count: torch.Tensor, min_count: int,
     p.kind_host = p.kind.cpu().tolist()
     p.anchor_k_host = p.anchor_k.cpu().tolist()
     return p
+
+
+def merge_intervals(plan: Plan, keep_count: torch.Tensor, min_count: int, percentile: float,
+                    stream=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """csa_merge_intervals (f2): fills the smallest gaps of rows wider than the
+    nearest-rank `percentile` of the plan's row widths, in keep_count (in place).  Recompile with
+    compile_plan(keep_count, min_count) for the merged plan.  Returns device (target, added)."""
+    dev = keep_count.device
+    assert keep_count.dtype == torch.uint16 and keep_count.is_contiguous()
+    target = torch.zeros(1, dtype=torch.int32, device=dev)
+    added = torch.zeros(1, dtype=torch.int64, device=dev)
+    nbytes = lib().csa_workspace_size(5, _layout(plan.lay), 0, 0)
+    ws = torch.empty(max(nbytes, 4), dtype=torch.uint8, device=dev)
+    s = plan.struct()
+    _check(lib().csa_merge_intervals(_layout(plan.lay), plan.n_cells, ctypes.byref(s),
+                                     float(percentile), int(min_count), _ptr(keep_count),
+                                     _ptr(target), _ptr(added), _ptr(ws), nbytes, _stream(stream)),
+           "csa_merge_intervals")
+    return target, added
+
+
+def share_timesteps(plan: Plan, keep_count: torch.Tensor, n_groups: int, n_steps: int,
+                    min_count: int, tau: float, stream=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """csa_share_timesteps (f2) over cells (t, g) = t * n_groups + g: skipped-set
+    IoU, greedy cliques with IoU >= tau, OR-shared masks written into keep_count (in place).
+    Returns device (cluster [n_groups, n_steps] int32, iou [n_groups, n_steps, n_steps] fp64)."""
+    dev = keep_count.device
+    assert keep_count.dtype == torch.uint16 and keep_count.is_contiguous()
+    cluster = torch.empty((n_groups, n_steps), dtype=torch.int32, device=dev)
+    iou = torch.empty((n_groups, n_steps, n_steps), dtype=torch.float64, device=dev)
+    s = plan.struct()
+    _check(lib().csa_share_timesteps(_layout(plan.lay), int(n_groups), int(n_steps),
+                                     ctypes.byref(s), float(tau), int(min_count), _ptr(keep_count),
+                                     _ptr(cluster), _ptr(iou), _stream(stream)),
+           "csa_share_timesteps")
+    return cluster, iou
 
 
 def validate_plan(plan: Plan, n_cells: int | None = None, stream=None) -> None:

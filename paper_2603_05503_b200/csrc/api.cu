@@ -146,6 +146,10 @@ csa_status_t csa_debug_trace(void* buf, int32_t mode) {
 size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_t head_dim) {
     (void)head_dim;
     if (which == CSA_WS_ATTN) return 256;  // attention: dynamic-scheduler counters
+    if (which == CSA_WS_MERGE) {          // interval-width histogram
+        if (check_layout(L, 0, 0) != CSA_OK) return 0;
+        return (size_t)(csa::make_geo(L).NB + 1) * sizeof(int32_t);
+    }
     if (which == CSA_WS_SIMILARITY) {     // per-token (dot, |p|^2, |p_a|^2) partials
         if (check_layout(L, 0, 0) != CSA_OK || n_heads < 1) return 0;
         return (size_t)n_heads * (size_t)L.frames * L.rows * L.cols * 3 * sizeof(float);
@@ -240,6 +244,58 @@ csa_status_t csa_spatial_similarity(csa_layout_t L, int32_t n_heads, int32_t hea
     a.cos_out = cos_out;
     cudaError_t e = csa::launch_similarity(a, head_dim, tq, tk, di.sms, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "similarity launch");
+    return ok();
+}
+
+csa_status_t csa_merge_intervals(csa_layout_t L, int64_t n_cells, const csa_plan_t* plan,
+                                 double percentile, int32_t min_count, uint16_t* keep_count,
+                                 int32_t* target_out, unsigned long long* added_out,
+                                 void* workspace, size_t workspace_bytes, csa_stream_t stream) {
+    csa_status_t st = check_layout(L, 0, 0);
+    if (st != CSA_OK) return st;
+    if (n_cells < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "n_cells must be >= 1");
+    if (!(percentile > 0.0) || percentile > 100.0)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "percentile must be in (0, 100]");
+    if (min_count < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "min_count must be >= 1");
+    if (!plan_ptrs_ok(plan, true) || plan->n_cells < n_cells)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "plan: missing buffers or fewer than n_cells cells");
+    if (!keep_count || !target_out || !added_out)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "keep_count, target_out and added_out are required");
+    const size_t need = csa_workspace_size(CSA_WS_MERGE, L, 0, 0);
+    if (!workspace || workspace_bytes < need || reinterpret_cast<uintptr_t>(workspace) % 4)
+        return fail(CSA_ERR_INVALID_ARGUMENT,
+                    "workspace: need %zu bytes (csa_workspace_size(CSA_WS_MERGE)), 4-byte aligned",
+                    need);
+    DeviceInfo di;
+    if ((st = device_info(&di)) != CSA_OK) return st;
+    cudaError_t e = csa::launch_merge_intervals(
+        csa::make_geo(L), n_cells, csa::to_dev(*plan), percentile, min_count, keep_count,
+        target_out, added_out, static_cast<int32_t*>(workspace), (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "merge launch");
+    return ok();
+}
+
+csa_status_t csa_share_timesteps(csa_layout_t L, int32_t n_groups, int32_t n_steps,
+                                 const csa_plan_t* plan, double tau, int32_t min_count,
+                                 uint16_t* keep_count, int32_t* cluster_out, double* iou_out,
+                                 csa_stream_t stream) {
+    csa_status_t st = check_layout(L, 0, 0);
+    if (st != CSA_OK) return st;
+    if (n_groups < 1 || n_steps < 1)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "n_groups and n_steps must be >= 1");
+    if (!(tau >= 0.0) || tau > 1.0) return fail(CSA_ERR_INVALID_ARGUMENT, "tau must be in [0, 1]");
+    if (min_count < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "min_count must be >= 1");
+    if (!plan_ptrs_ok(plan, false) || plan->n_cells < (int64_t)n_groups * n_steps)
+        return fail(CSA_ERR_INVALID_ARGUMENT,
+                    "plan: missing buffers or fewer than n_groups * n_steps cells");
+    if (!keep_count || !cluster_out || !iou_out)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "keep_count, cluster_out and iou_out are required");
+    DeviceInfo di;
+    if ((st = device_info(&di)) != CSA_OK) return st;
+    cudaError_t e = csa::launch_share_timesteps(csa::make_geo(L), n_groups, n_steps,
+                                                csa::to_dev(*plan), tau, min_count, keep_count,
+                                                cluster_out, iou_out, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "timestep-sharing launch");
     return ok();
 }
 

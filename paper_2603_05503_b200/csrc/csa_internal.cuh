@@ -82,6 +82,14 @@ cudaError_t set_calib_trace(void* buf, int mode);
 cudaError_t launch_calib(const CalibArgs& a, int head_dim, const CUtensorMap& tq,
                          const CUtensorMap& tk, int num_sms, cudaStream_t s);
 
+// f2 plan compaction (compact.cu)
+cudaError_t launch_merge_intervals(const Geo& g, int64_t n_cells, const PlanDev& p, double pct,
+                                   int32_t min_count, uint16_t* keep_count, int32_t* target,
+                                   unsigned long long* added, int32_t* hist_ws, cudaStream_t s);
+cudaError_t launch_share_timesteps(const Geo& g, int32_t n_groups, int32_t T, const PlanDev& p,
+                                   double tau, int32_t min_count, uint16_t* keep_count,
+                                   int32_t* cluster, double* iou, cudaStream_t s);
+
 // f1 spatial similarity (sim.cu)
 struct SimArgs {
     Geo g;

@@ -437,3 +437,96 @@ def test_spatial_similarity_wan480_sampled(csa):
         ref = oracle.spatial_cos(lay.F, lay.H, lay.W, qh, kh, scale, 5, f, i)
         assert abs(cos[h, f, i] - ref) <= 2e-5, (h, f, i)
     assert sim[1] / (lay.F * lay.H) > sim[0] / (lay.F * lay.H)  # the repetitive head scores higher
+
+
+# ---------------------------------------------------------------- f2 plan compaction
+def _row_intervals(mask_row):
+    ivl, c, nb = [], 0, len(mask_row)
+    while c < nb:
+        if mask_row[c]:
+            s = c
+            while c < nb and mask_row[c]:
+                c += 1
+            ivl.append((s, c))
+        else:
+            c += 1
+    return ivl
+
+
+@pytest.mark.parametrize("lay", [Layout(2, 5, 25, 64), Layout(21, 30, 52, 128)])
+@pytest.mark.parametrize("pct", [100.0, 90.0, 50.0])
+def test_merge_intervals_bit_exact(csa, lay, pct):
+    nb, cells = lay.NB, 4
+    counts_np = inputs.random_counts(nb, cells, 8, seed=nb + int(pct))
+    counts_np[2][:, ::2] = 8  # alternating rows: the widest rows
+    sim = torch.tensor([0.0, 0.0, 0.0, 1.0], dtype=torch.float64, device="cuda")  # cell 3 REPETITIVE
+    counts = u16_dev(counts_np)
+    plan = csa.compile_plan(lay, counts, 4, similarity=sim, anchor_k=min(5, lay.H))
+    bits = unpack_bits(plan.mask_bits.cpu().numpy(), nb).reshape(cells, nb, nb)
+    widths = [len(_row_intervals(bits[c, r])) for c in range(3) for r in range(nb)]
+    target_ref = oracle.percentile_nearest_rank(widths, pct)
+    target, added = csa.merge_intervals(plan, counts, 4, pct)
+    torch.cuda.synchronize()
+    assert int(target.item()) == target_ref
+    got = u16_np(counts).reshape(cells, nb, nb)
+    ref = counts_np.copy()
+    added_ref = 0
+    for c in range(3):
+        for r in range(nb):
+            merged, add = oracle.merge_row(_row_intervals(bits[c, r]), max(target_ref, 1))
+            added_ref += add
+            kept = np.zeros(nb, bool)
+            for s0, e0 in merged:
+                kept[s0:e0] = True
+            filled = kept & ~bits[c, r].astype(bool)
+            ref[c, r][filled] = 4
+    assert np.array_equal(got, ref)
+    assert int(added.item()) == added_ref
+    # recompiled plan: every row within the target, kept sets supersets
+    plan2 = csa.compile_plan(lay, counts, 4, similarity=sim, anchor_k=min(5, lay.H))
+    bits2 = unpack_bits(plan2.mask_bits.cpu().numpy(), nb).reshape(cells, nb, nb)
+    assert (bits2[:3] >= bits[:3]).all()
+    irp = plan2.ivl_row_ptr.cpu().numpy().reshape(cells, nb + 1)
+    assert np.diff(irp[:3], axis=1).max() <= max(target_ref, 1)
+
+
+def test_share_timesteps_bit_exact(csa):
+    lay = Layout(21, 30, 52, 128)
+    nb, T, G = lay.NB, 6, 3
+    rng = np.random.default_rng(12)
+    base = inputs.random_counts(nb, G, 8, seed=77)
+    counts_np = np.zeros((T, G, nb, nb), np.uint16)
+    for t in range(T):  # later timesteps drift less: the late ones become near-identical
+        noise = rng.random((G, nb, nb)) < 0.2 * (T - t) / T
+        counts_np[t] = np.where(noise, 8 - base, base)
+    sim = torch.zeros(T * G, dtype=torch.float64, device="cuda")
+    sim[(T - 1) * G + 2] = 1.0  # one REPETITIVE cell (t = T-1, g = 2)
+    counts = u16_dev(counts_np.reshape(-1, nb, nb))
+    plan = csa.compile_plan(lay, counts, 4, similarity=sim, anchor_k=5)
+    bits = unpack_bits(plan.mask_bits.cpu().numpy(), nb).reshape(T, G, nb, nb)
+    kind = plan.kind.cpu().numpy().reshape(T, G)
+    tau = 0.6
+    cluster, iou = csa.share_timesteps(plan, counts, G, T, 4, tau)
+    torch.cuda.synchronize()
+    iou = iou.cpu().numpy()
+    cluster = cluster.cpu().numpy()
+    got = u16_np(counts).reshape(T, G, nb, nb)
+    for g in range(G):
+        ref_iou = np.empty((T, T))
+        for t1 in range(T):
+            for t2 in range(T):
+                rep = kind[t1, g] or kind[t2, g]
+                ref_iou[t1, t2] = -1.0 if rep else oracle.skipped_iou(bits[t1, g], bits[t2, g])
+        assert np.array_equal(iou[g], ref_iou)  # exact ratio of integers
+        ref_cl = oracle.cluster_timesteps(ref_iou, tau)
+        assert np.array_equal(cluster[g], ref_cl)
+        for t in range(T):
+            if kind[t, g]:
+                assert np.array_equal(got[t, g], counts_np[t, g])  # untouched
+                continue
+            members = [u for u in range(T) if ref_cl[u] == ref_cl[t] and not kind[u, g]]
+            shared = np.zeros((nb, nb), bool)
+            for u in members:
+                shared |= bits[u, g].astype(bool)
+            assert np.array_equal(got[t, g], np.where(shared, 4, 0).astype(np.uint16))
+    assert len(set(cluster[0].tolist())) < T  # the late, near-identical timesteps share
