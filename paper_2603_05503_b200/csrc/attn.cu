@@ -44,6 +44,8 @@ static __device__ unsigned long long* g_trace;  // csa_debug_trace: CTA 0's firs
     } while (0)
 #endif
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr float kRedoSum = 32768.0f;        // lazy max: a tile's P row sum above 2^15 -> redo
+constexpr bool kLazyMax = false;            // A/B switch
 constexpr int kItemSlots = 4;
 constexpr int kEmuEvery = 0;  // every kEmuEvery-th element pair uses the polynomial exp2 (0:
                                // none -- measured fastest: the softmax is issue-bound, not MUFU-bound)
@@ -436,56 +438,86 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if (c * 32 + x >= tail_valid) r[c][x] = 0xff800000u;  // -inf
                 }
                 // row max: 8 independent FMNMX3 chains (short dependency depth), then combine
-                constexpr int kPer = BK / 8;  // elements per chain (even)
-                float mc[8];
+                auto row_max = [&]() -> float {
+                    constexpr int kPer = BK / 8;  // elements per chain (even)
+                    float mc[8];
 #pragma unroll
-                for (int q8 = 0; q8 < 8; ++q8) {
+                    for (int q8 = 0; q8 < 8; ++q8) {
 #define SV(e) __uint_as_float(r[(e) >> 5][(e) & 31])
-                    mc[q8] = SV(q8);
+                        mc[q8] = SV(q8);
 #pragma unroll
-                    for (int t = 1; t + 1 < kPer; t += 2)
-                        mc[q8] = fmax3(mc[q8], SV(q8 + 8 * t), SV(q8 + 8 * (t + 1)));
-                    mc[q8] = fmaxf(mc[q8], SV(q8 + 8 * (kPer - 1)));
+                        for (int t = 1; t + 1 < kPer; t += 2)
+                            mc[q8] = fmax3(mc[q8], SV(q8 + 8 * t), SV(q8 + 8 * (t + 1)));
+                        mc[q8] = fmaxf(mc[q8], SV(q8 + 8 * (kPer - 1)));
 #undef SV
-                }
-                const float mx = fmaxf(fmax3(mc[0], mc[1], mc[2]),
-                                       fmaxf(fmax3(mc[3], mc[4], mc[5]), fmaxf(mc[6], mc[7])));
-                const float m_new = fmaxf(m_run, mx * sl2);
-                float alpha = 1.0f;
-                bool need = false;
-                if (mine == 0) {
-                    m_run = m_new;
-                } else if (m_new > m_run + kRescaleThreshold) {
-                    alpha = ex2_approx(m_run - m_new);
-                    l_run *= alpha;
-                    m_run = m_new;
-                    need = true;
-                }
-                // tcgen05.ld/st are warp-collective (.sync.aligned): the O rescale below runs for
-                // the whole warp when any of its rows needs it (alpha = 1 for the others)
-                const bool rescale = __any_sync(0xffffffffu, need);
-                const uint64_t negm = f2(-m_run, -m_run);
-                uint64_t acc[4] = {0, 0, 0, 0};  // 4 packed partial sums (8 independent chains)
-#pragma unroll
-                for (int c = 0; c < BK / 32; ++c) {  // P overwrites the first BK/2 columns of S
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int x = 0; x < 32; x += 2) {
-                        const uint64_t sx = pk2(r[c][x], r[c][x + 1]);
-                        const uint64_t t = ffma2(sx, sl2x2, negm);
-                        uint64_t p;
-                        if (kEmuE > 0 && ((c * 16 + x / 2) % (kEmuE > 0 ? kEmuE : 1)) == kEmuE - 1) {
-                            p = exp2_poly2(t);
-                        } else {
-                            p = f2(ex2_approx(lo_f(t)), ex2_approx(hi_f(t)));
-                        }
-                        acc[(x / 2) & 3] = fadd2(acc[(x / 2) & 3], p);
-                        pk[x / 2] = pack_bf16(lo_f(p), hi_f(p));
                     }
-                    tmem_st16(lane_addr + s_col + c * 16, pk);
+                    return fmaxf(fmax3(mc[0], mc[1], mc[2]),
+                                 fmaxf(fmax3(mc[3], mc[4], mc[5]), fmaxf(mc[6], mc[7])));
+                };
+                // P = 2^(s*scale*log2e - m) -> bf16 over the first BK/2 columns of S; returns the
+                // fp32 row sum (4 packed partial sums, 8 independent chains)
+                auto exp_tile = [&](float m) -> float {
+                    const uint64_t negm = f2(-m, -m);
+                    uint64_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+                    for (int c = 0; c < BK / 32; ++c) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int x = 0; x < 32; x += 2) {
+                            const uint64_t sx = pk2(r[c][x], r[c][x + 1]);
+                            const uint64_t t = ffma2(sx, sl2x2, negm);
+                            uint64_t p;
+                            if (kEmuE > 0 &&
+                                ((c * 16 + x / 2) % (kEmuE > 0 ? kEmuE : 1)) == kEmuE - 1) {
+                                p = exp2_poly2(t);
+                            } else {
+                                p = f2(ex2_approx(lo_f(t)), ex2_approx(hi_f(t)));
+                            }
+                            acc[(x / 2) & 3] = fadd2(acc[(x / 2) & 3], p);
+                            pk[x / 2] = pack_bf16(lo_f(p), hi_f(p));
+                        }
+                        tmem_st16(lane_addr + s_col + c * 16, pk);
+                    }
+                    const uint64_t acc2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+                    return lo_f(acc2) + hi_f(acc2);
+                };
+                float alpha = 1.0f;
+                bool rescale = false;
+                float lsum;
+                if constexpr (kLazyMax) {
+                    // No max on the common tile: exponentials against the running max; only when
+                    // the tile's row sum passes 2^15 (an element may exceed 2^8, non-finite
+                    // included) is the max taken, l and O rescaled and the tile redone.
+                    if (mine == 0) m_run = row_max() * sl2;
+                    lsum = exp_tile(m_run);
+                    const bool need = mine > 0 && !(lsum <= kRedoSum);
+                    // tcgen05.ld/st are warp-collective: the whole warp redoes (alpha = 1 rows)
+                    if (__any_sync(0xffffffffu, need)) {
+                        const float m_new = need ? fmaxf(m_run, row_max() * sl2) : m_run;
+                        alpha = ex2_approx(m_run - m_new);
+                        l_run *= alpha;
+                        m_run = m_new;
+                        tmem_st_wait();
+                        lsum = exp_tile(m_run);
+                        rescale = true;
+                    }
+                } else {
+                    const float m_new = fmaxf(m_run, row_max() * sl2);
+                    bool need = false;
+                    if (mine == 0) {
+                        m_run = m_new;
+                    } else if (m_new > m_run + kRescaleThreshold) {
+                        alpha = ex2_approx(m_run - m_new);
+                        l_run *= alpha;
+                        m_run = m_new;
+                        need = true;
+                    }
+                    // tcgen05.ld/st are warp-collective (.sync.aligned): the O rescale below runs
+                    // for the whole warp when any of its rows needs it (alpha = 1 for the others)
+                    rescale = __any_sync(0xffffffffu, need);
+                    lsum = exp_tile(m_run);
                 }
-                const uint64_t acc2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-                l_run += lo_f(acc2) + hi_f(acc2);
+                l_run += lsum;
                 if (rescale) {
                     // O_grp holds only this group's earlier tiles; their P.V completed before
                     // this tile's S (issued after it on the in-order tensor pipe) was ready

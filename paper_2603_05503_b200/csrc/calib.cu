@@ -33,7 +33,8 @@ static __device__ unsigned long long* g_trace;  // csa_debug_trace (CTA 0, first
 static __device__ int g_debug_mode;  // csa_debug_trace mode: 11 skip softmax math, 12 also skip ld
 
 constexpr int kThreads = 384;
-constexpr int kCalibEmuPerOctet = 3;  // element pairs p with (p & 7) >= 8 - this -> exp2_poly5
+constexpr int kCalibEmuPerOctet = 0;  // pairs p with (p & 7) >= 8 - this -> exp2_poly5; A/B at Wan
+                                      // 720p: 0 -> 78 ms, 1 -> 78, 2 -> 81, 3 -> 87 (issue-bound)
 
 template <int BK, int D>
 struct CalibSmem {
