@@ -169,6 +169,17 @@ def workload(cfg, args, heads_lo, heads_hi, rank_dev):
     return lay, masks, detected, counts, min_count, calib
 
 
+def arm_config(cfg, batch, kept_fraction, rep, world):
+    """The workload description both arms print (the driver compares lines with equal config)."""
+    lay, H, d = cfg.layout, cfg.heads, cfg.d
+    return {"workload": f"{cfg.name} single attention layer",
+            "F_H_W": [lay.F, lay.H, lay.W], "tokens": lay.N, "heads": H, "head_dim": d,
+            "block": lay.B, "batch": batch, "kept_fraction": round(kept_fraction, 4),
+            "mask_sparsity_target": cfg.sparsity, "repetitive_heads": sorted(rep),
+            "anchor_k": 5, "parallelism": f"heads{world} (Ulysses a2a)" if world > 1 else "1 GPU",
+            "l2": "inputs 3x%.2f GB > 126 MB L2; no flush" % (batch * lay.N * H * d * 2 / 1e9)}
+
+
 def flops_of(lay, masks, rep, heads, d, batch, anchor_k=5):
     area = kept_area_host(masks, lay)
     tot = 0
@@ -338,12 +349,7 @@ def main():
                  if calib is None else
                  "synthetic (seeded N(0,1) bf16 Q/K/V; plan calibrated by this repo's a2-a6 path "
                  "on 8 generator-G prompts)"),
-        "config": {"workload": f"{cfg.name} single attention layer",
-                   "F_H_W": [lay.F, lay.H, lay.W], "tokens": lay.N, "heads": H, "head_dim": d,
-                   "block": lay.B, "batch": B, "kept_fraction": round(kept_fraction, 4),
-                   "mask_sparsity_target": cfg.sparsity, "repetitive_heads": sorted(rep),
-                   "anchor_k": 5, "parallelism": f"heads{world} (Ulysses a2a)" if world > 1 else "1 GPU",
-                   "l2": "inputs 3x%.2f GB > 126 MB L2; no flush" % (B * lay.N * H * d * 2 / 1e9)},
+        "config": arm_config(cfg, B, kept_fraction, rep, world),
         "gpu_launches": args.steps * 1,
         **({"calibration": calib} if calib is not None else {}),
         "clocks": clk.summary(),
@@ -513,7 +519,9 @@ def reference_arm(args, cfg, world, rank):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * statistics.mean(t_steps), 1), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} single attention layer (sampled units)"},
+        "config": arm_config(cfg, args.batch,
+                             flops_of(lay, masks, rep, range(cfg.heads), cfg.d, 1)[1]
+                             / (cfg.heads * float(lay.N) ** 2), rep, 1),
         "cpu_baseline": cb,
         "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
