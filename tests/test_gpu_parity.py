@@ -210,6 +210,27 @@ def test_attention_running_max_jumps(csa, variant, jump, monkeypatch):
         assert np.abs(lse_np[h] - ref_lse).max() <= 1e-3 * max(1.0, np.abs(ref_lse).max())
 
 
+def test_attention_repetitive_block128(csa):
+    """Anchor-row heads on the production kernel: k in {1, 2, 5, H}, ragged N, broadcast rows
+    bitwise equal to their anchor row, a MASK head alongside."""
+    lay = Layout(2, 9, 40, 128)
+    q, k, v = qkv(1, lay.N, 2, 128, seed=44, device="cuda")
+    rng = np.random.default_rng(2)
+    masks = (rng.random((2, lay.NB, lay.NB)) < 0.5).astype(np.uint8)
+    masks[:, np.arange(lay.NB), np.arange(lay.NB)] = 1
+    for kA in (1, 2, 5, lay.H):
+        out, lse, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[1], anchor_k=kA, lse=True)
+        ref, ref_lse = oracle_head(lay, q, k, v, 0, 1, rep_k=kA)
+        assert_close(out[0, :, 1].double().cpu().numpy(), ref, f"k={kA}")
+        assert np.abs(lse.view(2, lay.N)[1].cpu().numpy() - ref_lse).max() <= 1e-3
+        anchors = oracle.anchor_rows(lay.H, kA)
+        o3 = out[0, :, 1].view(lay.F, lay.H, lay.W, -1)
+        for i in range(lay.H):
+            assert torch.equal(o3[:, i], o3[:, anchors[oracle.nearest_anchor(lay.H, kA, i)]])
+        ref0, _ = oracle_head(lay, q, k, v, 0, 0, mask=masks[0])
+        assert_close(out[0, :, 0].double().cpu().numpy(), ref0, "mask head")
+
+
 def test_attention_tiny_repetitive(csa):
     cfg = CONFIGS["tiny"]
     lay = cfg.layout
@@ -229,9 +250,10 @@ def test_attention_tiny_repetitive(csa):
         assert_close(out[0, :, 0].double().cpu().numpy(), ref0, "dense head")
 
 
-def test_attention_batch2_shares_plan_and_is_deterministic(csa):
-    lay = Layout(2, 5, 25, 64)
-    q, k, v = qkv(2, lay.N, 3, 64, seed=7, device="cuda")
+@pytest.mark.parametrize("lay,d", [(Layout(2, 5, 25, 64), 64), (Layout(2, 9, 40, 128), 128)])
+def test_attention_batch2_shares_plan_and_is_deterministic(csa, lay, d):
+    """Both kernels: attn.cu (B 64) and the production Q-in-TMEM kernel (B 128, d 128)."""
+    q, k, v = qkv(2, lay.N, 3, d, seed=7, device="cuda")
     rng = np.random.default_rng(1)
     masks = (rng.random((3, lay.NB, lay.NB)) < 0.5).astype(np.uint8)
     masks[:, np.arange(lay.NB), np.arange(lay.NB)] = 1
