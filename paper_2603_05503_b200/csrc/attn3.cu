@@ -33,7 +33,7 @@ constexpr int kItemSlots3 = 4;
 // loaded it, so S-MMAs never wait for a P.V; the softmax waits for the previous tile's P.V
 // before overwriting P); false -> P over S[b]'s first 64 columns (S[b] released by the P.V).
 constexpr bool kSeparateP = false;
-constexpr int kEmu3 = 2;  // element pairs p with (p & 7) >= 8 - kEmu3 -> polynomial exp2 (A/B: 2 > 0, 3)
+constexpr int kEmu3 = 1;  // element pairs p with (p & 7) >= 8 - kEmu3 -> polynomial exp2 (A/B: 1 >= 2 > 0 > 3)
 static __device__ unsigned long long* g_trace;
 static __device__ int g_debug_mode;
 
@@ -47,7 +47,7 @@ struct Smem3 {
     static constexpr int kTile = 2 * kBox;      // 128 x 128 bf16 (Q, K or V tile)
     static constexpr int kQOff = 0;             // single Q buffer (freed once copied to TMEM)
     static constexpr int kKOff = kTile;
-    static constexpr int kKSlots = 3, kVSlots = CG == 2 ? 3 : 2;
+    static constexpr int kKSlots = CG == 2 ? 4 : 3, kVSlots = 2;  // A/B: K4V2 >= K3V3 >= K2V4
     static constexpr int kVOff = kKOff + kKSlots * kTile;
     static constexpr int kBarOff = kVOff + kVSlots * kTile;
     // q_full q_empty | k_full[KS] k_empty[KS] | v_full[VS] v_empty[VS] | s_full[2] s_free[2] |

@@ -552,3 +552,26 @@ def test_share_timesteps_bit_exact(csa):
                 shared |= bits[u, g].astype(bool)
             assert np.array_equal(got[t, g], np.where(shared, 4, 0).astype(np.uint16))
     assert len(set(cluster[0].tolist())) < T  # the late, near-identical timesteps share
+
+
+# ---------------------------------------------------------------- e: head sharding invariant
+@pytest.mark.parametrize("world", [2, 4])
+def test_head_sharded_launches_are_bitwise_equal_to_the_full_launch(csa, world):
+    """per-head outputs are bit-identical for any head partition P -- each rank's
+    launch sees only its heads' cells and a head-sliced (received) copy of Q, K, V."""
+    lay = Layout(21, 30, 52, 128)
+    heads = 8
+    q, k, v = qkv(1, lay.N, heads, 128, seed=61, device="cuda")
+    rng = np.random.default_rng(4)
+    masks = (rng.random((heads, lay.NB, lay.NB)) < 0.3).astype(np.uint8)
+    masks[:, np.arange(lay.NB), np.arange(lay.NB)] = 1
+    rep = [3]
+    full, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=rep, anchor_k=5)
+    hp = heads // world
+    for r in range(world):
+        sl = slice(r * hp, (r + 1) * hp)
+        part, _, _ = run_attention(csa, lay, q[:, :, sl].contiguous(), k[:, :, sl].contiguous(),
+                                   v[:, :, sl].contiguous(), masks=masks[sl],
+                                   rep=[h - r * hp for h in rep if r * hp <= h < (r + 1) * hp],
+                                   anchor_k=5)
+        assert torch.equal(part, full[:, :, sl])
