@@ -254,6 +254,16 @@ CSA_API csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t 
                                  int32_t max_work, int32_t pair_items, void* workspace,
                                  size_t workspace_bytes, csa_stream_t stream);
 
+/* ------------------------------------------------------------------------------------------
+ * csa_copy_heads -- runtime helper for streaming a layer through the API from host memory:
+ * copies heads [h0, h1) of a bf16 [1, N, n_heads, head_dim] tensor (head_dim contiguous, rows of
+ * n_heads * head_dim) between pinned host memory and device memory of the same layout, as one
+ * strided cudaMemcpy2DAsync on `stream` (height N, pitch n_heads * head_dim * 2 bytes).
+ * direction 0: host -> device (src host, dst device); 1: device -> host. */
+CSA_API csa_status_t csa_copy_heads(void* dst, const void* src, csa_layout_t L, int32_t n_heads,
+                            int32_t head_dim, int32_t h0, int32_t h1, int32_t direction,
+                            csa_stream_t stream);
+
 /* Workspace bytes for `which` (CSA_WS_*). */
 CSA_API size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_t head_dim);
 

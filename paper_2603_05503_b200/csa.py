@@ -53,7 +53,7 @@ class _PlanT(ctypes.Structure):
 EXPORTS = ["csa_calib_accumulate", "csa_compile_plan", "csa_build_work_list",
            "csa_sparse_attn_fwd", "csa_workspace_size", "csa_validate_plan", "csa_last_error",
            "csa_version", "csa_debug_trace", "csa_spatial_similarity", "csa_merge_intervals",
-           "csa_share_timesteps"]
+           "csa_share_timesteps", "csa_copy_heads"]
 
 _lib = None
 
@@ -94,6 +94,8 @@ def lib() -> ctypes.CDLL:
     L.csa_share_timesteps.restype = st
     L.csa_share_timesteps.argtypes = [_LayoutT, i32, i32, ctypes.POINTER(_PlanT), ctypes.c_double,
                                       i32, vp, vp, vp, vp]
+    L.csa_copy_heads.restype = st
+    L.csa_copy_heads.argtypes = [vp, vp, _LayoutT, i32, i32, i32, i32, i32, vp]
     L.csa_debug_trace.restype = st
     L.csa_debug_trace.argtypes = [vp, i32]
     L.csa_validate_plan.restype = st
@@ -280,6 +282,52 @@ def compile_plan(lay: Layout, keep_count: torch.Tensor, min_count: int,
     p.kind_host = p.kind.cpu().tolist()
     p.anchor_k_host = p.anchor_k.cpu().tolist()
     return p
+
+
+_HOST_BUFS: dict = {}
+
+
+def sparse_attn_fwd_host(q_h: torch.Tensor, k_h: torch.Tensor, v_h: torch.Tensor, plan: Plan,
+                         out_h: torch.Tensor, heads_per_chunk: int = 8,
+                         device: torch.device | str = "cuda") -> torch.Tensor:
+    """One layer from pinned host Q, K, V [1, N, H, d] to pinned host O, streamed by head chunks:
+    H2D of chunk c+1 (csa_copy_heads on a copy stream) overlaps the attention of chunk c (its
+    own heads' cells, work list and strided views of the device copies) and the D2H of chunk c-1.
+    Device staging buffers and per-chunk work lists are cached.  Returns out_h; synchronous on
+    return of the current stream (the caller synchronizes to read out_h)."""
+    _, n, heads, d = q_h.shape
+    lay = plan.lay
+    assert q_h.is_pinned() and out_h.is_pinned() and q_h.dtype == torch.bfloat16
+    key = (str(device), q_h.shape)
+    bufs = _HOST_BUFS.get(key)
+    if bufs is None:
+        bufs = {"q": torch.empty(q_h.shape, dtype=q_h.dtype, device=device),
+                "k": torch.empty(q_h.shape, dtype=q_h.dtype, device=device),
+                "v": torch.empty(q_h.shape, dtype=q_h.dtype, device=device),
+                "o": torch.empty(q_h.shape, dtype=q_h.dtype, device=device),
+                "s_in": torch.cuda.Stream(device=device), "s_out": torch.cuda.Stream(device=device)}
+        _HOST_BUFS[key] = bufs
+    chunks = [(h0, min(h0 + heads_per_chunk, heads)) for h0 in range(0, heads, heads_per_chunk)]
+    wkey = ("chunk_work", heads_per_chunk)
+    if getattr(plan, "_chunk_work", None) is None or plan._chunk_work[0] != wkey:
+        plan._chunk_work = (wkey, [build_work_list(plan, h0, h1 - h0) for h0, h1 in chunks])
+    works = plan._chunk_work[1]
+    comp = torch.cuda.current_stream(device)
+    s_in, s_out = bufs["s_in"], bufs["s_out"]
+    s_in.wait_stream(comp)  # staging buffers free (previous call's reads done)
+    for (h0, h1), work in zip(chunks, works):
+        for name, src in (("q", q_h), ("k", k_h), ("v", v_h)):
+            _check(lib().csa_copy_heads(_ptr(bufs[name]), _ptr(src), _layout(lay), heads, d, h0,
+                                        h1, 0, _stream(s_in)), "csa_copy_heads")
+        comp.wait_stream(s_in)
+        sl = slice(h0, h1)
+        sparse_attn_fwd(bufs["q"][:, :, sl], bufs["k"][:, :, sl], bufs["v"][:, :, sl], plan, work,
+                        cell_base=h0, out=bufs["o"][:, :, sl], stream=comp)
+        s_out.wait_stream(comp)
+        _check(lib().csa_copy_heads(_ptr(out_h), _ptr(bufs["o"]), _layout(lay), heads, d, h0, h1,
+                                    1, _stream(s_out)), "csa_copy_heads")
+    comp.wait_stream(s_out)
+    return out_h
 
 
 def merge_intervals(plan: Plan, keep_count: torch.Tensor, min_count: int, percentile: float,

@@ -299,6 +299,29 @@ csa_status_t csa_share_timesteps(csa_layout_t L, int32_t n_groups, int32_t n_ste
     return ok();
 }
 
+csa_status_t csa_copy_heads(void* dst, const void* src, csa_layout_t L, int32_t n_heads,
+                            int32_t head_dim, int32_t h0, int32_t h1, int32_t direction,
+                            csa_stream_t stream) {
+    csa_status_t st = check_layout(L, head_dim, n_heads);
+    if (st != CSA_OK) return st;
+    if (!dst || !src) return fail(CSA_ERR_INVALID_ARGUMENT, "null pointer");
+    if (n_heads < 1 || h0 < 0 || h1 > n_heads || h0 >= h1)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "head range [%d, %d) outside [0, %d)", h0, h1,
+                    n_heads);
+    if (direction != 0 && direction != 1)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "direction must be 0 (H2D) or 1 (D2H)");
+    const size_t pitch = (size_t)n_heads * head_dim * 2, off = (size_t)h0 * head_dim * 2;
+    const size_t width = (size_t)(h1 - h0) * head_dim * 2;
+    const size_t rows = (size_t)L.frames * L.rows * L.cols;
+    cudaError_t e = cudaMemcpy2DAsync(static_cast<char*>(dst) + off, pitch,
+                                      static_cast<const char*>(src) + off, pitch, width, rows,
+                                      direction == 0 ? cudaMemcpyHostToDevice
+                                                     : cudaMemcpyDeviceToHost,
+                                      (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync");
+    return ok();
+}
+
 csa_status_t csa_compile_plan(csa_layout_t L, int64_t n_cells, const uint16_t* keep_count,
                               int32_t min_count, const double* similarity, double gamma,
                               int32_t anchor_k, int32_t phase, const csa_plan_t* plan,

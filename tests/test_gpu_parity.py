@@ -575,3 +575,21 @@ def test_head_sharded_launches_are_bitwise_equal_to_the_full_launch(csa, world):
                                    rep=[h - r * hp for h in rep if r * hp <= h < (r + 1) * hp],
                                    anchor_k=5)
         assert torch.equal(part, full[:, :, sl])
+
+
+def test_host_streaming_api_equals_device_call(csa):
+    """csa.sparse_attn_fwd_host (pinned host in/out, head chunks with overlapped copies) gives
+    the device call's output bit for bit (per-head arithmetic is schedule- and chunk-free)."""
+    lay = Layout(21, 30, 52, 128)
+    heads = 10
+    q, k, v = qkv(1, lay.N, heads, 128, seed=62, device="cuda")
+    rng = np.random.default_rng(6)
+    masks = (rng.random((heads, lay.NB, lay.NB)) < 0.3).astype(np.uint8)
+    masks[:, np.arange(lay.NB), np.arange(lay.NB)] = 1
+    ref, _, plan = run_attention(csa, lay, q, k, v, masks=masks, rep=[4], anchor_k=5)
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    for chunk in (3, 4, 10):
+        ho = torch.zeros(q.shape, dtype=q.dtype).pin_memory()
+        csa.sparse_attn_fwd_host(hq, hk, hv, plan, ho, heads_per_chunk=chunk)
+        torch.cuda.synchronize()
+        assert torch.equal(ho, ref.cpu()), chunk
