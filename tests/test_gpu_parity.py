@@ -282,14 +282,15 @@ def sample_units(lay, heads, n, seed):
     return sorted(units)
 
 
-@pytest.mark.parametrize("name", ["wan480", "wan720"])
+@pytest.mark.parametrize("name", ["wan480", "wan720", "mochi"])
 def test_attention_full_size_sampled(csa, name):
-    """BASELINE configs at full size, bench launch configuration; oracle on sampled (h, r)."""
+    """BASELINE configs at full size, bench launch configuration; oracle on sampled (h, r)
+    (Mochi: generator-S masks at the paper's 69 % sparsity)."""
     cfg = CONFIGS[name]
     lay = cfg.layout
     q, k, v = qkv(1, lay.N, cfg.heads, cfg.d, seed=11, device="cuda")
-    masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity, seed=0)
-    rep = [3, 17, 29, 38]
+    masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity or 0.69, seed=0)
+    rep = [h for h in (3, 17, 29, 38) if h < cfg.heads]
     out, lse, plan = run_attention(csa, lay, q, k, v, masks=masks, rep=rep, anchor_k=5, lse=True)
     lse = lse.view(cfg.heads, lay.N).cpu().numpy()
     errs = []
@@ -346,8 +347,9 @@ def test_calibration_against_oracle(csa, lay, heads, d, single_pass):
             assert np.array_equal(oracle.select(E2[h, r], eps), c2[h, r])
 
 
-def test_calibration_wan480_sampled(csa):
-    cfg = CONFIGS["wan480"]
+@pytest.mark.parametrize("name", ["wan480", "wan720"])
+def test_calibration_full_size_sampled(csa, name):
+    cfg = CONFIGS[name]
     lay = cfg.layout
     heads = 4
     q, k, _ = inputs.structured_qk(lay, heads, cfg.d, 5, 0, alpha=[0.8, 1.0, 1.2, 1.5],
