@@ -24,11 +24,12 @@
 #include <cstdint>
 #include <cstdlib>
 
-#include "csa_internal.cuh"
-#include "tiles.cuh"
+#include "attn_common.cuh"
 
 namespace csa {
 namespace {
+
+using namespace attn;
 
 constexpr int kThreads = 384;
 static __device__ unsigned long long* g_trace;  // csa_debug_trace: CTA 0's first item timeline
@@ -43,7 +44,6 @@ static __device__ unsigned long long* g_trace;  // csa_debug_trace: CTA 0's firs
     do {                   \
     } while (0)
 #endif
-constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr float kRedoSum = 32768.0f;        // lazy max: a tile's P row sum above 2^15 -> redo
 constexpr bool kLazyMax = false;            // A/B switch
 constexpr int kItemSlots = 4;
@@ -68,110 +68,8 @@ struct AttnSmem {
     static_assert(kAlloc <= 232448, "smem");
 };
 
-struct Item {
-    uint32_t kind;  // 0 MASK, 1 REPETITIVE
-    int32_t h, idx, b;
-    int64_t cell;
-};
-
-__device__ __forceinline__ Item decode_item(const AttnArgs& a, int32_t item) {
-    const uint32_t code = a.work_list[item / a.batch];
-    Item it;
-    it.kind = code >> 31;
-    it.h = (int32_t)((code >> 20) & 0x7FFu);
-    it.idx = (int32_t)(code & 0xFFFFFu);
-    it.b = item % a.batch;
-    it.cell = a.cell_base + it.h;
-    return it;
-}
-
-// Kept key-block list of a MASK item (CSR), or all N_B blocks for a REPETITIVE item.
-struct TileList {
-    const uint16_t* idx;  // nullptr -> dense 0..n-1
-    int32_t n;
-    __device__ __forceinline__ int32_t at(int32_t j) const { return idx ? (int32_t)idx[j] : j; }
-};
-
-__device__ __forceinline__ TileList tile_list(const AttnArgs& a, const Item& it) {
-    TileList t;
-    if (it.kind) {
-        t.idx = nullptr;
-        t.n = a.g.NB;
-    } else {
-        const int32_t* rp = a.plan.blk_row_ptr + it.cell * (a.g.NB + 1);
-        const int32_t r0 = rp[it.idx], r1 = rp[it.idx + 1];
-        t.idx = a.plan.blk_idx + a.plan.blk_base[it.cell] + r0;
-        t.n = r1 - r0;
-    }
-    return t;
-}
-
-__device__ __forceinline__ int32_t anchor_row(int32_t H, int32_t k, int32_t m) {
-    return (int32_t)(((int64_t)(2 * m + 1) * H) / (2 * k));
-}
-
-// ------------------------------------------------------------------------ packed fp32 helpers
-__device__ __forceinline__ uint64_t pk2(uint32_t lo, uint32_t hi) {
-    return (uint64_t)lo | ((uint64_t)hi << 32);
-}
-__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
-    uint64_t d;
-    asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-    return d;
-}
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-    uint64_t d;
-    asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ uint64_t fadd2_rm(uint64_t a, uint64_t b) {
-    uint64_t d;
-    asm("add.rm.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
-    uint64_t d;
-    asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
-    uint64_t d;
-    asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ float lo_f(uint64_t v) { return __uint_as_float((uint32_t)v); }
-__device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
-__device__ __forceinline__ uint64_t f2(float lo, float hi) {
-    return pk2(__float_as_uint(lo), __float_as_uint(hi));
-}
-__device__ __forceinline__ float fmax3(float a, float b, float c) {
-    float d;
-    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-    return d;
-}
-
-// 2^x for a pair of x <= 8 on the FMA pipe: x = n + f, 2^f by a degree-3 minimax polynomial
-// (max rel. error 8.6e-5, far below the bf16 rounding of P), exponent added as integer.
-__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
-    const float x0 = fmaxf(lo_f(x), -127.0f), x1 = fmaxf(hi_f(x), -127.0f);
-    const uint64_t xc = f2(x0, x1);
-    const uint64_t kRound = f2(12582912.0f, 12582912.0f);  // 2^23 + 2^22
-    const uint64_t rnd = fadd2_rm(xc, kRound);               // floor(x) in the low mantissa bits
-    const uint64_t frac = fsub2(xc, fsub2(rnd, kRound));     // in [0, 1)
-    uint64_t p = f2(0.077066176f, 0.077066176f);
-    p = ffma2(p, frac, f2(0.22764593f, 0.22764593f));
-    p = ffma2(p, frac, f2(0.6951166f, 0.6951166f));
-    p = ffma2(p, frac, f2(1.0f, 1.0f));
-    const uint32_t e0 = (uint32_t)rnd << 23, e1 = (uint32_t)(rnd >> 32) << 23;
-    return pk2((uint32_t)p + e0, (uint32_t)(p >> 32) + e1);
-}
-
-__device__ __forceinline__ void set_maxnreg_dec56() {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
-}
-__device__ __forceinline__ void set_maxnreg_inc224() {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
-}
+// Item decoding, kept-tile lists, anchor rows, packed fp32 math, exp2_poly2 and setmaxnreg:
+// attn_common.cuh (shared with attn2.cu / attn3.cu).
 
 template <int BK, int D, int kEmuE = kEmuEvery>
 __global__ void __launch_bounds__(kThreads, 1)
