@@ -350,7 +350,7 @@ def main():
                  "synthetic (seeded N(0,1) bf16 Q/K/V; plan calibrated by this repo's a2-a6 path "
                  "on 8 generator-G prompts)"),
         "config": arm_config(cfg, B, kept_fraction, rep, world),
-        "gpu_launches": args.steps * 1,
+        "gpu_launches": args.steps * launches_per_call(lay, d),
         **({"calibration": calib} if calib is not None else {}),
         "clocks": clk.summary(),
     }
@@ -391,6 +391,21 @@ def main():
         torch.distributed.destroy_process_group()
 
 
+def attention_kernel_name(lay, d):
+    """The kernel csa_sparse_attn_fwd runs for this shape with a workspace (api.cu dispatch)."""
+    if lay.B == 128 and d == 128 and not os.environ.get("CSA_ATTN_V3"):
+        if os.environ.get("CSA_ATTN_RUNNING_MAX"):
+            return "sparse_attn_q_tmem_kernel (attn3.cu)"
+        return "sparse_attn_fixed_ref_kernel (attn4.cu)"
+    return f"sparse_attn_kernel<{lay.B},{d}> (attn.cu)"
+
+
+def launches_per_call(lay, d):
+    """Our kernels per csa_sparse_attn_fwd call: the fixed-reference kernel is followed by the
+    running-max kernel over its (normally empty) fallback list."""
+    return 2 if attention_kernel_name(lay, d).endswith("(attn4.cu)") else 1
+
+
 def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_all, dense_flop,
            kept_fraction, per, pk, stream, dev, csa):
     ms_kernel = statistics.mean(per)
@@ -406,9 +421,7 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
                           "frac": round(achieved / pk["bf16_tflops"], 4), "traffic": traffic,
                           "peak_src": f"{pk['src']} bf16 burst",
                           "frac_of_sustained": round(achieved / pk["bf16_tflops_sustained"], 4),
-                          "kernel": ("sparse_attn_q_tmem_kernel (attn3.cu)"
-                                     if lay.B == 128 and cfg.d == 128 and not os.environ.get("CSA_ATTN_V3")
-                                     else f"sparse_attn_kernel<{lay.B},{cfg.d}> (attn.cu)"),
+                          "kernel": attention_kernel_name(lay, cfg.d),
                           "algorithmic_flop_per_launch": flop_all}
     # ---- dense comparators: our kernel on an all-ones plan, and torch SDPA (cuDNN/flash)
     H, d, B = cfg.heads, cfg.d, args.batch
@@ -489,7 +502,7 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
     result["e2e"] = {"value": round(flop_all / (t_e2e * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
                      "ms_per_step": round(t_e2e, 3),
                      "h2d_bytes_per_step": 3 * q.numel() * 2, "d2h_bytes_per_step": out.numel() * 2}
-    result["gpu_launches"] = args.steps
+    result["gpu_launches"] = args.steps * launches_per_call(lay, cfg.d)
     # ---- CPU oracle baseline on a bounded sample of the same workload
     result["cpu_baseline"] = cpu_oracle_sample(lay, cfg, masks, rep, q, k, v)
 

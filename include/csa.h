@@ -242,10 +242,18 @@ CSA_API csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan,
  *   pair_items  0: single items (orders 0-2), one CTA per item;  1: pair items (order 3), two
  *               CTAs of a cluster per item (cta_group::2 MMAs, each CTA loads half of every K/V
  *               tile); requires block 128 and head_dim 128.  Results are identical per row.
- * Workspace: csa_workspace_size(CSA_WS_ATTN, ...) bytes of device memory holding the dynamic
- * scheduler's counters; it must be zero-filled before its first use and is left zero-filled when
- * the launch completes (so one buffer serves every launch on one stream).  NULL -> static
- * round-robin assignment of work items to CTAs (pair items are always assigned statically). */
+ * Workspace: csa_workspace_size(CSA_WS_ATTN, L, n_heads, ...) bytes of device memory (8-byte
+ * aligned).  Bytes [0, 256) hold the dynamic scheduler's counters: zero-filled before the first
+ * use, left zero-filled when the launch completes (one buffer serves every launch on one stream).
+ * NULL -> static round-robin assignment of work items to CTAs (pair items are always assigned
+ * statically).
+ * Kernels (block 128, head_dim 128, single items): with a workspace, the fixed-reference kernel
+ * (attn4.cu: each row's softmax shift is the max of its first kept tile, P:647-653 is
+ * shift-invariant); an item whose later scores exceed that shift by more than 2^56 in exp2 terms
+ * is listed in bytes [256, size) (rewritten every launch, needs max_work <= n_heads * N_B) and
+ * recomputed on the same stream by the running-max kernel (attn3.cu).  Without a workspace the
+ * running-max kernel runs the whole launch.  Each mode is deterministic; the two agree within
+ * bf16 rounding of P (not bitwise). */
 CSA_API csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
                                  int32_t head_dim, float softmax_scale, csa_tensor_t q,
                                  csa_tensor_t k, csa_tensor_t v, csa_tensor_t o, float* lse_out,

@@ -409,7 +409,8 @@ def sparse_attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: Pla
                     lse_out: torch.Tensor | None = None, scale: float | None = None,
                     stream=None, dynamic: bool = True) -> torch.Tensor:
     """csa_sparse_attn_fwd on q/k/v [batch, N, heads, d] (bf16, CUDA).  dynamic=False uses the
-    static round-robin item assignment (no scheduler workspace)."""
+    static round-robin item assignment without a workspace (block 128 / head_dim 128: the
+    running-max kernel instead of the fixed-reference kernel, csa.h)."""
     b, n, heads, d = q.shape
     assert n == plan.lay.N and k.shape == q.shape and v.shape == q.shape
     if out is None:
@@ -419,7 +420,8 @@ def sparse_attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: Pla
         assert lse_out.numel() == b * heads * n
     sc = default_scale(d) if scale is None else scale
     s = plan.struct()
-    ws = _sched_workspace(q.device) if dynamic else None
+    ws = _sched_workspace(q.device, lib().csa_workspace_size(3, _layout(plan.lay), heads, d),
+                          stream) if dynamic else None
     _check(lib().csa_sparse_attn_fwd(_layout(plan.lay), b, heads, d, sc, _tensor(q), _tensor(k),
                                      _tensor(v), _tensor(out), _ptr(lse_out), ctypes.byref(s),
                                      cell_base, _ptr(work.items), _ptr(work.n_work), work.max_work,
@@ -432,13 +434,18 @@ def sparse_attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: Pla
 _SCHED_WS: dict = {}
 
 
-def _sched_workspace(device) -> torch.Tensor:
-    """Zero-filled dynamic-scheduler workspace (left zero-filled by every launch, csa.h)."""
-    key = torch.device(device).index
-    if key not in _SCHED_WS:
-        n = lib().csa_workspace_size(3, _LayoutT(1, 1, 1, 128), 1, 128)
-        _SCHED_WS[key] = torch.zeros(n, dtype=torch.uint8, device=device)
-    return _SCHED_WS[key]
+def _sched_workspace(device, nbytes: int, stream=None) -> torch.Tensor:
+    """Zero-filled attention workspace (scheduler counters left zero-filled by every launch; the
+    fixed-reference kernel's fallback list rewritten by every launch, csa.h), grown on demand,
+    one per (device, stream) so launches on different streams never share counters."""
+    s = torch.cuda.current_stream(device) if stream is None else stream
+    key = (torch.device(device).index, s.cuda_stream)
+    buf = _SCHED_WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        with torch.cuda.stream(s):
+            buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        _SCHED_WS[key] = buf
+    return buf
 
 
 def version() -> str:

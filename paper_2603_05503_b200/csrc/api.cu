@@ -145,7 +145,12 @@ csa_status_t csa_debug_trace(void* buf, int32_t mode) {
 
 size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_t head_dim) {
     (void)head_dim;
-    if (which == CSA_WS_ATTN) return 256;  // attention: dynamic-scheduler counters
+    if (which == CSA_WS_ATTN) {  // dynamic-scheduler counters + the fixed-reference kernel's
+                                 // fallback list (count, item bitmap, codes; <= heads*N_B items)
+        if (n_heads < 1 || check_layout(L, 0, 0) != CSA_OK) return 256;
+        const size_t items = (size_t)n_heads * (size_t)csa::make_geo(L).NB;
+        return 256 + 4 * (1 + (items + 31) / 32 + items);
+    }
     if (which == CSA_WS_MERGE) {          // interval-width histogram
         if (check_layout(L, 0, 0) != CSA_OK) return 0;
         return (size_t)(csa::make_geo(L).NB + 1) * sizeof(int32_t);
@@ -434,6 +439,29 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
             return st;
         a.sched = nullptr;  // the pair kernel assigns pair items statically per cluster
         e = csa::launch_attn_pair(a, head_dim, tq, tk_half, tv, grid, (cudaStream_t)stream);
+    } else if (g.B == 128 && head_dim == 128 && workspace != nullptr &&
+               !std::getenv("CSA_ATTN_RUNNING_MAX") && !std::getenv("CSA_ATTN_V3")) {
+        // production (attn4.cu): fixed per-row reference max, two tiles in flight; items whose
+        // later scores overshoot it are recomputed right after by the running-max kernel
+        // (attn3.cu) from the fallback list in the workspace (256 bytes past the counters).
+        // Without a workspace (static assignment) the running-max kernel does the whole launch.
+        const size_t items = (size_t)n_heads * (size_t)g.NB;
+        if (workspace_bytes < csa_workspace_size(CSA_WS_ATTN, L, n_heads, head_dim) ||
+            (int64_t)max_work > (int64_t)items)
+            return fail(CSA_ERR_INVALID_ARGUMENT, "attention workspace too small");
+        uint32_t* base = static_cast<uint32_t*>(workspace) + 64;
+        const size_t flag_words = (items + 31) / 32;
+        csa::Fallback fb{base, base + 1, base + 1 + flag_words};
+        e = cudaMemsetAsync(base, 0, 4 * (1 + flag_words), (cudaStream_t)stream);
+        if (e == cudaSuccess)
+            e = csa::launch_attn_fixed_ref(a, tq, tk, tv, grid, fb, (cudaStream_t)stream);
+        if (e == cudaSuccess) {
+            csa::AttnArgs re = a;
+            re.work_list = fb.list;
+            re.n_work = reinterpret_cast<const int32_t*>(fb.count);
+            re.sched = nullptr;  // static assignment over an (almost always) empty list
+            e = csa::launch_attn_q_tmem(re, tq, tk, tv, di.sms, (cudaStream_t)stream);
+        }
     } else if (g.B == 128 && head_dim == 128 && !std::getenv("CSA_ATTN_V3")) {
         // production shape: Q resident in TMEM, column-split softmax (attn3.cu); CSA_ATTN_V3
         // selects the shared-memory-Q kernel (attn.cu, all other shapes) for A/B measurements

@@ -129,6 +129,18 @@ cudaError_t launch_attn(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
                         cudaStream_t s);
 cudaError_t set_attn2_trace(void* buf, int mode);
 cudaError_t set_attn3_trace(void* buf, int mode);
+// Fallback list of the fixed-reference kernel: work-list codes of items whose scores overshot
+// their reference max, recomputed by the running-max kernel.  count and flags (one bit per
+// work-list index) zero on entry; list has room for every work-list entry.
+struct Fallback {
+    uint32_t* count;
+    uint32_t* flags;
+    uint32_t* list;
+};
+// Block 128, head_dim 128, fixed per-row reference max (attn4.cu).
+cudaError_t launch_attn_fixed_ref(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                                  const CUtensorMap& tv, int grid, const Fallback& fb,
+                                  cudaStream_t s);
 // Block 128, head_dim 128, one CTA per query block with Q resident in TMEM (attn3.cu).
 cudaError_t launch_attn_q_tmem(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
                                const CUtensorMap& tv, int grid, cudaStream_t s);

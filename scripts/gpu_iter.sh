@@ -9,6 +9,6 @@ tail -n 4 gpurun_out/pytest_${TAG}.log
 timeout 600 python bench.py --config $CFG --steps 10 --warmup 3 --no-extras > gpurun_out/bench_${TAG}_${CFG}.log 2>&1
 tail -n 2 gpurun_out/bench_${TAG}_${CFG}.log
 if [ "$NCU" = "1" ]; then
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sparse_attn -s 1 -c 1 -o gpurun_out/prof_attn_${TAG}_${CFG} -f python bench.py --config $CFG --steps 1 --warmup 1 --no-extras > gpurun_out/prof_attn_${TAG}_${CFG}.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-sparse_attn_fixed_ref} -s 1 -c 1 -o gpurun_out/prof_attn_${TAG}_${CFG} -f python bench.py --config $CFG --steps 1 --warmup 1 --no-extras > gpurun_out/prof_attn_${TAG}_${CFG}.log 2>&1
 echo "ncu exit $?"
 fi

@@ -152,6 +152,13 @@ def run_attention(csa, lay, q, k, v, masks=None, rep=None, anchor_k=2, order=2, 
     return out, lse_t, plan
 
 
+def fallback_count(csa, q):
+    """Items the fixed-reference kernel (attn4.cu) handed to the running-max kernel in the last
+    dynamic launch on q's device: uint32 at byte 256 of the attention workspace (csa.h)."""
+    ws = csa._sched_workspace(q.device, 0)  # current stream: the one the test launched on
+    return int(ws[256:260].view(torch.int32).item())
+
+
 def oracle_head(lay, q, k, v, b, h, mask=None, rep_k=None, rows=None):
     scale = 1.0 / np.sqrt(q.shape[3])
     qh, kh, vh = head64(q, b, h), head64(k, b, h), head64(v, b, h)
@@ -181,14 +188,17 @@ def test_attention_tiny_masks(csa, name):
         assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 1e-3, cname
 
 
-@pytest.mark.parametrize("variant", [{}, {"CSA_ATTN_CG": "4"}, {"CSA_ATTN_V3": "1"},
-                                     {"CSA_ATTN_V3": "1", "CSA_EMU_EVERY": "4"}])
+@pytest.mark.parametrize("variant", [{}, {"CSA_ATTN_RUNNING_MAX": "1"},
+                                     {"CSA_ATTN_RUNNING_MAX": "1", "CSA_ATTN_CG": "4"},
+                                     {"CSA_ATTN_V3": "1"}, {"CSA_ATTN_V3": "1", "CSA_EMU_EVERY": "4"}])
 @pytest.mark.parametrize("jump", [3.0, 40.0])
 def test_attention_running_max_jumps(csa, variant, jump, monkeypatch):
     """Key blocks whose scores grow block by block: later tiles exceed the running max (lazy
     rescale / overflow-guard redo paths, including jumps far beyond 2^8); ragged last block.
-    Covers the production (Q-in-TMEM) kernel and the shared-memory-Q kernel with and without
-    its polynomial exp2."""
+    Covers the production fixed-reference kernel (jump 40 overshoots the reference max by far
+    more than 2^56: every such item goes through the fallback), the running-max Q-in-TMEM kernel
+    (column split over 2 or 4 warp groups) and the shared-memory-Q kernel with and without its
+    polynomial exp2."""
     for key, val in variant.items():
         monkeypatch.setenv(key, val)
     lay = Layout(2, 9, 40, 128)
@@ -208,6 +218,9 @@ def test_attention_running_max_jumps(csa, variant, jump, monkeypatch):
         ref, ref_lse = oracle_head(lay, q, k, v, 0, h, mask=masks[h])
         assert_close(out[0, :, h].double().cpu().numpy(), ref, f"{variant} jump {jump} h{h}")
         assert np.abs(lse_np[h] - ref_lse).max() <= 1e-3 * max(1.0, np.abs(ref_lse).max())
+    if not variant:
+        n_fb = fallback_count(csa, q)
+        assert (n_fb > 0) if jump > 10 else (n_fb == 0), n_fb
 
 
 def test_attention_repetitive_block128(csa):
@@ -262,7 +275,12 @@ def test_attention_batch2_shares_plan_and_is_deterministic(csa, lay, d):
         out2, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[2], anchor_k=2, order=order)
         assert torch.equal(out, out2)  # item order never changes per-item arithmetic
     static = csa.sparse_attn_fwd(q, k, v, plan, csa.build_work_list(plan, 0, 3), dynamic=False)
-    assert torch.equal(out, static)  # dynamic vs static scheduling
+    static2 = csa.sparse_attn_fwd(q, k, v, plan, csa.build_work_list(plan, 0, 3), dynamic=False)
+    assert torch.equal(static, static2)
+    if d == 128:  # static -> running-max kernel, dynamic -> fixed-reference kernel (csa.h)
+        assert (static.float() - out.float()).abs().max().item() <= 2 * MAX_ABS
+    else:
+        assert torch.equal(out, static)  # dynamic vs static scheduling, same kernel
     again, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[2], anchor_k=2)
     assert torch.equal(out, again)  # run-to-run determinism (scheduler counters self-reset)
     for b in range(2):
@@ -303,6 +321,8 @@ def test_attention_full_size_sampled(csa, name):
         assert np.abs(lse[h, rows[0]:rows[1]] - ref_lse).max() <= 1e-3
         errs.append(np.abs(got - ref).max())
     assert torch.isfinite(out).all()
+    if cfg.d == 128:
+        assert fallback_count(csa, q) == 0  # realistic rows never overshoot the reference max
 
 
 # ---------------------------------------------------------------- a2-a5 calibration
