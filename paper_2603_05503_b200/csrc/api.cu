@@ -138,6 +138,7 @@ csa_status_t csa_debug_trace(void* buf, int32_t mode) {
     cudaError_t e = csa::set_attn_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_attn2_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_attn3_trace(buf, mode);
+    if (e == cudaSuccess) e = csa::set_attn4_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_calib_trace(buf, mode);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyToSymbol");
     return ok();

@@ -24,23 +24,43 @@ namespace {
 
 using namespace attn;
 
-constexpr int kThreads4 = 384;
 constexpr int kItemSlots4 = 4;
+// CH4: column split of each softmax group: a group is 4 * CH4 warps, warp (quarter, ch) taking
+// rows 32 * quarter ... and key columns ch * 128 / CH4 ... of the group's tiles.
+constexpr int kCH4 = 2;
 constexpr float kGuard = 72057594037927936.0f;  // 2^56: a tile row sum above it flags the item
+static __device__ unsigned long long* g_trace4;
+static __device__ int g_debug_mode4;
+#ifdef CSA_ENABLE_TRACE  // trace builds only (see attn_common.cuh): CTA 0's first 1024 tiles
+#define TRACE4(slot, k, e)                                                                   \
+    do {                                                                                     \
+        if (g_trace4 != nullptr && blockIdx.x == 0 && (k) < 1024)                            \
+            g_trace4[((slot) * 1024 + (k)) * 8 + (e)] = clock64();                           \
+    } while (0)
+#define DEBUG4 (g_debug_mode4)
+#else
+#define TRACE4(slot, k, e) \
+    do {                   \
+    } while (0)
+#define DEBUG4 0
+#endif
 constexpr int kEmu4 = 1;  // element pairs p with (p & 7) >= 8 - kEmu4 -> polynomial exp2
 
+template <int CH>
 struct Smem4 {
+    static constexpr int kThreads = 128 + 256 * CH;
     static constexpr int kBox = 128 * 128;      // [128 rows][64 cols] bf16, SWIZZLE_128B
     static constexpr int kTile = 2 * kBox;      // 128 x 128 bf16
     static constexpr int kQOff = 0;             // single Q buffer (freed once copied to TMEM)
     static constexpr int kKVOff = kTile;
-    static constexpr int kSlots = 6;            // K/V ring, consumption order
+    static constexpr int kSlots = CH == 1 ? 6 : 5;  // K/V ring, consumption order
     static constexpr int kBarOff = kKVOff + kSlots * kTile;
     // q_full q_empty | kv_full[S] kv_empty[S] | s_full[2] p_full[2] | o_full o_empty | mref_full |
     // item_full[4] item_empty[4]
     static constexpr int kNumBars = 2 + 2 * kSlots + 4 + 2 + 1 + 2 * kItemSlots4;
-    static constexpr int kRowOff = kBarOff + kNumBars * 8;  // m_ref[128], l[2][128]
-    static constexpr int kItemOff = kRowOff + 3 * 128 * 4;
+    // m_ref[128] | l[2 * CH][128] | tile-0 max of each column part [CH][128]
+    static constexpr int kRowOff = kBarOff + kNumBars * 8;
+    static constexpr int kItemOff = kRowOff + (1 + 3 * CH) * 128 * 4;
     static constexpr int kFlagOff = kItemOff + kItemSlots4 * 4;
     static constexpr int kTmemPtrOff = kFlagOff + 16;
     static constexpr int kBytes = kTmemPtrOff + 16;
@@ -50,11 +70,12 @@ struct Smem4 {
     static constexpr uint32_t kIdescPV = umma_idesc_bf16(128, 128, 0, 1);
 };
 
-__global__ void __launch_bounds__(kThreads4, 1)
+template <int CH>
+__global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
     sparse_attn_fixed_ref_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tq,
                                  const __grid_constant__ CUtensorMap tk,
                                  const __grid_constant__ CUtensorMap tv, const Fallback fb) {
-    using L = Smem4;
+    using L = Smem4<CH>;
     constexpr int BK = 128, D = 128, S = L::kSlots;
     extern __shared__ __align__(1024) uint8_t smem[];
     if ((smem_u32(smem) & 1023u) != 0u) __trap();
@@ -71,7 +92,8 @@ __global__ void __launch_bounds__(kThreads4, 1)
     uint64_t* item_full = mref_full + 1;
     uint64_t* item_empty = item_full + kItemSlots4;
     float* mref_s = reinterpret_cast<float*>(smem + L::kRowOff);  // [128] (log2 domain)
-    float* row_l = mref_s + 128;                                   // [2][128]
+    float* row_l = mref_s + 128;                                   // [2 * CH][128]
+    float* mx_s = row_l + 2 * CH * 128;                            // [CH][128]
     volatile int32_t* item_slot = reinterpret_cast<int32_t*>(smem + L::kItemOff);
     volatile int32_t* flag_s = reinterpret_cast<int32_t*>(smem + L::kFlagOff);
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtrOff);
@@ -86,14 +108,14 @@ __global__ void __launch_bounds__(kThreads4, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(s_full + i, 1);
-            mbar_init(p_full + i, 4);
+            mbar_init(p_full + i, 4 * CH);
         }
         mbar_init(o_full, 1);
-        mbar_init(o_empty, 8);
-        mbar_init(mref_full, 4);
+        mbar_init(o_empty, 8 * CH);
+        mbar_init(mref_full, 4 * CH);
         for (int i = 0; i < kItemSlots4; ++i) {
             mbar_init(item_full + i, 1);
-            mbar_init(item_empty + i, 9);  // MMA warp + 8 softmax warps
+            mbar_init(item_empty + i, 1 + 8 * CH);  // MMA warp + the softmax warps
         }
         *flag_s = 0;
         fence_barrier_init();
@@ -121,6 +143,8 @@ __global__ void __launch_bounds__(kThreads4, 1)
     };
 
     if (warp < 4) {
+        // registers: launch 65536 / kThreads each; what the producer warps give back must cover
+        // what the softmax warps take (CH 2: 640 x 96 -> 4 warps at 56, 16 warps at 104)
         set_maxnreg_dec56();
         if (warp == 0) {
             // ------------------------------------------------------------ scheduler + producer
@@ -202,7 +226,7 @@ __global__ void __launch_bounds__(kThreads4, 1)
             }
         } else if (warp == 1) {
             // ------------------------------------------------------------------ MMA issuer
-            uint32_t cons = 0, pcount[2] = {0, 0};
+            uint32_t cons = 0, pcount[2] = {0, 0}, qk_tiles = 0, pv_tiles = 0;
             const uint32_t q_base = smem_u32(smem + L::kQOff);
             const uint32_t kv_base = smem_u32(smem + L::kKVOff);
             for (int32_t local = 0;; ++local) {
@@ -225,8 +249,10 @@ __global__ void __launch_bounds__(kThreads4, 1)
                 if (tl.n == 0) continue;
                 auto do_pv = [&](int32_t t) {
                     const int grp = t & 1;
+                    TRACE4(3, pv_tiles, 0);
                     mbar_wait(p_full + grp, pcount[grp] & 1);
                     ++pcount[grp];
+                    TRACE4(3, pv_tiles, 1);
                     if (t == 0) mbar_wait(o_empty, (local & 1) ^ 1);  // last item's epilogue
                     const uint32_t slot = cons % S, ph = (cons / S) & 1;
                     ++cons;
@@ -236,18 +262,26 @@ __global__ void __launch_bounds__(kThreads4, 1)
                         const uint32_t vb = kv_base + slot * L::kTile;
 #pragma unroll
                         for (int kk = 0; kk < BK / 16; ++kk)
-                            mma_ts(tmem + L::kO, tmem + L::kS + grp * BK + kk * 8,
+                            // P of column part q sits over the first half of S's part q
+                            mma_ts(tmem + L::kO,
+                                   tmem + L::kS + grp * BK + (kk * 16 / (BK / CH)) * (BK / CH) +
+                                       (kk * 16 % (BK / CH)) / 2,
                                    umma_desc_sw128(vb + kk * 16 * 128, L::kBox, 1024),
                                    L::kIdescPV, (t > 0 || kk > 0) ? 1u : 0u);
                         mma_commit(kv_empty + slot);
                     }
                     __syncwarp();
+                    TRACE4(3, pv_tiles, 2);
+                    ++pv_tiles;
                 };
                 for (int32_t j = 0; j < tl.n; ++j) {
                     const int grp = j & 1;
                     const uint32_t slot = cons % S, ph = (cons / S) & 1;
                     ++cons;
+                    TRACE4(2, qk_tiles, 0);
                     mbar_wait(kv_full + slot, ph);
+                    TRACE4(2, qk_tiles, 1);
+                    ++qk_tiles;
                     tc_fence_after();
                     if (elect_one()) {
                         const uint32_t kb = kv_base + slot * L::kTile;
@@ -270,17 +304,24 @@ __global__ void __launch_bounds__(kThreads4, 1)
         }
         __syncwarp();
     } else {
-        set_maxnreg_inc224();
+        if constexpr (CH == 1) {
+            set_maxnreg_inc224();
+        } else {
+            asm volatile("setmaxnreg.inc.sync.aligned.u32 104;" ::: "memory");
+        }
         // ------------------------------------------------------------------ softmax groups
-        const int grp = (warp - 4) >> 2;
+        constexpr int NC = BK / CH;  // key columns per thread
+        const int grp = (int)(warp - 4) / (4 * CH);
+        const int ch = (int)((warp - 4) >> 2) % CH;
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
-        const uint32_t s_col = L::kS + grp * BK;
+        const uint32_t s_col = L::kS + grp * BK + ch * NC;
+        const uint32_t p_col = s_col;  // P over the first half of this part's S columns
         const float sl2 = a.scale_log2;
         const uint64_t sl2x2 = f2(sl2, sl2);
         const int32_t tail_valid = g.N - (g.NB - 1) * BK;
-        uint32_t scount = 0;
+        uint32_t scount = 0, tbase = 0;
         for (int32_t local = 0;; ++local) {
             const int32_t item = next_item(local);
             if (item < 0) break;
@@ -295,24 +336,30 @@ __global__ void __launch_bounds__(kThreads4, 1)
                 have_ref = true;
             };
             for (int32_t j = grp; j < tl.n; j += 2) {
+                const uint32_t tk = tbase + (uint32_t)j;
+                (void)tk;
+                if (quarter == 0 && ch == 0 && lane == 0) TRACE4(grp, tk, 0);
                 mbar_wait(s_full + grp, scount & 1);
                 ++scount;
+                if (quarter == 0 && ch == 0 && lane == 0) TRACE4(grp, tk, 1);
                 tc_fence_after();
-                uint32_t r[BK / 32][32];
+                uint32_t r[NC / 32][32];
 #pragma unroll
-                for (int c = 0; c < BK / 32; ++c) tmem_ld32(lane_addr + s_col + c * 32, r[c]);
+                for (int c = 0; c < NC / 32; ++c) tmem_ld32(lane_addr + s_col + c * 32, r[c]);
 #pragma unroll
-                for (int c = 0; c < BK / 32; ++c) tmem_ld_wait(r[c]);
+                for (int c = 0; c < NC / 32; ++c) tmem_ld_wait(r[c]);
+                if (quarter == 0 && ch == 0 && lane == 0) TRACE4(grp, tk, 2);
                 if (last_ragged && j == tl.n - 1) {
 #pragma unroll
-                    for (int c = 0; c < BK / 32; ++c)
+                    for (int c = 0; c < NC / 32; ++c)
 #pragma unroll
                         for (int x = 0; x < 32; ++x)
-                            if (c * 32 + x >= tail_valid) r[c][x] = 0xff800000u;  // keys >= N
+                            if (ch * NC + c * 32 + x >= tail_valid)
+                                r[c][x] = 0xff800000u;  // keys >= N
                 }
                 if (j == 0) {
                     // the row's reference: the max of its first kept tile (8 FMNMX3 chains)
-                    constexpr int kPer = BK / 8;
+                    constexpr int kPer = NC / 8;
                     float mc[8];
 #pragma unroll
                     for (int q8 = 0; q8 < 8; ++q8) {
@@ -326,7 +373,13 @@ __global__ void __launch_bounds__(kThreads4, 1)
                     }
                     m_ref = fmaxf(fmax3(mc[0], mc[1], mc[2]),
                                   fmaxf(fmax3(mc[3], mc[4], mc[5]), fmaxf(mc[6], mc[7]))) * sl2;
-                    mref_s[row] = m_ref;
+                    if constexpr (CH > 1) {  // the row's max over the column parts (group 0)
+                        mx_s[ch * 128 + row] = m_ref;
+                        named_bar_sync(2, 128 * CH);
+#pragma unroll
+                        for (int o = 0; o < CH; ++o) m_ref = fmaxf(m_ref, mx_s[o * 128 + row]);
+                    }
+                    if (ch == 0) mref_s[row] = m_ref;
                     have_ref = true;
                     __syncwarp();
                     if (lane == 0) mbar_arrive(mref_full);
@@ -336,13 +389,15 @@ __global__ void __launch_bounds__(kThreads4, 1)
                 const uint64_t negm = f2(-m_ref, -m_ref);
                 uint64_t acc[4] = {0, 0, 0, 0};
 #pragma unroll
-                for (int c = 0; c < BK / 32; ++c) {  // P overwrites the first BK/2 columns of S
+                for (int c = 0; c < NC / 32; ++c) {  // P overwrites the first BK/2 columns of S
                     uint32_t pk[16];
 #pragma unroll
                     for (int x = 0; x < 32; x += 2) {
                         const uint64_t t = ffma2(pk2(r[c][x], r[c][x + 1]), sl2x2, negm);
                         uint64_t p;
-                        if (((c * 16 + x / 2) & 7) >= 8 - kEmu4) {
+                        if (DEBUG4 == 1) {
+                            p = t;
+                        } else if (((c * 16 + x / 2) & 7) >= 8 - kEmu4) {
                             p = exp2_poly2(t);
                         } else {
                             p = f2(ex2_approx(lo_f(t)), ex2_approx(hi_f(t)));
@@ -350,19 +405,22 @@ __global__ void __launch_bounds__(kThreads4, 1)
                         acc[(x / 2) & 3] = fadd2(acc[(x / 2) & 3], p);
                         pk[x / 2] = pack_bf16(lo_f(p), hi_f(p));
                     }
-                    tmem_st16(lane_addr + s_col + c * 16, pk);
+                    tmem_st16(lane_addr + p_col + c * 16, pk);
                 }
                 const uint64_t acc2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
                 const float lsum = lo_f(acc2) + hi_f(acc2);
                 bad |= !(lsum <= kGuard);  // also catches inf / NaN
                 l_run += lsum;
+                if (quarter == 0 && ch == 0 && lane == 0) TRACE4(grp, tk, 3);
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(p_full + grp);
+                if (quarter == 0 && ch == 0 && lane == 0) TRACE4(grp, tk, 4);
             }
+            tbase += (uint32_t)tl.n;
             if (grp == 0 && tl.n == 0) {  // corrupt plan: keep the per-item phase of mref_full
-                mref_s[row] = 0.0f;
+                if (ch == 0) mref_s[row] = 0.0f;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(mref_full);
             }
@@ -371,9 +429,11 @@ __global__ void __launch_bounds__(kThreads4, 1)
             if (__any_sync(0xffffffffu, bad) && lane == 0) *flag_s = 1;
             mbar_wait(o_full, local & 1);
             tc_fence_after();
-            row_l[grp * 128 + row] = l_run;
-            named_bar_sync(1, 256);
-            const float Lsum = row_l[row] + row_l[128 + row];
+            row_l[(grp * CH + ch) * 128 + row] = l_run;
+            named_bar_sync(1, 256 * CH);
+            float Lsum = 0.0f;
+#pragma unroll
+            for (int o = 0; o < 2 * CH; ++o) Lsum += row_l[o * 128 + row];
             const float inv = Lsum > 0.0f ? 1.0f / Lsum : 0.0f;
             const bool flagged = *flag_s != 0;
             int64_t tok0 = -1;
@@ -402,8 +462,8 @@ __global__ void __launch_bounds__(kThreads4, 1)
             __nv_bfloat16* obase = a.o + (int64_t)it.b * a.o_sb + (int64_t)it.h * a.o_sh;
             const uint64_t inv2 = f2(inv, inv);
 #pragma unroll
-            for (int cc = 0; cc < D / 2; cc += 32) {
-                const int col = grp * (D / 2) + cc;
+            for (int cc = 0; cc < D / (2 * CH); cc += 32) {
+                const int col = (grp * CH + ch) * (D / (2 * CH)) + cc;
                 uint32_t r0[32];
                 tmem_ld32(lane_addr + L::kO + col, r0);
                 tmem_ld_wait(r0);
@@ -422,14 +482,14 @@ __global__ void __launch_bounds__(kThreads4, 1)
                                             packed[4 * v + 3]);
                 }
             }
-            if (grp == 0 && a.lse_out != nullptr) {
+            if (grp == 0 && ch == 0 && a.lse_out != nullptr) {
                 const float lse = (m_ref + __log2f(Lsum)) * 0.69314718055994531f;
                 float* lb = a.lse_out + ((int64_t)it.b * a.n_heads + it.h) * (int64_t)g.N;
                 for (int32_t dI = 0; dI < n_dst; ++dI)
                     lb[tok0 + (int64_t)dI * dst_stride_rows] = lse;
             }
             tc_fence_before();
-            named_bar_sync(1, 256);  // every thread has read flag_s / row_l
+            named_bar_sync(1, 256 * CH);  // every thread has read flag_s / row_l
             if (threadIdx.x == 128) {
                 if (flagged) {  // recomputed by the running-max kernel after this launch
                     // one entry per work-list item (the fallback launch redoes every batch of it)
@@ -460,15 +520,22 @@ __global__ void __launch_bounds__(kThreads4, 1)
 
 }  // namespace
 
+cudaError_t set_attn4_trace(void* buf, int mode) {
+    unsigned long long* p = static_cast<unsigned long long*>(buf);
+    cudaError_t e = cudaMemcpyToSymbol(g_trace4, &p, sizeof(p));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyToSymbol(g_debug_mode4, &mode, sizeof(mode));
+}
+
 cudaError_t launch_attn_fixed_ref(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
                                   const CUtensorMap& tv, int grid, const Fallback& fb,
                                   cudaStream_t s) {
     if (a.g.B != 128) return cudaErrorInvalidValue;
-    auto kern = sparse_attn_fixed_ref_kernel;
-    const int smem = Smem4::kBytes;
+    auto kern = sparse_attn_fixed_ref_kernel<kCH4>;
+    const int smem = Smem4<kCH4>::kBytes;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kThreads4, smem, s>>>(a, tq, tk, tv, fb);
+    kern<<<grid, Smem4<kCH4>::kThreads, smem, s>>>(a, tq, tk, tv, fb);
     return cudaGetLastError();
 }
 

@@ -129,6 +129,7 @@ cudaError_t launch_attn(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
                         cudaStream_t s);
 cudaError_t set_attn2_trace(void* buf, int mode);
 cudaError_t set_attn3_trace(void* buf, int mode);
+cudaError_t set_attn4_trace(void* buf, int mode);
 // Fallback list of the fixed-reference kernel: work-list codes of items whose scores overshot
 // their reference max, recomputed by the running-max kernel.  count and flags (one bit per
 // work-list index) zero on entry; list has room for every work-list entry.
