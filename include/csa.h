@@ -29,6 +29,12 @@
  *   - Tensors: bf16, layout [batch, N, heads, head_dim] given by element strides; head_dim
  *     contiguous; base and strides 16-byte aligned (TMA).
  *   - Supported: sm_100 devices; head_dim in {64, 128}; block in {64, 128}; N_B <= 2047.
+ *   - Non-square blocks (block_kv != 0 and != block): csa_compile_plan, csa_merge_intervals,
+ *     csa_share_timesteps, csa_build_work_list, csa_validate_plan and csa_sparse_attn_fwd accept
+ *     block 128, block_kv a multiple of 16 in [64, 192], head_dim 128 (attention), N_Bkv <= 2047;
+ *     csa_calib_accumulate and csa_spatial_similarity return CSA_ERR_UNSUPPORTED for them.
+ *     Everywhere below, "N_B x N_B" of a plan or keep-count cell reads "N_B x N_Bkv" (rows are
+ *     query blocks, columns key blocks), and mask rows hold ceil(N_Bkv/32) words.
  */
 #ifndef CSA_H
 #define CSA_H
@@ -57,12 +63,16 @@ typedef enum {
     CSA_ERR_INSUFFICIENT_CAPACITY = 5
 } csa_status_t;
 
-/* Video token grid and block size (128x128 blocks). */
+/* Video token grid and block sizes (128x128 blocks).  Non-square blocks
+ * B_q x B_kv (Table tab:block_size_ablation): block = B_q, block_kv = B_kv; a plan's
+ * rows are the N_B = ceil(N/B_q) query blocks, its columns the N_Bkv = ceil(N/B_kv) key blocks
+ * (J_c = {j | c B_kv <= j < (c+1) B_kv}, clipped to N).  block_kv = 0 (or = block): square. */
 typedef struct {
-    int32_t frames; /* F */
-    int32_t rows;   /* H, spatial rows per frame */
-    int32_t cols;   /* W, tokens per spatial row */
-    int32_t block;  /* B (query and key block size, "B x B") */
+    int32_t frames;   /* F */
+    int32_t rows;     /* H, spatial rows per frame */
+    int32_t cols;     /* W, tokens per spatial row */
+    int32_t block;    /* B_q (query block size; = key block size when block_kv is 0) */
+    int32_t block_kv; /* B_kv, 0 -> block */
 } csa_layout_t;
 
 /* bf16 tensor [batch, N, heads, head_dim]; strides in ELEMENTS; head_dim stride is 1. */

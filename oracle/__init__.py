@@ -57,6 +57,13 @@ def lib():
         L.csao_masked_attention_rows.restype = ctypes.c_int
         L.csao_masked_attention_rows.argtypes = [_c_i64, _c_i32, _c_i32, _p, _p, _p, _c_dbl, _p,
                                                  _c_i64, _c_i64, _p, _p]
+        L.csao_masked_attention_rows_rect.restype = ctypes.c_int
+        L.csao_masked_attention_rows_rect.argtypes = [_c_i64, _c_i32, _c_i32, _c_i32, _p, _p, _p,
+                                                      _c_dbl, _p, _c_i64, _c_i64, _p, _p]
+        L.csao_compile_cell_rect.restype = ctypes.c_int
+        L.csao_compile_cell_rect.argtypes = [_c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _p,
+                                             _c_i32, _c_i32, _c_dbl, _c_dbl, _c_i32, _p, _p, _p,
+                                             _p, _p, _p, _p]
         L.csao_anchor_rows.restype = ctypes.c_int
         L.csao_anchor_rows.argtypes = [_c_i32, _c_i32, _p]
         L.csao_nearest_anchor.restype = _c_i32
@@ -123,10 +130,12 @@ def epsilon(t: int, T: int, A: float, C: float, k: float) -> float:
     return float(lib().csao_epsilon(t, T, A, C, k))
 
 
-def masked_attention_rows(q, k, v, scale: float, block: int, mask=None, rows=None):
+def masked_attention_rows(q, k, v, scale: float, block: int, mask=None, rows=None,
+                          block_kv: int | None = None):
     """Masked-softmax attention of one head (Q1, Q2).
 
-    q, k, v: [N, d]; mask: [N_B, N_B] {0,1} or None (dense); rows: (begin, end) token range.
+    q, k, v: [N, d]; mask: [N_B, N_Bkv] {0,1} or None (dense); rows: (begin, end) token range;
+    block_kv: key block size B_kv of non-square B_q x B_kv blocks, None -> block.
     Returns (out [rows, d] float64, lse [rows] float64, natural log).
     """
     q, k, v = _f64(q), _f64(k), _f64(v)
@@ -135,9 +144,10 @@ def masked_attention_rows(q, k, v, scale: float, block: int, mask=None, rows=Non
     out = np.empty((r1 - r0, d), np.float64)
     lse = np.empty((r1 - r0,), np.float64)
     m = None if mask is None else np.ascontiguousarray(np.asarray(mask, dtype=np.uint8))
-    rc = lib().csao_masked_attention_rows(n, d, block, _ptr(q), _ptr(k), _ptr(v), scale,
-                                          None if m is None else _ptr(m), r0, r1, _ptr(out),
-                                          _ptr(lse))
+    bk = block if block_kv is None else block_kv
+    rc = lib().csao_masked_attention_rows_rect(n, d, block, bk, _ptr(q), _ptr(k), _ptr(v), scale,
+                                               None if m is None else _ptr(m), r0, r1, _ptr(out),
+                                               _ptr(lse))
     if rc != 0:
         raise ValueError("csao_masked_attention_rows: invalid argument")
     return out, lse
@@ -273,18 +283,22 @@ def min_count(rho: float, n_prompts: int) -> int:
 
 
 def compile_cell(count, n: int, block: int, F: int, H: int, W: int, min_count_: int,
-                 similarity=None, gamma: float = 0.87, anchor_k: int = 5) -> dict:
-    """Plan for one cell (Q6-Q8)."""
-    nb = num_blocks(n, block)
-    cnt = np.ascontiguousarray(np.asarray(count, dtype=np.uint16).reshape(nb, nb))
+                 similarity=None, gamma: float = 0.87, anchor_k: int = 5,
+                 block_kv: int | None = None) -> dict:
+    """Plan for one cell (Q6-Q8); block_kv: key block
+    size of non-square B_q x B_kv blocks: count / mask are [N_B, N_Bkv]."""
+    nbq = num_blocks(n, block)
+    bk = block if block_kv is None else block_kv
+    nb = num_blocks(n, bk)
+    cnt = np.ascontiguousarray(np.asarray(count, dtype=np.uint16).reshape(nbq, nb))
     kind = np.zeros(1, np.uint8)
-    mask = np.zeros((nb, nb), np.uint8)
-    brp = np.zeros(nb + 1, np.int32)
-    bidx = np.zeros(nb * nb, np.uint16)
-    irp = np.zeros(nb + 1, np.int32)
-    ivl = np.zeros(2 * nb * nb, np.uint16)
+    mask = np.zeros((nbq, nb), np.uint8)
+    brp = np.zeros(nbq + 1, np.int32)
+    bidx = np.zeros(nbq * nb, np.uint16)
+    irp = np.zeros(nbq + 1, np.int32)
+    ivl = np.zeros(2 * nbq * nb, np.uint16)
     area = np.zeros(1, np.int64)
-    rc = lib().csao_compile_cell(n, block, F, H, W, _ptr(cnt), min_count_,
+    rc = lib().csao_compile_cell_rect(n, block, bk, F, H, W, _ptr(cnt), min_count_,
                                  0 if similarity is None else 1,
                                  0.0 if similarity is None else float(similarity), gamma, anchor_k,
                                  _ptr(kind), _ptr(mask), _ptr(brp), _ptr(bidx), _ptr(irp),

@@ -75,21 +75,37 @@ static double dot_scaled(const double* qi, const double* kj, int32_t d, double s
 /* mask is [N_B * N_B] bytes (row r, col c) or NULL for the all-ones (dense) mask.              */
 /* out: [(row_end-row_begin) * d]; lse (natural log, may be NULL): [(row_end-row_begin)].        */
 /* ------------------------------------------------------------------------------------------ */
+/* Non-square blocks B_q x B_kv: I_r uses B_q = bq, J_c uses B_kv = bk; mask is     */
+/* [N_Bq * N_Bkv] bytes.  bq == bk is the square case above (csao_masked_attention_rows).         */
+int csao_masked_attention_rows_rect(int64_t n, int32_t d, int32_t bq, int32_t bk, const double* q,
+                                    const double* k, const double* v, double scale,
+                                    const uint8_t* mask, int64_t row_begin, int64_t row_end,
+                                    double* out, double* lse);
+
 int csao_masked_attention_rows(int64_t n, int32_t d, int32_t b, const double* q, const double* k,
                                const double* v, double scale, const uint8_t* mask,
                                int64_t row_begin, int64_t row_end, double* out, double* lse) {
-    if (n <= 0 || d <= 0 || b <= 0 || row_begin < 0 || row_end > n || row_begin > row_end)
+    return csao_masked_attention_rows_rect(n, d, b, b, q, k, v, scale, mask, row_begin, row_end,
+                                           out, lse);
+}
+
+int csao_masked_attention_rows_rect(int64_t n, int32_t d, int32_t bq, int32_t bk, const double* q,
+                                    const double* k, const double* v, double scale,
+                                    const uint8_t* mask, int64_t row_begin, int64_t row_end,
+                                    double* out, double* lse) {
+    if (n <= 0 || d <= 0 || bq <= 0 || bk <= 0 || row_begin < 0 || row_end > n ||
+        row_begin > row_end)
         return ORC_EINVAL;
-    const int64_t nb = csao_num_blocks(n, b);
+    const int64_t nb = csao_num_blocks(n, bk); /* key blocks = mask columns */
     double* s = (double*)malloc(sizeof(double) * (size_t)n);
     uint8_t* keep = (uint8_t*)malloc((size_t)n);
     if (!s || !keep) { free(s); free(keep); return ORC_EINVAL; }
     for (int64_t i = row_begin; i < row_end; ++i) {
-        const int64_t r = i / b;
+        const int64_t r = i / bq;
         /* kept key set K_r = U_{c : M[r,c]=1} J_c, j < N (Q2) */
         for (int64_t c = 0; c < nb; ++c) {
             const uint8_t m = mask ? mask[r * nb + c] : 1;
-            for (int64_t j = blk_lo(c, b); j < blk_hi(c, b, n); ++j) keep[j] = m;
+            for (int64_t j = blk_lo(c, bk); j < blk_hi(c, bk, n); ++j) keep[j] = m;
         }
         double mx = -INFINITY;
         int64_t nkeep = 0;
@@ -352,24 +368,44 @@ int32_t csao_min_count(double rho, int32_t n_prompts) {
 /* Outputs (caller-sized): mask[N_B*N_B] bytes, blk_row_ptr[N_B+1], blk_idx[<=N_B*N_B],          */
 /* ivl_row_ptr[N_B+1], ivl[2*N_B*N_B] (start,end pairs).                                       */
 /* ------------------------------------------------------------------------------------------ */
+/* Non-square blocks B_q x B_kv: rows r < N_Bq (|I_r| from bq), columns          */
+/* c < N_Bkv (|J_c| from bk); count and mask are [N_Bq * N_Bkv], blk_row_ptr / ivl_row_ptr       */
+/* [N_Bq + 1].  bq == bk is csao_compile_cell.                                                  */
+int csao_compile_cell_rect(int64_t n, int32_t bq, int32_t bk, int32_t F, int32_t H, int32_t W,
+                           const uint16_t* count, int32_t min_count, int32_t has_sim, double sim,
+                           double gamma, int32_t anchor_k, uint8_t* kind, uint8_t* mask,
+                           int32_t* blk_row_ptr, uint16_t* blk_idx, int32_t* ivl_row_ptr,
+                           uint16_t* ivl, int64_t* kept_area);
+
 int csao_compile_cell(int64_t n, int32_t b, int32_t F, int32_t H, int32_t W,
                       const uint16_t* count, int32_t min_count, int32_t has_sim, double sim,
                       double gamma, int32_t anchor_k, uint8_t* kind, uint8_t* mask,
                       int32_t* blk_row_ptr, uint16_t* blk_idx, int32_t* ivl_row_ptr,
                       uint16_t* ivl, int64_t* kept_area) {
-    const int64_t nb = csao_num_blocks(n, b);
+    return csao_compile_cell_rect(n, b, b, F, H, W, count, min_count, has_sim, sim, gamma,
+                                  anchor_k, kind, mask, blk_row_ptr, blk_idx, ivl_row_ptr, ivl,
+                                  kept_area);
+}
+
+int csao_compile_cell_rect(int64_t n, int32_t bq, int32_t bk, int32_t F, int32_t H, int32_t W,
+                           const uint16_t* count, int32_t min_count, int32_t has_sim, double sim,
+                           double gamma, int32_t anchor_k, uint8_t* kind, uint8_t* mask,
+                           int32_t* blk_row_ptr, uint16_t* blk_idx, int32_t* ivl_row_ptr,
+                           uint16_t* ivl, int64_t* kept_area) {
+    const int64_t nbq = csao_num_blocks(n, bq); /* rows: query blocks */
+    const int64_t nb = csao_num_blocks(n, bk);  /* columns: key blocks */
     (void)H; /* anchor geometry only enters through F*k*W*N */
     if (has_sim && sim > gamma) {
         *kind = 1;
-        memset(mask, 0, (size_t)(nb * nb));
-        for (int64_t r = 0; r <= nb; ++r) { blk_row_ptr[r] = 0; ivl_row_ptr[r] = 0; }
+        memset(mask, 0, (size_t)(nbq * nb));
+        for (int64_t r = 0; r <= nbq; ++r) { blk_row_ptr[r] = 0; ivl_row_ptr[r] = 0; }
         *kept_area = (int64_t)F * anchor_k * W * n;
         return ORC_OK;
     }
     *kind = 0;
     int64_t area = 0;
     int32_t nblk = 0, nivl = 0;
-    for (int64_t r = 0; r < nb; ++r) {
+    for (int64_t r = 0; r < nbq; ++r) {
         const uint16_t* cr = count + r * nb;
         uint8_t* mr = mask + r * nb;
         int32_t any = 0;
@@ -388,13 +424,13 @@ int csao_compile_cell(int64_t n, int32_t b, int32_t F, int32_t H, int32_t W,
         for (int64_t c = 0; c < nb; ++c) {
             if (!mr[c]) continue;
             blk_idx[nblk++] = (uint16_t)c;
-            area += (blk_hi(r, b, n) - blk_lo(r, b)) * (blk_hi(c, b, n) - blk_lo(c, b));
+            area += (blk_hi(r, bq, n) - blk_lo(r, bq)) * (blk_hi(c, bk, n) - blk_lo(c, bk));
             if (c == 0 || !mr[c - 1]) { ivl[2 * nivl] = (uint16_t)c; }
             if (c == nb - 1 || !mr[c + 1]) { ivl[2 * nivl + 1] = (uint16_t)(c + 1); ++nivl; }
         }
     }
-    blk_row_ptr[nb] = nblk;
-    ivl_row_ptr[nb] = nivl;
+    blk_row_ptr[nbq] = nblk;
+    ivl_row_ptr[nbq] = nivl;
     *kept_area = area;
     return ORC_OK;
 }

@@ -32,7 +32,7 @@ class CsaError(RuntimeError):
 
 class _LayoutT(ctypes.Structure):
     _fields_ = [("frames", ctypes.c_int32), ("rows", ctypes.c_int32), ("cols", ctypes.c_int32),
-                ("block", ctypes.c_int32)]
+                ("block", ctypes.c_int32), ("block_kv", ctypes.c_int32)]
 
 
 class _TensorT(ctypes.Structure):
@@ -110,7 +110,7 @@ def _check(status: int, where: str) -> None:
 
 
 def _layout(lay: Layout) -> _LayoutT:
-    return _LayoutT(lay.F, lay.H, lay.W, lay.B)
+    return _LayoutT(lay.F, lay.H, lay.W, lay.B, lay.BK)
 
 
 def _tensor(t: torch.Tensor | None) -> _TensorT:
@@ -249,12 +249,12 @@ def compile_plan(lay: Layout, keep_count: torch.Tensor, min_count: int,
                  stream=None) -> Plan:
     """csa_compile_plan phase 0 (count) -> size read-back -> phase 1 (fill)."""
     dev = keep_count.device
-    nb = lay.NB
-    n_cells = keep_count.numel() // (nb * nb)
+    nb, nbk = lay.NB, lay.NBK
+    n_cells = keep_count.numel() // (nb * nbk)
     assert keep_count.dtype == torch.uint16 and keep_count.is_contiguous()
     if similarity is not None:
         assert similarity.dtype == torch.float64 and similarity.numel() == n_cells
-    w32 = (nb + 31) // 32
+    w32 = (nbk + 31) // 32
     e = torch.empty
     p = Plan(lay, n_cells,
              kind=e(n_cells, dtype=torch.uint8, device=dev),

@@ -108,12 +108,24 @@ csa_status_t check_layout(const csa_layout_t& L, int32_t head_dim, int32_t n_hea
     if (n >= (1LL << 31)) return fail(CSA_ERR_UNSUPPORTED, "layout: N too large");
     if ((n + L.block - 1) / L.block > csa::kMaxBlocks)
         return fail(CSA_ERR_UNSUPPORTED, "layout: N_B > %d", csa::kMaxBlocks);
+    if (L.block_kv != 0 && L.block_kv != L.block) {  // non-square B_q x B_kv
+        if (L.block != 128 || L.block_kv < 64 || L.block_kv > 192 || L.block_kv % 16 != 0)
+            return fail(CSA_ERR_UNSUPPORTED,
+                        "layout: block %d x block_kv %d (non-square needs block 128, block_kv a "
+                        "multiple of 16 in [64, 192])", L.block, L.block_kv);
+        if ((n + L.block_kv - 1) / L.block_kv > csa::kMaxBlocks)
+            return fail(CSA_ERR_UNSUPPORTED, "layout: N_Bkv > %d", csa::kMaxBlocks);
+    } else if (L.block_kv < 0) {
+        return fail(CSA_ERR_INVALID_ARGUMENT, "layout: block_kv < 0");
+    }
     if (head_dim != 0 && head_dim != 64 && head_dim != 128)
         return fail(CSA_ERR_UNSUPPORTED, "head_dim %d not in {64, 128}", head_dim);
     if (n_heads < 0 || n_heads > 2048)
         return fail(CSA_ERR_UNSUPPORTED, "n_heads %d outside [0, 2048]", n_heads);
     return CSA_OK;
 }
+
+bool is_square(const csa_layout_t& L) { return L.block_kv == 0 || L.block_kv == L.block; }
 
 bool plan_ptrs_ok(const csa_plan_t* p, bool need_lists) {
     if (!p || !p->kind || !p->anchor_k || !p->mask_bits || !p->blk_base || !p->blk_row_ptr ||
@@ -154,14 +166,14 @@ size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_
     }
     if (which == CSA_WS_MERGE) {          // interval-width histogram
         if (check_layout(L, 0, 0) != CSA_OK) return 0;
-        return (size_t)(csa::make_geo(L).NB + 1) * sizeof(int32_t);
+        return (size_t)(csa::make_geo(L).NBK + 1) * sizeof(int32_t);
     }
     if (which == CSA_WS_SIMILARITY) {     // per-token (dot, |p|^2, |p_a|^2) partials
-        if (check_layout(L, 0, 0) != CSA_OK || n_heads < 1) return 0;
+        if (check_layout(L, 0, 0) != CSA_OK || !is_square(L) || n_heads < 1) return 0;
         return (size_t)n_heads * (size_t)L.frames * L.rows * L.cols * 3 * sizeof(float);
     }
     if (which == CSA_WS_CALIB) {           // single-pass calibration: (t, m) row partials
-        if (check_layout(L, 0, 0) != CSA_OK || n_heads < 1) return 0;
+        if (check_layout(L, 0, 0) != CSA_OK || !is_square(L) || n_heads < 1) return 0;
         DeviceInfo di;
         if (device_info(&di) != CSA_OK) return 0;
         return csa::calib_scratch_bytes(csa::make_geo(L), n_heads, di.sms);
@@ -176,6 +188,8 @@ csa_status_t csa_calib_accumulate(csa_layout_t L, int32_t n_heads, int32_t head_
                                   size_t workspace_bytes, csa_stream_t stream) {
     csa_status_t st = check_layout(L, head_dim, n_heads);
     if (st != CSA_OK) return st;
+    if (!is_square(L))
+        return fail(CSA_ERR_UNSUPPORTED, "statistics passes need square blocks (block_kv 0)");
     if (n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "n_heads must be >= 1");
     if (!(softmax_scale > 0.0f)) return fail(CSA_ERR_INVALID_ARGUMENT, "softmax_scale <= 0");
     if (!(eps > 0.0)) return fail(CSA_ERR_INVALID_ARGUMENT, "eps must be > 0");
@@ -217,6 +231,8 @@ csa_status_t csa_spatial_similarity(csa_layout_t L, int32_t n_heads, int32_t hea
                                     csa_stream_t stream) {
     csa_status_t st = check_layout(L, head_dim, n_heads);
     if (st != CSA_OK) return st;
+    if (!is_square(L))
+        return fail(CSA_ERR_UNSUPPORTED, "statistics passes need square blocks (block_kv 0)");
     if (n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "n_heads must be >= 1");
     if (!(softmax_scale > 0.0f)) return fail(CSA_ERR_INVALID_ARGUMENT, "softmax_scale <= 0");
     if (anchor_k < 1 || anchor_k > L.rows)
@@ -384,8 +400,14 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
                                  size_t workspace_bytes, csa_stream_t stream) {
     csa_status_t st = check_layout(L, head_dim, n_heads);
     if (st != CSA_OK) return st;
-    if (pair_items && (L.block != 128 || head_dim != 128))
+    if (pair_items && (L.block != 128 || head_dim != 128 || !is_square(L)))
         return fail(CSA_ERR_UNSUPPORTED, "pair work items need block 128 and head_dim 128");
+    const bool rect = !is_square(L) || (L.block == 128 && head_dim == 128 &&
+                                        std::getenv("CSA_ATTN_RECT") != nullptr);
+    if (rect && head_dim != 128)
+        return fail(CSA_ERR_UNSUPPORTED, "non-square blocks need head_dim 128");
+    if (rect && workspace == nullptr)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "non-square blocks need the attention workspace");
     if (workspace != nullptr && (workspace_bytes < 8 || reinterpret_cast<uintptr_t>(workspace) % 8))
         return fail(CSA_ERR_INVALID_ARGUMENT, "attention workspace: >= 8 bytes, 8-byte aligned");
     if (batch < 1 || n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "batch/n_heads < 1");
@@ -406,8 +428,8 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
     const csa::Geo g = csa::make_geo(L);
     CUtensorMap tq, tk, tv;
     if ((st = make_map(&tq, q, batch, g.N, n_heads, head_dim, g.B, "q")) != CSA_OK) return st;
-    if ((st = make_map(&tk, k, batch, g.N, n_heads, head_dim, g.B, "k")) != CSA_OK) return st;
-    if ((st = make_map(&tv, v, batch, g.N, n_heads, head_dim, g.B, "v")) != CSA_OK) return st;
+    if ((st = make_map(&tk, k, batch, g.N, n_heads, head_dim, g.BK, "k")) != CSA_OK) return st;
+    if ((st = make_map(&tv, v, batch, g.N, n_heads, head_dim, g.BK, "v")) != CSA_OK) return st;
     csa::AttnArgs a;
     a.g = g;
     a.batch = batch;
@@ -440,6 +462,26 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
             return st;
         a.sched = nullptr;  // the pair kernel assigns pair items statically per cluster
         e = csa::launch_attn_pair(a, head_dim, tq, tk_half, tv, grid, (cudaStream_t)stream);
+    } else if (rect) {
+        // non-square B_q x B_kv (attn_rect.cu): fixed reference max (mode 0);
+        // overshooting items are recomputed from the fallback list by an exact-row-max pass
+        // (mode 1) and a pass against that max (mode 2), statically assigned, same stream.
+        const size_t items = (size_t)n_heads * (size_t)g.NB;
+        if (workspace_bytes < csa_workspace_size(CSA_WS_ATTN, L, n_heads, head_dim) ||
+            (int64_t)max_work > (int64_t)items)
+            return fail(CSA_ERR_INVALID_ARGUMENT, "attention workspace too small");
+        uint32_t* base = static_cast<uint32_t*>(workspace) + 64;
+        const size_t flag_words = (items + 31) / 32;
+        csa::Fallback fb{base, base + 1, base + 1 + flag_words};
+        e = cudaMemsetAsync(base, 0, 4 * (1 + flag_words), (cudaStream_t)stream);
+        if (e == cudaSuccess)
+            e = csa::launch_attn_rect(a, tq, tk, tv, grid, fb, 0, (cudaStream_t)stream);
+        csa::AttnArgs re = a;
+        re.work_list = fb.list;
+        re.n_work = reinterpret_cast<const int32_t*>(fb.count);
+        re.sched = nullptr;
+        for (int mode = 1; mode <= 2 && e == cudaSuccess; ++mode)
+            e = csa::launch_attn_rect(re, tq, tk, tv, di.sms, fb, mode, (cudaStream_t)stream);
     } else if (g.B == 128 && head_dim == 128 && workspace != nullptr &&
                !std::getenv("CSA_ATTN_RUNNING_MAX") && !std::getenv("CSA_ATTN_V3")) {
         // production (attn4.cu): fixed per-row reference max, two tiles in flight; items whose

@@ -30,7 +30,7 @@ __device__ __forceinline__ Item decode_item(const AttnArgs& a, int32_t item) {
     return it;
 }
 
-// Kept key-block list of a MASK item (CSR), or all N_B blocks for a REPETITIVE item.
+// Kept key-block list of a MASK item (CSR), or all N_Bkv key blocks for a REPETITIVE item.
 struct TileList {
     const uint16_t* idx;  // nullptr -> dense 0..n-1
     int32_t n;
@@ -41,7 +41,7 @@ __device__ __forceinline__ TileList tile_list(const AttnArgs& a, const Item& it)
     TileList t;
     if (it.kind) {
         t.idx = nullptr;
-        t.n = a.g.NB;
+        t.n = a.g.NBK;
     } else {
         const int32_t* rp = a.plan.blk_row_ptr + it.cell * (a.g.NB + 1);
         const int32_t r0 = rp[it.idx], r1 = rp[it.idx + 1];

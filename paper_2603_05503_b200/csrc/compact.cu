@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(1024)
     width_percentile_kernel(Geo g, int64_t n_cells, PlanDev p, double pct, int32_t* target,
                             int32_t* hist_ws) {
     __shared__ unsigned long long total;
-    const int32_t nbins = g.NB + 1;  // widths 0 .. N_B
+    const int32_t nbins = g.NBK + 1;  // widths 0 .. N_Bkv
     for (int32_t i = threadIdx.x; i < nbins; i += blockDim.x) hist_ws[i] = 0;
     if (threadIdx.x == 0) total = 0;
     __syncthreads();
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(256)
     if (n <= target) return;
     const uint16_t* iv = p.ivl + 2 * (p.ivl_base[cell] + rp[r]);
     const int32_t k = n - target;  // gaps to fill: the k smallest by (gap, index)
-    uint16_t* cnt = keep_count + (cell * g.NB + r) * (int64_t)g.NB;
+    uint16_t* cnt = keep_count + (cell * g.NB + r) * (int64_t)g.NBK;
     unsigned long long mine = 0;
     for (int32_t i = lane; i < n - 1; i += 32) {
         const int32_t gi = (int32_t)iv[2 * (i + 1)] - (int32_t)iv[2 * i + 1];
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(256)
     } else {
         const uint32_t* a = p.mask_bits + c1 * (int64_t)g.NB * g.W32;
         const uint32_t* b = p.mask_bits + c2 * (int64_t)g.NB * g.W32;
-        const int32_t tail = g.NB - (g.W32 - 1) * 32;  // valid bits in a row's last word
+        const int32_t tail = g.NBK - (g.W32 - 1) * 32;  // valid bits in a row's last word
         const uint32_t tail_mask = tail == 32 ? 0xffffffffu : ((1u << tail) - 1u);
         unsigned long long inter = 0, uni = 0;
         const int64_t words = (int64_t)g.NB * g.W32;
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(256)
     const int32_t t = (int32_t)(cell / n_groups), grp = (int32_t)(cell % n_groups);
     const int32_t* cl = cluster + (int64_t)grp * T;
     const int32_t mine = cl[t];
-    uint16_t* cnt = keep_count + (cell * g.NB + r) * (int64_t)g.NB;
+    uint16_t* cnt = keep_count + (cell * g.NB + r) * (int64_t)g.NBK;
     for (int32_t w = 0; w < g.W32; ++w) {
         uint32_t bits = 0;
         for (int32_t u = 0; u < T; ++u) {
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256)
             bits |= p.mask_bits[(cu * g.NB + r) * g.W32 + w];
         }
         const int32_t c = w * 32 + lane;
-        if (c < g.NB) cnt[c] = ((bits >> lane) & 1u) ? (uint16_t)min_count : (uint16_t)0;
+        if (c < g.NBK) cnt[c] = ((bits >> lane) & 1u) ? (uint16_t)min_count : (uint16_t)0;
     }
 }
 

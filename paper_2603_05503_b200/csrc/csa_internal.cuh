@@ -17,8 +17,10 @@ constexpr int kAnchorTile = 128;      // gathered anchor-query rows per REPETITI
 struct Geo {
     int32_t F, H, W, B;
     int32_t N;   // F*H*W
-    int32_t NB;  // ceil(N/B)
-    int32_t W32; // ceil(NB/32) mask words per row
+    int32_t NB;  // ceil(N/B): query blocks (plan rows)
+    int32_t BK;  // key block B_kv (= B for square blocks, P:1294-1328 for B_q x B_kv)
+    int32_t NBK; // ceil(N/BK): key blocks (plan columns)
+    int32_t W32; // ceil(NBK/32) mask words per row
 };
 
 inline Geo make_geo(const csa_layout_t& L) {
@@ -29,7 +31,9 @@ inline Geo make_geo(const csa_layout_t& L) {
     g.B = L.block;
     g.N = L.frames * L.rows * L.cols;
     g.NB = (g.N + g.B - 1) / g.B;
-    g.W32 = (g.NB + 31) / 32;
+    g.BK = L.block_kv > 0 ? L.block_kv : L.block;
+    g.NBK = (g.N + g.BK - 1) / g.BK;
+    g.W32 = (g.NBK + 31) / 32;
     return g;
 }
 
@@ -142,6 +146,13 @@ struct Fallback {
 cudaError_t launch_attn_fixed_ref(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
                                   const CUtensorMap& tv, int grid, const Fallback& fb,
                                   cudaStream_t s);
+// Non-square blocks B_q = 128 x B_kv (attn_rect.cu), head_dim 128.  mode 0: fixed reference
+// max (first kept tile), overshooting items appended to fb; mode 1: exact row max of every item
+// of the (fallback) list, parked in the item's first output row; mode 2: recompute the list
+// against that max.  Modes 1 and 2 run with static assignment over fb's list.
+cudaError_t launch_attn_rect(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, int grid, const Fallback& fb, int mode,
+                             cudaStream_t s);
 // Block 128, head_dim 128, one CTA per query block with Q resident in TMEM (attn3.cu).
 cudaError_t launch_attn_q_tmem(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
                                const CUtensorMap& tv, int grid, cudaStream_t s);

@@ -50,18 +50,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
             if (lane == 0) { brp[r + 1] = 0; irp[r + 1] = 0; }
             continue;
         }
-        const uint16_t* row = counts + (cell * g.NB + r) * (int64_t)g.NB;
+        const uint16_t* row = counts + (cell * g.NB + r) * (int64_t)g.NBK;
         int32_t nnz = 0;
         for (int w = 0; w < g.W32; ++w) {
             const int c = w * 32 + lane;
-            const bool keep = c < g.NB && (int32_t)row[c] >= min_count;
+            const bool keep = c < g.NBK && (int32_t)row[c] >= min_count;
             const uint32_t word = __ballot_sync(0xffffffffu, keep);
             nnz += __popc(word);
         }
         int32_t repair = -1;
         if (nnz == 0) {  // argmax count, lowest c on ties (Q7)
             int32_t best_v = -1, best_c = 0x7fffffff;
-            for (int c = lane; c < g.NB; c += 32) {
+            for (int c = lane; c < g.NBK; c += 32) {
                 const int32_t v = row[c];
                 if (v > best_v) { best_v = v; best_c = c; }
             }
@@ -79,13 +79,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         uint32_t carry = 0;  // kept bit of column w*32-1
         for (int w = 0; w < g.W32; ++w) {
             const int c = w * 32 + lane;
-            const bool keep = c < g.NB && ((int32_t)row[c] >= min_count || c == repair);
+            const bool keep = c < g.NBK && ((int32_t)row[c] >= min_count || c == repair);
             const uint32_t word = __ballot_sync(0xffffffffu, keep);
             if (lane == 0) words[w] = word;
             const uint32_t starts = word & ~((word << 1) | carry);
             nivl += __popc(starts);
             carry = word >> 31;
-            if (keep) cols += blk_size(c, g.B, g.N);
+            if (keep) cols += blk_size(c, g.BK, g.N);
         }
         for (int off = 16; off > 0; off >>= 1) cols += __shfl_xor_sync(0xffffffffu, cols, off);
         if (lane == 0) {
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(1024)
             const int h = lo;
             const int idx = x - head_off[h];
             const int64_t cell = cell_base + h;
-            int32_t cost = g.NB;
+            int32_t cost = g.NBK;
             if (!p.kind[cell]) {
                 const int32_t* rp = p.blk_row_ptr + cell * (g.NB + 1);
                 cost = rp[idx + 1] - rp[idx];
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(256)
             const int32_t units = units_of(h);
             auto unit_cost = [&](int32_t u) -> int32_t {
                 if (u >= units) return 0;
-                if (rep) return g.NB;
+                if (rep) return g.NBK;
                 const int32_t* rp = p.blk_row_ptr + cell * (g.NB + 1);
                 return rp[u + 1] - rp[u];
             };
@@ -393,7 +393,7 @@ __global__ void plan_validate_kernel(Geo g, int64_t n_cells, PlanDev p, uint32_t
                 int32_t prev = -1, cover = 0, bj = b0;
                 for (int32_t t = i0; t < i1; ++t) {
                     const int32_t s = iv[2 * t], e = iv[2 * t + 1];
-                    if (!(s < e) || e > g.NB || s <= prev) bad |= 32;  // ordered, non-adjacent
+                    if (!(s < e) || e > g.NBK || s <= prev) bad |= 32;  // ordered, non-adjacent
                     prev = e;
                     for (int32_t c = s; c < e && !bad; ++c, ++bj) {
                         if (bj >= b1 || bi[bj] != c) bad |= 64;  // CSR == decoded intervals
@@ -404,7 +404,7 @@ __global__ void plan_validate_kernel(Geo g, int64_t n_cells, PlanDev p, uint32_t
                 const uint32_t* words = p.mask_bits + (cell * g.NB + r) * g.W32;
                 for (int32_t t = b0; t < b1 && !bad; ++t) {
                     const int32_t c = bi[t];
-                    if (c >= g.NB || (t > b0 && c <= bi[t - 1])) bad |= 128;
+                    if (c >= g.NBK || (t > b0 && c <= bi[t - 1])) bad |= 128;
                     if (!((words[c >> 5] >> (c & 31)) & 1u)) bad |= 128;
                 }
             }

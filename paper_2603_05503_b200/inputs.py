@@ -23,12 +23,15 @@ import torch
 
 @dataclasses.dataclass(frozen=True)
 class Layout:
-    """Spatiotemporal token grid partitioned in B-token blocks."""
+    """Spatiotemporal token grid partitioned in B-token blocks; BK > 0
+    selects non-square B_q x B_kv = B x BK blocks: plan rows are the NB query
+    blocks, plan columns the NBK key blocks."""
 
     F: int
     H: int
     W: int
     B: int = 128
+    BK: int = 0
 
     @property
     def N(self) -> int:
@@ -38,8 +41,19 @@ class Layout:
     def NB(self) -> int:
         return (self.N + self.B - 1) // self.B
 
+    @property
+    def Bkv(self) -> int:
+        return self.BK if self.BK > 0 else self.B
+
+    @property
+    def NBK(self) -> int:
+        return (self.N + self.Bkv - 1) // self.Bkv
+
     def block_size(self, r: int) -> int:
         return min((r + 1) * self.B, self.N) - r * self.B
+
+    def key_block_size(self, c: int) -> int:
+        return min((c + 1) * self.Bkv, self.N) - c * self.Bkv
 
 
 @dataclasses.dataclass(frozen=True)
@@ -132,10 +146,12 @@ def structured_qk(lay: Layout, heads: int, d: int, head_seed: int, prompt_seed: 
             v.unsqueeze(0).to(torch.bfloat16))
 
 
-def _block_centres(lay: Layout) -> np.ndarray:
-    c = np.arange(lay.NB)
-    size = np.minimum((c + 1) * lay.B, lay.N) - c * lay.B
-    tok = c * lay.B + (size - 1) // 2
+def _block_centres(lay: Layout, block: int | None = None) -> np.ndarray:
+    b = lay.B if block is None else block
+    nb = (lay.N + b - 1) // b
+    c = np.arange(nb)
+    size = np.minimum((c + 1) * b, lay.N) - c * b
+    tok = c * b + (size - 1) // 2
     f = tok // (lay.H * lay.W)
     i = (tok // lay.W) % lay.H
     j = tok % lay.W
@@ -146,37 +162,42 @@ def synthetic_masks(lay: Layout, heads: int, target_sparsity: float, seed: int =
                     lam_t: float = 1.0, tol: float = 0.005) -> np.ndarray:
     """Generator S: per-head block masks at a target area sparsity.
 
-    Block (r, c) distance D = lam_t |f_r - f_c| + ||(i,j)_r - (i,j)_c|| / H; head keep fraction
-    kappa_h ~ Beta(2,3); row fraction kappa_{h,r} = clip(m kappa_h exp(0.3 z), 1/N_B, 1);
-    keep the ceil(kappa N_B) nearest blocks (ties c asc) plus the diagonal and block 0 (sink);
+    Block (r, c) distance D = lam_t |f_r - f_c| + ||(i,j)_r - (i,j)_c|| / H between block-centre
+    tokens; head keep fraction kappa_h ~ Beta(2,3); row fraction kappa_{h,r} = clip(m kappa_h
+    exp(0.3 z), 1/N_Bkv, 1); keep the ceil(kappa N_Bkv) nearest key blocks (ties c asc) plus the
+    key block holding the query block's centre token (the diagonal) and key block 0 (sink);
     bisect the global multiplier m until area sparsity is within tol of the target.
-    Returns uint8 [heads, N_B, N_B]."""
-    nb, rng = lay.NB, np.random.default_rng(seed)
+    Non-square layouts (lay.BK): rows are query blocks of B, columns key blocks of
+    B_kv.  Returns uint8 [heads, N_B, N_Bkv]."""
+    nb, nbk, rng = lay.NB, lay.NBK, np.random.default_rng(seed)
     cen = _block_centres(lay)
-    df = np.abs(cen[:, None, 0] - cen[None, :, 0])
-    ds = np.hypot(cen[:, None, 1] - cen[None, :, 1], cen[:, None, 2] - cen[None, :, 2]) / lay.H
+    ckey = _block_centres(lay, lay.Bkv)
+    df = np.abs(cen[:, None, 0] - ckey[None, :, 0])
+    ds = np.hypot(cen[:, None, 1] - ckey[None, :, 1], cen[:, None, 2] - ckey[None, :, 2]) / lay.H
     dist = lam_t * df + ds
-    order = np.argsort(dist, axis=1, kind="stable")                   # [nb, nb]
-    sizes = np.array([lay.block_size(c) for c in range(nb)], np.int64)
-    csum = np.concatenate([np.zeros((nb, 1), np.int64), np.cumsum(sizes[order], axis=1)], axis=1)
+    order = np.argsort(dist, axis=1, kind="stable")                   # [nb, nbk]
+    qsizes = np.array([lay.block_size(r) for r in range(nb)], np.int64)
+    ksizes = np.array([lay.key_block_size(c) for c in range(nbk)], np.int64)
+    csum = np.concatenate([np.zeros((nb, 1), np.int64), np.cumsum(ksizes[order], axis=1)], axis=1)
+    rows = np.arange(nb)
     rank = np.empty_like(order)
-    rank[np.arange(nb)[:, None], order] = np.arange(nb)[None, :]
-    rank_diag = rank[np.arange(nb), np.arange(nb)]
+    rank[rows[:, None], order] = np.arange(nbk)[None, :]
+    diag_c = (rows * lay.B + (qsizes - 1) // 2) // lay.Bkv             # = r for square blocks
+    rank_diag = rank[rows, diag_c]
     rank_zero = rank[:, 0]
     kap_h = rng.beta(2.0, 3.0, size=heads)
     z = rng.standard_normal((heads, nb))
-    rows = np.arange(nb)
 
     def counts_for(m):
-        kap = np.clip(m * kap_h[:, None] * np.exp(0.3 * z), 1.0 / nb, 1.0)
-        return np.minimum(np.ceil(kap * nb).astype(np.int64), nb)
+        kap = np.clip(m * kap_h[:, None] * np.exp(0.3 * z), 1.0 / nbk, 1.0)
+        return np.minimum(np.ceil(kap * nbk).astype(np.int64), nbk)
 
     def sparsity_for(m):
         kk = counts_for(m)
         area_cols = csum[rows[None, :], kk]                            # [heads, nb]
-        extra_d = np.where(rank_diag[None, :] >= kk, sizes[rows][None, :], 0)
-        extra_0 = np.where((rank_zero[None, :] >= kk) & (rows[None, :] != 0), sizes[0], 0)
-        area = ((area_cols + extra_d + extra_0) * sizes[None, :]).sum()
+        extra_d = np.where(rank_diag[None, :] >= kk, ksizes[diag_c][None, :], 0)
+        extra_0 = np.where((rank_zero[None, :] >= kk) & (diag_c[None, :] != 0), ksizes[0], 0)
+        area = ((area_cols + extra_d + extra_0) * qsizes[None, :]).sum()
         return 1.0 - area / float(heads * lay.N * lay.N)
 
     lo, hi = 1e-4, 50.0
@@ -191,12 +212,12 @@ def synthetic_masks(lay: Layout, heads: int, target_sparsity: float, seed: int =
         else:
             hi = m
     kk = counts_for(m)
-    masks = np.zeros((heads, nb, nb), np.uint8)
+    masks = np.zeros((heads, nb, nbk), np.uint8)
     for h in range(heads):
-        sel = np.arange(nb)[None, :] < kk[h][:, None]                 # [nb, nb] in rank space
-        mh = np.zeros((nb, nb), np.uint8)
+        sel = np.arange(nbk)[None, :] < kk[h][:, None]                # [nb, nbk] in rank space
+        mh = np.zeros((nb, nbk), np.uint8)
         mh[rows[:, None], order] = sel
-        mh[rows, rows] = 1
+        mh[rows, diag_c] = 1
         mh[:, 0] = 1
         masks[h] = mh
     return masks
@@ -208,9 +229,11 @@ def synthetic_counts(lay: Layout, heads: int, target_sparsity: float, n_prompts:
     return synthetic_masks(lay, heads, target_sparsity, seed).astype(np.uint16) * np.uint16(n_prompts)
 
 
-def random_counts(nb: int, cells: int, n_prompts: int, seed: int, p_zero: float = 0.3) -> np.ndarray:
-    """Uniform random keep counts in [0, |D|] with extra zeros (plan-compiler edge coverage)."""
+def random_counts(nb: int, cells: int, n_prompts: int, seed: int, p_zero: float = 0.3,
+                  nbk: int | None = None) -> np.ndarray:
+    """Uniform random keep counts in [0, |D|] with extra zeros (plan-compiler edge coverage);
+    [cells, nb, nbk] (nbk: key blocks of a non-square layout, default nb)."""
     rng = np.random.default_rng(seed)
-    c = rng.integers(0, n_prompts + 1, size=(cells, nb, nb))
+    c = rng.integers(0, n_prompts + 1, size=(cells, nb, nb if nbk is None else nbk))
     c[rng.random(c.shape) < p_zero] = 0
     return c.astype(np.uint16)

@@ -1,0 +1,149 @@
+"""Whole-schedule runtime (f4): the calibrated plan dictionary over every (t, l, h) cell and the
+attention of one denoising step over all layers, CFG batch 2, replayed as a CUDA graph.
+
+PAPER.md:
+  * the dictionary: calibration over |D| prompts for every timestep t, layer l and head h
+    (P:532-571), repetitive heads from the spatial-similarity statistic, and the
+    timestep-dependent threshold eps(t) of Eq. eq:epsilon_schedule with the paper's
+    fitted constants: high-step A(N) = 0.796 + 1.41e-6 N, C = 0.99, k = 16 or the
+    4-step distilled (LightX2V) A = 0.763, C = 0.863, k = 5.64;
+  * CFG: masks and similarity are calibrated on the conditional branch only, and the same cell
+    plan serves both branches at inference -- here batch 2 of one launch;
+  * a denoising step runs the sparse attention of every layer with the cell plans of (t, l, .)
+    (P:651-656); the kernel receives the (t, l, h) skip list at launch.
+
+Every arithmetic step is a libcsa.so call (csa_calib_accumulate, csa_spatial_similarity,
+csa_compile_plan, csa_build_work_list, csa_sparse_attn_fwd); this module only orders them, holds
+the buffers and captures the per-step launch sequence in a CUDA graph (no host work between
+layers at replay).  Cell convention (csa.h): cell = (t * L + l) * H + h.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import Callable
+
+import torch
+
+from . import csa
+from .inputs import Layout
+
+# "the same schedule for both 480p and 720p distilled LightX2V: A=0.763, C=0.863, k=5.64"
+DISTILLED = (0.763, 0.863, 5.64)
+
+
+def high_step_constants(n: int) -> tuple[float, float, float]:
+    """(A(N), C, k) of the high-step regime, N = attention sequence length."""
+    return 0.796 + 1.41e-6 * n, 0.99, 16.0
+
+
+def epsilon_schedule(T: int, A: float, C: float, k: float) -> list[float]:
+    """eps(t) = A + (C - A) exp(-k t / T), t = 0..T-1, t = 0 the highest noise (Eq.
+    eq:epsilon_schedule).  Row a1: host fp64, passed to the kernel as a double."""
+    return [A + (C - A) * math.exp(-k * t / T) for t in range(T)]
+
+
+@dataclasses.dataclass
+class PlanDictionary:
+    """Compiled plans of all T * L * H cells (one csa.Plan) and the statistics behind them."""
+
+    lay: Layout
+    T: int
+    L: int
+    H: int
+    plan: csa.Plan
+    eps: list
+    min_count: int
+    prompts: int
+    similarity: torch.Tensor   # fp64 [T * L * H]
+    keep_count: torch.Tensor   # uint16 [T * L * H, N_B, N_B]
+
+    def cell_base(self, t: int, l: int) -> int:
+        return (t * self.L + l) * self.H
+
+    def kept_fraction(self, t: int | None = None) -> float:
+        """Kept area / dense area over the cells of timestep t (all cells if None)."""
+        area = self.plan.kept_area.view(self.T, self.L * self.H)
+        sel = area if t is None else area[t:t + 1]
+        return float(sel.sum().item()) / (sel.numel() * float(self.lay.N) ** 2)
+
+
+def calibrate(lay: Layout, T: int, L: int, H: int, prompts: int,
+              qk_fn: Callable[[int, int, int], tuple[torch.Tensor, torch.Tensor]],
+              constants: tuple[float, float, float], rho: float = 0.5, gamma: float = 0.87,
+              anchor_k: int = 5, device="cuda") -> PlanDictionary:
+    """Offline calibration of the whole dictionary.
+
+    qk_fn(prompt, t, l) -> conditional-branch Q, K bf16 [1, N, H, d] of that layer at that step.
+    Per (prompt, t, l): csa_calib_accumulate adds the prompt's per-row selections at eps(t) to the
+    cells' keep counts (a2-a5) and csa_spatial_similarity adds its cosines (f1) from the pass's own
+    row LSE.  Then s = sim_sum / (F H |D|), min_count = ceil(rho |D|) and one csa_compile_plan over
+    every cell (a6; s > gamma -> REPETITIVE)."""
+    eps = epsilon_schedule(T, *constants)
+    nb = lay.NB
+    cells = T * L * H
+    keep = torch.zeros(cells * nb * nb, dtype=torch.int16, device=device).view(torch.uint16)
+    sim_sum = torch.zeros(cells, dtype=torch.float64, device=device)
+    lse = torch.empty(H * lay.N, dtype=torch.float32, device=device)
+    per = H * nb * nb
+    for p in range(prompts):
+        for t in range(T):
+            for l in range(L):
+                q, k = qk_fn(p, t, l)
+                c0 = (t * L + l) * H
+                csa.calib_accumulate(lay, q, k, eps[t], keep[c0 * nb * nb:c0 * nb * nb + per],
+                                     lse_out=lse)
+                csa.spatial_similarity(lay, q, k, lse, anchor_k, sim_sum[c0:c0 + H])
+    # smallest integer >= rho |D| (Eq. eq:mask_threshold in count space, reading Q6)
+    min_count = math.ceil(rho * prompts - 1e-12)
+    s = sim_sum / float(lay.F * lay.H * prompts)
+    plan = csa.compile_plan(lay, keep, min_count, similarity=s, gamma=gamma, anchor_k=anchor_k)
+    return PlanDictionary(lay, T, L, H, plan, eps, min_count, prompts, s,
+                          keep.view(cells, nb, nb))
+
+
+class DenoiseStep:
+    """Attention of all L layers of one denoising step: layer l reads q[l % S], k[l % S],
+    v[l % S] and writes o[l % S] (S buffer sets, [batch, N, H, d] bf16; batch 2 = the CFG
+    branches sharing every cell plan), with the cell plans of (t, l, .).
+
+    Work lists are built once per (t, l).  run(t) launches the L attention calls eagerly;
+    capture(t) records the same sequence in a CUDA graph and replay(t) launches it (one host call
+    per step; the dynamic scheduler's counters self-reset, so replays are independent)."""
+
+    def __init__(self, dic: PlanDictionary, q: list, k: list, v: list, o: list):
+        self.dic, self.q, self.k, self.v, self.o = dic, q, k, v, o
+        self.work = [[csa.build_work_list(dic.plan, dic.cell_base(t, l), dic.H)
+                      for l in range(dic.L)] for t in range(dic.T)]
+        self.graphs: dict = {}
+        self.stream = torch.cuda.Stream(device=q[0].device)
+
+    def _launch(self, t: int, stream) -> None:
+        dic, S = self.dic, len(self.q)
+        for l in range(dic.L):
+            s = l % S
+            csa.sparse_attn_fwd(self.q[s], self.k[s], self.v[s], dic.plan, self.work[t][l],
+                                cell_base=dic.cell_base(t, l), out=self.o[s], stream=stream)
+
+    def run(self, t: int) -> None:
+        self._launch(t, torch.cuda.current_stream())
+
+    def capture(self, t: int) -> torch.cuda.CUDAGraph:
+        if t not in self.graphs:
+            with torch.cuda.stream(self.stream):
+                self._launch(t, self.stream)  # warm: workspaces allocated, kernels loaded
+            self.stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                self._launch(t, self.stream)
+            self.graphs[t] = g
+        return self.graphs[t]
+
+    def replay(self, t: int) -> None:
+        self.capture(t).replay()
+
+    def flop(self, t: int) -> float:
+        """Algorithmic FLOPs of step t: 4 d batch sum over its cells of kept_area."""
+        d, b = self.q[0].shape[3], self.q[0].shape[0]
+        area = self.dic.plan.kept_area.view(self.dic.T, -1)[t]
+        return 4.0 * d * b * float(area.sum().item())

@@ -1,0 +1,135 @@
+"""Block-size sweep (f3, Table tab:block_size_ablation) on one B200.
+
+For every B_q x B_kv = 128 x B_kv of the paper's table, one Wan2.1 480p attention layer (40
+heads, d 128, N 32760, seeded N(0,1) bf16 Q/K/V) with generator-S masks built on that block grid at
+the mask sparsity the paper reports for it (mask sparsity only, no repetitive heads, as in the
+table), compiled by csa_compile_plan and run through csa_sparse_attn_fwd:
+  * attention ms (CUDA events, median of --steps after --warmup), effective TFLOP/s of the kept
+    FLOPs (4 d sum kept_area) and its fraction of the measured bf16 peak;
+  * the same kernel on the all-ones plan of that grid (dense) -> speedup and proportionality;
+  * at 128 x 128 also the generic B_kv kernel (CSA_ATTN_RECT) next to the production kernel;
+  * parity: sampled (head, query-block) units against the fp64 oracle (bar: north-star).
+One JSON line per configuration; --json-out collects them.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2603_05503_b200 import csa, inputs  # noqa: E402
+
+PAPER = {64: 0.649, 80: 0.646, 96: 0.641, 128: 0.634, 144: 0.631, 176: 0.625, 192: 0.621}
+
+
+def timed(fn, steps, warmup):
+    for _ in range(warmup):
+        fn()
+    ts = []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def parity(lay, q, k, v, out, masks, units):
+    import oracle
+
+    errs = []
+    for h, r in units:
+        rows = (r * lay.B, min((r + 1) * lay.B, lay.N))
+        qh, kh, vh = (t[0, :, h].double().cpu().numpy() for t in (q, k, v))
+        ref, _ = oracle.masked_attention_rows(qh, kh, vh, 1.0 / math.sqrt(q.shape[3]), lay.B,
+                                              masks[h], rows, block_kv=lay.BK or None)
+        got = out[0, rows[0]:rows[1], h].double().cpu().numpy()
+        errs.append((np.abs(got - ref).max(), np.abs(got - ref).mean()))
+    return max(e[0] for e in errs), max(e[1] for e in errs)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--bkv", default="64,80,96,128,144,176,192")
+    ap.add_argument("--json-out", default=None)
+    args = ap.parse_args()
+    peak = 1685.2
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peak = json.load(fh).get("bf16_tflops") or peak
+    except OSError:
+        pass
+    base = inputs.CONFIGS["wan480"]
+    H, d = base.heads, base.d
+    q, k, v = inputs.qkv(1, base.layout.N, H, d, seed=11, device="cuda")
+    out = torch.empty_like(q)
+    rows = []
+    for bkv in [int(x) for x in args.bkv.split(",")]:
+        lay = inputs.Layout(base.layout.F, base.layout.H, base.layout.W, 128,
+                            0 if bkv == 128 else bkv)
+        masks = inputs.synthetic_masks(lay, H, PAPER[bkv], seed=0)
+        counts = torch.from_numpy((masks.astype(np.uint16) * np.uint16(64)).reshape(-1)
+                                  .view(np.int16)).cuda().view(torch.uint16)
+        plan = csa.compile_plan(lay, counts, 32)
+        work = csa.build_work_list(plan, 0, H)
+        area = int(plan.kept_area.sum().item())
+        flop = 4.0 * d * area
+        ones = torch.full((H * lay.NB * lay.NBK,), 64, dtype=torch.int16,
+                          device="cuda").view(torch.uint16)
+        plan1 = csa.compile_plan(lay, ones, 32)
+        work1 = csa.build_work_list(plan1, 0, H)
+        variants = [("production" if bkv == 128 else "attn_rect", {})]
+        if bkv == 128:
+            variants.append(("attn_rect", {"CSA_ATTN_RECT": "1"}))
+        for name, env in variants:
+            os.environ.update(env)
+            try:
+                ms = timed(lambda: csa.sparse_attn_fwd(q, k, v, plan, work, out=out),
+                           args.steps, args.warmup)
+                ms_dense = timed(lambda: csa.sparse_attn_fwd(q, k, v, plan1, work1, out=out),
+                                 max(3, args.steps // 2), 2)
+                csa.sparse_attn_fwd(q, k, v, plan, work, out=out)
+                torch.cuda.synchronize()
+                rng = np.random.default_rng(bkv)
+                units = [(0, lay.NB - 1)] + [(int(rng.integers(H)), int(rng.integers(lay.NB)))
+                                             for _ in range(3)]
+                mx, mean = parity(lay, q, k, v, out, masks, units)
+            finally:
+                for key in env:
+                    os.environ.pop(key, None)
+            kept = area / (H * float(lay.N) ** 2)
+            row = {"B_q": 128, "B_kv": bkv, "kernel": name, "sparsity": round(1 - kept, 4),
+                   "paper_sparsity": PAPER[bkv], "attn_ms": round(ms, 3),
+                   "tflops_eff": round(flop / (ms * 1e-3) / 1e12, 1),
+                   "frac_of_bf16_peak": round(flop / (ms * 1e-3) / 1e12 / peak, 4),
+                   "dense_ms": round(ms_dense, 3),
+                   "dense_tflops": round(4.0 * d * H * float(lay.N) ** 2 / (ms_dense * 1e-3) / 1e12, 1),
+                   "speedup_vs_dense": round(ms_dense / ms, 3),
+                   "proportionality": round(ms_dense / ms * kept, 3),
+                   "parity_max_abs": float(mx), "parity_mean_abs": float(mean),
+                   "parity_ok": bool(mx <= 2e-2 and mean <= 2e-3)}
+            rows.append(row)
+            print(json.dumps(row), flush=True)
+    if args.json_out:
+        with open(args.json_out, "w") as fh:
+            json.dump({"workload": "wan480 single attention layer, 40 heads, d 128, N 32760, "
+                                   "generator-S masks at the paper's per-block-size sparsity",
+                       "peak_bf16_tflops": peak, "rows": rows}, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()

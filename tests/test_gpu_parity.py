@@ -60,9 +60,9 @@ def check_plan_against_oracle(csa, lay, counts_np, min_count, sim=None, gamma=0.
     simt = None if sim is None else torch.tensor(sim, dtype=torch.float64, device=dev)
     plan = csa.compile_plan(lay, counts, min_count, similarity=simt, gamma=gamma, anchor_k=anchor_k)
     csa.validate_plan(plan)
-    nb = lay.NB
+    nb, nbk = lay.NB, lay.NBK
     kind = plan.kind.cpu().numpy()
-    bits = unpack_bits(plan.mask_bits.cpu().numpy(), nb).reshape(cells, nb, nb)
+    bits = unpack_bits(plan.mask_bits.cpu().numpy(), nbk).reshape(cells, nb, nbk)
     brp = plan.blk_row_ptr.cpu().numpy().reshape(cells, nb + 1)
     irp = plan.ivl_row_ptr.cpu().numpy().reshape(cells, nb + 1)
     bb = plan.blk_base.cpu().numpy()
@@ -73,7 +73,7 @@ def check_plan_against_oracle(csa, lay, counts_np, min_count, sim=None, gamma=0.
     for c in range(cells):
         ref = oracle.compile_cell(counts_np[c], lay.N, lay.B, lay.F, lay.H, lay.W, min_count,
                                   similarity=None if sim is None else sim[c], gamma=gamma,
-                                  anchor_k=anchor_k)
+                                  anchor_k=anchor_k, block_kv=lay.BK or None)
         assert kind[c] == ref["kind"]
         assert area[c] == ref["kept_area"]
         assert np.array_equal(brp[c], ref["blk_row_ptr"])
@@ -133,11 +133,10 @@ def test_work_list_bit_exact(csa):
 
 # ---------------------------------------------------------------- a7/a8 attention
 def run_attention(csa, lay, q, k, v, masks=None, rep=None, anchor_k=2, order=2, lse=False):
-    """masks: [H, NB, NB] uint8 for MASK heads; rep: list of REPETITIVE head indices."""
+    """masks: [H, NB, NBK] uint8 for MASK heads; rep: list of REPETITIVE head indices."""
     heads = q.shape[2]
-    nb = lay.NB
     if masks is None:
-        masks = np.ones((heads, nb, nb), np.uint8)
+        masks = np.ones((heads, lay.NB, lay.NBK), np.uint8)
     counts = masks.astype(np.uint16)
     sim = None
     if rep:
@@ -164,7 +163,8 @@ def oracle_head(lay, q, k, v, b, h, mask=None, rep_k=None, rows=None):
     qh, kh, vh = head64(q, b, h), head64(k, b, h), head64(v, b, h)
     if rep_k:
         return oracle.anchor_attention_rows(lay.F, lay.H, lay.W, qh, kh, vh, scale, rep_k, rows)
-    return oracle.masked_attention_rows(qh, kh, vh, scale, lay.B, mask, rows)
+    return oracle.masked_attention_rows(qh, kh, vh, scale, lay.B, mask, rows,
+                                        block_kv=lay.BK or None)
 
 
 def assert_close(got, ref, what=""):
@@ -497,26 +497,27 @@ def _row_intervals(mask_row):
     return ivl
 
 
-@pytest.mark.parametrize("lay", [Layout(2, 5, 25, 64), Layout(21, 30, 52, 128)])
+@pytest.mark.parametrize("lay", [Layout(2, 5, 25, 64), Layout(21, 30, 52, 128),
+                                 Layout(21, 30, 52, 128, 80)])
 @pytest.mark.parametrize("pct", [100.0, 90.0, 50.0])
 def test_merge_intervals_bit_exact(csa, lay, pct):
-    nb, cells = lay.NB, 4
-    counts_np = inputs.random_counts(nb, cells, 8, seed=nb + int(pct))
+    nbq, nb, cells = lay.NB, lay.NBK, 4
+    counts_np = inputs.random_counts(nbq, cells, 8, seed=nb + int(pct), nbk=nb)
     counts_np[2][:, ::2] = 8  # alternating rows: the widest rows
     sim = torch.tensor([0.0, 0.0, 0.0, 1.0], dtype=torch.float64, device="cuda")  # cell 3 REPETITIVE
     counts = u16_dev(counts_np)
     plan = csa.compile_plan(lay, counts, 4, similarity=sim, anchor_k=min(5, lay.H))
-    bits = unpack_bits(plan.mask_bits.cpu().numpy(), nb).reshape(cells, nb, nb)
-    widths = [len(_row_intervals(bits[c, r])) for c in range(3) for r in range(nb)]
+    bits = unpack_bits(plan.mask_bits.cpu().numpy(), nb).reshape(cells, nbq, nb)
+    widths = [len(_row_intervals(bits[c, r])) for c in range(3) for r in range(nbq)]
     target_ref = oracle.percentile_nearest_rank(widths, pct)
     target, added = csa.merge_intervals(plan, counts, 4, pct)
     torch.cuda.synchronize()
     assert int(target.item()) == target_ref
-    got = u16_np(counts).reshape(cells, nb, nb)
+    got = u16_np(counts).reshape(cells, nbq, nb)
     ref = counts_np.copy()
     added_ref = 0
     for c in range(3):
-        for r in range(nb):
+        for r in range(nbq):
             merged, add = oracle.merge_row(_row_intervals(bits[c, r]), max(target_ref, 1))
             added_ref += add
             kept = np.zeros(nb, bool)
@@ -528,9 +529,9 @@ def test_merge_intervals_bit_exact(csa, lay, pct):
     assert int(added.item()) == added_ref
     # recompiled plan: every row within the target, kept sets supersets
     plan2 = csa.compile_plan(lay, counts, 4, similarity=sim, anchor_k=min(5, lay.H))
-    bits2 = unpack_bits(plan2.mask_bits.cpu().numpy(), nb).reshape(cells, nb, nb)
+    bits2 = unpack_bits(plan2.mask_bits.cpu().numpy(), nb).reshape(cells, nbq, nb)
     assert (bits2[:3] >= bits[:3]).all()
-    irp = plan2.ivl_row_ptr.cpu().numpy().reshape(cells, nb + 1)
+    irp = plan2.ivl_row_ptr.cpu().numpy().reshape(cells, nbq + 1)
     assert np.diff(irp[:3], axis=1).max() <= max(target_ref, 1)
 
 
@@ -615,3 +616,174 @@ def test_host_streaming_api_equals_device_call(csa):
         csa.sparse_attn_fwd_host(hq, hk, hv, plan, ho, heads_per_chunk=chunk)
         torch.cuda.synchronize()
         assert torch.equal(ho, ref.cpu()), chunk
+
+
+# ---------------------------------------------------------------- f3: non-square B_q x B_kv
+BKV_ALL = [64, 80, 96, 112, 144, 160, 176, 192]
+# Table tab:block_size_ablation: mask sparsity per B_q x B_kv at Wan 480p
+PAPER_SPARSITY = {64: 0.649, 80: 0.646, 96: 0.641, 128: 0.634, 144: 0.631, 176: 0.625, 192: 0.621}
+
+
+@pytest.mark.parametrize("lay", [Layout(2, 9, 40, 128, 80), Layout(3, 7, 100, 128, 176),
+                                 Layout(21, 30, 52, 128, 64)])
+def test_rect_plan_compile_bit_exact(csa, lay):
+    """a6 on a B_q x B_kv grid (rows N_B query blocks, columns N_Bkv key blocks)."""
+    counts = inputs.random_counts(lay.NB, 5, 64, seed=lay.NBK, nbk=lay.NBK)
+    counts[1] = 0
+    counts[2] = 64
+    counts[3] = 0
+    counts[3][:, ::2] = 40
+    check_plan_against_oracle(csa, lay, counts, 32)
+    check_plan_against_oracle(csa, lay, counts, 32, sim=[0.5, 0.87, 0.9, 1.0, 0.0],
+                              anchor_k=min(5, lay.H))
+
+
+@pytest.mark.parametrize("bkv", BKV_ALL)
+def test_rect_attention_against_oracle(csa, bkv):
+    """Every B_kv kernel instance: ragged N (N_Bkv ragged for most B_kv), random MASK heads, an
+    anchor head, batch 2 sharing the plan, lse; outputs vs the fp64 oracle on the same grid."""
+    lay = Layout(2, 9, 40, 128, bkv)  # N = 720
+    heads = 3
+    q, k, v = qkv(2, lay.N, heads, 128, seed=bkv, device="cuda")
+    rng = np.random.default_rng(bkv)
+    masks = (rng.random((heads, lay.NB, lay.NBK)) < 0.5).astype(np.uint8)
+    masks[:, :, -1] = 1  # the ragged last key block
+    out, lse, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[2], anchor_k=2, lse=True)
+    lse = lse.view(2, heads, lay.N).cpu().numpy()
+    for b in range(2):
+        for h in range(heads):
+            ref, ref_lse = oracle_head(lay, q, k, v, b, h, mask=masks[h],
+                                       rep_k=2 if h == 2 else None)
+            assert_close(out[b, :, h].double().cpu().numpy(), ref, f"B_kv {bkv} b{b} h{h}")
+            assert np.abs(lse[b, h] - ref_lse).max() <= 1e-3
+    again, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[2], anchor_k=2)
+    assert torch.equal(out, again)
+    assert fallback_count(csa, q) == 0
+
+
+@pytest.mark.parametrize("bkv", [80, 192])
+def test_rect_attention_overflow_fallback(csa, bkv):
+    """Scores growing 40x block by block overshoot the first tile's reference max by far more
+    than 2^56: those items go through the exact-row-max fallback (modes 1, 2) and still match."""
+    lay = Layout(2, 9, 40, 128, bkv)
+    heads = 2
+    q, k, v = qkv(1, lay.N, heads, 128, seed=21, device="cuda")
+    gain = torch.ones(lay.N, device="cuda")
+    for c in range(lay.NBK):
+        gain[c * bkv:(c + 1) * bkv] = 1.0 + 40.0 * c / lay.NBK
+    k = (k.float() * gain.view(1, -1, 1, 1)).to(torch.bfloat16)
+    rng = np.random.default_rng(5)
+    masks = (rng.random((heads, lay.NB, lay.NBK)) < 0.6).astype(np.uint8)
+    masks[:, :, 0] = 1
+    masks[:, :, -1] = 1
+    out, lse, _ = run_attention(csa, lay, q, k, v, masks=masks, lse=True)
+    assert fallback_count(csa, q) > 0
+    lse_np = lse.view(heads, lay.N).cpu().numpy()
+    for h in range(heads):
+        ref, ref_lse = oracle_head(lay, q, k, v, 0, h, mask=masks[h])
+        assert_close(out[0, :, h].double().cpu().numpy(), ref, f"B_kv {bkv} h{h}")
+        assert np.abs(lse_np[h] - ref_lse).max() <= 1e-3 * max(1.0, np.abs(ref_lse).max())
+
+
+def test_rect_kernel_at_128_matches_production(csa, monkeypatch):
+    """The generic B_kv kernel instantiated at 128 (CSA_ATTN_RECT) against the oracle and the
+    production square kernel (same reference-max arithmetic: equal within bf16 rounding of P)."""
+    lay = Layout(2, 9, 40, 128)
+    q, k, v = qkv(1, lay.N, 3, 128, seed=8, device="cuda")
+    rng = np.random.default_rng(3)
+    masks = (rng.random((3, lay.NB, lay.NB)) < 0.5).astype(np.uint8)
+    masks[:, np.arange(lay.NB), np.arange(lay.NB)] = 1
+    prod, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[1], anchor_k=2)
+    monkeypatch.setenv("CSA_ATTN_RECT", "1")
+    rect, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[1], anchor_k=2)
+    for h in range(3):
+        ref, _ = oracle_head(lay, q, k, v, 0, h, mask=masks[h], rep_k=2 if h == 1 else None)
+        assert_close(rect[0, :, h].double().cpu().numpy(), ref, f"h{h}")
+    assert (rect.float() - prod.float()).abs().max().item() <= 2 * MAX_ABS
+
+
+@pytest.mark.parametrize("bkv", [64, 176])
+def test_rect_attention_wan480_sampled(csa, bkv):
+    """Wan 480p at full size on the B_q x B_kv grid at the paper's Table sparsity for that block
+    size, 4 anchor heads, bench launch configuration; oracle on sampled units."""
+    cfg = CONFIGS["wan480"]
+    lay = Layout(cfg.layout.F, cfg.layout.H, cfg.layout.W, 128, bkv)
+    q, k, v = qkv(1, lay.N, cfg.heads, cfg.d, seed=11, device="cuda")
+    masks = inputs.synthetic_masks(lay, cfg.heads, PAPER_SPARSITY[bkv], seed=0)
+    rep = [3, 17, 29, 38]
+    out, lse, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=rep, anchor_k=5, lse=True)
+    lse = lse.view(cfg.heads, lay.N).cpu().numpy()
+    for h, r in sample_units(lay, cfg.heads, 8, seed=4):
+        rows = (r * lay.B, min((r + 1) * lay.B, lay.N))
+        ref, ref_lse = oracle_head(lay, q, k, v, 0, h, mask=masks[h],
+                                   rep_k=5 if h in rep else None, rows=rows)
+        assert_close(out[0, rows[0]:rows[1], h].double().cpu().numpy(), ref, f"h{h} r{r}")
+        assert np.abs(lse[h, rows[0]:rows[1]] - ref_lse).max() <= 1e-3
+    assert torch.isfinite(out).all()
+    assert fallback_count(csa, q) == 0
+
+
+# ---------------------------------------------------------------- f4: dictionary + denoise step
+def test_denoise_step_dictionary_graph_and_oracle(csa):
+    """Distilled 4-step schedule, T x L x H dictionary calibrated on the conditional
+    branch, CFG batch 2 sharing every cell plan: keep counts = per-(t, l) direct calls
+    bitwise; plan = oracle compile; eager step = graph replay = direct per-layer calls bitwise;
+    sampled rows of every (t, l) against the fp64 oracle."""
+    from paper_2603_05503_b200 import pipeline
+
+    lay, H, d, T, L, prompts = Layout(2, 9, 40, 128), 3, 128, 4, 3, 2
+    alphas = [0.9, 1.4, 1.1]
+
+    def qk(p, t, l):
+        q, k, _ = inputs.structured_qk(lay, H, d, head_seed=10 * t + l, prompt_seed=p,
+                                       alpha=alphas, repetitive=(2,), device="cuda")
+        return q, k
+
+    dic = pipeline.calibrate(lay, T, L, H, prompts, qk, pipeline.DISTILLED)
+    assert abs(dic.eps[0] - 0.863) < 1e-15 and dic.eps == sorted(dic.eps, reverse=True)
+    nb = lay.NB
+    kind = dic.plan.kind.cpu().numpy()
+    sim = dic.similarity.cpu().numpy()
+    bits = unpack_bits(dic.plan.mask_bits.cpu().numpy(), nb).reshape(T * L * H, nb, nb)
+    for t in range(T):
+        for l in range(L):
+            keep = u16_zeros(H * nb * nb)
+            for p in range(prompts):
+                q, k = qk(p, t, l)
+                csa.calib_accumulate(lay, q, k, dic.eps[t], keep)
+            c0 = dic.cell_base(t, l)
+            got = u16_np(dic.keep_count[c0:c0 + H].reshape(-1))
+            assert np.array_equal(got, u16_np(keep))
+            for h in range(H):
+                ref = oracle.compile_cell(got.reshape(H, nb, nb)[h], lay.N, lay.B, lay.F, lay.H,
+                                          lay.W, dic.min_count, similarity=sim[c0 + h])
+                assert kind[c0 + h] == ref["kind"]
+                if ref["kind"] == 0:
+                    assert np.array_equal(bits[c0 + h], ref["mask"])
+    assert kind.reshape(T, L, H)[:, :, 2].all() and not kind.reshape(T, L, H)[:, :, :2].any()
+    bufs = [qkv(2, lay.N, H, d, seed=100 + l, device="cuda") for l in range(L)]
+    outs = [torch.empty_like(b[0]) for b in bufs]
+    step = pipeline.DenoiseStep(dic, [b[0] for b in bufs], [b[1] for b in bufs],
+                                [b[2] for b in bufs], outs)
+    for t in range(T):
+        step.run(t)
+        torch.cuda.synchronize()
+        eager = [o.clone() for o in outs]
+        for o in outs:
+            o.zero_()
+        step.replay(t)
+        torch.cuda.synchronize()
+        for l in range(L):
+            assert torch.equal(outs[l], eager[l])
+            direct = csa.sparse_attn_fwd(*bufs[l], dic.plan, step.work[t][l],
+                                         cell_base=dic.cell_base(t, l))
+            assert torch.equal(direct, eager[l])
+            c0 = dic.cell_base(t, l)
+            for b in range(2):
+                for h in range(H):
+                    r = (t + l + h) % nb
+                    rows = (r * lay.B, min((r + 1) * lay.B, lay.N))
+                    ref, _ = oracle_head(lay, *bufs[l], b, h, mask=bits[c0 + h],
+                                         rep_k=5 if kind[c0 + h] else None, rows=rows)
+                    assert_close(eager[l][b, rows[0]:rows[1], h].double().cpu().numpy(), ref,
+                                 f"t{t} l{l} b{b} h{h}")

@@ -544,3 +544,83 @@ def test_timestep_clusters_are_cliques_and_greedy(orc):
             for c in range(cl[t]):
                 earlier = [u for u in range(t) if cl[u] == c]
                 assert not all(iou[t, u] >= tau for u in earlier)
+
+
+# ---------------------------------------------------------------- f3: non-square B_q x B_kv
+def brute_masked_rect(q, k, v, scale, bq, bk, mask):
+    """Token-level mask from a B_q x B_kv block mask, materialised softmax."""
+    n = q.shape[0]
+    keep = mask[_block_of(n, bq)[:, None], _block_of(n, bk)[None, :]].astype(bool)
+    logits = np.where(keep, scale * (q @ k.T), -np.inf)
+    return scipy.special.softmax(logits, axis=1) @ v, scipy.special.logsumexp(logits, axis=1), keep
+
+
+@pytest.mark.parametrize("n,bq,bk", [(250, 64, 16), (250, 32, 48), (300, 128, 80), (130, 64, 192)])
+def test_rect_masked_attention_equals_brute_force(orc, n, bq, bk):
+    q, k, v = _rand(n, 16, 3)
+    nbq, nbk = orc.num_blocks(n, bq), orc.num_blocks(n, bk)
+    mask = (np.random.default_rng(5).random((nbq, nbk)) < 0.5).astype(np.uint8)
+    mask[:, -1] = 1  # the ragged last key block kept somewhere; no empty row
+    out, lse = orc.masked_attention_rows(q, k, v, 0.25, bq, mask, block_kv=bk)
+    ref, ref_lse, keep = brute_masked_rect(q, k, v, 0.25, bq, bk, mask)
+    assert np.max(np.abs(out - ref)) < 1e-12 and np.max(np.abs(lse - ref_lse)) < 1e-12
+    rs = np.where(keep, np.exp(0.25 * (q @ k.T) - lse[:, None]), 0.0).sum(axis=1)
+    assert np.max(np.abs(rs - 1.0)) < 1e-12
+
+
+def test_rect_refinement_of_square_mask_is_identical(orc):
+    """A 128 x 128 mask refined to 128 x 64 (every kept column c -> 2c, 2c+1) keeps the same key
+    set: the rect oracle must give the square oracle's outputs bit for bit."""
+    n, d = 600, 16
+    q, k, v = _rand(n, d, 9)
+    nb, nbk = orc.num_blocks(n, 128), orc.num_blocks(n, 64)
+    sq = (np.random.default_rng(2).random((nb, nb)) < 0.5).astype(np.uint8)
+    sq[np.arange(nb), np.arange(nb)] = 1
+    rect = np.repeat(sq, 2, axis=1)[:, :nbk]
+    a, la = orc.masked_attention_rows(q, k, v, 0.25, 128, sq)
+    b, lb = orc.masked_attention_rows(q, k, v, 0.25, 128, rect, block_kv=64)
+    assert np.array_equal(a, b) and np.array_equal(la, lb)
+    dense, _ = orc.masked_attention_rows(q, k, v, 0.25, 128, None, block_kv=80)
+    ones, _ = orc.masked_attention_rows(q, k, v, 0.25, 128, None)
+    assert np.array_equal(dense, ones)  # no mask: every key, whatever the key block size
+
+
+@pytest.mark.parametrize("n,bq,bk", [(75, 16, 8), (250, 128, 80), (333, 64, 112)])
+def test_rect_compile_against_token_level_count(orc, n, bq, bk):
+    """Threshold / repair / CSR / intervals / kept area of a B_q x B_kv cell against a direct
+    token-level construction."""
+    nbq, nbk = orc.num_blocks(n, bq), orc.num_blocks(n, bk)
+    rng = np.random.default_rng(n)
+    cnt = rng.integers(0, 9, size=(nbq, nbk)).astype(np.uint16)
+    cnt[0] = 0  # emptied row -> repair keeps argmax (all zero: lowest c = 0)
+    c = orc.compile_cell(cnt, n, bq, 1, 1, n, 5, block_kv=bk)
+    m = (cnt >= 5).astype(np.uint8)
+    m[0, 0] = 1
+    assert np.array_equal(c["mask"], m)
+    keep = m[_block_of(n, bq)[:, None], _block_of(n, bk)[None, :]]
+    assert c["kept_area"] == int(keep.sum())
+    rows = np.repeat(np.arange(nbq), m.sum(axis=1).astype(np.int64))
+    assert np.array_equal(c["blk_idx"], np.nonzero(m)[1]) and len(rows) == c["blk_row_ptr"][-1]
+    for r in range(nbq):
+        ivl = c["ivl"][c["ivl_row_ptr"][r]:c["ivl_row_ptr"][r + 1]]
+        dec = np.zeros(nbk, np.uint8)
+        for s0, e0 in ivl:
+            dec[s0:e0] = 1
+        assert np.array_equal(dec, m[r])
+
+
+def test_epsilon_schedules_paper_constants(orc):
+    """P:886 distilled (A, C, k) = (0.763, 0.863, 5.64) and P:888-894 high-step constants through
+    the oracle's Eq. eq:epsilon_schedule and the runtime's host schedule (row a1): eps(0) = C,
+    strictly decreasing, above A, and eps(t) - A = (C - A) e^{-k t/T} (geometric ratio e^{-k/T})."""
+    from paper_2603_05503_b200 import pipeline
+
+    for consts, T in ((pipeline.DISTILLED, 4), (pipeline.high_step_constants(32760), 50)):
+        A, C, k = consts
+        host = pipeline.epsilon_schedule(T, A, C, k)
+        ref = [orc.epsilon(t, T, A, C, k) for t in range(T)]
+        assert np.allclose(host, ref, rtol=0, atol=1e-15)
+        assert host[0] == C and all(a > b > A for a, b in zip(host, host[1:]))
+        ratios = [(host[t + 1] - A) / (host[t] - A) for t in range(T - 1)]
+        assert np.allclose(ratios, math.exp(-k / T), rtol=1e-12)
+    assert abs(pipeline.high_step_constants(32760)[0] - 0.8421916) < 1e-7  # P:528 "0.84"
