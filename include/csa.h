@@ -29,10 +29,10 @@
  *   - Tensors: bf16, layout [batch, N, heads, head_dim] given by element strides; head_dim
  *     contiguous; base and strides 16-byte aligned (TMA).
  *   - Supported: sm_100 devices; head_dim in {64, 128}; block in {64, 128}; N_B <= 2047.
- *   - Non-square blocks (block_kv != 0 and != block): csa_compile_plan, csa_merge_intervals,
- *     csa_share_timesteps, csa_build_work_list, csa_validate_plan and csa_sparse_attn_fwd accept
- *     block 128, block_kv a multiple of 16 in [64, 192], head_dim 128 (attention), N_Bkv <= 2047;
- *     csa_calib_accumulate and csa_spatial_similarity return CSA_ERR_UNSUPPORTED for them.
+ *   - Non-square blocks (block_kv != 0 and != block): every entry point accepts block 128,
+ *     block_kv a multiple of 16 in [64, 192], N_Bkv <= 2047 (head_dim 128 for calibration and
+ *     attention; csa_sparse_attn_fwd then needs its workspace).  csa_spatial_similarity ignores
+ *     block_kv (the statistic is defined over all N keys).
  *     Everywhere below, "N_B x N_B" of a plan or keep-count cell reads "N_B x N_Bkv" (rows are
  *     query blocks, columns key blocks), and mask rows hold ceil(N_Bkv/32) words.
  */

@@ -87,6 +87,9 @@ def lib():
         L.csao_block_energy_rows.restype = ctypes.c_int
         L.csao_block_energy_rows.argtypes = [_c_i64, _c_i32, _c_i32, _p, _p, _c_dbl, _p,
                                              _c_i64, _c_i64, _p]
+        L.csao_block_energy_rows_rect.restype = ctypes.c_int
+        L.csao_block_energy_rows_rect.argtypes = [_c_i64, _c_i32, _c_i32, _c_i32, _p, _p, _c_dbl,
+                                                  _p, _c_i64, _c_i64, _p]
         L.csao_select.restype = _c_i32
         L.csao_select.argtypes = [_c_i32, _p, _c_dbl, _p]
         L.csao_accumulate.restype = None
@@ -245,16 +248,19 @@ def row_lse(q, k, scale: float, rows=None) -> np.ndarray:
     return out
 
 
-def block_energy(q, k, scale: float, block: int, lse=None, block_rows=None) -> np.ndarray:
-    """E_{r,c} (Eq. eq:block_energy; divides by |I_r|, Q2).  Returns [rows, N_B]."""
+def block_energy(q, k, scale: float, block: int, lse=None, block_rows=None,
+                 block_kv: int | None = None) -> np.ndarray:
+    """E_{r,c} (P:495-507, Eq. eq:block_energy; divides by |I_r|, Q2).  Returns [rows, N_Bkv];
+    block_kv: key block size of non-square B_q x B_kv blocks, None -> block."""
     q, k = _f64(q), _f64(k)
     n, d = q.shape
-    nb = num_blocks(n, block)
-    r0, r1 = (0, nb) if block_rows is None else block_rows
+    bk = block if block_kv is None else block_kv
+    nb = num_blocks(n, bk)
+    r0, r1 = (0, num_blocks(n, block)) if block_rows is None else block_rows
     out = np.empty((r1 - r0, nb), np.float64)
     l = None if lse is None else _f64(lse)
-    rc = lib().csao_block_energy_rows(n, d, block, _ptr(q), _ptr(k), scale,
-                                      None if l is None else _ptr(l), r0, r1, _ptr(out))
+    rc = lib().csao_block_energy_rows_rect(n, d, block, bk, _ptr(q), _ptr(k), scale,
+                                           None if l is None else _ptr(l), r0, r1, _ptr(out))
     if rc != 0:
         raise ValueError("block_energy: invalid argument")
     return out

@@ -276,15 +276,27 @@ int csao_row_lse(int64_t n, int32_t d, const double* q, const double* k, double 
 /* The paper writes 1/B; Q2 divides by the actual |I_r| so every row sums to 1.          */
 /* Block rows [r_begin,r_end); E_out is [(r_end-r_begin) * N_B].  lse may be NULL (computed).    */
 /* ------------------------------------------------------------------------------------------ */
+/* Non-square blocks B_q x B_kv: I_r from bq, J_c from bk; E_out is             */
+/* [(r_end-r_begin) * N_Bkv].  bq == bk is csao_block_energy_rows.                              */
+int csao_block_energy_rows_rect(int64_t n, int32_t d, int32_t bq, int32_t bk, const double* q,
+                                const double* k, double scale, const double* lse_in,
+                                int64_t r_begin, int64_t r_end, double* E_out);
+
 int csao_block_energy_rows(int64_t n, int32_t d, int32_t b, const double* q, const double* k,
                            double scale, const double* lse_in, int64_t r_begin, int64_t r_end,
                            double* E_out) {
-    const int64_t nb = csao_num_blocks(n, b);
-    if (r_begin < 0 || r_end > nb || r_begin > r_end) return ORC_EINVAL;
+    return csao_block_energy_rows_rect(n, d, b, b, q, k, scale, lse_in, r_begin, r_end, E_out);
+}
+
+int csao_block_energy_rows_rect(int64_t n, int32_t d, int32_t bq, int32_t b, const double* q,
+                                const double* k, double scale, const double* lse_in,
+                                int64_t r_begin, int64_t r_end, double* E_out) {
+    const int64_t nb = csao_num_blocks(n, b); /* key blocks (columns) of width b = B_kv */
+    if (r_begin < 0 || r_end > csao_num_blocks(n, bq) || r_begin > r_end) return ORC_EINVAL;
     for (int64_t r = r_begin; r < r_end; ++r) {
         double* E = E_out + (r - r_begin) * nb;
         for (int64_t c = 0; c < nb; ++c) E[c] = 0.0;
-        const int64_t i0 = blk_lo(r, b), i1 = blk_hi(r, b, n);
+        const int64_t i0 = blk_lo(r, bq), i1 = blk_hi(r, bq, n);
         for (int64_t i = i0; i < i1; ++i) {
             double li;
             if (lse_in) li = lse_in[i];

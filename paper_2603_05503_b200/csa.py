@@ -146,9 +146,9 @@ def calib_accumulate(lay: Layout, q: torch.Tensor, k: torch.Tensor, eps: float,
     None); False -> the two-pass path."""
     _, n, heads, d = q.shape
     assert n == lay.N and keep_count.dtype == torch.uint16 and keep_count.is_contiguous()
-    assert keep_count.numel() == heads * lay.NB * lay.NB
+    assert keep_count.numel() == heads * lay.NB * lay.NBK
     for t, shape in ((lse_in, heads * n), (lse_out, heads * n),
-                     (energy_out, heads * lay.NB * lay.NB)):
+                     (energy_out, heads * lay.NB * lay.NBK)):
         if t is not None:
             assert t.dtype == torch.float32 and t.is_contiguous() and t.numel() == shape
     sc = default_scale(d) if scale is None else scale

@@ -169,11 +169,11 @@ size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_
         return (size_t)(csa::make_geo(L).NBK + 1) * sizeof(int32_t);
     }
     if (which == CSA_WS_SIMILARITY) {     // per-token (dot, |p|^2, |p_a|^2) partials
-        if (check_layout(L, 0, 0) != CSA_OK || !is_square(L) || n_heads < 1) return 0;
+        if (check_layout(L, 0, 0) != CSA_OK || n_heads < 1) return 0;
         return (size_t)n_heads * (size_t)L.frames * L.rows * L.cols * 3 * sizeof(float);
     }
     if (which == CSA_WS_CALIB) {           // single-pass calibration: (t, m) row partials
-        if (check_layout(L, 0, 0) != CSA_OK || !is_square(L) || n_heads < 1) return 0;
+        if (check_layout(L, 0, 0) != CSA_OK || n_heads < 1) return 0;
         DeviceInfo di;
         if (device_info(&di) != CSA_OK) return 0;
         return csa::calib_scratch_bytes(csa::make_geo(L), n_heads, di.sms);
@@ -188,8 +188,8 @@ csa_status_t csa_calib_accumulate(csa_layout_t L, int32_t n_heads, int32_t head_
                                   size_t workspace_bytes, csa_stream_t stream) {
     csa_status_t st = check_layout(L, head_dim, n_heads);
     if (st != CSA_OK) return st;
-    if (!is_square(L))
-        return fail(CSA_ERR_UNSUPPORTED, "statistics passes need square blocks (block_kv 0)");
+    if (!is_square(L) && head_dim != 128)
+        return fail(CSA_ERR_UNSUPPORTED, "non-square calibration needs head_dim 128");
     if (n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "n_heads must be >= 1");
     if (!(softmax_scale > 0.0f)) return fail(CSA_ERR_INVALID_ARGUMENT, "softmax_scale <= 0");
     if (!(eps > 0.0)) return fail(CSA_ERR_INVALID_ARGUMENT, "eps must be > 0");
@@ -199,7 +199,7 @@ csa_status_t csa_calib_accumulate(csa_layout_t L, int32_t n_heads, int32_t head_
     const csa::Geo g = csa::make_geo(L);
     CUtensorMap tq, tk;
     if ((st = make_map(&tq, q, 1, g.N, n_heads, head_dim, g.B, "q")) != CSA_OK) return st;
-    if ((st = make_map(&tk, k, 1, g.N, n_heads, head_dim, g.B, "k")) != CSA_OK) return st;
+    if ((st = make_map(&tk, k, 1, g.N, n_heads, head_dim, g.BK, "k")) != CSA_OK) return st;
     csa::CalibArgs a;
     a.g = g;
     a.n_heads = n_heads;
@@ -231,8 +231,7 @@ csa_status_t csa_spatial_similarity(csa_layout_t L, int32_t n_heads, int32_t hea
                                     csa_stream_t stream) {
     csa_status_t st = check_layout(L, head_dim, n_heads);
     if (st != CSA_OK) return st;
-    if (!is_square(L))
-        return fail(CSA_ERR_UNSUPPORTED, "statistics passes need square blocks (block_kv 0)");
+    L.block_kv = 0;  // s is defined over all N keys: independent of B_kv
     if (n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "n_heads must be >= 1");
     if (!(softmax_scale > 0.0f)) return fail(CSA_ERR_INVALID_ARGUMENT, "softmax_scale <= 0");
     if (anchor_k < 1 || anchor_k > L.rows)

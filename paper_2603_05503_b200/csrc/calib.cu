@@ -36,16 +36,21 @@ constexpr int kThreads = 384;
 constexpr int kCalibEmuPerOctet = 0;  // pairs p with (p & 7) >= 8 - this -> exp2_poly5; A/B at Wan
                                       // 720p: 0 -> 78 ms, 1 -> 78, 2 -> 81, 3 -> 87 (issue-bound)
 
-template <int BK, int D>
+template <int BK, int D, int BKV = BK>
 struct CalibSmem {
     using C = TileCfg<BK, D>;
+    // key tiles of BKV rows (= BK for square blocks; B_q = 128 x B_kv, otherwise)
+    static constexpr int kKBoxV = BKV * 128;
+    static constexpr int kKVB = C::kBoxes * kKBoxV;
+    static constexpr uint32_t kSB = (BKV + 31) / 32 * 32;  // TMEM columns per S buffer
+    static constexpr uint32_t kIdescQKV = umma_idesc_bf16(128, BKV, 0, 0);
     // BK = 128: Q lives in TMEM (tcgen05.cp from the TMA'd tile) and S = Q K^T runs as a TS
     // MMA reading only K from shared memory -- measured 74 vs 107 cycles per 128x128x16
     // dispatch for the SS form (scripts/mma_bench.cu); S is then single-buffered per group
     // (TMEM: S[2] 256 + Q 64 columns).  BK = 64 (M = 64) keeps the SS form, S double-buffered.
     static constexpr bool kQT = BK == 128;
     static constexpr int kSBufs = kQT ? 1 : 2;
-    static constexpr uint32_t kQCol = 2 * kSBufs * BK;  // used when kQT
+    static constexpr uint32_t kQCol = 2 * kSBufs * kSB;  // used when kQT
     // One Q buffer (the next item's Q waits for this item's last MMA: one bubble per N_B tiles);
     // everything else not in the K ring is small, so the ring gets 4 slots of 128x128 bf16 --
     // the pass streams K from L2 and needs that many loads in flight.
@@ -53,8 +58,8 @@ struct CalibSmem {
     static constexpr int kQOff = 0;
     static constexpr int kKOff = C::kQBytes;
     static constexpr int kBudget = 232448 - kFixed;
-    static constexpr int kSlots = kBudget / C::kKVBytes > 8 ? 8 : kBudget / C::kKVBytes;
-    static constexpr int kERowOff = kKOff + kSlots * C::kKVBytes;  // float [2048]
+    static constexpr int kSlots = kBudget / kKVB > 8 ? 8 : kBudget / kKVB;
+    static constexpr int kERowOff = kKOff + kSlots * kKVB;  // float [2048]
     static constexpr int kSortOff = kERowOff + 2048 * 4;              // u64 [2048] (a4 sort)
     static constexpr int kBarOff = kSortOff + 2048 * 8;
     // q_full[2] q_empty[2] (entry 0 used) k_full[S] k_empty[S] s_full[2][2] s_empty[2][2]
@@ -66,6 +71,7 @@ struct CalibSmem {
     static constexpr int kBytes = kTmemPtrOff + 16;
     static constexpr int kAlloc = kBytes;
     static_assert(kSlots >= 2, "K ring");
+    static_assert(BKV == BK || (BK == 128 && BKV % 16 == 0 && kQCol + D / 2 <= 512), "B_kv");
     static_assert(kAlloc <= 232448, "smem");
 };
 
@@ -112,12 +118,12 @@ __device__ __forceinline__ float exp_sum(const uint32_t (&r)[BK], float sl2, flo
     return lo_f(s2) + hi_f(s2);
 }
 
-template <int BK, int D>
+template <int BK, int D, int BKV = BK>
 __global__ void __launch_bounds__(kThreads, 1)
     calib_kernel(const CalibArgs a, const __grid_constant__ CUtensorMap tq,
                  const __grid_constant__ CUtensorMap tk) {
     using C = TileCfg<BK, D>;
-    using L = CalibSmem<BK, D>;
+    using L = CalibSmem<BK, D, BKV>;
     constexpr int S = L::kSlots;
     extern __shared__ __align__(1024) uint8_t smem[];
     if ((smem_u32(smem) & 1023u) != 0u) __trap();
@@ -143,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool have_lse = a.lse_in != nullptr;
     const bool use_scratch = !have_lse && a.scratch != nullptr;
     const int32_t passes = (have_lse || use_scratch) ? 1 : 2;
-    const int32_t tiles_per_item = passes * g.NB;
+    const int32_t tiles_per_item = passes * g.NBK;
     const int dbg = g_debug_mode;
 
     if (threadIdx.x == 0) {
@@ -191,16 +197,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 __syncwarp();
                 for (int32_t j = 0; j < tiles_per_item; ++j) {
-                    const int32_t c = j % g.NB;
+                    const int32_t c = j % g.NBK;
                     const uint32_t slot = ld % S, ph = (ld / S) & 1;
                     ++ld;
                     if (local == 0 && lane == 0) CSA_TRACE(3, j, 0);
                     mbar_wait(k_empty + slot, ph ^ 1);
                     if (local == 0 && lane == 0) CSA_TRACE(3, j, 1);
                     if (elect_one()) {
-                        mbar_arrive_expect_tx(k_full + slot, C::kKVBytes);
-                        tma_tile<D>(smem + L::kKOff + slot * C::kKVBytes, C::kKBox, &tk,
-                                    k_full + slot, h, c * BK, 0, pol_k);
+                        mbar_arrive_expect_tx(k_full + slot, L::kKVB);
+                        tma_tile<D>(smem + L::kKOff + slot * L::kKVB, L::kKBoxV, &tk,
+                                    k_full + slot, h, c * BKV, 0, pol_k);
                     }
                     __syncwarp();
                 }
@@ -254,14 +260,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int kk = 0; kk < D / 16; ++kk) {
                                 const uint64_t b = umma_desc_sw128(
-                                    k_base + slot * C::kKVBytes + (kk >> 2) * C::kKBox +
+                                    k_base + slot * L::kKVB + (kk >> 2) * L::kKBoxV +
                                         (kk & 3) * 32, 16, 1024);
-                                mma_ts(tmem + sb * BK, tmem + L::kQCol + kk * 8, b, C::kIdescQK,
-                                       kk > 0 ? 1u : 0u);
+                                mma_ts(tmem + sb * L::kSB, tmem + L::kQCol + kk * 8, b,
+                                       L::kIdescQKV, kk > 0 ? 1u : 0u);
                             }
                         } else {
-                            issue_qk<BK, D>(tmem + sb * BK, q_base + qb * C::kQBytes,
-                                            k_base + slot * C::kKVBytes);
+                            issue_qk<BK, D>(tmem + sb * L::kSB, q_base + qb * C::kQBytes,
+                                            k_base + slot * L::kKVB);
                         }
                         mma_commit(s_full + sb);
                         mma_commit(k_empty + slot);
@@ -281,8 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int gtid = threadIdx.x - 128;  // 0..255
         const uint32_t s_lane = tmem + ((uint32_t)(quarter * 32) << 16);
         const float sl2 = a.scale_log2;
-        const int32_t tail_valid = g.N - (g.NB - 1) * BK;
-        float2* scr = use_scratch ? a.scratch + (int64_t)blockIdx.x * g.NB * 128 : nullptr;
+        const int32_t tail_valid = g.N - (g.NBK - 1) * BKV;
+        float2* scr = use_scratch ? a.scratch + (int64_t)blockIdx.x * g.NBK * 128 : nullptr;
         uint32_t scount = 0;
         int32_t local = 0;
         for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
@@ -293,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             float m_run = -INFINITY, l_run = 0.0f, lse2 = 0.0f;
             int32_t mine = 0;
             // S row of this group's next tile into registers; frees S[grp] for the next MMA
-            auto load_s = [&](uint32_t (&s)[BK], int32_t c) {
+            auto load_s = [&](uint32_t (&s)[BKV], int32_t c) {
                 const uint32_t sb = grp * L::kSBufs + (scount % L::kSBufs);
                 const bool tr = local == 0 && (warp & 3) == 0 && lane == 0;
                 if (tr) CSA_TRACE(grp, c, 0);
@@ -301,32 +307,35 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (tr) CSA_TRACE(grp, c, 1);
                 ++scount;
                 tc_fence_after();
-                const uint32_t s_addr = s_lane + sb * BK;
+                const uint32_t s_addr = s_lane + sb * L::kSB;
 #pragma unroll
-                for (int cc = 0; cc < BK; cc += 32) {
+                for (int cc = 0; cc + 32 <= BKV; cc += 32) {
                     uint32_t(&rr)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[cc]);
                     tmem_ld32(s_addr + cc, rr);
                 }
+                if constexpr (BKV % 32 == 16)
+                    tmem_ld16(s_addr + BKV - 16,
+                              *reinterpret_cast<uint32_t(*)[16]>(&s[BKV - 16]));
+                tmem_ld_wait();
 #pragma unroll
-                for (int cc = 0; cc < BK; cc += 32)
-                    tmem_ld_wait(*reinterpret_cast<uint32_t(*)[32]>(&s[cc]));
+                for (int x = 0; x < BKV; ++x) asm volatile("" : "+r"(s[x]));  // no use above
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(s_empty + sb);
                 if (tr) CSA_TRACE(grp, c, 2);
-                if (c == g.NB - 1 && tail_valid < BK) {  // keys >= N do not exist (Q2)
+                if (c == g.NBK - 1 && tail_valid < BKV) {  // keys >= N do not exist (Q2)
 #pragma unroll
-                    for (int x = 0; x < BK; ++x)
+                    for (int x = 0; x < BKV; ++x)
                         if (x >= tail_valid) s[x] = 0xff800000u;
                 }
             };
             // ---------------- LSE (a2): two-pass pass A, or the scratch single pass
             if (!have_lse) {
-                for (int32_t c = grp; c < g.NB; c += 2, ++mine) {
-                    uint32_t s[BK];
+                for (int32_t c = grp; c < g.NBK; c += 2, ++mine) {
+                    uint32_t s[BKV];
                     load_s(s, c);
                     if (dbg >= 11) continue;  // debug: pipeline without the softmax math
-                    const float mt = max_half<BK>(s) * sl2;
+                    const float mt = max_half<BKV>(s) * sl2;
                     float m_use = m_run;
                     if (mine == 0 || mt > m_run + kRescaleThreshold) {  // lazy running max
                         const float m_new = fmaxf(m_run, mt);
@@ -334,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         m_run = m_new;
                         m_use = m_new;
                     }
-                    const float t = exp_sum<BK>(s, sl2, m_use);
+                    const float t = exp_sum<BKV>(s, sl2, m_use);
                     l_run += t;
                     if (use_scratch) scr[(int64_t)c * 128 + row] = make_float2(t, m_use);
                     if (local == 0 && (warp & 3) == 0 && lane == 0) CSA_TRACE(grp, c, 3);
@@ -371,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     okr[q4] = lane + 32 * q4 < rows_valid;
                     lr[q4] = okr[q4] ? row_lse2[lane + 32 * q4] : 0.0f;  // no NaN from dead rows
                 }
-                for (int32_t c0 = w8; c0 < g.NB; c0 += 32) {
+                for (int32_t c0 = w8; c0 < g.NBK; c0 += 32) {
                     float v[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
@@ -379,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         float2 tm[4];
 #pragma unroll
                         for (int q4 = 0; q4 < 4; ++q4)
-                            tm[q4] = (c < g.NB && okr[q4])
+                            tm[q4] = (c < g.NBK && okr[q4])
                                          ? scr[(int64_t)c * 128 + lane + 32 * q4]
                                          : make_float2(0.0f, 0.0f);
                         float acc = 0.0f;
@@ -395,19 +404,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (lane == 0) {
 #pragma unroll
                         for (int u = 0; u < 4; ++u)
-                            if (c0 + 8 * u < g.NB) erow[c0 + 8 * u] = v[u] / (float)rows_valid;
+                            if (c0 + 8 * u < g.NBK) erow[c0 + 8 * u] = v[u] / (float)rows_valid;
                     }
                 }
             } else {
                 // ---------------- E tile by tile against the known lse (a3)
-                const int32_t first_b = passes == 2 ? g.NB : 0;
+                const int32_t first_b = passes == 2 ? g.NBK : 0;
                 int32_t nb_mine = 0;
                 for (int32_t j = first_b + (((first_b & 1) != grp) ? 1 : 0); j < tiles_per_item;
                      j += 2, ++nb_mine) {
                     const int32_t c = j - first_b;
-                    uint32_t s[BK];
+                    uint32_t s[BKV];
                     load_s(s, c);
-                    float acc = row_ok ? exp_sum<BK>(s, sl2, lse2) : 0.0f;
+                    float acc = row_ok ? exp_sum<BKV>(s, sl2, lse2) : 0.0f;
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1)
                         acc += __shfl_xor_sync(0xffffffffu, acc, off);
@@ -422,12 +431,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             named_bar_sync(1, 256);  // E row complete
             if (grp == 0) {
                 const int t = row;  // 0..127
-                float* eout = a.energy_out ? a.energy_out + ((int64_t)h * g.NB + r) * g.NB : nullptr;
+                float* eout = a.energy_out ? a.energy_out + ((int64_t)h * g.NB + r) * g.NBK : nullptr;
                 int32_t p2 = 1;
-                while (p2 < g.NB) p2 <<= 1;
+                while (p2 < g.NBK) p2 <<= 1;
                 for (int32_t x = t; x < p2; x += 128) {
                     uint64_t key = ~0ull;
-                    if (x < g.NB) {
+                    if (x < g.NBK) {
                         const float e = erow[x];
                         if (eout) eout[x] = e;
                         key = ((uint64_t)(0xFFFFFFFFu - __float_as_uint(e)) << 32) | (uint32_t)x;
@@ -451,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (t == 0) {
                     double acc = 0.0;
                     int32_t cnt = 0;
-                    for (int32_t x = 0; x < g.NB; ++x) {
+                    for (int32_t x = 0; x < g.NBK; ++x) {
                         const uint32_t c = (uint32_t)(keys[x] & 0xFFFFFFFFu);
                         ++cnt;
                         acc = __dadd_rn(acc, (double)erow[c]);
@@ -461,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 named_bar_sync(3, 128);
                 const int32_t cnt = *s_cnt;
-                uint16_t* kc = a.keep_count + ((int64_t)h * g.NB + r) * g.NB;
+                uint16_t* kc = a.keep_count + ((int64_t)h * g.NB + r) * g.NBK;
                 for (int32_t x = t; x < cnt; x += 128) {
                     const uint32_t c = (uint32_t)(keys[x] & 0xFFFFFFFFu);
                     const uint16_t v = kc[c];
@@ -479,11 +488,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-template <int BK, int D>
+template <int BK, int D, int BKV = BK>
 cudaError_t launch_t(const CalibArgs& a, const CUtensorMap& tq, const CUtensorMap& tk, int grid,
                      cudaStream_t s) {
-    auto kern = calib_kernel<BK, D>;
-    const int smem = CalibSmem<BK, D>::kAlloc;
+    auto kern = calib_kernel<BK, D, BKV>;
+    const int smem = CalibSmem<BK, D, BKV>::kAlloc;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<grid, kThreads, smem, s>>>(a, tq, tk);
@@ -498,7 +507,7 @@ static int calib_grid(const Geo& g, int32_t n_heads, int num_sms) {
 }
 
 size_t calib_scratch_bytes(const Geo& g, int32_t n_heads, int num_sms) {
-    return (size_t)calib_grid(g, n_heads, num_sms) * g.NB * 128 * sizeof(float2);
+    return (size_t)calib_grid(g, n_heads, num_sms) * g.NBK * 128 * sizeof(float2);
 }
 
 cudaError_t set_calib_trace(void* buf, int mode) {
@@ -511,6 +520,20 @@ cudaError_t set_calib_trace(void* buf, int mode) {
 cudaError_t launch_calib(const CalibArgs& a, int head_dim, const CUtensorMap& tq,
                          const CUtensorMap& tk, int num_sms, cudaStream_t s) {
     const int grid = calib_grid(a.g, a.n_heads, num_sms);
+    if (a.g.BK != a.g.B) {  // non-square B_q = 128 x B_kv, head_dim 128
+        if (a.g.B != 128 || head_dim != 128) return cudaErrorInvalidValue;
+        switch (a.g.BK) {
+            case 64: return launch_t<128, 128, 64>(a, tq, tk, grid, s);
+            case 80: return launch_t<128, 128, 80>(a, tq, tk, grid, s);
+            case 96: return launch_t<128, 128, 96>(a, tq, tk, grid, s);
+            case 112: return launch_t<128, 128, 112>(a, tq, tk, grid, s);
+            case 144: return launch_t<128, 128, 144>(a, tq, tk, grid, s);
+            case 160: return launch_t<128, 128, 160>(a, tq, tk, grid, s);
+            case 176: return launch_t<128, 128, 176>(a, tq, tk, grid, s);
+            case 192: return launch_t<128, 128, 192>(a, tq, tk, grid, s);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     if (a.g.B == 128 && head_dim == 128) return launch_t<128, 128>(a, tq, tk, grid, s);
     if (a.g.B == 128 && head_dim == 64) return launch_t<128, 64>(a, tq, tk, grid, s);
     if (a.g.B == 64 && head_dim == 128) return launch_t<64, 128>(a, tq, tk, grid, s);

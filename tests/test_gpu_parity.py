@@ -327,16 +327,19 @@ def test_attention_full_size_sampled(csa, name):
 
 # ---------------------------------------------------------------- a2-a5 calibration
 @pytest.mark.parametrize("lay,heads,d", [(Layout(2, 5, 25, 64), 2, 64), (Layout(4, 8, 8, 64), 1, 64),
-                                         (Layout(2, 9, 40, 128), 2, 128)])
+                                         (Layout(2, 9, 40, 128), 2, 128),
+                                         (Layout(2, 9, 40, 128, 80), 2, 128),
+                                         (Layout(2, 9, 40, 128, 192), 2, 128),
+                                         (Layout(3, 7, 100, 128, 64), 2, 128)])
 @pytest.mark.parametrize("single_pass", [True, False])
 def test_calibration_against_oracle(csa, lay, heads, d, single_pass):
     q, k, _ = inputs.structured_qk(lay, heads, d, head_seed=1, prompt_seed=2, alpha=1.0,
                                    device="cuda")
-    nb = lay.NB
+    nb, nbk = lay.NB, lay.NBK
     eps = 0.9
-    counts = u16_zeros(heads * nb * nb)
-    counts_np = np.zeros((heads, nb, nb), np.uint16)
-    energy = torch.empty(heads * nb * nb, dtype=torch.float32, device="cuda")
+    counts = u16_zeros(heads * nb * nbk)
+    counts_np = np.zeros((heads, nb, nbk), np.uint16)
+    energy = torch.empty(heads * nb * nbk, dtype=torch.float32, device="cuda")
     lse_out = torch.empty(heads * lay.N, dtype=torch.float32, device="cuda")
     scale = 1.0 / np.sqrt(d)
     for prompt in range(3):  # accumulate over prompts: integer counts exact
@@ -344,24 +347,24 @@ def test_calibration_against_oracle(csa, lay, heads, d, single_pass):
         csa.calib_accumulate(lay, q, k, eps, counts, energy_out=energy, lse_out=lse_out,
                              single_pass=single_pass)
         torch.cuda.synchronize()
-        E = energy.view(heads, nb, nb).double().cpu().numpy()
+        E = energy.view(heads, nb, nbk).double().cpu().numpy()
         lg = lse_out.view(heads, lay.N).double().cpu().numpy()
         for h in range(heads):
             qh, kh = head64(q, 0, h), head64(k, 0, h)
             ref_lse = oracle.row_lse(qh, kh, scale)
             assert np.abs(lg[h] - ref_lse).max() <= 1e-3
-            E_ref = oracle.block_energy(qh, kh, scale, lay.B)
+            E_ref = oracle.block_energy(qh, kh, scale, lay.B, block_kv=lay.BK or None)
             assert np.abs(E[h] - E_ref).max() <= 5e-5
             assert np.abs(E[h].sum(1) - 1).max() <= 1e-4
             for r in range(nb):
                 oracle.accumulate(oracle.select(E[h, r], eps), counts_np[h, r])
-        assert np.array_equal(u16_np(counts).reshape(heads, nb, nb), counts_np)
+        assert np.array_equal(u16_np(counts).reshape(heads, nb, nbk), counts_np)
     # LSE supplied from outside (the dense run's statistic) gives the same decisions on this E
-    counts2 = u16_zeros(heads * nb * nb)
+    counts2 = u16_zeros(heads * nb * nbk)
     csa.calib_accumulate(lay, q, k, eps, counts2, lse_in=lse_out, energy_out=energy)
     torch.cuda.synchronize()
-    E2 = energy.view(heads, nb, nb).double().cpu().numpy()
-    c2 = u16_np(counts2).reshape(heads, nb, nb)
+    E2 = energy.view(heads, nb, nbk).double().cpu().numpy()
+    c2 = u16_np(counts2).reshape(heads, nb, nbk)
     for h in range(heads):
         for r in range(nb):
             assert np.array_equal(oracle.select(E2[h, r], eps), c2[h, r])

@@ -624,3 +624,21 @@ def test_epsilon_schedules_paper_constants(orc):
         ratios = [(host[t + 1] - A) / (host[t] - A) for t in range(T - 1)]
         assert np.allclose(ratios, math.exp(-k / T), rtol=1e-12)
     assert abs(pipeline.high_step_constants(32760)[0] - 0.8421916) < 1e-7  # P:528 "0.84"
+
+
+@pytest.mark.parametrize("n,bq,bk", [(250, 64, 16), (300, 128, 80), (130, 32, 48)])
+def test_rect_block_energy_against_materialised_P(orc, n, bq, bk):
+    """E on a B_q x B_kv grid (P:495-507 with P:1294-1328) = block sums of the materialised
+    dense P / |I_r|; rows sum to 1; summing the 16-wide columns of a refined grid gives E."""
+    q, k, _ = _rand(n, 16, 4)
+    P = scipy.special.softmax(0.25 * (q @ k.T), axis=1)
+    E = orc.block_energy(q, k, 0.25, bq, block_kv=bk)
+    rb, cb = _block_of(n, bq), _block_of(n, bk)
+    ref = np.zeros_like(E)
+    np.add.at(ref, (rb[:, None].repeat(n, 1), cb[None, :].repeat(n, 0)), P)
+    ref /= np.bincount(rb)[:, None]
+    assert np.max(np.abs(E - ref)) < 1e-12 and np.allclose(E.sum(axis=1), 1.0, atol=1e-12)
+    fine = orc.block_energy(q, k, 0.25, bq, block_kv=16)
+    coarse = np.zeros_like(E)
+    np.add.at(coarse, (slice(None), (np.arange(fine.shape[1]) * 16) // bk), fine)
+    assert np.max(np.abs(coarse - E)) < 1e-12
