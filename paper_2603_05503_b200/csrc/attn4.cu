@@ -28,6 +28,15 @@ constexpr int kItemSlots4 = 4;
 // CH4: column split of each softmax group: a group is 4 * CH4 warps, warp (quarter, ch) taking
 // rows 32 * quarter ... and key columns ch * 128 / CH4 ... of the group's tiles.
 constexpr int kCH4 = 2;
+// kSplit4: the S-MMA of a tile is issued as two N = 64 halves (one per column part) with their
+// own completion barriers, and the P.V as two K = 64 halves waiting for their own part's P: a
+// column part's softmax starts when its half of S is done, and its half of P.V when its own P
+// is stored (the chain QK -> softmax -> PV no longer waits for the whole tile).  CH 2 only.
+// Measured slower (same box, Wan 720p: 1049 vs 1150 TF/s): off by default.
+#ifndef CSA_ATTN4_SPLIT
+#define CSA_ATTN4_SPLIT 0
+#endif
+constexpr bool kSplit4 = CSA_ATTN4_SPLIT != 0;
 constexpr float kGuard = 72057594037927936.0f;  // 2^56: a tile row sum above it flags the item
 static __device__ unsigned long long* g_trace4;
 static __device__ int g_debug_mode4;
@@ -55,9 +64,9 @@ struct Smem4 {
     static constexpr int kKVOff = kTile;
     static constexpr int kSlots = CH == 1 ? 6 : 5;  // K/V ring, consumption order
     static constexpr int kBarOff = kKVOff + kSlots * kTile;
-    // q_full q_empty | kv_full[S] kv_empty[S] | s_full[2] p_full[2] | o_full o_empty | mref_full |
-    // item_full[4] item_empty[4]
-    static constexpr int kNumBars = 2 + 2 * kSlots + 4 + 2 + 1 + 2 * kItemSlots4;
+    // q_full q_empty | kv_full[S] kv_empty[S] | s_full[2][2] p_full[2][2] | o_full o_empty |
+    // mref_full | item_full[4] item_empty[4]   ([grp][half]; only [grp][0] without kSplit4)
+    static constexpr int kNumBars = 2 + 2 * kSlots + 8 + 2 + 1 + 2 * kItemSlots4;
     // m_ref[128] | l[2 * CH][128] | tile-0 max of each column part [CH][128]
     static constexpr int kRowOff = kBarOff + kNumBars * 8;
     static constexpr int kItemOff = kRowOff + (1 + 3 * CH) * 128 * 4;
@@ -67,6 +76,7 @@ struct Smem4 {
     static_assert(kBytes <= 232448, "smem");
     static constexpr uint32_t kS = 0, kO = 256, kQ = 384;
     static constexpr uint32_t kIdescQK = umma_idesc_bf16(128, 128, 0, 0);
+    static constexpr uint32_t kIdescQK64 = umma_idesc_bf16(128, 64, 0, 0);
     static constexpr uint32_t kIdescPV = umma_idesc_bf16(128, 128, 0, 1);
 };
 
@@ -84,9 +94,10 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
     uint64_t* q_empty = bars + 1;
     uint64_t* kv_full = bars + 2;
     uint64_t* kv_empty = kv_full + S;
-    uint64_t* s_full = kv_empty + S;  // [grp]
-    uint64_t* p_full = s_full + 2;    // [grp]
-    uint64_t* o_full = p_full + 2;
+    constexpr bool kSplit = kSplit4 && CH == 2;
+    uint64_t* s_full = kv_empty + S;  // [grp][half]
+    uint64_t* p_full = s_full + 4;    // [grp][half]
+    uint64_t* o_full = p_full + 4;
     uint64_t* o_empty = o_full + 1;
     uint64_t* mref_full = o_empty + 1;
     uint64_t* item_full = mref_full + 1;
@@ -106,9 +117,9 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
             mbar_init(kv_full + i, 1);
             mbar_init(kv_empty + i, 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 4; ++i) {
             mbar_init(s_full + i, 1);
-            mbar_init(p_full + i, 4 * CH);
+            mbar_init(p_full + i, kSplit ? 4 : 4 * CH);
         }
         mbar_init(o_full, 1);
         mbar_init(o_empty, 8 * CH);
@@ -250,7 +261,36 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
                 auto do_pv = [&](int32_t t) {
                     const int grp = t & 1;
                     TRACE4(3, pv_tiles, 0);
-                    mbar_wait(p_full + grp, pcount[grp] & 1);
+                    if constexpr (kSplit) {
+                        const uint32_t slot = cons % S, ph = (cons / S) & 1;
+                        ++cons;
+                        const uint32_t vb = kv_base + slot * L::kTile;
+#pragma unroll
+                        for (int half = 0; half < 2; ++half) {
+                            mbar_wait(p_full + grp * 2 + half, pcount[grp] & 1);
+                            if (half == 0) {
+                                if (t == 0) mbar_wait(o_empty, (local & 1) ^ 1);
+                                mbar_wait(kv_full + slot, ph);
+                            }
+                            tc_fence_after();
+                            if (elect_one()) {
+#pragma unroll
+                                for (int k4 = 0; k4 < 4; ++k4) {
+                                    const int kk = half * 4 + k4;  // P of part `half`
+                                    mma_ts(tmem + L::kO, tmem + L::kS + grp * BK + half * 64 + k4 * 8,
+                                           umma_desc_sw128(vb + kk * 16 * 128, L::kBox, 1024),
+                                           L::kIdescPV, (t > 0 || kk > 0) ? 1u : 0u);
+                                }
+                                if (half == 1) mma_commit(kv_empty + slot);
+                            }
+                            __syncwarp();
+                        }
+                        ++pcount[grp];
+                        TRACE4(3, pv_tiles, 2);
+                        ++pv_tiles;
+                        return;
+                    }
+                    mbar_wait(p_full + grp * 2, pcount[grp] & 1);
                     ++pcount[grp];
                     TRACE4(3, pv_tiles, 1);
                     if (t == 0) mbar_wait(o_empty, (local & 1) ^ 1);  // last item's epilogue
@@ -285,13 +325,30 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
                     tc_fence_after();
                     if (elect_one()) {
                         const uint32_t kb = kv_base + slot * L::kTile;
+                        if constexpr (kSplit) {
+                            // two N = 64 halves: keys [64 half, 64 half + 64) of the tile are
+                            // rows 64 half.. of the K-major tile (8 KB in, atom-aligned)
 #pragma unroll
-                        for (int kk = 0; kk < D / 16; ++kk)
-                            mma_ts(tmem + L::kS + grp * BK, tmem + L::kQ + kk * 8,
-                                   umma_desc_sw128(kb + (kk >> 2) * L::kBox + (kk & 3) * 32, 16,
-                                                   1024),
-                                   L::kIdescQK, kk > 0 ? 1u : 0u);
-                        mma_commit(s_full + grp);
+                            for (int half = 0; half < 2; ++half) {
+#pragma unroll
+                                for (int kk = 0; kk < D / 16; ++kk)
+                                    mma_ts(tmem + L::kS + grp * BK + half * 64,
+                                           tmem + L::kQ + kk * 8,
+                                           umma_desc_sw128(kb + (kk >> 2) * L::kBox +
+                                                               (kk & 3) * 32 + half * 64 * 128,
+                                                           16, 1024),
+                                           L::kIdescQK64, kk > 0 ? 1u : 0u);
+                                mma_commit(s_full + grp * 2 + half);
+                            }
+                        } else {
+#pragma unroll
+                            for (int kk = 0; kk < D / 16; ++kk)
+                                mma_ts(tmem + L::kS + grp * BK, tmem + L::kQ + kk * 8,
+                                       umma_desc_sw128(kb + (kk >> 2) * L::kBox + (kk & 3) * 32,
+                                                       16, 1024),
+                                       L::kIdescQK, kk > 0 ? 1u : 0u);
+                            mma_commit(s_full + grp * 2);
+                        }
                         mma_commit(kv_empty + slot);
                     }
                     __syncwarp();
@@ -339,7 +396,7 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
                 const uint32_t tk = tbase + (uint32_t)j;
                 (void)tk;
                 if (quarter == 0 && ch == 0 && lane == 0) TRACE4(grp, tk, 0);
-                mbar_wait(s_full + grp, scount & 1);
+                mbar_wait(s_full + grp * 2 + (kSplit ? ch : 0), scount & 1);
                 ++scount;
                 if (quarter == 0 && ch == 0 && lane == 0) TRACE4(grp, tk, 1);
                 tc_fence_after();
@@ -415,7 +472,7 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(p_full + grp);
+                if (lane == 0) mbar_arrive(p_full + grp * 2 + (kSplit ? ch : 0));
                 if (quarter == 0 && ch == 0 && lane == 0) TRACE4(grp, tk, 4);
             }
             tbase += (uint32_t)tl.n;

@@ -38,6 +38,21 @@ __global__ void k(float* out, long long* cyc, int iters) {
                 asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x[i]), "f"(x[(i + 4) & 7]));
                 u[i] ^= r;
             }
+            if (MODE == 5) {  // packed half-precision exp2: two elements per instruction
+                uint32_t h = u[i];
+                asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(h));
+                u[i] = h;
+            }
+            if (MODE == 6) {
+                uint32_t h = u[i];
+                asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(h));
+                u[i] = h;
+            }
+            if (MODE == 7) {  // f32 pair -> f16x2 convert (cvt.rn.f16x2.f32)
+                uint32_t r;
+                asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x[i]), "f"(x[(i + 1) & 7]));
+                u[i] ^= r;
+            }
         }
     }
     long long t1 = clock64();
@@ -71,5 +86,8 @@ int main() {
     run<2>("EX2 + F2FP (per pair)", 2);
     run<3>("IADD+IADD+PRMT+LOP (pack)", 1);
     run<4>("2 EX2 + 1 F2FP", 3);
+    run<5>("EX2 f16x2 (2 elements)", 1);
+    run<6>("EX2 bf16x2 (2 elements)", 1);
+    run<7>("F2FP f16x2", 1);
     return 0;
 }
