@@ -30,7 +30,7 @@ import torch
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_2603_05503_b200 import inputs  # noqa: E402
+from paper_2603_05503_b200 import inputs, ulysses  # noqa: E402
 
 METRIC = "effective attn TFLOP/s & % bf16 roofline, speedup vs dense, 1/2/4/8 B200"
 
@@ -296,10 +296,14 @@ def main():
     hp = H // world
     h_lo, h_hi = rank * hp, (rank + 1) * hp
     lay, masks, rep, counts_all, min_count, calib = workload(cfg, args, 0, H, dev)
-    my_heads = list(range(h_lo, h_hi))
+    # head order of the exchange: LPT over the heads' kept areas (ulysses.balance_heads; a model
+    # folds it into its projections), so every rank gets H/P heads of near-equal total work
+    head_cost = [flops_of(lay, masks, rep, [h], d, 1)[1] for h in range(H)]
+    perm = list(range(H)) if world == 1 else ulysses.balance_heads(head_cost, world)
+    my_heads = perm[h_lo:h_hi]
 
     # ---- plan for this rank's heads (a6 through the C ABI), REPETITIVE via similarity > gamma
-    counts_np = np.ascontiguousarray(counts_all[h_lo:h_hi], dtype=np.uint16)
+    counts_np = np.ascontiguousarray(counts_all[my_heads], dtype=np.uint16)
     counts = torch.from_numpy(counts_np.reshape(-1).view(np.int16)).to(dev).view(torch.uint16)
     sim = torch.tensor([calib["similarity"][h] if calib is not None else (1.0 if h in rep else 0.0)
                         for h in my_heads], dtype=torch.float64, device=dev)
@@ -321,9 +325,9 @@ def main():
         def step():
             return csa.sparse_attn_fwd(q, k, v, plan, work, out=out)
     else:
-        from paper_2603_05503_b200 import ulysses
-
-        ql, kl, vl = (ulysses.sequence_shard(t, world, rank) for t in (q, k, v))
+        # kernel-only reference for the roofline: this rank's heads, full sequence
+        qh0, kh0, vh0 = (t[:, :, my_heads].contiguous() for t in (q, k, v))
+        ql, kl, vl = (ulysses.sequence_shard(t[:, :, perm], world, rank) for t in (q, k, v))
         del q, k, v
         q = k = v = None
 
@@ -355,6 +359,22 @@ def main():
         "clocks": clk.summary(),
     }
     if world > 1:
+        # roofline of the attention kernel on this rank (launches alone, no exchange), the
+        # slowest rank's: achieved = its kept FLOPs / its mean launch time
+        _, per_k = time_loop(lambda: run_heads(qh0, kh0, vh0), args.steps, 2, stream)
+        ms_k = statistics.mean(per_k)
+        mk = torch.tensor([ms_k, flop_rank, -ms_k], device=dev, dtype=torch.float64)
+        gathered = [torch.zeros_like(mk) for _ in range(world)]
+        torch.distributed.all_gather(gathered, mk)
+        slow = max(gathered, key=lambda t: float(t[0]))
+        ach = float(slow[1]) / (float(slow[0]) * 1e-3) / 1e12
+        result["roofline"] = {"bound": "tensor", "achieved": round(ach, 2),
+                              "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                              "frac": round(ach / pk["bf16_tflops"], 4), "traffic": None,
+                              "peak_src": f"{pk['src']} bf16 burst",
+                              "kernel": attention_kernel_name(lay, cfg.d) + ", slowest rank",
+                              "algorithmic_flop_per_launch": float(slow[1]),
+                              "kernel_ms_per_rank": [round(float(t[0]), 3) for t in gathered]}
         # e2e at N GPUs through the public API: every step copies this rank's sequence shard of
         # Q, K, V in from pinned host memory, runs the head-sharded layer (a2a, attention, a2a)
         # and copies the rank's output shard back; max over ranks.  Bytes are whole-job totals.

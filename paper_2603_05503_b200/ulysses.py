@@ -21,6 +21,25 @@ def head_range(n_heads: int, world: int, rank: int) -> tuple[int, int]:
     return rank * hp, (rank + 1) * hp
 
 
+def balance_heads(cost, world: int) -> list[int]:
+    """Head order for the exchange (SURVEY 8.6 load balance): heads differ in kept area, a rank's
+    time is the sum over its heads, so assign heads longest-first to the least-loaded rank that
+    still has room (every rank takes H/P heads: the all-to-all splits stay equal); ties -> lower
+    rank.  Returns perm (position -> head), rank r's heads at perm[r*H/P:(r+1)*H/P] ascending.
+    A model folds perm into its QKV projection rows and the inverse into its output projection,
+    so the reordering costs nothing at run time; the exchange itself is unchanged."""
+    n = len(cost)
+    if n % world:
+        raise ValueError(f"{n} heads not divisible by {world} ranks")
+    hp = n // world
+    load, groups = [0.0] * world, [[] for _ in range(world)]
+    for h in sorted(range(n), key=lambda x: (-float(cost[x]), x)):
+        r = min((r for r in range(world) if len(groups[r]) < hp), key=lambda r: (load[r], r))
+        groups[r].append(h)
+        load[r] += float(cost[h])
+    return [h for g in groups for h in sorted(g)]
+
+
 def scatter_heads(x_loc: torch.Tensor, world: int, group=None) -> torch.Tensor:
     """[B, N/P, H, d] (this rank's tokens, all heads) -> [B, N, H/P, d] (all tokens, this rank's
     heads).  Send block p holds head group p; the received blocks are in source-rank order, i.e.

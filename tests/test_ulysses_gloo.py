@@ -38,7 +38,13 @@ def _worker(rank, world, port, batch, results):
         y_loc = step()
         ref = (x * (torch.arange(h, dtype=x.dtype).view(1, 1, -1, 1) + 1))
         ok_layer = torch.equal(y_loc, ulysses.sequence_shard(ref, world, rank))
-        results[rank] = (ok_scatter, ok_roundtrip, ok_layer)
+        # a balanced head order (folded into the projections in a model): rank r receives the
+        # heads perm[r*H/P:(r+1)*H/P] and the layer still commutes with the exchange
+        perm = ulysses.balance_heads([5.0, 1.0, 4.0, 2.0], world)
+        xp = x[:, :, perm]
+        xph = ulysses.scatter_heads(ulysses.sequence_shard(xp, world, rank), world)
+        ok_perm = torch.equal(xph, x[:, :, perm[h0:h1]])
+        results[rank] = (ok_scatter, ok_roundtrip, ok_layer and ok_perm)
     finally:
         dist.destroy_process_group()
 
@@ -49,6 +55,19 @@ def test_ulysses_exchange_gloo_world2(batch):
     results = mgr.dict()
     mp.spawn(_worker, args=(2, _free_port(), batch, results), nprocs=2, join=True)
     assert dict(results) == {0: (True, True, True), 1: (True, True, True)}
+
+
+def test_balance_heads_lpt():
+    cost = [9, 1, 8, 2, 7, 3, 6, 4]
+    for world in (1, 2, 4, 8):
+        perm = ulysses.balance_heads(cost, world)
+        assert sorted(perm) == list(range(8))
+        hp = 8 // world
+        loads = [sum(cost[h] for h in perm[r * hp:(r + 1) * hp]) for r in range(world)]
+        assert max(loads) - min(loads) <= max(cost)  # LPT: spread within one job
+    assert ulysses.balance_heads(cost, 2) == [0, 1, 6, 7, 2, 3, 4, 5]  # 20 / 20
+    with pytest.raises(ValueError):
+        ulysses.balance_heads(cost, 3)
 
 
 def test_head_range_and_shard_checks():
