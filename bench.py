@@ -46,6 +46,13 @@ def parse():
     ap.add_argument("--rep-heads", type=int, default=4, help="REPETITIVE (anchor) heads, k=5")
     ap.add_argument("--no-extras", action="store_true", help="skip dense/SDPA/e2e/cpu legs")
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--overlap-chunks", type=int, default=1,
+                    help="head chunks of the exchange overlapped with the attention (N > 1); "
+                         "1: no overlap (default; single-GPU NCCL check: 5 chunks cost 7.6 %% "
+                         "more, the overlap pays only when the exchange crosses NVLink), 0: auto "
+                         "(largest divisor of H/N up to 5)")
+    ap.add_argument("--exchange", action="store_true",
+                    help="run the head-sharded exchange path even at N = 1 (NCCL, one rank)")
     return ap.parse_args()
 
 
@@ -287,6 +294,14 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         torch.distributed.init_process_group("nccl", device_id=dev)
+    elif args.exchange:  # single-rank NCCL group: exercises the exchange path on one GPU
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        torch.distributed.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}",
+                                             rank=0, world_size=1, device_id=dev)
+    exchange = world > 1 or args.exchange
     from paper_2603_05503_b200 import csa
 
     stream = torch.cuda.current_stream()
@@ -321,7 +336,8 @@ def main():
     q, k, v = inputs.qkv(B, lay.N, H, d, seed=11, device=dev)
     out = torch.empty((B, lay.N, hp, d), dtype=torch.bfloat16, device=dev)
 
-    if world == 1:
+    chunks = args.overlap_chunks or max(c for c in range(1, 6) if hp % c == 0)
+    if not exchange:
         def step():
             return csa.sparse_attn_fwd(q, k, v, plan, work, out=out)
     else:
@@ -333,13 +349,28 @@ def main():
 
         def run_heads(qh, kh, vh):
             return csa.sparse_attn_fwd(qh, kh, vh, plan, work, out=out)
-        step = ulysses.make_layer_step(ql, kl, vl, world, run_heads)
+
+        hc = hp // chunks
+        works = [csa.build_work_list(plan, c * hc, hc, order=csa.default_order(lay, d))
+                 for c in range(chunks)]
+        outs_c = [torch.empty((B, lay.N, hc, d), dtype=torch.bfloat16, device=dev)
+                  for _ in range(chunks)]
+
+        def run_chunk(c, qh, kh, vh):  # heads c*hc .. of this rank: cells c*hc ..
+            return csa.sparse_attn_fwd(qh, kh, vh, plan, works[c], cell_base=c * hc,
+                                       out=outs_c[c])
+
+        def layer_step(a, b_, c_):
+            if chunks == 1:
+                return ulysses.make_layer_step(a, b_, c_, world, run_heads)
+            return ulysses.make_layer_step_chunked(a, b_, c_, world, run_chunk, chunks)
+        step = layer_step(ql, kl, vl)
 
     with ClockSampler(local) as clk:
         total_ms, per = time_loop(step, args.steps, args.warmup, stream)
     ms = total_ms / args.steps
     ms_t = torch.tensor([ms], device=dev)
-    if world > 1:
+    if exchange:
         torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
     ms = float(ms_t.item())
     value = flop_all / (ms * 1e-3) / 1e12
@@ -354,11 +385,12 @@ def main():
                  "synthetic (seeded N(0,1) bf16 Q/K/V; plan calibrated by this repo's a2-a6 path "
                  "on 8 generator-G prompts)"),
         "config": arm_config(cfg, B, kept_fraction, rep, world),
-        "gpu_launches": args.steps * launches_per_call(lay, d),
+        "gpu_launches": args.steps * launches_per_call(lay, d) * (chunks if exchange else 1),
         **({"calibration": calib} if calib is not None else {}),
         "clocks": clk.summary(),
     }
-    if world > 1:
+    if exchange:
+        result["config"]["exchange_overlap_chunks"] = chunks
         # roofline of the attention kernel on this rank (launches alone, no exchange), the
         # slowest rank's: achieved = its kept FLOPs / its mean launch time
         _, per_k = time_loop(lambda: run_heads(qh0, kh0, vh0), args.steps, 2, stream)
@@ -380,7 +412,7 @@ def main():
         # and copies the rank's output shard back; max over ranks.  Bytes are whole-job totals.
         hq, hk, hv = (t.cpu().pin_memory() for t in (ql, kl, vl))
         dq, dk, dv = (torch.empty_like(t) for t in (ql, kl, vl))
-        step_e2e = ulysses.make_layer_step(dq, dk, dv, world, run_heads)
+        step_e2e = layer_step(dq, dk, dv)
         ho = torch.empty(ql.shape, dtype=ql.dtype).pin_memory()
 
         def e2e_step():
@@ -398,7 +430,7 @@ def main():
                          "ms_per_step": round(t_e2e, 3),
                          "h2d_bytes_per_step": 3 * ql.numel() * 2 * world,
                          "d2h_bytes_per_step": ql.numel() * 2 * world}
-    if rank == 0 and world == 1 and not args.no_extras:
+    if rank == 0 and not exchange and not args.no_extras:
         extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_all, dense_flop,
                kept_fraction, per, pk, stream, dev, csa)
     if rank == 0:
@@ -407,7 +439,7 @@ def main():
         if args.json_out:
             with open(args.json_out, "w") as fh:
                 fh.write(line + "\n")
-    if world > 1:
+    if exchange:
         torch.distributed.destroy_process_group()
 
 

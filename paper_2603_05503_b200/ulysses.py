@@ -86,3 +86,80 @@ def make_layer_step(q_loc, k_loc, v_loc, world: int, attention, group=None):
         return gather_heads(attention(qh, kh, vh), world, group)
 
     return step
+
+
+def make_layer_step_chunked(q_loc, k_loc, v_loc, world: int, attention, chunks: int, group=None):
+    """One head-sharded layer with the exchange overlapped with the attention: this
+    rank's H/P heads are split into `chunks` head chunks; the all-to-all of chunk c+1's Q, K, V
+    (and of chunk c-1's output) runs on a communication stream while chunk c's attention runs on
+    the current stream.  attention(c, qh, kh, vh) maps chunk c's [B, N, H/(P chunks), d] tensors
+    (heads c*hc .. of this rank) to an output of the same shape.  Every rank must use the same
+    `chunks`; the result equals make_layer_step's bit for bit (head-local attention, the same
+    bytes moved).  On CPU tensors (gloo) the same schedule runs without streams."""
+    b, n_loc, h, d = q_loc.shape
+    hp = h // world
+    if hp % chunks:
+        raise ValueError(f"{hp} heads per rank not divisible into {chunks} chunks")
+    hc = hp // chunks
+    cuda = q_loc.is_cuda
+    comm = torch.cuda.Stream(device=q_loc.device) if cuda else None
+    n = n_loc * world
+    # send buffers, chunk c: [P_dst, B, N/P, hc, d] = heads p*hp + c*hc .. of this rank's tokens
+    send = [[torch.empty((world, b, n_loc, hc, d), dtype=x.dtype, device=x.device)
+             for x in (q_loc, k_loc, v_loc)] for _ in range(chunks)]
+    recv = [[torch.empty_like(s) for s in sc] for sc in send]
+    o_send = [torch.empty((world, b, n_loc, hc, d), dtype=q_loc.dtype, device=q_loc.device)
+              for _ in range(chunks)]
+    o_recv = [torch.empty_like(s) for s in o_send]
+    out = torch.empty((b, n_loc, h, d), dtype=q_loc.dtype, device=q_loc.device)
+
+    def ctx(stream):
+        return torch.cuda.stream(stream) if cuda else _Null()
+
+    def head_major(r):  # [P_src, B, N/P, hc, d] -> [B, N, hc, d] (token order = source order)
+        return r.view(1, n, hc, d) if b == 1 else r.permute(1, 0, 2, 3, 4).reshape(b, n, hc, d)
+
+    def step():
+        cur = torch.cuda.current_stream(q_loc.device) if cuda else None
+        ev_in, ev_out = [], []
+        if cuda:
+            comm.wait_stream(cur)  # inputs written on the current stream
+        with ctx(comm):
+            for c in range(chunks):
+                for x, sbuf, rbuf in zip((q_loc, k_loc, v_loc), send[c], recv[c]):
+                    sbuf.copy_(x.view(b, n_loc, world, hp, d)[:, :, :, c * hc:(c + 1) * hc]
+                               .permute(2, 0, 1, 3, 4))
+                    dist.all_to_all_single(rbuf, sbuf, group=group)
+                if cuda:
+                    e = torch.cuda.Event()
+                    e.record(comm)
+                    ev_in.append(e)
+        for c in range(chunks):
+            if cuda:
+                cur.wait_event(ev_in[c])
+            oh = attention(c, *(head_major(r) for r in recv[c]))
+            o_send[c].copy_(oh.view(b, world, n_loc, hc, d).permute(1, 0, 2, 3, 4))
+            if cuda:
+                e = torch.cuda.Event()
+                e.record(cur)
+                ev_out.append(e)
+            with ctx(comm):
+                if cuda:
+                    comm.wait_event(ev_out[c])
+                dist.all_to_all_single(o_recv[c], o_send[c], group=group)
+                # [P_src = head group, B, N/P, hc, d] -> heads p*hp + c*hc .. of this rank's tokens
+                out.view(b, n_loc, world, hp, d)[:, :, :, c * hc:(c + 1) * hc].copy_(
+                    o_recv[c].permute(1, 2, 0, 3, 4))
+        if cuda:
+            cur.wait_stream(comm)
+        return out
+
+    return step
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False

@@ -358,6 +358,11 @@ def test_calibration_against_oracle(csa, lay, heads, d, single_pass):
             assert np.abs(E[h].sum(1) - 1).max() <= 1e-4
             for r in range(nb):
                 oracle.accumulate(oracle.select(E[h, r], eps), counts_np[h, r])
+                # SURVEY 8.4 contract 4: the oracle's selection on its OWN fp64 E may differ
+                # from the GPU's only on borderline rows (cut within 1e-5 of eps, or a tie
+                # within 1e-5 at the cut)
+                if not np.array_equal(oracle.select(E_ref[r], eps), oracle.select(E[h, r], eps)):
+                    assert _borderline(E_ref[r], eps), (h, r)
         assert np.array_equal(u16_np(counts).reshape(heads, nb, nbk), counts_np)
     # LSE supplied from outside (the dense run's statistic) gives the same decisions on this E
     counts2 = u16_zeros(heads * nb * nbk)
@@ -368,6 +373,15 @@ def test_calibration_against_oracle(csa, lay, heads, d, single_pass):
     for h in range(heads):
         for r in range(nb):
             assert np.array_equal(oracle.select(E2[h, r], eps), c2[h, r])
+
+
+def _borderline(e_row, eps, tol=1e-5):
+    e = np.sort(np.asarray(e_row, np.float64))[::-1]
+    cs = np.cumsum(e)
+    k = int(np.searchsorted(cs, eps))  # first prefix reaching eps
+    near_cut = np.min(np.abs(cs - eps)) < tol
+    tie = k + 1 < len(e) and abs(e[min(k, len(e) - 1)] - e[k + 1]) < tol
+    return bool(near_cut or tie)
 
 
 @pytest.mark.parametrize("name", ["wan480", "wan720"])
@@ -389,10 +403,12 @@ def test_calibration_full_size_sampled(csa, name):
     for h in range(heads):
         for r in range(nb):  # bit-exact selection on the GPU's own E, every row
             assert np.array_equal(oracle.select(E[h, r], eps), cnt[h, r])
-    for h, r in ((0, 0), (3, nb - 1)):
+    for h, r in ((0, 0), (3, nb - 1), (1, nb // 2)):
         qh, kh = head64(q, 0, h), head64(k, 0, h)
         E_ref = oracle.block_energy(qh, kh, scale, lay.B, block_rows=(r, r + 1))
         assert np.abs(E[h, r] - E_ref[0]).max() <= 5e-5
+        if not np.array_equal(oracle.select(E_ref[0], eps), cnt[h, r]):  # contract 4
+            assert _borderline(E_ref[0], eps), (h, r)
 
 
 # ---------------------------------------------------------------- CTA-pair kernel (order 3)

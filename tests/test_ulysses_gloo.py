@@ -44,7 +44,15 @@ def _worker(rank, world, port, batch, results):
         xp = x[:, :, perm]
         xph = ulysses.scatter_heads(ulysses.sequence_shard(xp, world, rank), world)
         ok_perm = torch.equal(xph, x[:, :, perm[h0:h1]])
-        results[rank] = (ok_scatter, ok_roundtrip, ok_layer and ok_perm)
+        # head-chunked overlapped schedule: identical result for every chunk count
+        ok_chunk = True
+        for chunks in (1, 2):
+            stepc = ulysses.make_layer_step_chunked(
+                x_loc, x_loc, x_loc, world,
+                lambda c, q, k, v, hc=(h1 - h0) // chunks: q * (scale[:, :, c * hc:(c + 1) * hc]),
+                chunks)
+            ok_chunk &= torch.equal(stepc(), y_loc)
+        results[rank] = (ok_scatter, ok_roundtrip, ok_layer and ok_perm and ok_chunk)
     finally:
         dist.destroy_process_group()
 
