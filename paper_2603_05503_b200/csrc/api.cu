@@ -401,10 +401,12 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
     if (st != CSA_OK) return st;
     if (pair_items && (L.block != 128 || head_dim != 128 || !is_square(L)))
         return fail(CSA_ERR_UNSUPPORTED, "pair work items need block 128 and head_dim 128");
-    const bool rect = !is_square(L) || (L.block == 128 && head_dim == 128 &&
-                                        std::getenv("CSA_ATTN_RECT") != nullptr);
-    if (rect && head_dim != 128)
-        return fail(CSA_ERR_UNSUPPORTED, "non-square blocks need head_dim 128");
+    // attn_rect.cu: non-square blocks, the d = 64 path at block 128 (CSA_ATTN_V3 -> attn.cu),
+    // and block 128 / d 128 on request (CSA_ATTN_RECT, A/B against attn4.cu)
+    const bool rect = !is_square(L) ||
+                      (L.block == 128 && head_dim == 64 && workspace != nullptr &&
+                       std::getenv("CSA_ATTN_V3") == nullptr) ||
+                      (L.block == 128 && head_dim == 128 && std::getenv("CSA_ATTN_RECT") != nullptr);
     if (rect && workspace == nullptr)
         return fail(CSA_ERR_INVALID_ARGUMENT, "non-square blocks need the attention workspace");
     if (workspace != nullptr && (workspace_bytes < 8 || reinterpret_cast<uintptr_t>(workspace) % 8))
@@ -433,6 +435,7 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
     a.g = g;
     a.batch = batch;
     a.n_heads = n_heads;
+    a.head_dim = head_dim;
     a.scale_log2 = softmax_scale * 1.4426950408889634f;
     a.q = static_cast<const __nv_bfloat16*>(q.ptr);
     a.o = static_cast<__nv_bfloat16*>(o.ptr);

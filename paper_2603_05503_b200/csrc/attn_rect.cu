@@ -34,18 +34,24 @@ using namespace attn;
 
 constexpr int kItemSlotsR = 4;
 constexpr float kGuardR = 72057594037927936.0f;  // 2^56
-constexpr int kEmuR = 1;  // element pairs p with (p & 7) >= 8 - kEmuR -> polynomial exp2
+// element pairs p with (p & 7) >= 8 - kEmu -> polynomial exp2 (FMA pipe) instead of MUFU
+#ifndef CSA_RECT_EMU64
+#define CSA_RECT_EMU64 1
+#endif
+template <int D>
+constexpr int kEmuR = D == 64 ? CSA_RECT_EMU64 : 1;
 
-template <int BKV>
+template <int BKV, int D = 128>
 struct SmemR {
     static constexpr int kThreads = 384;
-    static constexpr int kQBox = 128 * 128;   // [128 rows][64] bf16, SWIZZLE_128B
-    static constexpr int kQTile = 2 * kQBox;  // 128 x 128
-    static constexpr int kKVBox = BKV * 128;  // [B_kv rows][64]
-    static constexpr int kTile = 2 * kKVBox;  // B_kv x 128
+    static constexpr int kBoxes = D / 64;          // 128-byte-wide boxes per row
+    static constexpr int kQBox = 128 * 128;        // [128 rows][64] bf16, SWIZZLE_128B
+    static constexpr int kQTile = kBoxes * kQBox;  // 128 x D
+    static constexpr int kKVBox = BKV * 128;       // [B_kv rows][64]
+    static constexpr int kTile = kBoxes * kKVBox;  // B_kv x D
     static constexpr uint32_t kSB = (BKV + 31) / 32 * 32;
-    static constexpr bool kQT = 2 * kSB + 128 + 64 <= 512;
-    static constexpr uint32_t kS = 0, kO = 2 * kSB, kQ = 2 * kSB + 128;
+    static constexpr bool kQT = 2 * kSB + D + D / 2 <= 512;
+    static constexpr uint32_t kS = 0, kO = 2 * kSB, kQ = 2 * kSB + D;
     static constexpr int kQOff = 0;
     static constexpr int kKVOff = kQTile;
     static constexpr int kSlotsFit = (232448 - kQTile - 2048) / kTile;
@@ -62,9 +68,10 @@ struct SmemR {
     static_assert(kBytes <= 232448, "smem");
     static_assert(kSlots >= 3, "K/V ring");
     static_assert(BKV % 16 == 0 && BKV >= 64 && BKV <= 192, "B_kv");
-    static_assert(2 * kSB + 128 <= 512 && (!kQT || kQ + 64 <= 512), "TMEM");
+    static_assert(2 * kSB + D <= 512 && (!kQT || kQ + D / 2 <= 512), "TMEM");
+    static_assert(D == 64 || D == 128, "head_dim");
     static constexpr uint32_t kIdescQK = umma_idesc_bf16(128, BKV, 0, 0);
-    static constexpr uint32_t kIdescPV = umma_idesc_bf16(128, 128, 0, 1);
+    static constexpr uint32_t kIdescPV = umma_idesc_bf16(128, D, 0, 1);
 };
 
 // Load W (multiple of 16, <= 64) consecutive TMEM columns of this thread's lane into r[0, W).
@@ -122,7 +129,7 @@ __device__ __forceinline__ float max_part(const uint32_t (&r)[64]) {
 }
 
 // exp2(s * sl2 - m) of W scores -> packed bf16 pk[W/2]; returns their fp32 sum.
-template <int W>
+template <int W, int kEmu>
 __device__ __forceinline__ float exp_part(const uint32_t (&r)[64], uint64_t sl2x2, uint64_t negm,
                                           uint32_t (&pk)[32]) {
     uint64_t acc[4] = {0, 0, 0, 0};
@@ -130,7 +137,7 @@ __device__ __forceinline__ float exp_part(const uint32_t (&r)[64], uint64_t sl2x
     for (int x = 0; x < W; x += 2) {
         const uint64_t t = ffma2(pk2(r[x], r[x + 1]), sl2x2, negm);
         uint64_t p;
-        if (((x / 2) & 7) >= 8 - kEmuR) {
+        if (((x / 2) & 7) >= 8 - kEmu) {
             p = exp2_poly2(t);
         } else {
             p = f2(ex2_approx(lo_f(t)), ex2_approx(hi_f(t)));
@@ -149,14 +156,14 @@ struct Part {
     static constexpr int kW = BKV - kCol < 64 ? BKV - kCol : 64;
 };
 
-template <int BKV>
-__global__ void __launch_bounds__(SmemR<BKV>::kThreads, 1)
+template <int BKV, int D>
+__global__ void __launch_bounds__(SmemR<BKV, D>::kThreads, 1)
     sparse_attn_rect_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tq,
                             const __grid_constant__ CUtensorMap tk,
                             const __grid_constant__ CUtensorMap tv, const Fallback fb,
                             const int mode) {
-    using L = SmemR<BKV>;
-    constexpr int D = 128, S = L::kSlots;
+    using L = SmemR<BKV, D>;
+    constexpr int S = L::kSlots;
     constexpr int kParts = (BKV + 63) / 64;
     extern __shared__ __align__(1024) uint8_t smem[];
     if ((smem_u32(smem) & 1023u) != 0u) __trap();
@@ -475,7 +482,7 @@ __global__ void __launch_bounds__(SmemR<BKV>::kThreads, 1)
                         ld_part<PT::kW>(lane_addr + s_col + PT::kCol, r);
                         if (ragged) mask_part<PT::kW>(r, PT::kCol, tail_valid);
                         uint32_t pk[32];
-                        lsum += exp_part<PT::kW>(r, sl2x2, negm, pk);
+                        lsum += exp_part<PT::kW, kEmuR<D>>(r, sl2x2, negm, pk);
                         // P of columns [c, c + w) -> packed columns [c/2, c/2 + w/2): below
                         // every column this thread still has to load
                         st_part<PT::kW>(lane_addr + s_col + PT::kCol / 2, pk);
@@ -572,16 +579,24 @@ __global__ void __launch_bounds__(SmemR<BKV>::kThreads, 1)
     }
 }
 
+template <int BKV, int D>
+cudaError_t launch_rect_d(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                          const CUtensorMap& tv, int grid, const Fallback& fb, int mode,
+                          cudaStream_t s) {
+    auto kern = sparse_attn_rect_kernel<BKV, D>;
+    const int smem = SmemR<BKV, D>::kBytes;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, SmemR<BKV, D>::kThreads, smem, s>>>(a, tq, tk, tv, fb, mode);
+    return cudaGetLastError();
+}
+
 template <int BKV>
 cudaError_t launch_rect(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
                         const CUtensorMap& tv, int grid, const Fallback& fb, int mode,
                         cudaStream_t s) {
-    auto kern = sparse_attn_rect_kernel<BKV>;
-    const int smem = SmemR<BKV>::kBytes;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    kern<<<grid, SmemR<BKV>::kThreads, smem, s>>>(a, tq, tk, tv, fb, mode);
-    return cudaGetLastError();
+    return a.head_dim == 64 ? launch_rect_d<BKV, 64>(a, tq, tk, tv, grid, fb, mode, s)
+                            : launch_rect_d<BKV, 128>(a, tq, tk, tv, grid, fb, mode, s);
 }
 
 }  // namespace

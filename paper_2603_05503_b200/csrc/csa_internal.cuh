@@ -114,6 +114,7 @@ struct AttnArgs {
     Geo g;
     int32_t batch;
     int32_t n_heads;
+    int32_t head_dim;
     float scale_log2;
     // q (for anchor-row gathers) and o: raw pointers + element strides
     const __nv_bfloat16* q;

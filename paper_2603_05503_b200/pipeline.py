@@ -56,7 +56,7 @@ class PlanDictionary:
     min_count: int
     prompts: int
     similarity: torch.Tensor   # fp64 [T * L * H]
-    keep_count: torch.Tensor   # uint16 [T * L * H, N_B, N_B]
+    keep_count: torch.Tensor   # uint16 [T * L * H, N_B, N_Bkv]
 
     def cell_base(self, t: int, l: int) -> int:
         return (t * self.L + l) * self.H
@@ -80,18 +80,18 @@ def calibrate(lay: Layout, T: int, L: int, H: int, prompts: int,
     row LSE.  Then s = sim_sum / (F H |D|), min_count = ceil(rho |D|) and one csa_compile_plan over
     every cell (a6; s > gamma -> REPETITIVE)."""
     eps = epsilon_schedule(T, *constants)
-    nb = lay.NB
+    nb, nbk = lay.NB, lay.NBK  # query blocks x key blocks (non-square B_q x B_kv: P:1294-1328)
     cells = T * L * H
-    keep = torch.zeros(cells * nb * nb, dtype=torch.int16, device=device).view(torch.uint16)
+    keep = torch.zeros(cells * nb * nbk, dtype=torch.int16, device=device).view(torch.uint16)
     sim_sum = torch.zeros(cells, dtype=torch.float64, device=device)
     lse = torch.empty(H * lay.N, dtype=torch.float32, device=device)
-    per = H * nb * nb
+    per = H * nb * nbk
     for p in range(prompts):
         for t in range(T):
             for l in range(L):
                 q, k = qk_fn(p, t, l)
                 c0 = (t * L + l) * H
-                csa.calib_accumulate(lay, q, k, eps[t], keep[c0 * nb * nb:c0 * nb * nb + per],
+                csa.calib_accumulate(lay, q, k, eps[t], keep[c0 * nb * nbk:c0 * nb * nbk + per],
                                      lse_out=lse)
                 csa.spatial_similarity(lay, q, k, lse, anchor_k, sim_sum[c0:c0 + H])
     # smallest integer >= rho |D| (Eq. eq:mask_threshold in count space, reading Q6)
@@ -99,7 +99,7 @@ def calibrate(lay: Layout, T: int, L: int, H: int, prompts: int,
     s = sim_sum / float(lay.F * lay.H * prompts)
     plan = csa.compile_plan(lay, keep, min_count, similarity=s, gamma=gamma, anchor_k=anchor_k)
     return PlanDictionary(lay, T, L, H, plan, eps, min_count, prompts, s,
-                          keep.view(cells, nb, nb))
+                          keep.view(cells, nb, nbk))
 
 
 class DenoiseStep:

@@ -71,6 +71,7 @@ def main():
                          "eps(t=25 of 50) of Eq. eq:epsilon_schedule, rho 0.5) instead of the "
                          "paper's per-size sparsity")
     ap.add_argument("--prompts", type=int, default=4)
+    ap.add_argument("--d", type=int, default=0, help="head_dim (default: the config's, 128)")
     args = ap.parse_args()
     peak = 1685.2
     try:
@@ -79,7 +80,7 @@ def main():
     except OSError:
         pass
     base = inputs.CONFIGS["wan480"]
-    H, d = base.heads, base.d
+    H, d = base.heads, args.d or base.d
     q, k, v = inputs.qkv(1, base.layout.N, H, d, seed=11, device="cuda")
     out = torch.empty_like(q)
     rows = []

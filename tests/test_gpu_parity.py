@@ -657,13 +657,14 @@ def test_rect_plan_compile_bit_exact(csa, lay):
                               anchor_k=min(5, lay.H))
 
 
-@pytest.mark.parametrize("bkv", BKV_ALL)
-def test_rect_attention_against_oracle(csa, bkv):
-    """Every B_kv kernel instance: ragged N (N_Bkv ragged for most B_kv), random MASK heads, an
-    anchor head, batch 2 sharing the plan, lse; outputs vs the fp64 oracle on the same grid."""
-    lay = Layout(2, 9, 40, 128, bkv)  # N = 720
+@pytest.mark.parametrize("bkv,d", [(b, 128) for b in BKV_ALL] + [(64, 64), (128, 64), (176, 64)])
+def test_rect_attention_against_oracle(csa, bkv, d):
+    """Every B_kv kernel instance (head_dim 128; head_dim 64 at 64, square 128 -- the d = 64 path
+    -- and 176): ragged N (N_Bkv ragged for most B_kv), random MASK heads, an anchor head,
+    batch 2 sharing the plan, lse; outputs vs the fp64 oracle on the same grid."""
+    lay = Layout(2, 9, 40, 128, 0 if bkv == 128 else bkv)  # N = 720
     heads = 3
-    q, k, v = qkv(2, lay.N, heads, 128, seed=bkv, device="cuda")
+    q, k, v = qkv(2, lay.N, heads, d, seed=bkv + d, device="cuda")
     rng = np.random.default_rng(bkv)
     masks = (rng.random((heads, lay.NB, lay.NBK)) < 0.5).astype(np.uint8)
     masks[:, :, -1] = 1  # the ragged last key block
@@ -680,13 +681,13 @@ def test_rect_attention_against_oracle(csa, bkv):
     assert fallback_count(csa, q) == 0
 
 
-@pytest.mark.parametrize("bkv", [80, 192])
-def test_rect_attention_overflow_fallback(csa, bkv):
+@pytest.mark.parametrize("bkv,d", [(80, 128), (192, 128), (128, 64)])
+def test_rect_attention_overflow_fallback(csa, bkv, d):
     """Scores growing 40x block by block overshoot the first tile's reference max by far more
     than 2^56: those items go through the exact-row-max fallback (modes 1, 2) and still match."""
-    lay = Layout(2, 9, 40, 128, bkv)
+    lay = Layout(2, 9, 40, 128, 0 if bkv == 128 else bkv)
     heads = 2
-    q, k, v = qkv(1, lay.N, heads, 128, seed=21, device="cuda")
+    q, k, v = qkv(1, lay.N, heads, d, seed=21, device="cuda")
     gain = torch.ones(lay.N, device="cuda")
     for c in range(lay.NBK):
         gain[c * bkv:(c + 1) * bkv] = 1.0 + 40.0 * c / lay.NBK
