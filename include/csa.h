@@ -263,7 +263,12 @@ CSA_API csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan,
  * is listed in bytes [256, size) (rewritten every launch, needs max_work <= n_heads * N_B) and
  * recomputed on the same stream by the running-max kernel (attn3.cu).  Without a workspace the
  * running-max kernel runs the whole launch.  Each mode is deterministic; the two agree within
- * bf16 rounding of P (not bitwise). */
+ * bf16 rounding of P (not bitwise).
+ * Non-square blocks (block 128 x block_kv) and block 128 / head_dim 64 run attn_rect.cu (the same
+ * fixed-reference design with B_kv-wide key tiles; the workspace is REQUIRED for non-square
+ * layouts): overshooting items are recomputed on the same stream by an exact-row-max pass (the
+ * row max is parked in the first 4 bytes of the row's first output row) and a pass against that
+ * max.  Other shapes (block 64) run attn.cu. */
 CSA_API csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
                                  int32_t head_dim, float softmax_scale, csa_tensor_t q,
                                  csa_tensor_t k, csa_tensor_t v, csa_tensor_t o, float* lse_out,
