@@ -809,3 +809,37 @@ def test_denoise_step_dictionary_graph_and_oracle(csa):
                                          rep_k=5 if kind[c0 + h] else None, rows=rows)
                     assert_close(eager[l][b, rows[0]:rows[1], h].double().cpu().numpy(), ref,
                                  f"t{t} l{l} b{b} h{h}")
+
+
+@pytest.mark.parametrize("lay", [Layout(1, 1, 100, 128, 192), Layout(1, 3, 50, 128, 64),
+                                 Layout(1, 1, 100, 128), Layout(1, 2, 65, 128, 112),
+                                 Layout(3, 1, 43, 128, 144)])
+def test_rect_edge_layouts_calibrate_compile_attend(csa, lay):
+    """Degenerate grids: N below one block (N_B = N_Bkv = 1), a key tail of a few tokens, query
+    and key grids with different raggedness, one spatial row per frame (anchor k = H = 1).  The
+    whole path: calibration (E, selection), compile, attention (MASK + REPETITIVE), vs oracle."""
+    heads, d = 2, 128
+    q, k, v = qkv(1, lay.N, heads, d, seed=lay.N + lay.Bkv, device="cuda")
+    nb, nbk = lay.NB, lay.NBK
+    counts = u16_zeros(heads * nb * nbk)
+    energy = torch.empty(heads * nb * nbk, dtype=torch.float32, device="cuda")
+    csa.calib_accumulate(lay, q, k, 0.8, counts, energy_out=energy)
+    torch.cuda.synchronize()
+    E = energy.view(heads, nb, nbk).double().cpu().numpy()
+    cnt = u16_np(counts).reshape(heads, nb, nbk)
+    scale = 1.0 / np.sqrt(d)
+    for h in range(heads):
+        E_ref = oracle.block_energy(head64(q, 0, h), head64(k, 0, h), scale, lay.B,
+                                    block_kv=lay.BK or None)
+        assert np.abs(E[h] - E_ref).max() <= 5e-5
+        for r in range(nb):
+            assert np.array_equal(oracle.select(E[h, r], 0.8), cnt[h, r])
+    plan = check_plan_against_oracle(csa, lay, cnt, 1, sim=[0.0, 1.0], anchor_k=1)
+    work = csa.build_work_list(plan, 0, heads)
+    out = csa.sparse_attn_fwd(q, k, v, plan, work)
+    torch.cuda.synchronize()
+    mask0 = (cnt[0] >= 1).astype(np.uint8)
+    ref0, _ = oracle_head(lay, q, k, v, 0, 0, mask=mask0)
+    assert_close(out[0, :, 0].double().cpu().numpy(), ref0, "mask head")
+    ref1, _ = oracle_head(lay, q, k, v, 0, 1, rep_k=1)
+    assert_close(out[0, :, 1].double().cpu().numpy(), ref1, "anchor head")
