@@ -48,6 +48,19 @@ __global__ void k(float* out, long long* cyc, int iters) {
                 asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(h));
                 u[i] = h;
             }
+            if (MODE == 8) {  // F2FP in a dependent chain that cannot be folded away
+                uint32_t r;
+                asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x[i]), "f"(x[(i + 1) & 7]));
+                x[i] = __uint_as_float(r);
+            }
+            if (MODE == 9) {  // 7 EX2 + 4 F2FP: the attention softmax's per-octet mix
+                asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x[i]));
+                if (i & 1) {
+                    uint32_t r;
+                    asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x[i]), "f"(x[i ^ 1]));
+                    u[i] ^= r;
+                }
+            }
             if (MODE == 7) {  // f32 pair -> f16x2 convert (cvt.rn.f16x2.f32)
                 uint32_t r;
                 asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x[i]), "f"(x[(i + 1) & 7]));
@@ -89,5 +102,7 @@ int main() {
     run<5>("EX2 f16x2 (2 elements)", 1);
     run<6>("EX2 bf16x2 (2 elements)", 1);
     run<7>("F2FP f16x2", 1);
+    run<8>("F2FP bf16x2 (dependent)", 1);
+    run<9>("8 EX2 + 4 F2FP (per 12)", 1);
     return 0;
 }
