@@ -37,6 +37,11 @@ constexpr int kCH4 = 2;
 #define CSA_ATTN4_SPLIT 0
 #endif
 constexpr bool kSplit4 = CSA_ATTN4_SPLIT != 0;
+// CSA_ATTN4_PHASED: the softmax computes all exp2 arguments, then issues the exponentials back
+// to back, then sums / packs (A/B against the interleaved loop).
+#ifndef CSA_ATTN4_PHASED
+#define CSA_ATTN4_PHASED 0
+#endif
 constexpr float kGuard = 72057594037927936.0f;  // 2^56: a tile row sum above it flags the item
 static __device__ unsigned long long* g_trace4;
 static __device__ int g_debug_mode4;
@@ -445,6 +450,38 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
                 }
                 const uint64_t negm = f2(-m_ref, -m_ref);
                 uint64_t acc[4] = {0, 0, 0, 0};
+#if CSA_ATTN4_PHASED
+                // phased: all arguments first, then the exponentials back to back (one MUFU
+                // stream per warp), then sums and packing
+                uint64_t tt[NC / 2];
+#pragma unroll
+                for (int c = 0; c < NC / 32; ++c)
+#pragma unroll
+                    for (int x = 0; x < 32; x += 2)
+                        tt[c * 16 + x / 2] = ffma2(pk2(r[c][x], r[c][x + 1]), sl2x2, negm);
+#pragma unroll
+                for (int i = 0; i < NC / 2; ++i) {
+                    if ((i & 7) >= 8 - kEmu4) {
+                        tt[i] = exp2_poly2(tt[i]);
+                    } else {
+                        float e0, e1;
+                        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(lo_f(tt[i])));
+                        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(hi_f(tt[i])));
+                        tt[i] = f2(e0, e1);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < NC / 32; ++c) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int x = 0; x < 16; ++x) {
+                        const uint64_t p = tt[c * 16 + x];
+                        acc[x & 3] = fadd2(acc[x & 3], p);
+                        pk[x] = pack_bf16(lo_f(p), hi_f(p));
+                    }
+                    tmem_st16(lane_addr + p_col + c * 16, pk);
+                }
+#else
 #pragma unroll
                 for (int c = 0; c < NC / 32; ++c) {  // P overwrites the first BK/2 columns of S
                     uint32_t pk[16];
@@ -464,6 +501,7 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
                     }
                     tmem_st16(lane_addr + p_col + c * 16, pk);
                 }
+#endif
                 const uint64_t acc2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
                 const float lsum = lo_f(acc2) + hi_f(acc2);
                 bad |= !(lsum <= kGuard);  // also catches inf / NaN

@@ -42,7 +42,24 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
+// CSA_MBAR_SUSPEND_NS: suspend-time hint of try_wait (the waiting thread sleeps until the phase
+// completes or the hint elapses instead of re-polling): spinning waiters otherwise take issue
+// slots from the warps doing the work on the same SMSP.  0 = plain polling try_wait.
+#ifndef CSA_MBAR_SUSPEND_NS
+#define CSA_MBAR_SUSPEND_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if CSA_MBAR_SUSPEND_NS > 0
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(CSA_MBAR_SUSPEND_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
@@ -52,6 +69,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 
 // --------------------------------------------------------------------------------------- fences

@@ -76,19 +76,20 @@ __global__ void k(float* out, long long* cyc, int iters) {
 }
 
 template <int MODE>
-void run(const char* name, int ops_per_iter) {
+void run(const char* name, int ops_per_iter, int threads = 512) {
     float* out;
     long long* cyc;
     cudaMalloc(&out, 148 * 512 * 4);
     cudaMalloc(&cyc, 148 * 8);
     int iters = 4096;
-    k<MODE><<<148, 512>>>(out, cyc, iters);
-    k<MODE><<<148, 512>>>(out, cyc, iters);
+    k<MODE><<<148, threads>>>(out, cyc, iters);
+    k<MODE><<<148, threads>>>(out, cyc, iters);
     cudaDeviceSynchronize();
     long long c;
     cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
-    double warp_instr_per_smsp = 4.0 * iters * 8 * ops_per_iter;  // 16 warps / 4 SMSPs
-    printf("%-28s %8.2f cycles per warp-instruction per SMSP\n", name, c / warp_instr_per_smsp);
+    double warp_instr_per_smsp = threads / 128.0 * iters * 8 * ops_per_iter;  // warps / 4 SMSPs
+    printf("%-28s %4d thr %8.2f cycles per warp-instruction per SMSP\n", name, threads,
+           c / warp_instr_per_smsp);
     cudaFree(out);
     cudaFree(cyc);
 }
@@ -104,5 +105,7 @@ int main() {
     run<7>("F2FP f16x2", 1);
     run<8>("F2FP bf16x2 (dependent)", 1);
     run<9>("8 EX2 + 4 F2FP (per 12)", 1);
+    for (int thr : {128, 256, 384, 512}) run<0>("MUFU.EX2 (warps per SMSP)", 1, thr);
+    for (int thr : {128, 256, 512}) run<9>("8 EX2 + 4 F2FP (warps/SMSP)", 1, thr);
     return 0;
 }
