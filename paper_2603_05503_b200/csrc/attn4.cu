@@ -27,7 +27,16 @@ using namespace attn;
 constexpr int kItemSlots4 = 4;
 // CH4: column split of each softmax group: a group is 4 * CH4 warps, warp (quarter, ch) taking
 // rows 32 * quarter ... and key columns ch * 128 / CH4 ... of the group's tiles.
-constexpr int kCH4 = 2;
+#ifndef CSA_ATTN4_CH
+#define CSA_ATTN4_CH 2
+#endif
+#ifndef CSA_ATTN4_NG
+#define CSA_ATTN4_NG 2
+#endif
+constexpr int kCH4 = CSA_ATTN4_CH;
+// NG: softmax groups = tiles in softmax at once (2: groups on alternate tiles, S buffer = group;
+// 1: one group of 4 CH warps takes every tile, the two S buffers alternate under it)
+constexpr int kNG4 = CSA_ATTN4_NG;
 // kSplit4: the S-MMA of a tile is issued as two N = 64 halves (one per column part) with their
 // own completion barriers, and the P.V as two K = 64 halves waiting for their own part's P: a
 // column part's softmax starts when its half of S is done, and its half of P.V when its own P
@@ -60,9 +69,9 @@ static __device__ int g_debug_mode4;
 #endif
 constexpr int kEmu4 = 1;  // element pairs p with (p & 7) >= 8 - kEmu4 -> polynomial exp2
 
-template <int CH>
+template <int CH, int NG>
 struct Smem4 {
-    static constexpr int kThreads = 128 + 256 * CH;
+    static constexpr int kThreads = 128 + 128 * NG * CH;
     static constexpr int kBox = 128 * 128;      // [128 rows][64 cols] bf16, SWIZZLE_128B
     static constexpr int kTile = 2 * kBox;      // 128 x 128 bf16
     static constexpr int kQOff = 0;             // single Q buffer (freed once copied to TMEM)
@@ -74,7 +83,7 @@ struct Smem4 {
     static constexpr int kNumBars = 2 + 2 * kSlots + 8 + 2 + 1 + 2 * kItemSlots4;
     // m_ref[128] | l[2 * CH][128] | tile-0 max of each column part [CH][128]
     static constexpr int kRowOff = kBarOff + kNumBars * 8;
-    static constexpr int kItemOff = kRowOff + (1 + 3 * CH) * 128 * 4;
+    static constexpr int kItemOff = kRowOff + (1 + NG * CH + CH) * 128 * 4;
     static constexpr int kFlagOff = kItemOff + kItemSlots4 * 4;
     static constexpr int kTmemPtrOff = kFlagOff + 16;
     static constexpr int kBytes = kTmemPtrOff + 16;
@@ -85,12 +94,12 @@ struct Smem4 {
     static constexpr uint32_t kIdescPV = umma_idesc_bf16(128, 128, 0, 1);
 };
 
-template <int CH>
-__global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
+template <int CH, int NG>
+__global__ void __launch_bounds__(Smem4<CH, NG>::kThreads, 1)
     sparse_attn_fixed_ref_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tq,
                                  const __grid_constant__ CUtensorMap tk,
                                  const __grid_constant__ CUtensorMap tv, const Fallback fb) {
-    using L = Smem4<CH>;
+    using L = Smem4<CH, NG>;
     constexpr int BK = 128, D = 128, S = L::kSlots;
     extern __shared__ __align__(1024) uint8_t smem[];
     if ((smem_u32(smem) & 1023u) != 0u) __trap();
@@ -99,7 +108,7 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
     uint64_t* q_empty = bars + 1;
     uint64_t* kv_full = bars + 2;
     uint64_t* kv_empty = kv_full + S;
-    constexpr bool kSplit = kSplit4 && CH == 2;
+    constexpr bool kSplit = kSplit4 && CH == 2 && NG == 2;
     uint64_t* s_full = kv_empty + S;  // [grp][half]
     uint64_t* p_full = s_full + 4;    // [grp][half]
     uint64_t* o_full = p_full + 4;
@@ -108,8 +117,8 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
     uint64_t* item_full = mref_full + 1;
     uint64_t* item_empty = item_full + kItemSlots4;
     float* mref_s = reinterpret_cast<float*>(smem + L::kRowOff);  // [128] (log2 domain)
-    float* row_l = mref_s + 128;                                   // [2 * CH][128]
-    float* mx_s = row_l + 2 * CH * 128;                            // [CH][128]
+    float* row_l = mref_s + 128;                                   // [NG * CH][128]
+    float* mx_s = row_l + NG * CH * 128;                           // [CH][128]
     volatile int32_t* item_slot = reinterpret_cast<int32_t*>(smem + L::kItemOff);
     volatile int32_t* flag_s = reinterpret_cast<int32_t*>(smem + L::kFlagOff);
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtrOff);
@@ -127,11 +136,11 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
             mbar_init(p_full + i, kSplit ? 4 : 4 * CH);
         }
         mbar_init(o_full, 1);
-        mbar_init(o_empty, 8 * CH);
+        mbar_init(o_empty, 4 * NG * CH);
         mbar_init(mref_full, 4 * CH);
         for (int i = 0; i < kItemSlots4; ++i) {
             mbar_init(item_full + i, 1);
-            mbar_init(item_empty + i, 1 + 8 * CH);  // MMA warp + the softmax warps
+            mbar_init(item_empty + i, 1 + 4 * NG * CH);  // MMA warp + the softmax warps
         }
         *flag_s = 0;
         fence_barrier_init();
@@ -378,8 +387,7 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
-        const uint32_t s_col = L::kS + grp * BK + ch * NC;
-        const uint32_t p_col = s_col;  // P over the first half of this part's S columns
+        uint32_t sc1 = 0;  // uses of S buffer 1 (NG 1; scount counts buffer 0 / the own one)
         const float sl2 = a.scale_log2;
         const uint64_t sl2x2 = f2(sl2, sl2);
         const int32_t tail_valid = g.N - (g.NB - 1) * BK;
@@ -397,12 +405,20 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
                 m_ref = mref_s[row];
                 have_ref = true;
             };
-            for (int32_t j = grp; j < tl.n; j += 2) {
+            for (int32_t j = grp; j < tl.n; j += NG) {
                 const uint32_t tk = tbase + (uint32_t)j;
                 (void)tk;
+                const uint32_t sb = (uint32_t)j & 1u;  // S buffer of tile j (= grp for NG 2)
+                const uint32_t s_col = L::kS + sb * BK + ch * NC;
+                const uint32_t p_col = s_col;  // P over the first half of this part's S columns
                 if (quarter == 0 && ch == 0 && lane == 0) TRACE4(grp, tk, 0);
-                mbar_wait(s_full + grp * 2 + (kSplit ? ch : 0), scount & 1);
-                ++scount;
+                uint32_t sph;
+                if (NG == 1 && sb) {
+                    sph = sc1++;
+                } else {
+                    sph = scount++;
+                }
+                mbar_wait(s_full + sb * 2 + (kSplit ? ch : 0), sph & 1);
                 if (quarter == 0 && ch == 0 && lane == 0) TRACE4(grp, tk, 1);
                 tc_fence_after();
                 uint32_t r[NC / 32][32];
@@ -443,8 +459,10 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
                     }
                     if (ch == 0) mref_s[row] = m_ref;
                     have_ref = true;
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(mref_full);
+                    if constexpr (NG > 1) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(mref_full);
+                    }
                 } else if (!have_ref) {
                     get_ref();
                 }
@@ -499,6 +517,13 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
                         acc[(x / 2) & 3] = fadd2(acc[(x / 2) & 3], p);
                         pk[x / 2] = pack_bf16(lo_f(p), hi_f(p));
                     }
+                    if (DEBUG4 == 2) {  // debug: no P store (timeline of the rest)
+                        uint32_t sink = 0;
+#pragma unroll
+                        for (int x = 0; x < 16; ++x) sink ^= pk[x];
+                        if (sink == 0x12345678u) mref_s[0] = 0.0f;
+                        continue;
+                    }
                     tmem_st16(lane_addr + p_col + c * 16, pk);
                 }
 #endif
@@ -510,11 +535,15 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(p_full + grp * 2 + (kSplit ? ch : 0));
+                if (lane == 0) mbar_arrive(p_full + sb * 2 + (kSplit ? ch : 0));
                 if (quarter == 0 && ch == 0 && lane == 0) TRACE4(grp, tk, 4);
             }
             tbase += (uint32_t)tl.n;
-            if (grp == 0 && tl.n == 0) {  // corrupt plan: keep the per-item phase of mref_full
+            if (NG == 1 && !have_ref) {  // corrupt plan (empty row): no reference needed
+                m_ref = 0.0f;
+                have_ref = true;
+            }
+            if (NG > 1 && grp == 0 && tl.n == 0) {  // corrupt plan: keep mref_full's phase
                 if (ch == 0) mref_s[row] = 0.0f;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(mref_full);
@@ -525,10 +554,10 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
             mbar_wait(o_full, local & 1);
             tc_fence_after();
             row_l[(grp * CH + ch) * 128 + row] = l_run;
-            named_bar_sync(1, 256 * CH);
+            named_bar_sync(1, 128 * NG * CH);
             float Lsum = 0.0f;
 #pragma unroll
-            for (int o = 0; o < 2 * CH; ++o) Lsum += row_l[o * 128 + row];
+            for (int o = 0; o < NG * CH; ++o) Lsum += row_l[o * 128 + row];
             const float inv = Lsum > 0.0f ? 1.0f / Lsum : 0.0f;
             const bool flagged = *flag_s != 0;
             int64_t tok0 = -1;
@@ -557,8 +586,8 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
             __nv_bfloat16* obase = a.o + (int64_t)it.b * a.o_sb + (int64_t)it.h * a.o_sh;
             const uint64_t inv2 = f2(inv, inv);
 #pragma unroll
-            for (int cc = 0; cc < D / (2 * CH); cc += 32) {
-                const int col = (grp * CH + ch) * (D / (2 * CH)) + cc;
+            for (int cc = 0; cc < D / (NG * CH); cc += 32) {
+                const int col = (grp * CH + ch) * (D / (NG * CH)) + cc;
                 uint32_t r0[32];
                 tmem_ld32(lane_addr + L::kO + col, r0);
                 tmem_ld_wait(r0);
@@ -584,7 +613,7 @@ __global__ void __launch_bounds__(Smem4<CH>::kThreads, 1)
                     lb[tok0 + (int64_t)dI * dst_stride_rows] = lse;
             }
             tc_fence_before();
-            named_bar_sync(1, 256 * CH);  // every thread has read flag_s / row_l
+            named_bar_sync(1, 128 * NG * CH);  // every thread has read flag_s / row_l
             if (threadIdx.x == 128) {
                 if (flagged) {  // recomputed by the running-max kernel after this launch
                     // one entry per work-list item (the fallback launch redoes every batch of it)
@@ -626,11 +655,11 @@ cudaError_t launch_attn_fixed_ref(const AttnArgs& a, const CUtensorMap& tq, cons
                                   const CUtensorMap& tv, int grid, const Fallback& fb,
                                   cudaStream_t s) {
     if (a.g.B != 128) return cudaErrorInvalidValue;
-    auto kern = sparse_attn_fixed_ref_kernel<kCH4>;
-    const int smem = Smem4<kCH4>::kBytes;
+    auto kern = sparse_attn_fixed_ref_kernel<kCH4, kNG4>;
+    const int smem = Smem4<kCH4, kNG4>::kBytes;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, Smem4<kCH4>::kThreads, smem, s>>>(a, tq, tk, tv, fb);
+    kern<<<grid, Smem4<kCH4, kNG4>::kThreads, smem, s>>>(a, tq, tk, tv, fb);
     return cudaGetLastError();
 }
 
