@@ -151,6 +151,7 @@ csa_status_t csa_debug_trace(void* buf, int32_t mode) {
     if (e == cudaSuccess) e = csa::set_attn2_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_attn3_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_attn4_trace(buf, mode);
+    if (e == cudaSuccess) e = csa::set_attn5_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_calib_trace(buf, mode);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyToSymbol");
     return ok();
@@ -499,7 +500,9 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
         csa::Fallback fb{base, base + 1, base + 1 + flag_words};
         e = cudaMemsetAsync(base, 0, 4 * (1 + flag_words), (cudaStream_t)stream);
         if (e == cudaSuccess)
-            e = csa::launch_attn_fixed_ref(a, tq, tk, tv, grid, fb, (cudaStream_t)stream);
+            e = std::getenv("CSA_ATTN5")
+                    ? csa::launch_attn_sepp(a, tq, tk, tv, grid, fb, (cudaStream_t)stream)
+                    : csa::launch_attn_fixed_ref(a, tq, tk, tv, grid, fb, (cudaStream_t)stream);
         if (e == cudaSuccess) {
             csa::AttnArgs re = a;
             re.work_list = fb.list;

@@ -1,0 +1,484 @@
+// attn5.cu -- a7 + a8 for block 128, head_dim 128: fixed reference max, one softmax group on
+// every tile, P in its own TMEM buffer.
+//
+// Same mathematics as attn4.cu (readings Q1, Q2, Q9, Q10, Q29:
+// each row's softmax shift is the max of its first kept tile; an overshoot beyond 2^56 flags the
+// item for the running-max fallback).  What changes is the pipeline:
+//   TMEM (512 columns): S0 [0,128) S1 [128,256) | O [256,384) | Q [384,448) | P [448,512)
+//   * all 16 softmax warps take every tile (4 column parts of 32 keys: 4 warps per SMSP keep the
+//     MUFU fed -- attn4.cu's two alternating groups leave 2 per SMSP on a tile);
+//   * S_j is released as soon as it is loaded (s_empty), P_j goes to the separate P buffer, so
+//     QK_{j+2} is issued while the softmax still works on tile j, and P.V_j waits only for P_j;
+//   * the issue order is QK_0, QK_1, then per tile j: QK_{j+2}, P.V_j; the producer loads the
+//     ring in that order (K0, K1, K2, V0, K3, V1, ...).
+// The softmax of tile j+1 starts as soon as it finished tile j (S_{j+1} is long ready), and its
+// P store waits only for P.V_j to have read P_j (p_empty).
+#include <cstdint>
+
+#include "attn_common.cuh"
+
+namespace csa {
+namespace {
+
+using namespace attn;
+
+constexpr int kItemSlots5 = 4;
+constexpr int kCH5 = 4;                          // column parts (32 keys each)
+constexpr float kGuard5 = 72057594037927936.0f;  // 2^56
+constexpr int kEmu5 = 1;  // element pairs p with (p & 7) >= 8 - kEmu5 -> polynomial exp2
+static __device__ unsigned long long* g_trace5;
+#ifdef CSA_ENABLE_TRACE
+#define TRACE5(slot, k, e)                                                                   \
+    do {                                                                                     \
+        if (g_trace5 != nullptr && blockIdx.x == 0 && (k) < 1024)                            \
+            g_trace5[((slot) * 1024 + (k)) * 8 + (e)] = clock64();                           \
+    } while (0)
+#else
+#define TRACE5(slot, k, e) \
+    do {                   \
+    } while (0)
+#endif
+
+struct Smem5 {
+    static constexpr int kThreads = 128 + 128 * kCH5;
+    static constexpr int kBox = 128 * 128;  // [128 rows][64 cols] bf16, SWIZZLE_128B
+    static constexpr int kTile = 2 * kBox;  // 128 x 128 bf16
+    static constexpr int kQOff = 0;
+    static constexpr int kKVOff = kTile;
+    static constexpr int kSlots = 5;
+    static constexpr int kBarOff = kKVOff + kSlots * kTile;
+    // q_full q_empty | kv_full[S] kv_empty[S] | s_full[2] s_empty[2] | p_full p_empty |
+    // o_full o_empty | item_full[4] item_empty[4]
+    static constexpr int kNumBars = 2 + 2 * kSlots + 4 + 2 + 2 + 2 * kItemSlots5;
+    static constexpr int kRowOff = kBarOff + kNumBars * 8;  // l[CH][128] | tile-0 max [CH][128]
+    static constexpr int kItemOff = kRowOff + 2 * kCH5 * 128 * 4;
+    static constexpr int kFlagOff = kItemOff + kItemSlots5 * 4;
+    static constexpr int kTmemPtrOff = kFlagOff + 16;
+    static constexpr int kBytes = kTmemPtrOff + 16;
+    static_assert(kBytes <= 232448, "smem");
+    static constexpr uint32_t kS = 0, kO = 256, kQ = 384, kP = 448;
+    static constexpr uint32_t kIdescQK = umma_idesc_bf16(128, 128, 0, 0);
+    static constexpr uint32_t kIdescPV = umma_idesc_bf16(128, 128, 0, 1);
+};
+
+__global__ void __launch_bounds__(Smem5::kThreads, 1)
+    sparse_attn_sepp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tq,
+                            const __grid_constant__ CUtensorMap tk,
+                            const __grid_constant__ CUtensorMap tv, const Fallback fb) {
+    using L = Smem5;
+    constexpr int BK = 128, D = 128, S = L::kSlots, CH = kCH5;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    if ((smem_u32(smem) & 1023u) != 0u) __trap();
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+    uint64_t* q_full = bars;
+    uint64_t* q_empty = bars + 1;
+    uint64_t* kv_full = bars + 2;
+    uint64_t* kv_empty = kv_full + S;
+    uint64_t* s_full = kv_empty + S;  // [buffer]
+    uint64_t* s_empty = s_full + 2;   // [buffer]
+    uint64_t* p_full = s_empty + 2;
+    uint64_t* p_empty = p_full + 1;
+    uint64_t* o_full = p_empty + 1;
+    uint64_t* o_empty = o_full + 1;
+    uint64_t* item_full = o_empty + 1;
+    uint64_t* item_empty = item_full + kItemSlots5;
+    float* row_l = reinterpret_cast<float*>(smem + L::kRowOff);  // [CH][128]
+    float* mx_s = row_l + CH * 128;                               // [CH][128]
+    volatile int32_t* item_slot = reinterpret_cast<int32_t*>(smem + L::kItemOff);
+    volatile int32_t* flag_s = reinterpret_cast<int32_t*>(smem + L::kFlagOff);
+    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + L::kTmemPtrOff);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
+        for (int i = 0; i < S; ++i) {
+            mbar_init(kv_full + i, 1);
+            mbar_init(kv_empty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(s_full + i, 1);
+            mbar_init(s_empty + i, 4 * CH);
+        }
+        mbar_init(p_full, 4 * CH);
+        mbar_init(p_empty, 1);
+        mbar_init(o_full, 1);
+        mbar_init(o_empty, 4 * CH);
+        for (int i = 0; i < kItemSlots5; ++i) {
+            mbar_init(item_full + i, 1);
+            mbar_init(item_empty + i, 1 + 4 * CH);  // MMA warp + the softmax warps
+        }
+        *flag_s = 0;
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_ptr);
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tq);
+        tma_prefetch(&tk);
+        tma_prefetch(&tv);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_ptr;
+    const int32_t n_items = (*a.n_work) * a.batch;
+    const Geo& g = a.g;
+
+    auto next_item = [&](int32_t local) -> int32_t {
+        const int s = local % kItemSlots5;
+        mbar_wait(item_full + s, (local / kItemSlots5) & 1);
+        const int32_t idx = item_slot[s];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(item_empty + s);
+        return idx;
+    };
+
+    if (warp < 4) {
+        set_maxnreg_dec56();
+        if (warp == 0) {
+            // ------------------------------------------------------------ scheduler + producer
+            const uint64_t pol_q = policy_evict_first();
+            const uint64_t pol_kv = policy_evict_last();
+            uint32_t ld = 0;
+            for (int32_t local = 0;; ++local) {
+                const int s = local % kItemSlots5;
+                mbar_wait(item_empty + s, ((local / kItemSlots5) & 1) ^ 1);
+                int32_t item = 0;
+                if (lane == 0) {
+                    item = a.sched ? (int32_t)atomicAdd(a.sched, 1u)
+                                   : (int32_t)blockIdx.x + local * (int32_t)gridDim.x;
+                    if (item >= n_items) item = -1;
+                    item_slot[s] = item;
+                    mbar_arrive(item_full + s);
+                }
+                item = __shfl_sync(0xffffffffu, item, 0);
+                if (item < 0) break;
+                const Item it = decode_item(a, item);
+                const TileList tl = tile_list(a, it);
+                uint8_t* qdst = smem + L::kQOff;
+                mbar_wait(q_empty, (local & 1) ^ 1);
+                if (it.kind == 0) {
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(q_full, L::kTile);
+                        tma_tile<D>(qdst, L::kBox, &tq, q_full, it.h, it.idx * BK, it.b, pol_q);
+                    }
+                    __syncwarp();
+                } else {
+                    const int32_t kA = a.plan.anchor_k[it.cell];
+                    const int32_t per_frame = kA * g.W;
+                    const int32_t n_anchor = g.F * per_frame;
+                    const __nv_bfloat16* qb_ptr =
+                        a.q + (int64_t)it.b * a.q_sb + (int64_t)it.h * a.q_sh;
+                    constexpr int kChunks = D / 8;
+                    for (int x = lane; x < 128 * kChunks; x += 32) {
+                        const int row = x / kChunks, chk = x % kChunks;
+                        const int32_t gi = it.idx * 128 + row;
+                        uint4 val = make_uint4(0u, 0u, 0u, 0u);
+                        if (gi < n_anchor) {
+                            const int32_t f = gi / per_frame;
+                            const int32_t m = (gi / g.W) % kA;
+                            const int32_t j = gi % g.W;
+                            const int64_t tok = (int64_t)f * g.H * g.W +
+                                                (int64_t)anchor_row(g.H, kA, m) * g.W + j;
+                            val = *reinterpret_cast<const uint4*>(qb_ptr + tok * a.q_sn + chk * 8);
+                        }
+                        *reinterpret_cast<uint4*>(qdst + (chk >> 3) * L::kBox +
+                                                  sw128_offset(row, chk & 7)) = val;
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(q_full);
+                }
+                // ring order = issue order: K0, K1, then per step s >= 2: K_s, V_{s-2}; V tail
+                auto load = [&](int kv, int32_t j) {
+                    const uint32_t slot = ld % S, ph = (ld / S) & 1;
+                    ++ld;
+                    const int32_t c = tl.at(j);
+                    mbar_wait(kv_empty + slot, ph ^ 1);
+                    if (elect_one()) {
+                        uint8_t* dst = smem + L::kKVOff + slot * L::kTile;
+                        mbar_arrive_expect_tx(kv_full + slot, L::kTile);
+                        tma_tile<D>(dst, L::kBox, kv == 0 ? &tk : &tv, kv_full + slot, it.h,
+                                    c * BK, it.b, pol_kv);
+                    }
+                    __syncwarp();
+                };
+                for (int32_t step = 0; step < tl.n + 2; ++step) {
+                    if (step < tl.n) load(0, step);
+                    if (step >= 2) load(1, step - 2);
+                }
+            }
+        } else if (warp == 1) {
+            // ------------------------------------------------------------------ MMA issuer
+            uint32_t cons = 0, sis0 = 0, sis1 = 0, pcnt = 0, tiles = 0;
+            const uint32_t q_base = smem_u32(smem + L::kQOff);
+            const uint32_t kv_base = smem_u32(smem + L::kKVOff);
+            for (int32_t local = 0;; ++local) {
+                const int32_t item = next_item(local);
+                if (item < 0) break;
+                const Item it = decode_item(a, item);
+                const TileList tl = tile_list(a, it);
+                mbar_wait(q_full, local & 1);
+                tc_fence_after();
+                if (elect_one()) {  // Q -> TMEM, in order with this thread's MMAs
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk)
+                        tmem_cp_128x256b(tmem + L::kQ + kk * 8,
+                                         umma_desc_sw128(q_base + (kk >> 2) * L::kBox +
+                                                             (kk & 3) * 32, 16, 1024));
+                    mma_commit(q_empty);
+                    if (tl.n == 0) mma_commit(o_full);  // corrupt plan (empty row): no tiles
+                }
+                __syncwarp();
+                if (tl.n == 0) continue;
+                auto issue_qk = [&](int32_t j) {
+                    const uint32_t b = (uint32_t)j & 1u;
+                    const uint32_t use = b ? sis1++ : sis0++;
+                    TRACE5(2, tiles + (uint32_t)j, 0);
+                    mbar_wait(s_empty + b, (use & 1) ^ 1);  // softmax loaded S_{j-2}
+                    const uint32_t slot = cons % S, ph = (cons / S) & 1;
+                    ++cons;
+                    mbar_wait(kv_full + slot, ph);
+                    TRACE5(2, tiles + (uint32_t)j, 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t kb = kv_base + slot * L::kTile;
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk)
+                            mma_ts(tmem + L::kS + b * BK, tmem + L::kQ + kk * 8,
+                                   umma_desc_sw128(kb + (kk >> 2) * L::kBox + (kk & 3) * 32, 16,
+                                                   1024),
+                                   L::kIdescQK, kk > 0 ? 1u : 0u);
+                        mma_commit(s_full + b);
+                        mma_commit(kv_empty + slot);
+                    }
+                    __syncwarp();
+                };
+                issue_qk(0);
+                if (tl.n > 1) issue_qk(1);
+                for (int32_t j = 0; j < tl.n; ++j) {
+                    if (j + 2 < tl.n) issue_qk(j + 2);
+                    TRACE5(3, tiles + (uint32_t)j, 0);
+                    mbar_wait(p_full, pcnt & 1);
+                    ++pcnt;
+                    TRACE5(3, tiles + (uint32_t)j, 1);
+                    if (j == 0) mbar_wait(o_empty, (local & 1) ^ 1);  // last item's epilogue
+                    const uint32_t slot = cons % S, ph = (cons / S) & 1;
+                    ++cons;
+                    mbar_wait(kv_full + slot, ph);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t vb = kv_base + slot * L::kTile;
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk)
+                            mma_ts(tmem + L::kO, tmem + L::kP + kk * 8,
+                                   umma_desc_sw128(vb + kk * 16 * 128, L::kBox, 1024),
+                                   L::kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
+                        mma_commit(p_empty);
+                        mma_commit(kv_empty + slot);
+                    }
+                    __syncwarp();
+                    TRACE5(3, tiles + (uint32_t)j, 2);
+                }
+                tiles += (uint32_t)tl.n;
+                if (elect_one()) mma_commit(o_full);
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 104;" ::: "memory");
+        // ------------------------------------------------------------------ softmax (16 warps)
+        constexpr int NC = BK / CH;  // 32 key columns per thread
+        const int ch = (int)(warp - 4) >> 2;
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+        const float sl2 = a.scale_log2;
+        const uint64_t sl2x2 = f2(sl2, sl2);
+        const int32_t tail_valid = g.N - (g.NB - 1) * BK;
+        uint32_t sc0 = 0, sc1 = 0, pst = 0, tbase = 0;
+        const bool tr = quarter == 0 && ch == 0 && lane == 0;
+        (void)tr;
+        for (int32_t local = 0;; ++local) {
+            const int32_t item = next_item(local);
+            if (item < 0) break;
+            const Item it = decode_item(a, item);
+            const TileList tl = tile_list(a, it);
+            const bool last_ragged = tail_valid < BK && tl.n > 0 && tl.at(tl.n - 1) == g.NB - 1;
+            float m_ref = 0.0f, l_run = 0.0f;
+            bool bad = false;
+            for (int32_t j = 0; j < tl.n; ++j) {
+                const uint32_t b = (uint32_t)j & 1u;
+                const uint32_t use = b ? sc1++ : sc0++;
+                if (tr) TRACE5(0, tbase + (uint32_t)j, 0);
+                mbar_wait(s_full + b, use & 1);
+                if (tr) TRACE5(0, tbase + (uint32_t)j, 1);
+                tc_fence_after();
+                uint32_t r[NC];
+                tmem_ld32(lane_addr + L::kS + b * BK + ch * NC, r);
+                tmem_ld_wait(r);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(s_empty + b);  // S_j may be overwritten (QK_{j+2})
+                if (tr) TRACE5(0, tbase + (uint32_t)j, 2);
+                if (last_ragged && j == tl.n - 1) {
+#pragma unroll
+                    for (int x = 0; x < NC; ++x)
+                        if (ch * NC + x >= tail_valid) r[x] = 0xff800000u;  // keys >= N
+                }
+                if (j == 0) {  // the row's reference: the max of its first kept tile
+                    float mc[8];
+#pragma unroll
+                    for (int q8 = 0; q8 < 8; ++q8)
+                        mc[q8] = fmax3(__uint_as_float(r[q8]), __uint_as_float(r[q8 + 8]),
+                                       fmaxf(__uint_as_float(r[q8 + 16]),
+                                             __uint_as_float(r[q8 + 24])));
+                    m_ref = fmaxf(fmax3(mc[0], mc[1], mc[2]),
+                                  fmaxf(fmax3(mc[3], mc[4], mc[5]), fmaxf(mc[6], mc[7]))) * sl2;
+                    mx_s[ch * 128 + row] = m_ref;
+                    named_bar_sync(2, 128 * CH);
+                    m_ref = fmaxf(fmaxf(mx_s[row], mx_s[128 + row]),
+                                  fmaxf(mx_s[256 + row], mx_s[384 + row]));
+                }
+                const uint64_t negm = f2(-m_ref, -m_ref);
+                uint64_t acc[4] = {0, 0, 0, 0};
+                uint32_t pk[16];
+#pragma unroll
+                for (int x = 0; x < NC; x += 2) {
+                    const uint64_t t = ffma2(pk2(r[x], r[x + 1]), sl2x2, negm);
+                    uint64_t p;
+                    if (((x / 2) & 7) >= 8 - kEmu5) {
+                        p = exp2_poly2(t);
+                    } else {
+                        p = f2(ex2_approx(lo_f(t)), ex2_approx(hi_f(t)));
+                    }
+                    acc[(x / 2) & 3] = fadd2(acc[(x / 2) & 3], p);
+                    pk[x / 2] = pack_bf16(lo_f(p), hi_f(p));
+                }
+                const uint64_t acc2 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+                const float lsum = lo_f(acc2) + hi_f(acc2);
+                bad |= !(lsum <= kGuard5);  // also catches inf / NaN
+                l_run += lsum;
+                if (tr) TRACE5(0, tbase + (uint32_t)j, 3);
+                mbar_wait(p_empty, (pst & 1) ^ 1);  // P.V_{j-1} has read the P buffer
+                ++pst;
+                tc_fence_after();
+                tmem_st16(lane_addr + L::kP + ch * (NC / 2), pk);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(p_full);
+                if (tr) TRACE5(0, tbase + (uint32_t)j, 4);
+            }
+            tbase += (uint32_t)tl.n;
+            // -------------------------------------------------------------- epilogue
+            if (__any_sync(0xffffffffu, bad) && lane == 0) *flag_s = 1;
+            mbar_wait(o_full, local & 1);
+            tc_fence_after();
+            row_l[ch * 128 + row] = l_run;
+            named_bar_sync(1, 128 * CH);
+            const float Lsum = (row_l[row] + row_l[128 + row]) + (row_l[256 + row] + row_l[384 + row]);
+            const float inv = Lsum > 0.0f ? 1.0f / Lsum : 0.0f;
+            const bool flagged = *flag_s != 0;
+            int64_t tok0 = -1;
+            int32_t n_dst = 0, dst_stride_rows = 0;
+            if (it.kind == 0) {
+                const int64_t t = (int64_t)it.idx * BK + row;
+                if (t < g.N) {
+                    tok0 = t;
+                    n_dst = 1;
+                }
+            } else {
+                const int32_t kA = a.plan.anchor_k[it.cell];
+                const int32_t per_frame = kA * g.W;
+                const int32_t gi = it.idx * 128 + row;
+                if (gi < g.F * per_frame) {
+                    const int32_t f = gi / per_frame, m = (gi / g.W) % kA, jj = gi % g.W;
+                    const int32_t am = anchor_row(g.H, kA, m);
+                    const int32_t lo = m == 0 ? 0 : (anchor_row(g.H, kA, m - 1) + am) / 2 + 1;
+                    const int32_t hi =
+                        m == kA - 1 ? g.H : (am + anchor_row(g.H, kA, m + 1)) / 2 + 1;
+                    tok0 = (int64_t)f * g.H * g.W + (int64_t)lo * g.W + jj;
+                    n_dst = hi - lo;
+                    dst_stride_rows = g.W;
+                }
+            }
+            __nv_bfloat16* obase = a.o + (int64_t)it.b * a.o_sb + (int64_t)it.h * a.o_sh;
+            const uint64_t inv2 = f2(inv, inv);
+            {
+                const int col = ch * (D / CH);
+                uint32_t r0[32];
+                tmem_ld32(lane_addr + L::kO + col, r0);
+                tmem_ld_wait(r0);
+                uint32_t packed[16];
+#pragma unroll
+                for (int x = 0; x < 32; x += 2) {
+                    const uint64_t v = fmul2(pk2(r0[x], r0[x + 1]), inv2);
+                    packed[x / 2] = pack_bf16(lo_f(v), hi_f(v));
+                }
+                for (int32_t dI = 0; dI < n_dst; ++dI) {
+                    uint4* dst = reinterpret_cast<uint4*>(
+                        obase + (tok0 + (int64_t)dI * dst_stride_rows) * a.o_sn + col);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v)
+                        dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2],
+                                            packed[4 * v + 3]);
+                }
+            }
+            if (ch == 0 && a.lse_out != nullptr) {
+                const float lse = (m_ref + __log2f(Lsum)) * 0.69314718055994531f;
+                float* lb = a.lse_out + ((int64_t)it.b * a.n_heads + it.h) * (int64_t)g.N;
+                for (int32_t dI = 0; dI < n_dst; ++dI)
+                    lb[tok0 + (int64_t)dI * dst_stride_rows] = lse;
+            }
+            tc_fence_before();
+            named_bar_sync(1, 128 * CH);  // every thread has read flag_s / row_l
+            if (threadIdx.x == 128) {
+                if (flagged) {  // recomputed by the running-max kernel after this launch
+                    const uint32_t w = (uint32_t)(item / a.batch), bit = 1u << (w & 31u);
+                    if ((atomicOr(fb.flags + (w >> 5), bit) & bit) == 0u)
+                        fb.list[atomicAdd(fb.count, 1u)] = a.work_list[w];
+                }
+                *flag_s = 0;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(o_empty);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+    if (threadIdx.x == 0 && a.sched != nullptr) {
+        __threadfence();
+        if (atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
+            atomicExch(a.sched, 0u);
+            atomicExch(a.sched + 1, 0u);
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t set_attn5_trace(void* buf, int mode) {
+    (void)mode;
+    unsigned long long* p = static_cast<unsigned long long*>(buf);
+    return cudaMemcpyToSymbol(g_trace5, &p, sizeof(p));
+}
+
+cudaError_t launch_attn_sepp(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, int grid, const Fallback& fb,
+                             cudaStream_t s) {
+    if (a.g.B != 128 || a.head_dim != 128) return cudaErrorInvalidValue;
+    const int smem = Smem5::kBytes;
+    cudaError_t e = cudaFuncSetAttribute(sparse_attn_sepp_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    sparse_attn_sepp_kernel<<<grid, Smem5::kThreads, smem, s>>>(a, tq, tk, tv, fb);
+    return cudaGetLastError();
+}
+
+}  // namespace csa

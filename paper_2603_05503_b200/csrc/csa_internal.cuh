@@ -147,6 +147,11 @@ struct Fallback {
 cudaError_t launch_attn_fixed_ref(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
                                   const CUtensorMap& tv, int grid, const Fallback& fb,
                                   cudaStream_t s);
+// Block 128, head_dim 128, one softmax group on every tile, P in its own TMEM buffer (attn5.cu).
+cudaError_t set_attn5_trace(void* buf, int mode);
+cudaError_t launch_attn_sepp(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, int grid, const Fallback& fb,
+                             cudaStream_t s);
 // Non-square blocks B_q = 128 x B_kv (attn_rect.cu), head_dim 128.  mode 0: fixed reference
 // max (first kept tile), overshooting items appended to fb; mode 1: exact row max of every item
 // of the (fallback) list, parked in the item's first output row; mode 2: recompute the list
