@@ -26,6 +26,38 @@ constexpr int kItemSlots5 = 4;
 constexpr int kCH5 = 4;                          // column parts (32 keys each)
 constexpr float kGuard5 = 72057594037927936.0f;  // 2^56
 constexpr int kEmu5 = 1;  // element pairs p with (p & 7) >= 8 - kEmu5 -> polynomial exp2
+// Two MMA issuer warps (warp 1: Q copy + QK, warp 3: P.V): every mbarrier wait costs ~140
+// cycles even when its phase is already complete (scripts/mbar_micro.cu) and every 8-MMA batch
+// blocks its issuing thread ~600 cycles; one issuer serialises all of it per tile.
+#ifndef CSA_ATTN5_SPLIT_ISSUE
+#define CSA_ATTN5_SPLIT_ISSUE 1
+#endif
+constexpr bool kSplitIssue5 = CSA_ATTN5_SPLIT_ISSUE != 0;
+
+// Ring positions (per item, n kept tiles) of the producer order K0, K1, then per step s >= 2:
+// K_s (s < n), V_{s-2}: K_j after j K's and max(0, j-2) V's; V_j after min(j+2, n-1)+1 K's and
+// j V's.
+__device__ __forceinline__ uint32_t kpos5(int32_t j) { return (uint32_t)(j + (j > 2 ? j - 2 : 0)); }
+__device__ __forceinline__ uint32_t vpos5(int32_t j, int32_t n) {
+    return (uint32_t)((j + 2 < n - 1 ? j + 2 : n - 1) + 1 + j);
+}
+// Early barrier probe: test_wait is non-blocking; issued as soon as the next wait's phase is
+// known, its ~140-cycle round trip overlaps the exponentials, and the blocking wait is skipped
+// when the phase had already completed (the common case for S and for the P buffer).
+#ifndef CSA_ATTN5_PROBE
+#define CSA_ATTN5_PROBE 1
+#endif
+__device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok;
+}
 static __device__ unsigned long long* g_trace5;
 #ifdef CSA_ENABLE_TRACE
 #define TRACE5(slot, k, e)                                                                   \
@@ -106,7 +138,7 @@ __global__ void __launch_bounds__(Smem5::kThreads, 1)
         mbar_init(o_empty, 4 * CH);
         for (int i = 0; i < kItemSlots5; ++i) {
             mbar_init(item_full + i, 1);
-            mbar_init(item_empty + i, 1 + 4 * CH);  // MMA warp + the softmax warps
+            mbar_init(item_empty + i, (kSplitIssue5 ? 2 : 1) + 4 * CH);  // issuers + softmax
         }
         *flag_s = 0;
         fence_barrier_init();
@@ -208,7 +240,94 @@ __global__ void __launch_bounds__(Smem5::kThreads, 1)
                     if (step >= 2) load(1, step - 2);
                 }
             }
-        } else if (warp == 1) {
+        } else if (kSplitIssue5 && warp == 1) {
+            // ------------------------------------------------------- QK issuer (Q copy, S_j)
+            uint32_t base = 0, sis0 = 0, sis1 = 0, tiles = 0;
+            const uint32_t q_base = smem_u32(smem + L::kQOff);
+            const uint32_t kv_base = smem_u32(smem + L::kKVOff);
+            for (int32_t local = 0;; ++local) {
+                const int32_t item = next_item(local);
+                if (item < 0) break;
+                const Item it = decode_item(a, item);
+                const TileList tl = tile_list(a, it);
+                mbar_wait(q_full, local & 1);
+                tc_fence_after();
+                if (elect_one()) {  // Q -> TMEM, in order with this thread's MMAs
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk)
+                        tmem_cp_128x256b(tmem + L::kQ + kk * 8,
+                                         umma_desc_sw128(q_base + (kk >> 2) * L::kBox +
+                                                             (kk & 3) * 32, 16, 1024));
+                    mma_commit(q_empty);
+                }
+                __syncwarp();
+                for (int32_t j = 0; j < tl.n; ++j) {
+                    const uint32_t b = (uint32_t)j & 1u;
+                    const uint32_t use = b ? sis1++ : sis0++;
+                    TRACE5(2, tiles + (uint32_t)j, 0);
+                    mbar_wait(s_empty + b, (use & 1) ^ 1);  // softmax loaded S_{j-2}
+                    const uint32_t pos = base + kpos5(j), slot = pos % S, ph = (pos / S) & 1;
+                    mbar_wait(kv_full + slot, ph);
+                    TRACE5(2, tiles + (uint32_t)j, 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t kb = kv_base + slot * L::kTile;
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk)
+                            mma_ts(tmem + L::kS + b * BK, tmem + L::kQ + kk * 8,
+                                   umma_desc_sw128(kb + (kk >> 2) * L::kBox + (kk & 3) * 32, 16,
+                                                   1024),
+                                   L::kIdescQK, kk > 0 ? 1u : 0u);
+                        mma_commit(s_full + b);
+                        mma_commit(kv_empty + slot);
+                    }
+                    __syncwarp();
+                }
+                base += 2u * (uint32_t)tl.n;
+                tiles += (uint32_t)tl.n;
+            }
+        } else if (kSplitIssue5 && warp == 3) {
+            // ------------------------------------------------------------- P.V issuer (O)
+            uint32_t base = 0, pcnt = 0, tiles = 0;
+            const uint32_t kv_base = smem_u32(smem + L::kKVOff);
+            for (int32_t local = 0;; ++local) {
+                const int32_t item = next_item(local);
+                if (item < 0) break;
+                const Item it = decode_item(a, item);
+                const TileList tl = tile_list(a, it);
+                if (tl.n == 0) {  // corrupt plan (empty row): no tiles
+                    if (elect_one()) mma_commit(o_full);
+                    __syncwarp();
+                    continue;
+                }
+                for (int32_t j = 0; j < tl.n; ++j) {
+                    TRACE5(3, tiles + (uint32_t)j, 0);
+                    mbar_wait(p_full, pcnt & 1);
+                    ++pcnt;
+                    TRACE5(3, tiles + (uint32_t)j, 1);
+                    if (j == 0) mbar_wait(o_empty, (local & 1) ^ 1);  // last item's epilogue
+                    const uint32_t pos = base + vpos5(j, tl.n), slot = pos % S, ph = (pos / S) & 1;
+                    mbar_wait(kv_full + slot, ph);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t vb = kv_base + slot * L::kTile;
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk)
+                            mma_ts(tmem + L::kO, tmem + L::kP + kk * 8,
+                                   umma_desc_sw128(vb + kk * 16 * 128, L::kBox, 1024),
+                                   L::kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
+                        mma_commit(p_empty);
+                        mma_commit(kv_empty + slot);
+                    }
+                    __syncwarp();
+                    TRACE5(3, tiles + (uint32_t)j, 2);
+                }
+                base += 2u * (uint32_t)tl.n;
+                tiles += (uint32_t)tl.n;
+                if (elect_one()) mma_commit(o_full);
+                __syncwarp();
+            }
+        } else if (!kSplitIssue5 && warp == 1) {
             // ------------------------------------------------------------------ MMA issuer
             uint32_t cons = 0, sis0 = 0, sis1 = 0, pcnt = 0, tiles = 0;
             const uint32_t q_base = smem_u32(smem + L::kQOff);
@@ -308,11 +427,12 @@ __global__ void __launch_bounds__(Smem5::kThreads, 1)
             const bool last_ragged = tail_valid < BK && tl.n > 0 && tl.at(tl.n - 1) == g.NB - 1;
             float m_ref = 0.0f, l_run = 0.0f;
             bool bad = false;
+            uint32_t s_ready = 0;  // probe result for the next tile's S (CSA_ATTN5_PROBE)
             for (int32_t j = 0; j < tl.n; ++j) {
                 const uint32_t b = (uint32_t)j & 1u;
                 const uint32_t use = b ? sc1++ : sc0++;
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 0);
-                mbar_wait(s_full + b, use & 1);
+                if (!s_ready) mbar_wait(s_full + b, use & 1);
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 1);
                 tc_fence_after();
                 uint32_t r[NC];
@@ -321,6 +441,11 @@ __global__ void __launch_bounds__(Smem5::kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(s_empty + b);  // S_j may be overwritten (QK_{j+2})
+                // probes: the P buffer (P.V_{j-1} done) and the next tile's S, resolved later
+                const uint32_t p_ready = CSA_ATTN5_PROBE ? mbar_test(p_empty, (pst & 1) ^ 1) : 0u;
+                s_ready = (CSA_ATTN5_PROBE && j + 1 < tl.n)
+                              ? mbar_test(s_full + (b ^ 1u), (b ? sc0 : sc1) & 1)
+                              : 0u;
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 2);
                 if (last_ragged && j == tl.n - 1) {
 #pragma unroll
@@ -361,7 +486,7 @@ __global__ void __launch_bounds__(Smem5::kThreads, 1)
                 bad |= !(lsum <= kGuard5);  // also catches inf / NaN
                 l_run += lsum;
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 3);
-                mbar_wait(p_empty, (pst & 1) ^ 1);  // P.V_{j-1} has read the P buffer
+                if (!p_ready) mbar_wait(p_empty, (pst & 1) ^ 1);  // P.V_{j-1} read the P buffer
                 ++pst;
                 tc_fence_after();
                 tmem_st16(lane_addr + L::kP + ch * (NC / 2), pk);
