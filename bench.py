@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="csa", choices=["csa", "reference"])
-    ap.add_argument("--config", default="wan720", choices=["wan480", "wan720", "mochi"])
+    ap.add_argument("--config", default="wan720", choices=["wan480", "wan720", "mochi", "mochi85"])
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--rep-heads", type=int, default=4, help="REPETITIVE (anchor) heads, k=5")
     ap.add_argument("--no-extras", action="store_true", help="skip dense/SDPA/e2e/cpu legs")
