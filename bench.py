@@ -543,7 +543,7 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
 
     def e2e_step():
         if B == 1:
-            csa.sparse_attn_fwd_host(hq, hk, hv, plan, ho, heads_per_chunk=8, device=dev)
+            csa.sparse_attn_fwd_host(hq, hk, hv, plan, ho, heads_per_chunk=2, device=dev)
         else:  # batch > 1: whole-tensor copies around the device call
             dq, dk, dv = (t.to(dev, non_blocking=True) for t in (hq, hk, hv))
             ho.copy_(csa.sparse_attn_fwd(dq, dk, dv, plan, work, out=out), non_blocking=True)

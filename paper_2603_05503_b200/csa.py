@@ -288,7 +288,7 @@ _HOST_BUFS: dict = {}
 
 
 def sparse_attn_fwd_host(q_h: torch.Tensor, k_h: torch.Tensor, v_h: torch.Tensor, plan: Plan,
-                         out_h: torch.Tensor, heads_per_chunk: int = 8,
+                         out_h: torch.Tensor, heads_per_chunk: int = 2,
                          device: torch.device | str = "cuda") -> torch.Tensor:
     """One layer from pinned host Q, K, V [1, N, H, d] to pinned host O, streamed by head chunks:
     H2D of chunk c+1 (csa_copy_heads on a copy stream) overlaps the attention of chunk c (its
