@@ -72,6 +72,10 @@ def main():
                          "paper's per-size sparsity")
     ap.add_argument("--prompts", type=int, default=4)
     ap.add_argument("--d", type=int, default=0, help="head_dim (default: the config's, 128)")
+    ap.add_argument("--config", default="wan480", choices=["wan480", "wan720"])
+    ap.add_argument("--sparsity", type=float, default=0.0,
+                    help="generator-S sparsity for every block size (default: the paper's "
+                         "per-size Table values, which are for Wan 480p)")
     args = ap.parse_args()
     peak = 1685.2
     try:
@@ -79,7 +83,7 @@ def main():
             peak = json.load(fh).get("bf16_tflops") or peak
     except OSError:
         pass
-    base = inputs.CONFIGS["wan480"]
+    base = inputs.CONFIGS[args.config]
     H, d = base.heads, args.d or base.d
     q, k, v = inputs.qkv(1, base.layout.N, H, d, seed=11, device="cuda")
     out = torch.empty_like(q)
@@ -105,7 +109,7 @@ def main():
             masks = np.unpackbits(bits.view(np.uint8), bitorder="little").reshape(
                 H, lay.NB, w32 * 32)[:, :, :lay.NBK]
         else:
-            masks = inputs.synthetic_masks(lay, H, PAPER[bkv], seed=0)
+            masks = inputs.synthetic_masks(lay, H, args.sparsity or PAPER[bkv], seed=0)
             counts = torch.from_numpy((masks.astype(np.uint16) * np.uint16(64)).reshape(-1)
                                       .view(np.int16)).cuda().view(torch.uint16)
             plan = csa.compile_plan(lay, counts, 32)
@@ -150,7 +154,8 @@ def main():
             print(json.dumps(row), flush=True)
     if args.json_out:
         with open(args.json_out, "w") as fh:
-            json.dump({"workload": "wan480 single attention layer, 40 heads, d 128, N 32760, " + (
+            json.dump({"workload": f"{args.config} single attention layer, 40 heads, d {d}, "
+                                   f"N {base.layout.N}, " + (
                            f"masks calibrated on each grid ({args.prompts} generator-G prompts, "
                            "eps(25/50), rho 0.5)" if args.calibrated else
                            "generator-S masks at the paper's per-block-size sparsity"),
