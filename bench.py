@@ -448,14 +448,16 @@ def attention_kernel_name(lay, d):
     if lay.B == 128 and d == 128 and not os.environ.get("CSA_ATTN_V3"):
         if os.environ.get("CSA_ATTN_RUNNING_MAX"):
             return "sparse_attn_q_tmem_kernel (attn3.cu)"
-        return "sparse_attn_fixed_ref_kernel (attn4.cu)"
+        if os.environ.get("CSA_ATTN4"):
+            return "sparse_attn_fixed_ref_kernel (attn4.cu)"
+        return "sparse_attn_sepp_kernel (attn5.cu)"
     return f"sparse_attn_kernel<{lay.B},{d}> (attn.cu)"
 
 
 def launches_per_call(lay, d):
     """Our kernels per csa_sparse_attn_fwd call: the fixed-reference kernel is followed by the
     running-max kernel over its (normally empty) fallback list."""
-    return 2 if attention_kernel_name(lay, d).endswith("(attn4.cu)") else 1
+    return 2 if attention_kernel_name(lay, d).endswith(("(attn4.cu)", "(attn5.cu)")) else 1
 
 
 def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_all, dense_flop,

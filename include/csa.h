@@ -258,8 +258,8 @@ CSA_API csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan,
  * NULL -> static round-robin assignment of work items to CTAs (pair items are always assigned
  * statically).
  * Kernels (block 128, head_dim 128, single items): with a workspace, the fixed-reference kernel
- * (attn4.cu: each row's softmax shift is the max of its first kept tile, P:647-653 is
- * shift-invariant); an item whose later scores exceed that shift by more than 2^56 in exp2 terms
+ * (attn5.cu -- attn4.cu with env CSA_ATTN4 -- each row's softmax shift is the max of its first
+ * kept tile, P:647-653 is shift-invariant); an item whose later scores exceed that shift by more than 2^56 in exp2 terms
  * is listed in bytes [256, size) (rewritten every launch, needs max_work <= n_heads * N_B) and
  * recomputed on the same stream by the running-max kernel (attn3.cu).  Without a workspace the
  * running-max kernel runs the whole launch.  Each mode is deterministic; the two agree within

@@ -487,8 +487,8 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
             e = csa::launch_attn_rect(re, tq, tk, tv, di.sms, fb, mode, (cudaStream_t)stream);
     } else if (g.B == 128 && head_dim == 128 && workspace != nullptr &&
                !std::getenv("CSA_ATTN_RUNNING_MAX") && !std::getenv("CSA_ATTN_V3")) {
-        // production (attn4.cu): fixed per-row reference max, two tiles in flight; items whose
-        // later scores overshoot it are recomputed right after by the running-max kernel
+        // production (attn5.cu; attn4.cu with CSA_ATTN4): fixed per-row reference max; items
+        // whose later scores overshoot it are recomputed right after by the running-max kernel
         // (attn3.cu) from the fallback list in the workspace (256 bytes past the counters).
         // Without a workspace (static assignment) the running-max kernel does the whole launch.
         const size_t items = (size_t)n_heads * (size_t)g.NB;
@@ -500,9 +500,9 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
         csa::Fallback fb{base, base + 1, base + 1 + flag_words};
         e = cudaMemsetAsync(base, 0, 4 * (1 + flag_words), (cudaStream_t)stream);
         if (e == cudaSuccess)
-            e = std::getenv("CSA_ATTN5")
-                    ? csa::launch_attn_sepp(a, tq, tk, tv, grid, fb, (cudaStream_t)stream)
-                    : csa::launch_attn_fixed_ref(a, tq, tk, tv, grid, fb, (cudaStream_t)stream);
+            e = std::getenv("CSA_ATTN4")  // A/B: the two-group fixed-reference kernel
+                    ? csa::launch_attn_fixed_ref(a, tq, tk, tv, grid, fb, (cudaStream_t)stream)
+                    : csa::launch_attn_sepp(a, tq, tk, tv, grid, fb, (cudaStream_t)stream);
         if (e == cudaSuccess) {
             csa::AttnArgs re = a;
             re.work_list = fb.list;

@@ -58,6 +58,12 @@ __device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok;
 }
+// Prefetch (off: the second register set spills at the 104-register softmax budget, measured
+// 1077 vs 1161 TF/s): with the probe seeing S_{j+1} complete, its TMEM load is issued before tile j's P
+// store / publish (two register sets alternate between tiles).
+#ifndef CSA_ATTN5_PREFETCH
+#define CSA_ATTN5_PREFETCH 0
+#endif
 static __device__ unsigned long long* g_trace5;
 #ifdef CSA_ENABLE_TRACE
 #define TRACE5(slot, k, e)                                                                   \
@@ -166,7 +172,7 @@ __global__ void __launch_bounds__(Smem5::kThreads, 1)
     };
 
     if (warp < 4) {
-        set_maxnreg_dec56();
+        set_maxnreg_dec56();  // 4 x 56 + 16 x 104 fits the 640 x 96 launch allocation
         if (warp == 0) {
             // ------------------------------------------------------------ scheduler + producer
             const uint64_t pol_q = policy_evict_first();
@@ -428,15 +434,18 @@ __global__ void __launch_bounds__(Smem5::kThreads, 1)
             float m_ref = 0.0f, l_run = 0.0f;
             bool bad = false;
             uint32_t s_ready = 0;  // probe result for the next tile's S (CSA_ATTN5_PROBE)
-            for (int32_t j = 0; j < tl.n; ++j) {
+            bool inflight = false; // the next tile's S already loading into the other buffer
+            uint32_t rA[NC], rB[NC];
+            auto tile = [&](uint32_t (&r)[NC], uint32_t (&rn)[NC], int32_t j) {
                 const uint32_t b = (uint32_t)j & 1u;
                 const uint32_t use = b ? sc1++ : sc0++;
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 0);
-                if (!s_ready) mbar_wait(s_full + b, use & 1);
+                if (!inflight) {
+                    if (!s_ready) mbar_wait(s_full + b, use & 1);
+                    tc_fence_after();
+                    tmem_ld32(lane_addr + L::kS + b * BK + ch * NC, r);
+                }
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 1);
-                tc_fence_after();
-                uint32_t r[NC];
-                tmem_ld32(lane_addr + L::kS + b * BK + ch * NC, r);
                 tmem_ld_wait(r);
                 tc_fence_before();
                 __syncwarp();
@@ -486,6 +495,13 @@ __global__ void __launch_bounds__(Smem5::kThreads, 1)
                 bad |= !(lsum <= kGuard5);  // also catches inf / NaN
                 l_run += lsum;
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 3);
+                // prefetch: S_{j+1} is complete (probe) -> start loading it now; its latency
+                // overlaps the P store / publish of tile j (warp-uniform decision)
+                inflight = CSA_ATTN5_PREFETCH && __all_sync(0xffffffffu, s_ready != 0u);
+                if (inflight) {
+                    tc_fence_after();
+                    tmem_ld32(lane_addr + L::kS + (b ^ 1u) * BK + ch * NC, rn);
+                }
                 if (!p_ready) mbar_wait(p_empty, (pst & 1) ^ 1);  // P.V_{j-1} read the P buffer
                 ++pst;
                 tc_fence_after();
@@ -495,6 +511,10 @@ __global__ void __launch_bounds__(Smem5::kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(p_full);
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 4);
+            };
+            for (int32_t j = 0; j < tl.n; j += 2) {
+                tile(rA, rB, j);
+                if (j + 1 < tl.n) tile(rB, rA, j + 1);
             }
             tbase += (uint32_t)tl.n;
             // -------------------------------------------------------------- epilogue

@@ -12,6 +12,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2603_05503_b200 import csa, inputs  # noqa: E402
 
+os.environ["CSA_ATTN4"] = "1"  # attn5.cu is the default path
+
 cfg = inputs.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "wan720"]
 lay = cfg.layout
 masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity or 0.69, seed=0)

@@ -152,7 +152,7 @@ def run_attention(csa, lay, q, k, v, masks=None, rep=None, anchor_k=2, order=2, 
 
 
 def fallback_count(csa, q):
-    """Items the fixed-reference kernel (attn4.cu) handed to the running-max kernel in the last
+    """Items the fixed-reference kernel (attn5.cu / attn4.cu) handed to the running-max kernel in the last
     dynamic launch on q's device: uint32 at byte 256 of the attention workspace (csa.h)."""
     ws = csa._sched_workspace(q.device, 0)  # current stream: the one the test launched on
     return int(ws[256:260].view(torch.int32).item())
@@ -188,7 +188,7 @@ def test_attention_tiny_masks(csa, name):
         assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 1e-3, cname
 
 
-@pytest.mark.parametrize("variant", [{}, {"CSA_ATTN_RUNNING_MAX": "1"},
+@pytest.mark.parametrize("variant", [{}, {"CSA_ATTN4": "1"}, {"CSA_ATTN_RUNNING_MAX": "1"},
                                      {"CSA_ATTN_RUNNING_MAX": "1", "CSA_ATTN_CG": "4"},
                                      {"CSA_ATTN_V3": "1"}, {"CSA_ATTN_V3": "1", "CSA_EMU_EVERY": "4"}])
 @pytest.mark.parametrize("jump", [3.0, 40.0])
@@ -218,7 +218,7 @@ def test_attention_running_max_jumps(csa, variant, jump, monkeypatch):
         ref, ref_lse = oracle_head(lay, q, k, v, 0, h, mask=masks[h])
         assert_close(out[0, :, h].double().cpu().numpy(), ref, f"{variant} jump {jump} h{h}")
         assert np.abs(lse_np[h] - ref_lse).max() <= 1e-3 * max(1.0, np.abs(ref_lse).max())
-    if not variant:
+    if not variant or "CSA_ATTN4" in variant:  # the fixed-reference kernels (attn5 / attn4)
         n_fb = fallback_count(csa, q)
         assert (n_fb > 0) if jump > 10 else (n_fb == 0), n_fb
 
