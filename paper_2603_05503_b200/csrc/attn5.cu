@@ -25,7 +25,7 @@ using namespace attn;
 constexpr int kItemSlots5 = 4;
 constexpr int kCH5 = 4;                          // column parts (32 keys each)
 constexpr float kGuard5 = 72057594037927936.0f;  // 2^56
-constexpr int kEmu5 = 1;  // element pairs p with (p & 7) >= 8 - kEmu5 -> polynomial exp2
+constexpr int kEmu5 = 0;  // pairs p with (p & 7) >= 8 - kEmu5 -> polynomial exp2 (A/B: 0 1172, 1/8 1164, 1/4 1121)
 // Two MMA issuer warps (warp 1: Q copy + QK, warp 3: P.V): every mbarrier wait costs ~140
 // cycles even when its phase is already complete (scripts/mbar_micro.cu) and every 8-MMA batch
 // blocks its issuing thread ~600 cycles; one issuer serialises all of it per tile.
