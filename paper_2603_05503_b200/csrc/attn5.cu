@@ -61,6 +61,9 @@ __device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
 // Prefetch (off: the second register set spills at the 104-register softmax budget, measured
 // 1077 vs 1161 TF/s): with the probe seeing S_{j+1} complete, its TMEM load is issued before tile j's P
 // store / publish (two register sets alternate between tiles).
+#ifndef CSA_ATTN5_LATE_PROBE
+#define CSA_ATTN5_LATE_PROBE 1
+#endif
 #ifndef CSA_ATTN5_PREFETCH
 #define CSA_ATTN5_PREFETCH 0
 #endif
@@ -452,9 +455,10 @@ __global__ void __launch_bounds__(Smem5::kThreads, 1)
                 if (lane == 0) mbar_arrive(s_empty + b);  // S_j may be overwritten (QK_{j+2})
                 // probes: the P buffer (P.V_{j-1} done) and the next tile's S, resolved later
                 const uint32_t p_ready = CSA_ATTN5_PROBE ? mbar_test(p_empty, (pst & 1) ^ 1) : 0u;
-                s_ready = (CSA_ATTN5_PROBE && j + 1 < tl.n)
-                              ? mbar_test(s_full + (b ^ 1u), (b ? sc0 : sc1) & 1)
-                              : 0u;
+                if (!CSA_ATTN5_LATE_PROBE)
+                    s_ready = (CSA_ATTN5_PROBE && j + 1 < tl.n)
+                                  ? mbar_test(s_full + (b ^ 1u), (b ? sc0 : sc1) & 1)
+                                  : 0u;
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 2);
                 if (last_ragged && j == tl.n - 1) {
 #pragma unroll
@@ -495,6 +499,10 @@ __global__ void __launch_bounds__(Smem5::kThreads, 1)
                 bad |= !(lsum <= kGuard5);  // also catches inf / NaN
                 l_run += lsum;
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 3);
+                if (CSA_ATTN5_LATE_PROBE)  // probe the next S after the exponentials: its round
+                    s_ready = (CSA_ATTN5_PROBE && j + 1 < tl.n)  // trip hides under the P store
+                                  ? mbar_test(s_full + (b ^ 1u), (b ? sc0 : sc1) & 1)
+                                  : 0u;
                 // prefetch: S_{j+1} is complete (probe) -> start loading it now; its latency
                 // overlaps the P store / publish of tile j (warp-uniform decision)
                 inflight = CSA_ATTN5_PREFETCH && __all_sync(0xffffffffu, s_ready != 0u);
