@@ -264,8 +264,8 @@ CSA_API csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan,
  * recomputed on the same stream by the running-max kernel (attn3.cu).  Without a workspace the
  * running-max kernel runs the whole launch.  Each mode is deterministic; the two agree within
  * bf16 rounding of P (not bitwise).
- * Non-square blocks (block 128 x block_kv) and block 128 / head_dim 64 run attn_rect.cu (the same
- * fixed-reference design with B_kv-wide key tiles; the workspace is REQUIRED for non-square
+ * Non-square blocks (block 128 x block_kv) run attn_rect.cu and block 128 / head_dim 64 runs
+ * attn5.cu<64> (the same fixed-reference design; attn_rect.cu with B_kv-wide key tiles; the workspace is REQUIRED for non-square
  * layouts): overshooting items are recomputed on the same stream by an exact-row-max pass (the
  * row max is parked in the first 4 bytes of the row's first output row) and a pass against that
  * max.  Other shapes (block 64) run attn.cu. */

@@ -477,8 +477,12 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
         const size_t flag_words = (items + 31) / 32;
         csa::Fallback fb{base, base + 1, base + 1 + flag_words};
         e = cudaMemsetAsync(base, 0, 4 * (1 + flag_words), (cudaStream_t)stream);
+        // block 128 / d 64 (square): the mode-0 pass is attn5.cu's one-group kernel (4 warps per
+        // SMSP feed the MUFU, which bounds d 64); CSA_ATTN_RECT keeps attn_rect.cu for A/B
+        const bool sepp64 = is_square(L) && head_dim == 64 && !std::getenv("CSA_ATTN_RECT");
         if (e == cudaSuccess)
-            e = csa::launch_attn_rect(a, tq, tk, tv, grid, fb, 0, (cudaStream_t)stream);
+            e = sepp64 ? csa::launch_attn_sepp(a, tq, tk, tv, grid, fb, (cudaStream_t)stream)
+                       : csa::launch_attn_rect(a, tq, tk, tv, grid, fb, 0, (cudaStream_t)stream);
         csa::AttnArgs re = a;
         re.work_list = fb.list;
         re.n_work = reinterpret_cast<const int32_t*>(fb.count);

@@ -80,13 +80,15 @@ static __device__ unsigned long long* g_trace5;
     } while (0)
 #endif
 
+template <int D>
 struct Smem5 {
     static constexpr int kThreads = 128 + 128 * kCH5;
-    static constexpr int kBox = 128 * 128;  // [128 rows][64 cols] bf16, SWIZZLE_128B
-    static constexpr int kTile = 2 * kBox;  // 128 x 128 bf16
+    static constexpr int kBox = 128 * 128;          // [128 rows][64 cols] bf16, SWIZZLE_128B
+    static constexpr int kTile = (D / 64) * kBox;   // 128 x D bf16 (Q, K and V tiles alike)
     static constexpr int kQOff = 0;
     static constexpr int kKVOff = kTile;
-    static constexpr int kSlots = 5;
+    static constexpr int kSlotsFit = (232448 - kTile - 6144) / kTile;
+    static constexpr int kSlots = kSlotsFit > 8 ? 8 : kSlotsFit;
     static constexpr int kBarOff = kKVOff + kSlots * kTile;
     // q_full q_empty | kv_full[S] kv_empty[S] | s_full[2] s_empty[2] | p_full p_empty |
     // o_full o_empty | item_full[4] item_empty[4]
@@ -97,17 +99,20 @@ struct Smem5 {
     static constexpr int kTmemPtrOff = kFlagOff + 16;
     static constexpr int kBytes = kTmemPtrOff + 16;
     static_assert(kBytes <= 232448, "smem");
-    static constexpr uint32_t kS = 0, kO = 256, kQ = 384, kP = 448;
+    // TMEM: S0 [0,128) S1 [128,256) | O [256, 256+D) | Q (D/2 columns) | P (64 columns)
+    static constexpr uint32_t kS = 0, kO = 256, kQ = 256 + D, kP = 256 + D + D / 2;
+    static_assert(kP + 64 <= 512 && (D == 64 || D == 128), "TMEM / head_dim");
     static constexpr uint32_t kIdescQK = umma_idesc_bf16(128, 128, 0, 0);
-    static constexpr uint32_t kIdescPV = umma_idesc_bf16(128, 128, 0, 1);
+    static constexpr uint32_t kIdescPV = umma_idesc_bf16(128, D, 0, 1);
 };
 
-__global__ void __launch_bounds__(Smem5::kThreads, 1)
+template <int D>
+__global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
     sparse_attn_sepp_kernel(const AttnArgs a, const __grid_constant__ CUtensorMap tq,
                             const __grid_constant__ CUtensorMap tk,
                             const __grid_constant__ CUtensorMap tv, const Fallback fb) {
-    using L = Smem5;
-    constexpr int BK = 128, D = 128, S = L::kSlots, CH = kCH5;
+    using L = Smem5<D>;
+    constexpr int BK = 128, S = L::kSlots, CH = kCH5;
     extern __shared__ __align__(1024) uint8_t smem[];
     if ((smem_u32(smem) & 1023u) != 0u) __trap();
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
@@ -560,13 +565,21 @@ __global__ void __launch_bounds__(Smem5::kThreads, 1)
             __nv_bfloat16* obase = a.o + (int64_t)it.b * a.o_sb + (int64_t)it.h * a.o_sh;
             const uint64_t inv2 = f2(inv, inv);
             {
-                const int col = ch * (D / CH);
+                constexpr int NO = D / CH;  // output columns of this thread's part (32 or 16)
+                const int col = ch * NO;
                 uint32_t r0[32];
-                tmem_ld32(lane_addr + L::kO + col, r0);
-                tmem_ld_wait(r0);
+                if constexpr (NO == 32) {
+                    tmem_ld32(lane_addr + L::kO + col, r0);
+                    tmem_ld_wait(r0);
+                } else {
+                    tmem_ld16(lane_addr + L::kO + col, *reinterpret_cast<uint32_t(*)[16]>(&r0[0]));
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int x = 0; x < 16; ++x) asm volatile("" : "+r"(r0[x]));
+                }
                 uint32_t packed[16];
 #pragma unroll
-                for (int x = 0; x < 32; x += 2) {
+                for (int x = 0; x < NO; x += 2) {
                     const uint64_t v = fmul2(pk2(r0[x], r0[x + 1]), inv2);
                     packed[x / 2] = pack_bf16(lo_f(v), hi_f(v));
                 }
@@ -574,7 +587,7 @@ __global__ void __launch_bounds__(Smem5::kThreads, 1)
                     uint4* dst = reinterpret_cast<uint4*>(
                         obase + (tok0 + (int64_t)dI * dst_stride_rows) * a.o_sn + col);
 #pragma unroll
-                    for (int v = 0; v < 4; ++v)
+                    for (int v = 0; v < NO / 8; ++v)
                         dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2],
                                             packed[4 * v + 3]);
                 }
@@ -622,16 +635,26 @@ cudaError_t set_attn5_trace(void* buf, int mode) {
     return cudaMemcpyToSymbol(g_trace5, &p, sizeof(p));
 }
 
+namespace {
+template <int D>
+cudaError_t launch_sepp_d(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
+                          const CUtensorMap& tv, int grid, const Fallback& fb, cudaStream_t s) {
+    const int smem = Smem5<D>::kBytes;
+    cudaError_t e = cudaFuncSetAttribute(sparse_attn_sepp_kernel<D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    sparse_attn_sepp_kernel<D><<<grid, Smem5<D>::kThreads, smem, s>>>(a, tq, tk, tv, fb);
+    return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t launch_attn_sepp(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
                              const CUtensorMap& tv, int grid, const Fallback& fb,
                              cudaStream_t s) {
-    if (a.g.B != 128 || a.head_dim != 128) return cudaErrorInvalidValue;
-    const int smem = Smem5::kBytes;
-    cudaError_t e = cudaFuncSetAttribute(sparse_attn_sepp_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    sparse_attn_sepp_kernel<<<grid, Smem5::kThreads, smem, s>>>(a, tq, tk, tv, fb);
-    return cudaGetLastError();
+    if (a.g.B != 128 || a.g.BK != 128) return cudaErrorInvalidValue;
+    if (a.head_dim == 128) return launch_sepp_d<128>(a, tq, tk, tv, grid, fb, s);
+    if (a.head_dim == 64) return launch_sepp_d<64>(a, tq, tk, tv, grid, fb, s);
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace csa
