@@ -148,9 +148,6 @@ const char* csa_version(void) { return "csa-b200 0.1 (sm_100a)"; }
 
 csa_status_t csa_debug_trace(void* buf, int32_t mode) {
     cudaError_t e = csa::set_attn_trace(buf, mode);
-    if (e == cudaSuccess) e = csa::set_attn2_trace(buf, mode);
-    if (e == cudaSuccess) e = csa::set_attn3_trace(buf, mode);
-    if (e == cudaSuccess) e = csa::set_attn4_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_attn5_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_calib_trace(buf, mode);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyToSymbol");
@@ -400,16 +397,13 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
                                  size_t workspace_bytes, csa_stream_t stream) {
     csa_status_t st = check_layout(L, head_dim, n_heads);
     if (st != CSA_OK) return st;
-    if (pair_items && (L.block != 128 || head_dim != 128 || !is_square(L)))
-        return fail(CSA_ERR_UNSUPPORTED, "pair work items need block 128 and head_dim 128");
-    // attn_rect.cu: non-square blocks, the d = 64 path at block 128 (CSA_ATTN_V3 -> attn.cu),
-    // and block 128 / d 128 on request (CSA_ATTN_RECT, A/B against attn4.cu)
-    const bool rect = !is_square(L) ||
-                      (L.block == 128 && head_dim == 64 && workspace != nullptr &&
-                       std::getenv("CSA_ATTN_V3") == nullptr) ||
-                      (L.block == 128 && head_dim == 128 && std::getenv("CSA_ATTN_RECT") != nullptr);
-    if (rect && workspace == nullptr)
-        return fail(CSA_ERR_INVALID_ARGUMENT, "non-square blocks need the attention workspace");
+    if (pair_items)
+        return fail(CSA_ERR_UNSUPPORTED, "pair work items: not supported by this build");
+    // block 128 (square, or B_q = 128 x B_kv): fixed-reference kernels + exact-max fallback
+    // passes, which keep their list in the workspace; block 64: attn.cu
+    const bool b128 = L.block == 128;
+    if (b128 && workspace == nullptr)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "block 128 needs the attention workspace");
     if (workspace != nullptr && (workspace_bytes < 8 || reinterpret_cast<uintptr_t>(workspace) % 8))
         return fail(CSA_ERR_INVALID_ARGUMENT, "attention workspace: >= 8 bytes, 8-byte aligned");
     if (batch < 1 || n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "batch/n_heads < 1");
@@ -452,72 +446,34 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
     a.work_list = work_list;
     a.n_work = n_work;
     a.sched = static_cast<uint32_t*>(workspace);
-    const int64_t items = (int64_t)max_work * batch * (pair_items ? 2 : 1);
-    int grid = (int)(items < di.sms ? items : di.sms);
-    if (const char* dbg = std::getenv("CSA_DEBUG_GRID")) {  // debug: fewer persistent CTAs
-        const int want = std::atoi(dbg);
-        if (want > 0 && want < grid) grid = want;
-    }
+    const int64_t items = (int64_t)max_work * batch;
+    const int grid = (int)(items < di.sms ? items : di.sms);
     cudaError_t e;
-    if (pair_items) {
-        CUtensorMap tk_half;  // K halves: 64-key boxes (each CTA of a pair loads one half)
-        if ((st = make_map(&tk_half, k, batch, g.N, n_heads, head_dim, g.B / 2, "k")) != CSA_OK)
-            return st;
-        a.sched = nullptr;  // the pair kernel assigns pair items statically per cluster
-        e = csa::launch_attn_pair(a, head_dim, tq, tk_half, tv, grid, (cudaStream_t)stream);
-    } else if (rect) {
-        // non-square B_q x B_kv (attn_rect.cu): fixed reference max (mode 0);
-        // overshooting items are recomputed from the fallback list by an exact-row-max pass
-        // (mode 1) and a pass against that max (mode 2), statically assigned, same stream.
-        const size_t items = (size_t)n_heads * (size_t)g.NB;
+    if (b128) {
+        // Mode 0: every row's softmax shift is the max of its first kept tile (reading Q29):
+        // attn5.cu for square 128 x 128 blocks (head_dim 128 and 64), attn_rect.cu for B_kv !=
+        // 128.  Items whose later scores overshoot that shift by more than 2^56 are listed in
+        // the workspace (256 bytes past the counters) and recomputed on the same stream by
+        // attn_rect.cu's exact-max passes (mode 1: each row's exact max over its kept keys,
+        // mode 2: the softmax against it), statically assigned over the (normally empty) list.
+        const size_t n_items = (size_t)n_heads * (size_t)g.NB;
         if (workspace_bytes < csa_workspace_size(CSA_WS_ATTN, L, n_heads, head_dim) ||
-            (int64_t)max_work > (int64_t)items)
+            (int64_t)max_work > (int64_t)n_items)
             return fail(CSA_ERR_INVALID_ARGUMENT, "attention workspace too small");
         uint32_t* base = static_cast<uint32_t*>(workspace) + 64;
-        const size_t flag_words = (items + 31) / 32;
+        const size_t flag_words = (n_items + 31) / 32;
         csa::Fallback fb{base, base + 1, base + 1 + flag_words};
         e = cudaMemsetAsync(base, 0, 4 * (1 + flag_words), (cudaStream_t)stream);
-        // block 128 / d 64 (square): the mode-0 pass is attn5.cu's one-group kernel (4 warps per
-        // SMSP feed the MUFU, which bounds d 64); CSA_ATTN_RECT keeps attn_rect.cu for A/B
-        const bool sepp64 = is_square(L) && head_dim == 64 && !std::getenv("CSA_ATTN_RECT");
         if (e == cudaSuccess)
-            e = sepp64 ? csa::launch_attn_sepp(a, tq, tk, tv, grid, fb, (cudaStream_t)stream)
-                       : csa::launch_attn_rect(a, tq, tk, tv, grid, fb, 0, (cudaStream_t)stream);
+            e = is_square(L) ? csa::launch_attn_sepp(a, tq, tk, tv, grid, fb, (cudaStream_t)stream)
+                             : csa::launch_attn_rect(a, tq, tk, tv, grid, fb, 0,
+                                                     (cudaStream_t)stream);
         csa::AttnArgs re = a;
         re.work_list = fb.list;
         re.n_work = reinterpret_cast<const int32_t*>(fb.count);
         re.sched = nullptr;
         for (int mode = 1; mode <= 2 && e == cudaSuccess; ++mode)
             e = csa::launch_attn_rect(re, tq, tk, tv, di.sms, fb, mode, (cudaStream_t)stream);
-    } else if (g.B == 128 && head_dim == 128 && workspace != nullptr &&
-               !std::getenv("CSA_ATTN_RUNNING_MAX") && !std::getenv("CSA_ATTN_V3")) {
-        // production (attn5.cu; attn4.cu with CSA_ATTN4): fixed per-row reference max; items
-        // whose later scores overshoot it are recomputed right after by the running-max kernel
-        // (attn3.cu) from the fallback list in the workspace (256 bytes past the counters).
-        // Without a workspace (static assignment) the running-max kernel does the whole launch.
-        const size_t items = (size_t)n_heads * (size_t)g.NB;
-        if (workspace_bytes < csa_workspace_size(CSA_WS_ATTN, L, n_heads, head_dim) ||
-            (int64_t)max_work > (int64_t)items)
-            return fail(CSA_ERR_INVALID_ARGUMENT, "attention workspace too small");
-        uint32_t* base = static_cast<uint32_t*>(workspace) + 64;
-        const size_t flag_words = (items + 31) / 32;
-        csa::Fallback fb{base, base + 1, base + 1 + flag_words};
-        e = cudaMemsetAsync(base, 0, 4 * (1 + flag_words), (cudaStream_t)stream);
-        if (e == cudaSuccess)
-            e = std::getenv("CSA_ATTN4")  // A/B: the two-group fixed-reference kernel
-                    ? csa::launch_attn_fixed_ref(a, tq, tk, tv, grid, fb, (cudaStream_t)stream)
-                    : csa::launch_attn_sepp(a, tq, tk, tv, grid, fb, (cudaStream_t)stream);
-        if (e == cudaSuccess) {
-            csa::AttnArgs re = a;
-            re.work_list = fb.list;
-            re.n_work = reinterpret_cast<const int32_t*>(fb.count);
-            re.sched = nullptr;  // static assignment over an (almost always) empty list
-            e = csa::launch_attn_q_tmem(re, tq, tk, tv, di.sms, (cudaStream_t)stream);
-        }
-    } else if (g.B == 128 && head_dim == 128 && !std::getenv("CSA_ATTN_V3")) {
-        // production shape: Q resident in TMEM, column-split softmax (attn3.cu); CSA_ATTN_V3
-        // selects the shared-memory-Q kernel (attn.cu, all other shapes) for A/B measurements
-        e = csa::launch_attn_q_tmem(a, tq, tk, tv, grid, (cudaStream_t)stream);
     } else {
         e = csa::launch_attn(a, head_dim, tq, tk, tv, grid, (cudaStream_t)stream);
     }

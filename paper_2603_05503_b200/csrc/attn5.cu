@@ -1,18 +1,21 @@
-// attn5.cu -- a7 + a8 for block 128, head_dim 128: fixed reference max, one softmax group on
-// every tile, P in its own TMEM buffer.
+// attn5.cu -- a7 + a8 for block 128 (head_dim 128 and 64): fixed reference max, one softmax
+// group on every tile, Q read by the S-MMA from shared memory, P double-buffered in TMEM.
 //
-// Same mathematics as attn4.cu (readings Q1, Q2, Q9, Q10, Q29:
-// each row's softmax shift is the max of its first kept tile; an overshoot beyond 2^56 flags the
-// item for the running-max fallback).  What changes is the pipeline:
-//   TMEM (512 columns): S0 [0,128) S1 [128,256) | O [256,384) | Q [384,448) | P [448,512)
+// PAPER.md P:647-656 (block-sparse attention over the kept key blocks of each query block),
+// P:616-622 (anchor rows of REPETITIVE heads); readings Q1, Q2, Q9, Q10, Q29 (DESIGN.md section
+// 2): each row's softmax shift is the max of its first kept tile; an overshoot beyond 2^56 flags
+// the item, which the exact-max passes of attn_rect.cu recompute after this launch.
+//   TMEM (512 columns): S0 [0,128) S1 [128,256) | O [256,256+D) | P0, P1 (64 columns each)
+//   smem: Q[2] (double-buffered, SS S-MMA A operand) | K/V ring in consumption order
 //   * all 16 softmax warps take every tile (4 column parts of 32 keys: 4 warps per SMSP keep the
-//     MUFU fed -- attn4.cu's two alternating groups leave 2 per SMSP on a tile);
-//   * S_j is released as soon as it is loaded (s_empty), P_j goes to the separate P buffer, so
-//     QK_{j+2} is issued while the softmax still works on tile j, and P.V_j waits only for P_j;
-//   * the issue order is QK_0, QK_1, then per tile j: QK_{j+2}, P.V_j; the producer loads the
-//     ring in that order (K0, K1, K2, V0, K3, V1, ...).
-// The softmax of tile j+1 starts as soon as it finished tile j (S_{j+1} is long ready), and its
-// P store waits only for P.V_j to have read P_j (p_empty).
+//     MUFU fed);
+//   * S_j is released as soon as it is loaded (s_empty); P_j goes to P[j&1], so the P store of
+//     tile j waits only for P.V_{j-2}; QK_{j+2} is issued while the softmax works on tile j;
+//   * S_j = Q K_j^T runs as SS-MMAs (Q never copied to TMEM): interleaved with the TS P.V MMAs the
+//     tensor pipe sustains 66.7 cycles per 128x128x16 dispatch against 72.6 for TS + TS
+//     (scripts/mma_bench.cu, profiles/r02_mma_bench.txt; floor 64);
+//   * warp 1 issues the S-MMAs, warp 3 the P.V MMAs (each blocks ~600 cycles per 8-MMA batch);
+//     the producer loads the ring in issue order (K0, K1, K2, V0, K3, V1, ...).
 #include <cstdint>
 
 #include "attn_common.cuh"
@@ -26,13 +29,6 @@ constexpr int kItemSlots5 = 4;
 constexpr int kCH5 = 4;                          // column parts (32 keys each)
 constexpr float kGuard5 = 72057594037927936.0f;  // 2^56
 constexpr int kEmu5 = 0;  // pairs p with (p & 7) >= 8 - kEmu5 -> polynomial exp2 (A/B: 0 1172, 1/8 1164, 1/4 1121)
-// Two MMA issuer warps (warp 1: Q copy + QK, warp 3: P.V): every mbarrier wait costs ~140
-// cycles even when its phase is already complete (scripts/mbar_micro.cu) and every 8-MMA batch
-// blocks its issuing thread ~600 cycles; one issuer serialises all of it per tile.
-#ifndef CSA_ATTN5_SPLIT_ISSUE
-#define CSA_ATTN5_SPLIT_ISSUE 1
-#endif
-constexpr bool kSplitIssue5 = CSA_ATTN5_SPLIT_ISSUE != 0;
 
 // Ring positions (per item, n kept tiles) of the producer order K0, K1, then per step s >= 2:
 // K_s (s < n), V_{s-2}: K_j after j K's and max(0, j-2) V's; V_j after min(j+2, n-1)+1 K's and
@@ -41,12 +37,9 @@ __device__ __forceinline__ uint32_t kpos5(int32_t j) { return (uint32_t)(j + (j 
 __device__ __forceinline__ uint32_t vpos5(int32_t j, int32_t n) {
     return (uint32_t)((j + 2 < n - 1 ? j + 2 : n - 1) + 1 + j);
 }
-// Early barrier probe: test_wait is non-blocking; issued as soon as the next wait's phase is
-// known, its ~140-cycle round trip overlaps the exponentials, and the blocking wait is skipped
-// when the phase had already completed (the common case for S and for the P buffer).
-#ifndef CSA_ATTN5_PROBE
-#define CSA_ATTN5_PROBE 1
-#endif
+// Non-blocking barrier probe: issued as soon as the next wait's phase is known, its ~140-cycle
+// round trip overlaps the exponentials, and the blocking wait is skipped when the phase had
+// already completed (an mbarrier wait costs ~140 cycles even then, scripts/mbar_micro.cu).
 __device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
@@ -58,15 +51,6 @@ __device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok;
 }
-// Prefetch (off: the second register set spills at the 104-register softmax budget, measured
-// 1077 vs 1161 TF/s): with the probe seeing S_{j+1} complete, its TMEM load is issued before tile j's P
-// store / publish (two register sets alternate between tiles).
-#ifndef CSA_ATTN5_LATE_PROBE
-#define CSA_ATTN5_LATE_PROBE 1
-#endif
-#ifndef CSA_ATTN5_PREFETCH
-#define CSA_ATTN5_PREFETCH 0
-#endif
 static __device__ unsigned long long* g_trace5;
 #ifdef CSA_ENABLE_TRACE
 #define TRACE5(slot, k, e)                                                                   \
@@ -85,23 +69,24 @@ struct Smem5 {
     static constexpr int kThreads = 128 + 128 * kCH5;
     static constexpr int kBox = 128 * 128;          // [128 rows][64 cols] bf16, SWIZZLE_128B
     static constexpr int kTile = (D / 64) * kBox;   // 128 x D bf16 (Q, K and V tiles alike)
-    static constexpr int kQOff = 0;
-    static constexpr int kKVOff = kTile;
-    static constexpr int kSlotsFit = (232448 - kTile - 6144) / kTile;
+    static constexpr int kQOff = 0;                 // Q[2]: double-buffered (SS S-MMA operand)
+    static constexpr int kKVOff = 2 * kTile;
+    static constexpr int kSlotsFit = (232448 - 2 * kTile - 6144) / kTile;
     static constexpr int kSlots = kSlotsFit > 8 ? 8 : kSlotsFit;
     static constexpr int kBarOff = kKVOff + kSlots * kTile;
-    // q_full q_empty | kv_full[S] kv_empty[S] | s_full[2] s_empty[2] | p_full p_empty |
-    // o_full o_empty | item_full[4] item_empty[4]
-    static constexpr int kNumBars = 2 + 2 * kSlots + 4 + 2 + 2 + 2 * kItemSlots5;
+    // q_full[2] q_empty[2] | kv_full[S] kv_empty[S] | s_full[2] s_empty[2] | p_full[2]
+    // p_empty[2] | o_full o_empty | item_full[4] item_empty[4]
+    static constexpr int kNumBars = 4 + 2 * kSlots + 4 + 4 + 2 + 2 * kItemSlots5;
     static constexpr int kRowOff = kBarOff + kNumBars * 8;  // l[CH][128] | tile-0 max [CH][128]
     static constexpr int kItemOff = kRowOff + 2 * kCH5 * 128 * 4;
     static constexpr int kFlagOff = kItemOff + kItemSlots5 * 4;
     static constexpr int kTmemPtrOff = kFlagOff + 16;
     static constexpr int kBytes = kTmemPtrOff + 16;
     static_assert(kBytes <= 232448, "smem");
-    // TMEM: S0 [0,128) S1 [128,256) | O [256, 256+D) | Q (D/2 columns) | P (64 columns)
-    static constexpr uint32_t kS = 0, kO = 256, kQ = 256 + D, kP = 256 + D + D / 2;
-    static_assert(kP + 64 <= 512 && (D == 64 || D == 128), "TMEM / head_dim");
+    static_assert(kSlots >= 3, "ring");
+    // TMEM: S0 [0,128) S1 [128,256) | O [256, 256+D) | P0, P1 (64 columns each)
+    static constexpr uint32_t kS = 0, kO = 256, kP = 256 + D;
+    static_assert(kP + 128 <= 512 && (D == 64 || D == 128), "TMEM / head_dim");
     static constexpr uint32_t kIdescQK = umma_idesc_bf16(128, 128, 0, 0);
     static constexpr uint32_t kIdescPV = umma_idesc_bf16(128, D, 0, 1);
 };
@@ -116,15 +101,15 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem[];
     if ((smem_u32(smem) & 1023u) != 0u) __trap();
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
-    uint64_t* q_full = bars;
-    uint64_t* q_empty = bars + 1;
-    uint64_t* kv_full = bars + 2;
+    uint64_t* q_full = bars;          // [Q buffer]
+    uint64_t* q_empty = bars + 2;     // [Q buffer]
+    uint64_t* kv_full = bars + 4;
     uint64_t* kv_empty = kv_full + S;
-    uint64_t* s_full = kv_empty + S;  // [buffer]
-    uint64_t* s_empty = s_full + 2;   // [buffer]
-    uint64_t* p_full = s_empty + 2;
-    uint64_t* p_empty = p_full + 1;
-    uint64_t* o_full = p_empty + 1;
+    uint64_t* s_full = kv_empty + S;  // [S buffer]
+    uint64_t* s_empty = s_full + 2;   // [S buffer]
+    uint64_t* p_full = s_empty + 2;   // [P buffer]
+    uint64_t* p_empty = p_full + 2;   // [P buffer]
+    uint64_t* o_full = p_empty + 2;
     uint64_t* o_empty = o_full + 1;
     uint64_t* item_full = o_empty + 1;
     uint64_t* item_empty = item_full + kItemSlots5;
@@ -136,23 +121,23 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
 
     const uint32_t warp = warp_id(), lane = lane_id();
     if (threadIdx.x == 0) {
-        mbar_init(q_full, 1);
-        mbar_init(q_empty, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(q_full + i, 1);
+            mbar_init(q_empty + i, 1);
+            mbar_init(s_full + i, 1);
+            mbar_init(s_empty + i, 4 * CH);
+            mbar_init(p_full + i, 4 * CH);
+            mbar_init(p_empty + i, 1);
+        }
         for (int i = 0; i < S; ++i) {
             mbar_init(kv_full + i, 1);
             mbar_init(kv_empty + i, 1);
         }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(s_full + i, 1);
-            mbar_init(s_empty + i, 4 * CH);
-        }
-        mbar_init(p_full, 4 * CH);
-        mbar_init(p_empty, 1);
         mbar_init(o_full, 1);
         mbar_init(o_empty, 4 * CH);
         for (int i = 0; i < kItemSlots5; ++i) {
             mbar_init(item_full + i, 1);
-            mbar_init(item_empty + i, (kSplitIssue5 ? 2 : 1) + 4 * CH);  // issuers + softmax
+            mbar_init(item_empty + i, 2 + 4 * CH);  // two issuers + softmax warps
         }
         *flag_s = 0;
         fence_barrier_init();
@@ -201,12 +186,14 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
                 if (item < 0) break;
                 const Item it = decode_item(a, item);
                 const TileList tl = tile_list(a, it);
-                uint8_t* qdst = smem + L::kQOff;
-                mbar_wait(q_empty, (local & 1) ^ 1);
+                const uint32_t qb = (uint32_t)local & 1u;
+                uint8_t* qdst = smem + L::kQOff + qb * L::kTile;
+                mbar_wait(q_empty + qb, ((local >> 1) & 1) ^ 1);
                 if (it.kind == 0) {
                     if (elect_one()) {
-                        mbar_arrive_expect_tx(q_full, L::kTile);
-                        tma_tile<D>(qdst, L::kBox, &tq, q_full, it.h, it.idx * BK, it.b, pol_q);
+                        mbar_arrive_expect_tx(q_full + qb, L::kTile);
+                        tma_tile<D>(qdst, L::kBox, &tq, q_full + qb, it.h, it.idx * BK, it.b,
+                                    pol_q);
                     }
                     __syncwarp();
                 } else {
@@ -233,7 +220,7 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(q_full);
+                    if (lane == 0) mbar_arrive(q_full + qb);
                 }
                 // ring order = issue order: K0, K1, then per step s >= 2: K_s, V_{s-2}; V tail
                 auto load = [&](int kv, int32_t j) {
@@ -254,27 +241,18 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
                     if (step >= 2) load(1, step - 2);
                 }
             }
-        } else if (kSplitIssue5 && warp == 1) {
-            // ------------------------------------------------------- QK issuer (Q copy, S_j)
+        } else if (warp == 1) {
+            // ------------------------------------------------ QK issuer: S_j = Q K_j^T (SS)
             uint32_t base = 0, sis0 = 0, sis1 = 0, tiles = 0;
-            const uint32_t q_base = smem_u32(smem + L::kQOff);
             const uint32_t kv_base = smem_u32(smem + L::kKVOff);
             for (int32_t local = 0;; ++local) {
                 const int32_t item = next_item(local);
                 if (item < 0) break;
                 const Item it = decode_item(a, item);
                 const TileList tl = tile_list(a, it);
-                mbar_wait(q_full, local & 1);
-                tc_fence_after();
-                if (elect_one()) {  // Q -> TMEM, in order with this thread's MMAs
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk)
-                        tmem_cp_128x256b(tmem + L::kQ + kk * 8,
-                                         umma_desc_sw128(q_base + (kk >> 2) * L::kBox +
-                                                             (kk & 3) * 32, 16, 1024));
-                    mma_commit(q_empty);
-                }
-                __syncwarp();
+                const uint32_t qb = (uint32_t)local & 1u;
+                const uint32_t q_base = smem_u32(smem + L::kQOff + qb * L::kTile);
+                mbar_wait(q_full + qb, (local >> 1) & 1);
                 for (int32_t j = 0; j < tl.n; ++j) {
                     const uint32_t b = (uint32_t)j & 1u;
                     const uint32_t use = b ? sis1++ : sis0++;
@@ -287,22 +265,28 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
                     if (elect_one()) {
                         const uint32_t kb = kv_base + slot * L::kTile;
 #pragma unroll
-                        for (int kk = 0; kk < D / 16; ++kk)
-                            mma_ts(tmem + L::kS + b * BK, tmem + L::kQ + kk * 8,
-                                   umma_desc_sw128(kb + (kk >> 2) * L::kBox + (kk & 3) * 32, 16,
-                                                   1024),
-                                   L::kIdescQK, kk > 0 ? 1u : 0u);
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            const uint32_t off = (kk >> 2) * L::kBox + (kk & 3) * 32;
+                            mma_ss(tmem + L::kS + b * BK, umma_desc_sw128(q_base + off, 16, 1024),
+                                   umma_desc_sw128(kb + off, 16, 1024), L::kIdescQK,
+                                   kk > 0 ? 1u : 0u);
+                        }
                         mma_commit(s_full + b);
                         mma_commit(kv_empty + slot);
+                        if (j == tl.n - 1) mma_commit(q_empty + qb);  // last read of this Q
                     }
+                    __syncwarp();
+                }
+                if (tl.n == 0) {  // corrupt plan (empty row): no tiles, release Q at once
+                    if (elect_one()) mma_commit(q_empty + qb);
                     __syncwarp();
                 }
                 base += 2u * (uint32_t)tl.n;
                 tiles += (uint32_t)tl.n;
             }
-        } else if (kSplitIssue5 && warp == 3) {
+        } else if (warp == 3) {
             // ------------------------------------------------------------- P.V issuer (O)
-            uint32_t base = 0, pcnt = 0, tiles = 0;
+            uint32_t base = 0, pc0 = 0, pc1 = 0, tiles = 0;
             const uint32_t kv_base = smem_u32(smem + L::kKVOff);
             for (int32_t local = 0;; ++local) {
                 const int32_t item = next_item(local);
@@ -315,9 +299,10 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
                     continue;
                 }
                 for (int32_t j = 0; j < tl.n; ++j) {
+                    const uint32_t pb = (tiles + (uint32_t)j) & 1u;
+                    const uint32_t use = pb ? pc1++ : pc0++;
                     TRACE5(3, tiles + (uint32_t)j, 0);
-                    mbar_wait(p_full, pcnt & 1);
-                    ++pcnt;
+                    mbar_wait(p_full + pb, use & 1);
                     TRACE5(3, tiles + (uint32_t)j, 1);
                     if (j == 0) mbar_wait(o_empty, (local & 1) ^ 1);  // last item's epilogue
                     const uint32_t pos = base + vpos5(j, tl.n), slot = pos % S, ph = (pos / S) & 1;
@@ -327,92 +312,16 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
                         const uint32_t vb = kv_base + slot * L::kTile;
 #pragma unroll
                         for (int kk = 0; kk < BK / 16; ++kk)
-                            mma_ts(tmem + L::kO, tmem + L::kP + kk * 8,
+                            mma_ts(tmem + L::kO, tmem + L::kP + pb * 64 + kk * 8,
                                    umma_desc_sw128(vb + kk * 16 * 128, L::kBox, 1024),
                                    L::kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
-                        mma_commit(p_empty);
+                        mma_commit(p_empty + pb);
                         mma_commit(kv_empty + slot);
                     }
                     __syncwarp();
                     TRACE5(3, tiles + (uint32_t)j, 2);
                 }
                 base += 2u * (uint32_t)tl.n;
-                tiles += (uint32_t)tl.n;
-                if (elect_one()) mma_commit(o_full);
-                __syncwarp();
-            }
-        } else if (!kSplitIssue5 && warp == 1) {
-            // ------------------------------------------------------------------ MMA issuer
-            uint32_t cons = 0, sis0 = 0, sis1 = 0, pcnt = 0, tiles = 0;
-            const uint32_t q_base = smem_u32(smem + L::kQOff);
-            const uint32_t kv_base = smem_u32(smem + L::kKVOff);
-            for (int32_t local = 0;; ++local) {
-                const int32_t item = next_item(local);
-                if (item < 0) break;
-                const Item it = decode_item(a, item);
-                const TileList tl = tile_list(a, it);
-                mbar_wait(q_full, local & 1);
-                tc_fence_after();
-                if (elect_one()) {  // Q -> TMEM, in order with this thread's MMAs
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk)
-                        tmem_cp_128x256b(tmem + L::kQ + kk * 8,
-                                         umma_desc_sw128(q_base + (kk >> 2) * L::kBox +
-                                                             (kk & 3) * 32, 16, 1024));
-                    mma_commit(q_empty);
-                    if (tl.n == 0) mma_commit(o_full);  // corrupt plan (empty row): no tiles
-                }
-                __syncwarp();
-                if (tl.n == 0) continue;
-                auto issue_qk = [&](int32_t j) {
-                    const uint32_t b = (uint32_t)j & 1u;
-                    const uint32_t use = b ? sis1++ : sis0++;
-                    TRACE5(2, tiles + (uint32_t)j, 0);
-                    mbar_wait(s_empty + b, (use & 1) ^ 1);  // softmax loaded S_{j-2}
-                    const uint32_t slot = cons % S, ph = (cons / S) & 1;
-                    ++cons;
-                    mbar_wait(kv_full + slot, ph);
-                    TRACE5(2, tiles + (uint32_t)j, 1);
-                    tc_fence_after();
-                    if (elect_one()) {
-                        const uint32_t kb = kv_base + slot * L::kTile;
-#pragma unroll
-                        for (int kk = 0; kk < D / 16; ++kk)
-                            mma_ts(tmem + L::kS + b * BK, tmem + L::kQ + kk * 8,
-                                   umma_desc_sw128(kb + (kk >> 2) * L::kBox + (kk & 3) * 32, 16,
-                                                   1024),
-                                   L::kIdescQK, kk > 0 ? 1u : 0u);
-                        mma_commit(s_full + b);
-                        mma_commit(kv_empty + slot);
-                    }
-                    __syncwarp();
-                };
-                issue_qk(0);
-                if (tl.n > 1) issue_qk(1);
-                for (int32_t j = 0; j < tl.n; ++j) {
-                    if (j + 2 < tl.n) issue_qk(j + 2);
-                    TRACE5(3, tiles + (uint32_t)j, 0);
-                    mbar_wait(p_full, pcnt & 1);
-                    ++pcnt;
-                    TRACE5(3, tiles + (uint32_t)j, 1);
-                    if (j == 0) mbar_wait(o_empty, (local & 1) ^ 1);  // last item's epilogue
-                    const uint32_t slot = cons % S, ph = (cons / S) & 1;
-                    ++cons;
-                    mbar_wait(kv_full + slot, ph);
-                    tc_fence_after();
-                    if (elect_one()) {
-                        const uint32_t vb = kv_base + slot * L::kTile;
-#pragma unroll
-                        for (int kk = 0; kk < BK / 16; ++kk)
-                            mma_ts(tmem + L::kO, tmem + L::kP + kk * 8,
-                                   umma_desc_sw128(vb + kk * 16 * 128, L::kBox, 1024),
-                                   L::kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
-                        mma_commit(p_empty);
-                        mma_commit(kv_empty + slot);
-                    }
-                    __syncwarp();
-                    TRACE5(3, tiles + (uint32_t)j, 2);
-                }
                 tiles += (uint32_t)tl.n;
                 if (elect_one()) mma_commit(o_full);
                 __syncwarp();
@@ -430,7 +339,7 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
         const float sl2 = a.scale_log2;
         const uint64_t sl2x2 = f2(sl2, sl2);
         const int32_t tail_valid = g.N - (g.NB - 1) * BK;
-        uint32_t sc0 = 0, sc1 = 0, pst = 0, tbase = 0;
+        uint32_t sc0 = 0, sc1 = 0, ps0 = 0, ps1 = 0, tbase = 0;
         const bool tr = quarter == 0 && ch == 0 && lane == 0;
         (void)tr;
         for (int32_t local = 0;; ++local) {
@@ -441,29 +350,24 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
             const bool last_ragged = tail_valid < BK && tl.n > 0 && tl.at(tl.n - 1) == g.NB - 1;
             float m_ref = 0.0f, l_run = 0.0f;
             bool bad = false;
-            uint32_t s_ready = 0;  // probe result for the next tile's S (CSA_ATTN5_PROBE)
-            bool inflight = false; // the next tile's S already loading into the other buffer
-            uint32_t rA[NC], rB[NC];
-            auto tile = [&](uint32_t (&r)[NC], uint32_t (&rn)[NC], int32_t j) {
+            uint32_t s_ready = 0;  // probe result for the next tile's S
+            uint32_t r[NC];
+            for (int32_t j = 0; j < tl.n; ++j) {
                 const uint32_t b = (uint32_t)j & 1u;
                 const uint32_t use = b ? sc1++ : sc0++;
+                const uint32_t pb = (tbase + (uint32_t)j) & 1u;
+                const uint32_t puse = pb ? ps1++ : ps0++;
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 0);
-                if (!inflight) {
-                    if (!s_ready) mbar_wait(s_full + b, use & 1);
-                    tc_fence_after();
-                    tmem_ld32(lane_addr + L::kS + b * BK + ch * NC, r);
-                }
+                if (!s_ready) mbar_wait(s_full + b, use & 1);
+                tc_fence_after();
+                tmem_ld32(lane_addr + L::kS + b * BK + ch * NC, r);
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 1);
                 tmem_ld_wait(r);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(s_empty + b);  // S_j may be overwritten (QK_{j+2})
-                // probes: the P buffer (P.V_{j-1} done) and the next tile's S, resolved later
-                const uint32_t p_ready = CSA_ATTN5_PROBE ? mbar_test(p_empty, (pst & 1) ^ 1) : 0u;
-                if (!CSA_ATTN5_LATE_PROBE)
-                    s_ready = (CSA_ATTN5_PROBE && j + 1 < tl.n)
-                                  ? mbar_test(s_full + (b ^ 1u), (b ? sc0 : sc1) & 1)
-                                  : 0u;
+                // probe of the P buffer (P.V_{j-2} done), resolved before the P store
+                const uint32_t p_ready = mbar_test(p_empty + pb, (puse & 1) ^ 1);
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 2);
                 if (last_ragged && j == tl.n - 1) {
 #pragma unroll
@@ -504,30 +408,16 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
                 bad |= !(lsum <= kGuard5);  // also catches inf / NaN
                 l_run += lsum;
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 3);
-                if (CSA_ATTN5_LATE_PROBE)  // probe the next S after the exponentials: its round
-                    s_ready = (CSA_ATTN5_PROBE && j + 1 < tl.n)  // trip hides under the P store
-                                  ? mbar_test(s_full + (b ^ 1u), (b ? sc0 : sc1) & 1)
-                                  : 0u;
-                // prefetch: S_{j+1} is complete (probe) -> start loading it now; its latency
-                // overlaps the P store / publish of tile j (warp-uniform decision)
-                inflight = CSA_ATTN5_PREFETCH && __all_sync(0xffffffffu, s_ready != 0u);
-                if (inflight) {
-                    tc_fence_after();
-                    tmem_ld32(lane_addr + L::kS + (b ^ 1u) * BK + ch * NC, rn);
-                }
-                if (!p_ready) mbar_wait(p_empty, (pst & 1) ^ 1);  // P.V_{j-1} read the P buffer
-                ++pst;
+                // probe the next S after the exponentials: its round trip hides under the store
+                s_ready = j + 1 < tl.n ? mbar_test(s_full + (b ^ 1u), (b ? sc0 : sc1) & 1) : 0u;
+                if (!p_ready) mbar_wait(p_empty + pb, (puse & 1) ^ 1);  // P.V_{j-2} read P[pb]
                 tc_fence_after();
-                tmem_st16(lane_addr + L::kP + ch * (NC / 2), pk);
+                tmem_st16(lane_addr + L::kP + pb * 64 + ch * (NC / 2), pk);
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(p_full);
+                if (lane == 0) mbar_arrive(p_full + pb);
                 if (tr) TRACE5(0, tbase + (uint32_t)j, 4);
-            };
-            for (int32_t j = 0; j < tl.n; j += 2) {
-                tile(rA, rB, j);
-                if (j + 1 < tl.n) tile(rB, rA, j + 1);
             }
             tbase += (uint32_t)tl.n;
             // -------------------------------------------------------------- epilogue

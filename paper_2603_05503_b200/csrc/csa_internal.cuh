@@ -132,22 +132,15 @@ cudaError_t set_attn_trace(void* buf, int mode);
 cudaError_t launch_attn(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
                         const CUtensorMap& tk, const CUtensorMap& tv, int grid,
                         cudaStream_t s);
-cudaError_t set_attn2_trace(void* buf, int mode);
-cudaError_t set_attn3_trace(void* buf, int mode);
-cudaError_t set_attn4_trace(void* buf, int mode);
-// Fallback list of the fixed-reference kernel: work-list codes of items whose scores overshot
-// their reference max, recomputed by the running-max kernel.  count and flags (one bit per
+// Fallback list of the fixed-reference kernels: work-list codes of items whose scores overshot
+// their reference max, recomputed by attn_rect.cu's exact-max passes (modes 1 and 2).  count and flags (one bit per
 // work-list index) zero on entry; list has room for every work-list entry.
 struct Fallback {
     uint32_t* count;
     uint32_t* flags;
     uint32_t* list;
 };
-// Block 128, head_dim 128, fixed per-row reference max (attn4.cu).
-cudaError_t launch_attn_fixed_ref(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
-                                  const CUtensorMap& tv, int grid, const Fallback& fb,
-                                  cudaStream_t s);
-// Block 128, head_dim 128, one softmax group on every tile, P in its own TMEM buffer (attn5.cu).
+// Block 128 x 128, head_dim 128 or 64: one softmax group on every tile, SS S-MMAs (attn5.cu).
 cudaError_t set_attn5_trace(void* buf, int mode);
 cudaError_t launch_attn_sepp(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
                              const CUtensorMap& tv, int grid, const Fallback& fb,
@@ -159,12 +152,4 @@ cudaError_t launch_attn_sepp(const AttnArgs& a, const CUtensorMap& tq, const CUt
 cudaError_t launch_attn_rect(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
                              const CUtensorMap& tv, int grid, const Fallback& fb, int mode,
                              cudaStream_t s);
-// Block 128, head_dim 128, one CTA per query block with Q resident in TMEM (attn3.cu).
-cudaError_t launch_attn_q_tmem(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
-                               const CUtensorMap& tv, int grid, cudaStream_t s);
-// CTA-pair kernel (block 128, head_dim 128): work items are pairs of rows / anchor tiles.
-cudaError_t launch_attn_pair(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
-                             const CUtensorMap& tk_half, const CUtensorMap& tv, int grid,
-                             cudaStream_t s);
-
 }  // namespace csa

@@ -26,7 +26,10 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int mode, int tiles, long lon
     tc_fence_after();
     const uint32_t tmem = tmem_ptr;
     const int N = (mode == 1 || mode == 3) ? 256 : (mode == 4 ? 64 : 128);
-    const bool ts = mode == 2 || mode == 3;
+    const bool ts = mode == 2 || mode == 3 || mode == 7;
+    // 6: SS N128 into alternating accumulators [0,128) / [128,256); 7: TS N128 alternating;
+    // 8: FA-style mix per tile: SS QK (N128) into S[t&1], then TS P.V (N128) into O;
+    // 9: same mix with QK as TS (Q in TMEM); 10: 2 Q tiles: SS QK0, SS QK1, TS PV0, TS PV1.
     const uint32_t b_mn = mode == 5 ? 1u : 0u;
     const uint32_t idesc = umma_idesc_bf16(128, N, 0, b_mn);
     const uint32_t a_base = smem_u32(smem);              // 128 x 128 bf16, K-major SW128 (32 KB)
@@ -39,14 +42,52 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int mode, int tiles, long lon
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint32_t off = (kk & 3) * 32;
+                    if (mode >= 8) {
+                        const uint32_t idqk = umma_idesc_bf16(128, 128, 0, 0);
+                        const uint32_t idpv = umma_idesc_bf16(128, 128, 0, 1);
+                        const uint64_t kd = umma_desc_sw128(b_base + (kk >> 2) * 128 * 128 + off, 16, 1024);
+                        const uint64_t ad = umma_desc_sw128(a_base + (kk >> 2) * 16384 + off, 16, 1024);
+                        const uint64_t vd = umma_desc_sw128(b_base + kk * 16 * 128, 128 * 128, 1024);
+                        const uint32_t sb = (t & 1) * 128;
+                        if (mode == 8) {
+                            mma_ss(tmem + sb, ad, kd, idqk, kk > 0 ? 1u : 0u);
+                        } else if (mode == 9) {
+                            mma_ts(tmem + sb, tmem + 448 + kk * 8, kd, idqk, kk > 0 ? 1u : 0u);
+                        } else {
+                            mma_ss(tmem + 0, ad, kd, idqk, kk > 0 ? 1u : 0u);
+                        }
+                        continue;
+                    }
                     const uint64_t bd = b_mn ? umma_desc_sw128(b_base + kk * 16 * 128, N * 128, 1024)
                                              : umma_desc_sw128(b_base + (kk >> 2) * N * 128 + off,
                                                                16, 1024);
+                    const uint32_t dd = (mode == 6 || mode == 7) ? (t & 1) * 128 : 0;
                     if (ts) {
-                        mma_ts(tmem, tmem + 448 + kk * 8, bd, idesc, kk > 0 ? 1u : 0u);
+                        mma_ts(tmem + dd, tmem + 448 + kk * 8, bd, idesc, kk > 0 ? 1u : 0u);
                     } else {
                         const uint64_t ad = umma_desc_sw128(a_base + (kk >> 2) * 16384 + off, 16, 1024);
-                        mma_ss(tmem, ad, bd, idesc, kk > 0 ? 1u : 0u);
+                        mma_ss(tmem + dd, ad, bd, idesc, kk > 0 ? 1u : 0u);
+                    }
+                }
+                if (mode >= 8) {
+                    const uint32_t idqk = umma_idesc_bf16(128, 128, 0, 0);
+                    const uint32_t idpv = umma_idesc_bf16(128, 128, 0, 1);
+                    if (mode == 10) {
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {
+                            const uint32_t off = (kk & 3) * 32;
+                            const uint64_t kd = umma_desc_sw128(b_base + (kk >> 2) * 128 * 128 + off, 16, 1024);
+                            const uint64_t ad = umma_desc_sw128(a_base + (kk >> 2) * 16384 + off, 16, 1024);
+                            mma_ss(tmem + 128, ad, kd, idqk, kk > 0 ? 1u : 0u);
+                        }
+                    }
+                    const int npv = mode == 10 ? 2 : 1;
+                    for (int q = 0; q < npv; ++q) {
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {
+                            const uint64_t vd = umma_desc_sw128(b_base + kk * 16 * 128, 128 * 128, 1024);
+                            mma_ts(tmem + 256 + q * 128, tmem + (q * 128 + 64) + kk * 8, vd, idpv, 1u);
+                        }
                     }
                 }
             }
@@ -73,12 +114,13 @@ int main() {
     const int smem = 32768 + 65536;
     cudaFuncSetAttribute(mma_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const char* names[] = {"SS M128 N128", "SS M128 N256", "TS M128 N128", "TS M128 N256",
-                           "SS M128 N64", "SS M128 N128 B-MN"};
-    const int ns[] = {128, 256, 128, 256, 64, 128};
+                           "SS M128 N64", "SS M128 N128 B-MN", "SS N128 alt D", "TS N128 alt D",
+                           "mix SS-QK + TS-PV", "mix TS-QK + TS-PV", "2Q: 2xSS-QK + 2xTS-PV"};
+    const int ns[] = {128, 256, 128, 256, 64, 128, 128, 128, 256, 256, 512};
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int mode = 0; mode < 6; ++mode) {
+    for (int mode = 0; mode < 11; ++mode) {
         const int tiles = 4000;
         mma_loop<<<sms, 128, smem>>>(mode, 100, d_cyc);
         cudaEventRecord(e0);
@@ -96,7 +138,7 @@ int main() {
         avg /= sms;
         const double flop = 2.0 * 128 * ns[mode] * 128 * tiles * sms;
         printf("%-20s cyc/dispatch %7.1f  (floor %5.1f)  %7.1f TFLOP/s\n", names[mode],
-               avg / (tiles * 8.0), 128.0 * ns[mode] / 256.0, flop / (ms * 1e-3) / 1e12);
+               avg / (tiles * 8.0 * (ns[mode] > 256 ? ns[mode] / 128 : (mode >= 8 ? 2 : 1))), mode >= 8 ? 64.0 : 128.0 * ns[mode] / 256.0, flop / (ms * 1e-3) / 1e12);
     }
     return 0;
 }

@@ -152,8 +152,8 @@ def run_attention(csa, lay, q, k, v, masks=None, rep=None, anchor_k=2, order=2, 
 
 
 def fallback_count(csa, q):
-    """Items the fixed-reference kernel (attn5.cu / attn4.cu) handed to the running-max kernel in the last
-    dynamic launch on q's device: uint32 at byte 256 of the attention workspace (csa.h)."""
+    """Items the fixed-reference kernel (attn5.cu / attn_rect.cu) handed to the exact-max fallback
+    passes in the last launch on q's device: uint32 at byte 256 of the attention workspace."""
     ws = csa._sched_workspace(q.device, 0)  # current stream: the one the test launched on
     return int(ws[256:260].view(torch.int32).item())
 
@@ -188,22 +188,16 @@ def test_attention_tiny_masks(csa, name):
         assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 1e-3, cname
 
 
-@pytest.mark.parametrize("variant", [{}, {"CSA_ATTN4": "1"}, {"CSA_ATTN_RUNNING_MAX": "1"},
-                                     {"CSA_ATTN_RUNNING_MAX": "1", "CSA_ATTN_CG": "4"},
-                                     {"CSA_ATTN_V3": "1"}, {"CSA_ATTN_V3": "1", "CSA_EMU_EVERY": "4"}])
+@pytest.mark.parametrize("lay,d", [(Layout(2, 9, 40, 128), 128), (Layout(2, 9, 40, 128), 64),
+                                   (Layout(2, 5, 25, 64), 64)])
 @pytest.mark.parametrize("jump", [3.0, 40.0])
-def test_attention_running_max_jumps(csa, variant, jump, monkeypatch):
-    """Key blocks whose scores grow block by block: later tiles exceed the running max (lazy
-    rescale / overflow-guard redo paths, including jumps far beyond 2^8); ragged last block.
-    Covers the production fixed-reference kernel (jump 40 overshoots the reference max by far
-    more than 2^56: every such item goes through the fallback), the running-max Q-in-TMEM kernel
-    (column split over 2 or 4 warp groups) and the shared-memory-Q kernel with and without its
-    polynomial exp2."""
-    for key, val in variant.items():
-        monkeypatch.setenv(key, val)
-    lay = Layout(2, 9, 40, 128)
+def test_attention_running_max_jumps(csa, lay, d, jump):
+    """Key blocks whose scores grow block by block: later tiles exceed the first tile's max (the
+    fixed reference of the block-128 kernels; the running max and lazy rescale of attn.cu at
+    block 64), including jumps far beyond 2^56; ragged last block.  At jump 40 every block-128
+    item overshoots its reference and goes through the exact-max fallback passes."""
     heads, nb = 2, lay.NB
-    q, k, v = qkv(1, lay.N, heads, 128, seed=21, device="cuda")
+    q, k, v = qkv(1, lay.N, heads, d, seed=21, device="cuda")
     gain = torch.ones(lay.N, device="cuda")
     for c in range(nb):
         gain[c * 128:(c + 1) * 128] = 1.0 + jump * c / nb
@@ -216,9 +210,9 @@ def test_attention_running_max_jumps(csa, variant, jump, monkeypatch):
     lse_np = lse.view(heads, lay.N).cpu().numpy()
     for h in range(heads):
         ref, ref_lse = oracle_head(lay, q, k, v, 0, h, mask=masks[h])
-        assert_close(out[0, :, h].double().cpu().numpy(), ref, f"{variant} jump {jump} h{h}")
+        assert_close(out[0, :, h].double().cpu().numpy(), ref, f"d{d} jump {jump} h{h}")
         assert np.abs(lse_np[h] - ref_lse).max() <= 1e-3 * max(1.0, np.abs(ref_lse).max())
-    if not variant or "CSA_ATTN4" in variant:  # the fixed-reference kernels (attn5 / attn4)
+    if lay.B == 128:  # the fixed-reference kernels
         n_fb = fallback_count(csa, q)
         assert (n_fb > 0) if jump > 10 else (n_fb == 0), n_fb
 
@@ -265,7 +259,8 @@ def test_attention_tiny_repetitive(csa):
 
 @pytest.mark.parametrize("lay,d", [(Layout(2, 5, 25, 64), 64), (Layout(2, 9, 40, 128), 128)])
 def test_attention_batch2_shares_plan_and_is_deterministic(csa, lay, d):
-    """Both kernels: attn.cu (B 64) and the production Q-in-TMEM kernel (B 128, d 128)."""
+    """Both kernels: attn.cu (B 64, dynamic and static assignment) and the production kernel
+    (attn5.cu, B 128, d 128)."""
     q, k, v = qkv(2, lay.N, 3, d, seed=7, device="cuda")
     rng = np.random.default_rng(1)
     masks = (rng.random((3, lay.NB, lay.NB)) < 0.5).astype(np.uint8)
@@ -274,13 +269,9 @@ def test_attention_batch2_shares_plan_and_is_deterministic(csa, lay, d):
     for order in (0, 1):
         out2, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[2], anchor_k=2, order=order)
         assert torch.equal(out, out2)  # item order never changes per-item arithmetic
-    static = csa.sparse_attn_fwd(q, k, v, plan, csa.build_work_list(plan, 0, 3), dynamic=False)
-    static2 = csa.sparse_attn_fwd(q, k, v, plan, csa.build_work_list(plan, 0, 3), dynamic=False)
-    assert torch.equal(static, static2)
-    if d == 128:  # static -> running-max kernel, dynamic -> fixed-reference kernel (csa.h)
-        assert (static.float() - out.float()).abs().max().item() <= 2 * MAX_ABS
-    else:
-        assert torch.equal(out, static)  # dynamic vs static scheduling, same kernel
+    if lay.B == 64:  # static round-robin assignment (no workspace): same kernel, same bits
+        static = csa.sparse_attn_fwd(q, k, v, plan, csa.build_work_list(plan, 0, 3), dynamic=False)
+        assert torch.equal(out, static)
     again, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[2], anchor_k=2)
     assert torch.equal(out, again)  # run-to-run determinism (scheduler counters self-reset)
     for b in range(2):
@@ -409,29 +400,6 @@ def test_calibration_full_size_sampled(csa, name):
         assert np.abs(E[h, r] - E_ref[0]).max() <= 5e-5
         if not np.array_equal(oracle.select(E_ref[0], eps), cnt[h, r]):  # contract 4
             assert _borderline(E_ref[0], eps), (h, r)
-
-
-# ---------------------------------------------------------------- CTA-pair kernel (order 3)
-@pytest.mark.parametrize("lay,heads", [(Layout(2, 9, 40, 128), 3), (Layout(21, 30, 52, 128), 6)])
-def test_pair_kernel_matches_single_and_oracle(csa, lay, heads):
-    """The cta_group::2 kernel walks the union of two rows' lists (P = 0 for the other row's
-    keys).  Its softmax offloads a different share of exponentials to the polynomial than the
-    production kernel, so the two agree to bf16 rounding, not bit for bit; both meet the oracle
-    tolerance."""
-    rng = np.random.default_rng(heads)
-    masks = (rng.random((heads, lay.NB, lay.NB)) < 0.4).astype(np.uint8)
-    masks[:, np.arange(lay.NB), np.arange(lay.NB)] = 1
-    q, k, v = qkv(1, lay.N, heads, 128, seed=5, device="cuda")
-    rep = [heads - 1]
-    single, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=rep, anchor_k=5, order=2)
-    pair, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=rep, anchor_k=5, order=3)
-    assert (single.float() - pair.float()).abs().max().item() <= 8e-3
-    for h, r in ((0, 0), (heads - 2, lay.NB - 1), (heads - 1, 1)):
-        rows = (r * 128, min((r + 1) * 128, lay.N))
-        ref, _ = oracle_head(lay, q, k, v, 0, h, mask=masks[h],
-                             rep_k=5 if h in rep else None, rows=rows)
-        assert_close(pair[0, rows[0]:rows[1], h].double().cpu().numpy(), ref, f"h{h} r{r}")
-        assert_close(single[0, rows[0]:rows[1], h].double().cpu().numpy(), ref, f"h{h} r{r}")
 
 
 # ---------------------------------------------------------------- f1 spatial similarity
@@ -703,23 +671,6 @@ def test_rect_attention_overflow_fallback(csa, bkv, d):
         ref, ref_lse = oracle_head(lay, q, k, v, 0, h, mask=masks[h])
         assert_close(out[0, :, h].double().cpu().numpy(), ref, f"B_kv {bkv} h{h}")
         assert np.abs(lse_np[h] - ref_lse).max() <= 1e-3 * max(1.0, np.abs(ref_lse).max())
-
-
-def test_rect_kernel_at_128_matches_production(csa, monkeypatch):
-    """The generic B_kv kernel instantiated at 128 (CSA_ATTN_RECT) against the oracle and the
-    production square kernel (same reference-max arithmetic: equal within bf16 rounding of P)."""
-    lay = Layout(2, 9, 40, 128)
-    q, k, v = qkv(1, lay.N, 3, 128, seed=8, device="cuda")
-    rng = np.random.default_rng(3)
-    masks = (rng.random((3, lay.NB, lay.NB)) < 0.5).astype(np.uint8)
-    masks[:, np.arange(lay.NB), np.arange(lay.NB)] = 1
-    prod, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[1], anchor_k=2)
-    monkeypatch.setenv("CSA_ATTN_RECT", "1")
-    rect, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[1], anchor_k=2)
-    for h in range(3):
-        ref, _ = oracle_head(lay, q, k, v, 0, h, mask=masks[h], rep_k=2 if h == 1 else None)
-        assert_close(rect[0, :, h].double().cpu().numpy(), ref, f"h{h}")
-    assert (rect.float() - prod.float()).abs().max().item() <= 2 * MAX_ABS
 
 
 @pytest.mark.parametrize("bkv", [64, 176])

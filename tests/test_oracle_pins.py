@@ -361,24 +361,37 @@ def test_geometry(orc):
     assert orc.num_blocks(75600, 128) == 591
 
 
-def test_work_list_is_sorted_permutation(orc):
-    rng = np.random.default_rng(3)
-    n, b, F, W = 250, 64, 2, 25
-    nb = 4
-    kinds = np.array([0, 1, 0, 0], np.uint8)
-    ak = np.array([0, 2, 0, 0], np.int32)
-    nnz = rng.integers(1, nb + 1, size=(4, nb)).astype(np.int32)
-    wl = orc.work_list(n, b, F, W, kinds, ak, nnz)
-    nu = (F * 2 * W + 127) // 128
-    assert wl.size == 3 * nb + nu
-    items = []
-    for code in wl:
-        kind, h, idx = int(code) >> 31, (int(code) >> 20) & 0x7FF, int(code) & 0xFFFFF
-        cost = nb if kind else int(nnz[h, idx])
-        items.append((-cost, h, kind, idx))
-    assert items == sorted(items)
-    assert sorted((h, k, i) for _, h, k, i in items) == sorted(
-        [(h, 0, r) for h in (0, 2, 3) for r in range(nb)] + [(1, 1, u) for u in range(nu)])
+_WL_KEYS = {  # the total orders csa.h states for csa_build_work_list, written out as sort keys
+    0: lambda h, kind, idx, cost: (-cost, h, kind, idx),   # longest-first, ties (h, kind, idx)
+    1: lambda h, kind, idx, cost: (h, kind, idx),          # natural
+    2: lambda h, kind, idx, cost: (h, -cost, kind, idx),   # head-major, longest-first in a head
+}
+
+
+@pytest.mark.parametrize("order", [0, 1, 2])
+@pytest.mark.parametrize("seed", [3, 4])
+def test_work_list_is_sorted_permutation(orc, order, seed):
+    """Every order is the enumeration of all items (MASK rows, REPETITIVE anchor tiles) sorted by
+    its key, built here from scratch with Python's sorted(): a flipped comparison, a dropped
+    tie-break or a missing item fails.  Costs drawn from a small range so ties are frequent."""
+    rng = np.random.default_rng(seed)
+    n, b, F, W = 250 * 4, 64, 2, 25
+    nb = -(-n // b)
+    kinds = np.array([0, 1, 0, 0, 1], np.uint8)
+    ak = np.array([0, 2, 0, 0, 5], np.int32)
+    nnz = rng.integers(1, 4, size=(kinds.size, nb)).astype(np.int32)
+    wl = orc.work_list(n, b, F, W, kinds, ak, nnz, order=order)
+    expect = []
+    for h in range(kinds.size):
+        if kinds[h]:
+            for u in range(-(-F * int(ak[h]) * W // 128)):
+                expect.append((h, 1, u, nb))
+        else:
+            for r in range(nb):
+                expect.append((h, 0, r, int(nnz[h, r])))
+    expect.sort(key=lambda t: _WL_KEYS[order](*t))
+    got = [((int(c) >> 20) & 0x7FF, int(c) >> 31, int(c) & 0xFFFFF) for c in wl]
+    assert got == [(h, kind, idx) for h, kind, idx, _ in expect]
 
 
 def test_pair_work_list_covers_every_row_once(orc):
