@@ -33,6 +33,8 @@ sys.path.insert(0, ROOT)
 from paper_2603_05503_b200 import inputs, ulysses  # noqa: E402
 
 METRIC = "effective attn TFLOP/s & % bf16 roofline, speedup vs dense, 1/2/4/8 B200"
+ANCHOR_K = 5          # anchor rows of a REPETITIVE head (k of P:616-622, Table)
+MAX_ABS, MEAN_ABS = 2e-2, 2e-3   # north-star tolerances (bf16 I/O, fp32 accumulation)
 
 
 def parse():
@@ -130,7 +132,16 @@ def workload(cfg, args, heads_lo, heads_hi, rank_dev):
     lay = cfg.layout
     rep = set(np.linspace(0, cfg.heads - 1, args.rep_heads).astype(int).tolist()) if args.rep_heads else set()
     if cfg.sparsity is not None:
-        masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity, seed=0)
+        # The BASELINE sparsity is the layer's TOTAL (P:680 / P:688 count the repetition heads'
+        # anchor-only area too, reading Q19): the MASK heads' generator-S target is set so that
+        # sum(MASK kept areas) + |rep| * F k W N = (1 - sparsity) H N^2, i.e. every anchor head
+        # keeps k / H_rows of its dense area.
+        mask_heads = [h for h in range(cfg.heads) if h not in rep]
+        rep_kept = ANCHOR_K / lay.H
+        mask_kept = ((1.0 - cfg.sparsity) * cfg.heads - len(rep) * rep_kept) / len(mask_heads)
+        mm = inputs.synthetic_masks(lay, len(mask_heads), 1.0 - mask_kept, seed=0)
+        masks = np.ones((cfg.heads, lay.NB, lay.NB), np.uint8)   # REPETITIVE cells: unused
+        masks[mask_heads] = mm
         counts = masks.astype(np.uint16) * np.uint16(64)
         return lay, masks, rep, counts, 32, None
     from paper_2603_05503_b200 import csa
@@ -196,6 +207,9 @@ def flops_of(lay, masks, rep, heads, d, batch, anchor_k=5):
 
 
 def time_loop(fn, steps, warmup, stream):
+    """W untimed warm-ups, then K steps bracketed by (barrier +) synchronize on both sides, CUDA
+    events on `stream` around the whole region and around every step.  Returns (total ms, per-step
+    ms list, the last step's return value -- the timed output the parity gate checks)."""
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
@@ -205,84 +219,184 @@ def time_loop(fn, steps, warmup, stream):
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     per = []
+    last = None
     start.record(stream)
     for _ in range(steps):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        fn()
+        last = fn()
         e1.record(stream)
         per.append((e0, e1))
     end.record(stream)
     torch.cuda.synchronize()
+    if torch.distributed.is_initialized():
+        torch.distributed.barrier()
     total = start.elapsed_time(end)
-    return total, [a.elapsed_time(b) for a, b in per]
+    return total, [a.elapsed_time(b) for a, b in per], last
 
 
-def cpu_oracle_sample(lay, cfg, masks, rep, q, k, v, seconds_target=12.0, anchor_k=5):
-    """The fp64 oracle, as it stands, on a bounded sample of (head, query-block) units of the same
-    workload, one host thread per unit (ctypes releases the GIL)."""
-    import concurrent.futures
+def pct(xs, p):
+    xs = sorted(xs)
+    return xs[min(len(xs) - 1, max(0, int(round(p / 100.0 * (len(xs) - 1)))))]
 
+
+def host_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"host_cores": os.cpu_count() or 1,
+            "host_cores_usable": len(os.sched_getaffinity(0)), "cpu_model": model}
+
+
+class OracleHeads:
+    """fp64 host copies of single heads of Q, K, V (the oracle's inputs: the same bf16 values
+    the GPU reads, widened exactly)."""
+
+    def __init__(self, q, k, v):
+        self.t = (q, k, v)
+        self.cache = {}
+
+    def __call__(self, h):
+        if h not in self.cache:
+            self.cache[h] = tuple(x[0, :, h].double().cpu().numpy() for x in self.t)
+        return self.cache[h]
+
+
+def oracle_unit(lay, heads64, masks, rep, h, rows, d):
+    """Oracle output rows [r0, r1) of head h (MASK: masked softmax over the kept blocks, P:647-653;
+    REPETITIVE: anchor-row attention + broadcast) and the unit's kept FLOPs."""
     import oracle
 
-    cores = os.cpu_count() or 1
-    threads = min(cores, 16)
-    rng = np.random.default_rng(0)
-    heads = list(range(cfg.heads))
-    units = []
+    qh, kh, vh = heads64(h)
+    scale = 1.0 / math.sqrt(d)
+    if h in rep:
+        out, _ = oracle.anchor_attention_rows(lay.F, lay.H, lay.W, qh, kh, vh, scale, ANCHOR_K, rows)
+        return out, 4.0 * d * (rows[1] - rows[0]) * lay.N * ANCHOR_K / lay.H
+    out, _ = oracle.masked_attention_rows(qh, kh, vh, scale, lay.B, masks[h], rows)
     sizes = np.array([lay.block_size(c) for c in range(lay.NB)], np.int64)
-    # probe one unit to size the sample to ~seconds_target of wall time
-    t_probe = None
-    done_flops = 0.0
-    q64 = {}
+    r = rows[0] // lay.B
+    return out, 4.0 * d * (rows[1] - rows[0]) * float(masks[h, r].astype(np.int64) @ sizes)
 
-    def head_arrays(h):
-        if h not in q64:
-            q64[h] = tuple(t[0, :, h].double().cpu().numpy() for t in (q, k, v))
-        return q64[h]
 
-    def run(unit):
-        h, r = unit
-        qh, kh, vh = head_arrays(h)
-        rows = (r * lay.B, min((r + 1) * lay.B, lay.N))
-        scale = 1.0 / math.sqrt(q.shape[3])
-        if h in rep:
-            oracle.anchor_attention_rows(lay.F, lay.H, lay.W, qh, kh, vh, scale, anchor_k, rows)
-            return 4.0 * q.shape[3] * (rows[1] - rows[0]) * lay.N
-        oracle.masked_attention_rows(qh, kh, vh, scale, lay.B, masks[h], rows)
-        return 4.0 * q.shape[3] * (rows[1] - rows[0]) * float(masks[h, r].astype(np.int64) @ sizes)
-
+def parity_units(lay, masks, rep, heads, seed, n_random=8, row_range=None):
+    """Sampled (head, rows) units of a launch: per sampled MASK head the rows of its emptiest,
+    median and fullest query block, block 0 and the ragged last block; REPETITIVE heads' first
+    and last block (the broadcast rows); plus random blocks.  row_range restricts rows to a
+    token shard (multi-GPU: the rank's sequence shard)."""
+    rng = np.random.default_rng(seed)
+    lo, hi = (0, lay.N) if row_range is None else row_range
+    blocks = [r for r in range(lay.NB) if r * lay.B < hi and min((r + 1) * lay.B, lay.N) > lo]
     mask_heads = [h for h in heads if h not in rep]
-    probe = (mask_heads[0], lay.NB // 2)
-    head_arrays(probe[0])
-    t0 = time.perf_counter()
-    run(probe)
-    t_probe = time.perf_counter() - t0
-    n_units = max(threads, int(seconds_target / max(t_probe, 1e-3)) * threads // max(threads, 1))
-    n_units = min(n_units, 4 * threads)
-    for _ in range(n_units):
-        h = int(rng.choice(mask_heads))
-        units.append((h, int(rng.integers(lay.NB))))
-    for h in {u[0] for u in units}:
-        head_arrays(h)
+    rep_heads = [h for h in heads if h in rep]
+    units = set()
+    for h in (mask_heads[:1] + mask_heads[-1:] + list(rng.choice(mask_heads, 2))):
+        h = int(h)
+        nnz = masks[h][blocks].sum(axis=1)
+        order = np.argsort(nnz, kind="stable")
+        for r in {blocks[order[0]], blocks[order[len(order) // 2]], blocks[order[-1]],
+                  blocks[0], blocks[-1]}:
+            units.add((h, r))
+    for h in rep_heads[:2]:
+        units.add((h, blocks[0]))
+        units.add((h, blocks[-1]))
+    for _ in range(n_random):
+        units.add((int(rng.choice(list(heads))), int(rng.choice(blocks))))
+    return [(h, (max(r * lay.B, lo), min((r + 1) * lay.B, lay.N, hi))) for h, r in sorted(units)]
+
+
+def run_oracle(units, fn, threads):
+    """fn(unit) on a host thread pool (the C oracle releases the GIL).  Returns (results, wall s)."""
+    import concurrent.futures
+
     t0 = time.perf_counter()
     with concurrent.futures.ThreadPoolExecutor(threads) as ex:
-        done_flops = sum(ex.map(run, units))
-    wall = time.perf_counter() - t0
-    return {"value": done_flops / wall / 1e12, "unit": "TFLOP/s", "cores": threads,
-            "kind": "oracle",
-            "sample": f"{len(units)} random (head, query-block) MASK units of {cfg.name} "
-                      f"(128 query rows each, kept keys only), fp64 C oracle, {threads} host "
-                      f"threads, {wall:.1f} s wall; value = sampled kept FLOP / wall"}
+        res = list(ex.map(fn, units))
+    return res, time.perf_counter() - t0
+
+
+def parity_stats(got_rows, ref_rows):
+    """(max |dO|, sum |dO|, count) over compared elements."""
+    mx, sm, cnt = 0.0, 0.0, 0
+    for g, r in zip(got_rows, ref_rows):
+        e = np.abs(g - r)
+        mx = max(mx, float(e.max()))
+        sm += float(e.sum())
+        cnt += e.size
+    return mx, sm, cnt
+
+
+def parity_record(mx, sm, cnt, n_units, where):
+    mean = sm / max(cnt, 1)
+    return {"max_abs": mx, "mean_abs": mean, "units": n_units, "elements": cnt,
+            "tol": {"max_abs": MAX_ABS, "mean_abs": MEAN_ABS},
+            "pass": bool(mx <= MAX_ABS and mean <= MEAN_ABS), "checked": where}
+
+
+def cpu_oracle_sample(lay, cfg, masks, rep, heads64, seconds_target=12.0, extra_units=()):
+    """The fp64 oracle, as it stands, on a bounded sample of (head, query-block) units of the same
+    workload (~seconds_target of host wall time), one host thread per unit.  extra_units are
+    computed in the same pool (the parity units); returns (cpu_baseline dict, their outputs)."""
+    threads = len(os.sched_getaffinity(0))
+    rng = np.random.default_rng(0)
+    mask_heads = [h for h in range(cfg.heads) if h not in rep]
+    probe = (mask_heads[0], (lay.NB // 2 * lay.B, lay.NB // 2 * lay.B + lay.B))
+    t0 = time.perf_counter()
+    oracle_unit(lay, heads64, masks, rep, probe[0], probe[1], cfg.d)
+    t_probe = time.perf_counter() - t0
+    n_units = int(seconds_target / max(t_probe, 1e-3)) * threads
+    n_units = max(threads, min(n_units, 4 * threads) - len(extra_units))
+    units = list(extra_units)
+    for _ in range(n_units):
+        h = int(rng.choice(mask_heads))
+        r = int(rng.integers(lay.NB))
+        units.append((h, (r * lay.B, min((r + 1) * lay.B, lay.N))))
+    for h in {u[0] for u in units}:
+        heads64(h)
+    res, wall = run_oracle(units, lambda u: oracle_unit(lay, heads64, masks, rep, u[0], u[1], cfg.d),
+                           threads)
+    flops = sum(f for _, f in res)
+    return ({"value": flops / wall / 1e12, "unit": "TFLOP/s", "cores": threads, **host_info(),
+             "kind": "oracle",
+             "sample": f"{len(units)} (head, query-block) units of {cfg.name} ({len(extra_units)} "
+                       f"stratified parity units incl. anchor heads and the ragged last block, "
+                       f"the rest random MASK blocks; 128 query rows each, kept keys only), fp64 C "
+                       f"oracle, {threads} host threads, {wall:.1f} s wall; value = sampled kept "
+                       f"FLOP / wall"},
+            [o for o, _ in res[:len(extra_units)]])
+
+
+def relaunch(args):
+    """`bench.py --gpus N` (N > 1) started without torchrun: re-exec under torch.distributed.run
+    with one rank per GPU, or fail loudly when fewer than N GPUs are visible."""
+    n_dev = torch.cuda.device_count()
+    if n_dev < args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus}: only {n_dev} CUDA device(s) visible; "
+                         f"refusing to report a smaller job")
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        sys.exit(relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.gpus != world and world > 1:
+    if args.impl != "reference" and args.gpus != world:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
     cfg = inputs.CONFIGS[args.config]
     lay = cfg.layout
@@ -322,9 +436,7 @@ def main():
     counts = torch.from_numpy(counts_np.reshape(-1).view(np.int16)).to(dev).view(torch.uint16)
     sim = torch.tensor([calib["similarity"][h] if calib is not None else (1.0 if h in rep else 0.0)
                         for h in my_heads], dtype=torch.float64, device=dev)
-    t0 = time.perf_counter()
-    plan = csa.compile_plan(lay, counts, min_count, similarity=sim, gamma=0.87, anchor_k=5)
-    # pair items for the CTA-pair kernel (block 128, d 128), else head-major single items
+    plan = csa.compile_plan(lay, counts, min_count, similarity=sim, gamma=0.87, anchor_k=ANCHOR_K)
     work = csa.build_work_list(plan, 0, hp, order=csa.default_order(lay, d))
     torch.cuda.synchronize()
     flop_rank, _ = flops_of(lay, masks, rep, my_heads, d, B)
@@ -335,15 +447,22 @@ def main():
     # ---- inputs: full-sequence tensors generated identically on every rank, then sliced
     q, k, v = inputs.qkv(B, lay.N, H, d, seed=11, device=dev)
     out = torch.empty((B, lay.N, hp, d), dtype=torch.bfloat16, device=dev)
+    heads64 = OracleHeads(q, k, v)
 
     chunks = args.overlap_chunks or max(c for c in range(1, 6) if hp % c == 0)
     if not exchange:
         def step():
             return csa.sparse_attn_fwd(q, k, v, plan, work, out=out)
+        units = parity_units(lay, masks, rep, list(range(H)), seed=rank)
     else:
         # kernel-only reference for the roofline: this rank's heads, full sequence
         qh0, kh0, vh0 = (t[:, :, my_heads].contiguous() for t in (q, k, v))
         ql, kl, vl = (ulysses.sequence_shard(t[:, :, perm], world, rank) for t in (q, k, v))
+        n_loc = lay.N // world
+        units = parity_units(lay, masks, rep, list(range(H)), seed=rank, n_random=2,
+                             row_range=(rank * n_loc, (rank + 1) * n_loc))
+        for h in {u[0] for u in units}:
+            heads64(h)            # host copies before the full tensors are dropped
         del q, k, v
         q = k = v = None
 
@@ -367,7 +486,7 @@ def main():
         step = layer_step(ql, kl, vl)
 
     with ClockSampler(local) as clk:
-        total_ms, per = time_loop(step, args.steps, args.warmup, stream)
+        total_ms, per, last = time_loop(step, args.steps, args.warmup, stream)
     ms = total_ms / args.steps
     ms_t = torch.tensor([ms], device=dev)
     if exchange:
@@ -375,7 +494,36 @@ def main():
     ms = float(ms_t.item())
     value = flop_all / (ms * 1e-3) / 1e12
 
+    # ---- parity gate on the TIMED output (the last timed step's result), sampled units
+    if exchange:
+        # last: this rank's [B, N/P, H, d] sequence shard, head positions in perm order
+        n_loc = lay.N // world
+        got = [last[0, r0 - rank * n_loc:r1 - rank * n_loc, perm.index(h)].double().cpu().numpy()
+               for h, (r0, r1) in units]
+        refs, _ = run_oracle(units, lambda u: oracle_unit(lay, heads64, masks, rep, u[0], u[1], d)[0],
+                             len(os.sched_getaffinity(0)))
+        mx, sm, cnt = parity_stats(got, refs)
+        st = torch.tensor([mx, sm, cnt, len(units)], device=dev, dtype=torch.float64)
+        mx_t, rest = st[:1].clone(), st[1:].clone()
+        torch.distributed.all_reduce(mx_t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(rest, op=torch.distributed.ReduceOp.SUM)
+        parity = parity_record(float(mx_t), float(rest[0]), int(rest[1]), int(rest[2]),
+                               "every rank's sequence shard of the timed output vs fp64 oracle")
+        cpu_base = None
+    else:
+        got = [last[0, r0:r1, h].double().cpu().numpy() for h, (r0, r1) in units]
+        cpu_base, refs = (None, None)
+        if rank == 0 and not args.no_extras:
+            cpu_base, refs = cpu_oracle_sample(lay, cfg, masks, rep, heads64, extra_units=units)
+        else:
+            refs, _ = run_oracle(units,
+                                 lambda u: oracle_unit(lay, heads64, masks, rep, u[0], u[1], d)[0],
+                                 len(os.sched_getaffinity(0)))
+        parity = parity_record(*parity_stats(got, refs), len(units),
+                               "timed output vs fp64 oracle")
+
     pk = peaks()
+    per_ms = sorted(per)
     result = {
         "metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
@@ -385,15 +533,19 @@ def main():
                  "synthetic (seeded N(0,1) bf16 Q/K/V; plan calibrated by this repo's a2-a6 path "
                  "on 8 generator-G prompts)"),
         "config": arm_config(cfg, B, kept_fraction, rep, world),
+        "t_ms": {"median": round(statistics.median(per_ms), 4), "p10": round(pct(per_ms, 10), 4),
+                 "p90": round(pct(per_ms, 90), 4), "rank": rank},
+        "parity": parity,
         "gpu_launches": args.steps * launches_per_call(lay, d) * (chunks if exchange else 1),
         **({"calibration": calib} if calib is not None else {}),
         "clocks": clk.summary(),
     }
     if exchange:
         result["config"]["exchange_overlap_chunks"] = chunks
+        result["config"]["exchange"] = "stacked QKV all_to_all_single (1 per chunk) + O return"
         # roofline of the attention kernel on this rank (launches alone, no exchange), the
         # slowest rank's: achieved = its kept FLOPs / its mean launch time
-        _, per_k = time_loop(lambda: run_heads(qh0, kh0, vh0), args.steps, 2, stream)
+        _, per_k, _ = time_loop(lambda: run_heads(qh0, kh0, vh0), args.steps, 2, stream)
         ms_k = statistics.mean(per_k)
         mk = torch.tensor([ms_k, flop_rank, -ms_k], device=dev, dtype=torch.float64)
         gathered = [torch.zeros_like(mk) for _ in range(world)]
@@ -406,7 +558,8 @@ def main():
                               "peak_src": f"{pk['src']} bf16 burst",
                               "kernel": attention_kernel_name(lay, cfg.d) + ", slowest rank",
                               "algorithmic_flop_per_launch": float(slow[1]),
-                              "kernel_ms_per_rank": [round(float(t[0]), 3) for t in gathered]}
+                              "kernel_ms_per_rank": [round(float(t[0]), 3) for t in gathered],
+                              "step_ms_vs_kernel_ms": round(ms / float(slow[0]), 4)}
         # e2e at N GPUs through the public API: every step copies this rank's sequence shard of
         # Q, K, V in from pinned host memory, runs the head-sharded layer (a2a, attention, a2a)
         # and copies the rank's output shard back; max over ranks.  Bytes are whole-job totals.
@@ -422,7 +575,7 @@ def main():
             ho.copy_(step_e2e(), non_blocking=True)
 
         n_e2e = max(2, args.steps // 3)
-        t_e2e, _ = time_loop(e2e_step, n_e2e, 1, stream)
+        t_e2e, _, _ = time_loop(e2e_step, n_e2e, 1, stream)
         te = torch.tensor([t_e2e / n_e2e], device=dev)
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
         t_e2e = float(te.item())
@@ -433,7 +586,11 @@ def main():
     if rank == 0 and not exchange and not args.no_extras:
         extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_all, dense_flop,
                kept_fraction, per, pk, stream, dev, csa)
+        result["cpu_baseline"] = cpu_base
     if rank == 0:
+        if not parity["pass"]:  # a perf number without passing parity is not reported
+            result["value"] = None
+            result["parity_failed"] = True
         line = json.dumps(result)
         print(line, flush=True)
         if args.json_out:
@@ -441,23 +598,23 @@ def main():
                 fh.write(line + "\n")
     if exchange:
         torch.distributed.destroy_process_group()
+    if not parity["pass"]:
+        sys.exit(3)
 
 
 def attention_kernel_name(lay, d):
-    """The kernel csa_sparse_attn_fwd runs for this shape with a workspace (api.cu dispatch)."""
-    if lay.B == 128 and d == 128 and not os.environ.get("CSA_ATTN_V3"):
-        if os.environ.get("CSA_ATTN_RUNNING_MAX"):
-            return "sparse_attn_q_tmem_kernel (attn3.cu)"
-        if os.environ.get("CSA_ATTN4"):
-            return "sparse_attn_fixed_ref_kernel (attn4.cu)"
+    """The kernel csa_sparse_attn_fwd runs for this shape (api.cu dispatch)."""
+    if lay.B == 128 and lay.Bkv == 128:
         return "sparse_attn_sepp_kernel (attn5.cu)"
+    if lay.B == 128:
+        return f"sparse_attn_rect_kernel<{lay.Bkv},{d}> (attn_rect.cu)"
     return f"sparse_attn_kernel<{lay.B},{d}> (attn.cu)"
 
 
 def launches_per_call(lay, d):
-    """Our kernels per csa_sparse_attn_fwd call: the fixed-reference kernel is followed by the
-    running-max kernel over its (normally empty) fallback list."""
-    return 2 if attention_kernel_name(lay, d).endswith(("(attn4.cu)", "(attn5.cu)")) else 1
+    """Our kernels per csa_sparse_attn_fwd call: at block 128 the fixed-reference kernel is
+    followed by the two exact-max passes over its (normally empty) fallback list."""
+    return 3 if lay.B == 128 else 1
 
 
 def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_all, dense_flop,
@@ -482,14 +639,14 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
     ones = torch.full((H * lay.NB * lay.NB,), 64, dtype=torch.int16, device=dev).view(torch.uint16)
     plan1 = csa.compile_plan(lay, ones, 32)
     work1 = csa.build_work_list(plan1, 0, H, order=csa.default_order(lay, d))
-    t_dense, _ = time_loop(lambda: csa.sparse_attn_fwd(q, k, v, plan1, work1, out=out),
-                           max(2, args.steps // 3), 2, stream)
+    t_dense, _, _ = time_loop(lambda: csa.sparse_attn_fwd(q, k, v, plan1, work1, out=out),
+                              max(2, args.steps // 3), 2, stream)
     t_dense /= max(2, args.steps // 3)
     sdpa_ms = None
     try:
         qt, kt, vt = (t.transpose(1, 2) for t in (q, k, v))
         f = lambda: torch.nn.functional.scaled_dot_product_attention(qt, kt, vt)
-        t_s, _ = time_loop(f, 2, 1, stream)
+        t_s, _, _ = time_loop(f, 2, 1, stream)
         sdpa_ms = t_s / 2
     except Exception as e:  # library comparator only
         sdpa_ms = f"unavailable: {e}"
@@ -508,13 +665,14 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
     counts_c = torch.zeros(H * lay.NB * lay.NB, dtype=torch.int16, device=dev).view(torch.uint16)
     # eps(t=25 of T=50) from Eq. eq:epsilon_schedule with A(N), host fp64
     eps = 0.796 + 1.41e-6 * lay.N + (0.99 - (0.796 + 1.41e-6 * lay.N)) * math.exp(-16 * 25 / 50)
-    t_cal, _ = time_loop(lambda: csa.calib_accumulate(lay, q[:1], k[:1], eps, counts_c), 1, 1, stream)
-    t_cal2, _ = time_loop(lambda: csa.calib_accumulate(lay, q[:1], k[:1], eps, counts_c,
+    t_cal, _, _ = time_loop(lambda: csa.calib_accumulate(lay, q[:1], k[:1], eps, counts_c), 1, 1,
+                            stream)
+    t_cal2, _, _ = time_loop(lambda: csa.calib_accumulate(lay, q[:1], k[:1], eps, counts_c,
                                                        single_pass=False), 1, 1, stream)
     lse_c = torch.empty(H * lay.N, dtype=torch.float32, device=dev)
     csa.calib_accumulate(lay, q[:1], k[:1], eps, counts_c, lse_out=lse_c)
     sim_c = torch.zeros(H, dtype=torch.float64, device=dev)
-    t_sim, _ = time_loop(lambda: csa.spatial_similarity(lay, q[:1], k[:1], lse_c, 5, sim_c), 1, 1,
+    t_sim, _, _ = time_loop(lambda: csa.spatial_similarity(lay, q[:1], k[:1], lse_c, 5, sim_c), 1, 1,
                          stream)
     ph["spatial_similarity_ms"] = round(t_sim, 3)          # f1: 2 exps per score
     ph["calib_accumulate_ms"] = round(t_cal, 3)             # single exponential pass (scratch)
@@ -551,14 +709,12 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
             ho.copy_(csa.sparse_attn_fwd(dq, dk, dv, plan, work, out=out), non_blocking=True)
 
     n_e2e = max(2, args.steps // 3)
-    t_e2e, _ = time_loop(e2e_step, n_e2e, 1, stream)
+    t_e2e, _, _ = time_loop(e2e_step, n_e2e, 1, stream)
     t_e2e /= n_e2e
     result["e2e"] = {"value": round(flop_all / (t_e2e * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
                      "ms_per_step": round(t_e2e, 3),
                      "h2d_bytes_per_step": 3 * q.numel() * 2, "d2h_bytes_per_step": out.numel() * 2}
     result["gpu_launches"] = args.steps * launches_per_call(lay, cfg.d)
-    # ---- CPU oracle baseline on a bounded sample of the same workload
-    result["cpu_baseline"] = cpu_oracle_sample(lay, cfg, masks, rep, q, k, v)
 
 
 def reference_arm(args, cfg, world, rank):
@@ -567,16 +723,17 @@ def reference_arm(args, cfg, world, rank):
     if rank != 0:
         return
     lay = cfg.layout
-    if cfg.sparsity is None and torch.cuda.is_available():  # the calibrated plan of our arm
-        _, masks, rep, _, _, _ = workload(cfg, args, 0, cfg.heads, torch.device("cuda"))
-    else:
-        masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity or 0.69, seed=0)
-        rep = set(np.linspace(0, cfg.heads - 1, args.rep_heads).astype(int).tolist()) if args.rep_heads else set()
+    world = world if "WORLD_SIZE" in os.environ else args.gpus
+    # the same plan as our arm: generator S at the total sparsity, or (Mochi) the calibration
+    # path, which needs the GPU
+    _, masks, rep, _, _, _ = workload(cfg, args, 0, cfg.heads,
+                                      torch.device("cuda" if cfg.sparsity is None else "cpu"))
     q, k, v = inputs.qkv(1, lay.N, cfg.heads, cfg.d, seed=11, device="cpu")
+    heads64 = OracleHeads(q, k, v)
     vals, t_steps = [], []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        cb = cpu_oracle_sample(lay, cfg, masks, rep, q, k, v, seconds_target=4.0)
+        cb, _ = cpu_oracle_sample(lay, cfg, masks, rep, heads64, seconds_target=4.0)
         if i >= args.warmup:
             vals.append(cb["value"])
             t_steps.append(time.perf_counter() - t0)

@@ -290,9 +290,12 @@ CSA_API csa_status_t csa_copy_heads(void* dst, const void* src, csa_layout_t L, 
 /* Workspace bytes for `which` (CSA_WS_*). */
 CSA_API size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_t head_dim);
 
-/* Structural check of cells [0, n_cells) of a plan (row pointers monotone, indices ascending and
- * < N_B, MASK rows non-empty, intervals maximal/ordered and consistent with blk_idx, bases within
- * capacities).  Synchronises `stream`.  CSA_OK or CSA_ERR_CORRUPT_PLAN. */
+/* Structural check of cells [0, n_cells) of a plan: kind in {0 MASK, 1 REPETITIVE}; REPETITIVE
+ * anchor_k in [1, rows]; blk_base[0] = ivl_base[0] = 0, bases non-negative, monotone and within
+ * the capacities; every cell's row pointers start at 0, are monotone and stay inside the cell's
+ * list; MASK rows non-empty with indices ascending and < N_B (N_Bkv) and set in mask_bits;
+ * intervals maximal/ordered and equal to the decoded blk_idx.  No read leaves the plan's buffers
+ * once a bound is found broken.  Synchronises `stream`.  CSA_OK or CSA_ERR_CORRUPT_PLAN. */
 CSA_API csa_status_t csa_validate_plan(const csa_plan_t* plan, csa_layout_t L, int64_t n_cells,
                                csa_stream_t stream);
 

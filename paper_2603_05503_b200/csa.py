@@ -295,9 +295,15 @@ def sparse_attn_fwd_host(q_h: torch.Tensor, k_h: torch.Tensor, v_h: torch.Tensor
     own heads' cells, work list and strided views of the device copies) and the D2H of chunk c-1.
     Device staging buffers and per-chunk work lists are cached.  Returns out_h; synchronous on
     return of the current stream (the caller synchronizes to read out_h)."""
-    _, n, heads, d = q_h.shape
+    b, n, heads, d = q_h.shape
     lay = plan.lay
-    assert q_h.is_pinned() and out_h.is_pinned() and q_h.dtype == torch.bfloat16
+    if b != 1:
+        raise ValueError("sparse_attn_fwd_host: batch 1 only (csa_copy_heads moves one sequence)")
+    for name, t in (("q", q_h), ("k", k_h), ("v", v_h), ("out", out_h)):
+        if t.shape != q_h.shape or t.dtype != torch.bfloat16 or not t.is_pinned() \
+                or not t.is_contiguous():
+            raise ValueError(f"sparse_attn_fwd_host: {name} must be a pinned, contiguous bf16 "
+                             f"tensor of shape {tuple(q_h.shape)} (dense [1, N, H, d] rows)")
     key = (str(device), q_h.shape)
     bufs = _HOST_BUFS.get(key)
     if bufs is None:
@@ -378,21 +384,20 @@ class WorkList:
     items: torch.Tensor   # uint32 codes (stored as int32)
     n_work: torch.Tensor  # device int32 [1]
     max_work: int
-    pairs: bool = False   # order 3: items are (row 2p, row 2p+1) pairs for the CTA-pair kernel
+    pairs: bool = False   # order 3: items stand for rows (2p, 2p+1) (no kernel consumes them yet)
 
 
 def default_order(lay: Layout, d: int) -> int:
-    """Work-list order of the production path: 2 (head-major single items, one CTA per query
-    block).  Order 3 selects the CTA-pair kernel (block 128, head_dim 128), bit-identical but
-    currently slower on B200; it stays opt-in."""
+    """Work-list order of the production path: 2 (head-major, longest row first within a head,
+    one CTA per query block at a time)."""
     del lay, d
     return 2
 
 
 def build_work_list(plan: Plan, cell_base: int, n_heads: int, order: int = 2,
                     stream=None) -> WorkList:
-    """csa_build_work_list.  order 2: head-major, longest row first (one CTA per item);
-    order 3: pair items for the CTA-pair kernel (block 128, head_dim 128)."""
+    """csa_build_work_list (orders 0-3, include/csa.h).  order 2: head-major, longest row first
+    (the production order)."""
     cap = plan.items(cell_base, n_heads, pairs=(order == 3))
     items = torch.empty(max(cap, 1), dtype=torch.int32, device=plan.kind.device)
     n_work = torch.empty(1, dtype=torch.int32, device=plan.kind.device)
@@ -408,9 +413,9 @@ def sparse_attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: Pla
                     work: WorkList, cell_base: int = 0, out: torch.Tensor | None = None,
                     lse_out: torch.Tensor | None = None, scale: float | None = None,
                     stream=None, dynamic: bool = True) -> torch.Tensor:
-    """csa_sparse_attn_fwd on q/k/v [batch, N, heads, d] (bf16, CUDA).  dynamic=False uses the
-    static round-robin item assignment without a workspace (block 128 / head_dim 128: the
-    running-max kernel instead of the fixed-reference kernel, csa.h)."""
+    """csa_sparse_attn_fwd on q/k/v [batch, N, heads, d] (bf16, CUDA; any token / head stride,
+    head_dim contiguous).  dynamic=False: static round-robin item assignment without a workspace
+    (block 64 only; block-128 layouts need the workspace for the fallback list, csa.h)."""
     b, n, heads, d = q.shape
     assert n == plan.lay.N and k.shape == q.shape and v.shape == q.shape
     if out is None:
@@ -432,16 +437,21 @@ def sparse_attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: Pla
 
 
 _SCHED_WS: dict = {}
+_RETIRED_WS: list = []
 
 
 def _sched_workspace(device, nbytes: int, stream=None) -> torch.Tensor:
     """Zero-filled attention workspace (scheduler counters left zero-filled by every launch; the
     fixed-reference kernel's fallback list rewritten by every launch, csa.h), grown on demand,
-    one per (device, stream) so launches on different streams never share counters."""
+    one per (device, stream) so launches on different streams never share counters.  A buffer
+    replaced by a larger one is kept alive (never freed): a captured CUDA graph may still hold
+    its address (stream handles are recycled by torch's stream pool)."""
     s = torch.cuda.current_stream(device) if stream is None else stream
     key = (torch.device(device).index, s.cuda_stream)
     buf = _SCHED_WS.get(key)
     if buf is None or buf.numel() < nbytes:
+        if buf is not None:
+            _RETIRED_WS.append(buf)
         with torch.cuda.stream(s):
             buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
         _SCHED_WS[key] = buf

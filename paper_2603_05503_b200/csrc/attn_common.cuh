@@ -98,7 +98,10 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 // 2^x for a pair of x <= 127 on the FMA pipe: x = n + f, 2^f by a degree-3 minimax polynomial
 // (max rel. error 8.6e-5, far below the bf16 rounding of P), exponent added as integer.
 __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
-    const float x0 = fmaxf(lo_f(x), -127.0f), x1 = fmaxf(hi_f(x), -127.0f);
+    // clamp to [-127, 128]: above 128 the exponent add overflows to inf / NaN, which the
+    // kernels' overflow guard (!(sum <= 2^56)) catches instead of wrapping into the sign bit
+    const float x0 = fminf(fmaxf(lo_f(x), -127.0f), 128.0f);
+    const float x1 = fminf(fmaxf(hi_f(x), -127.0f), 128.0f);
     const uint64_t xc = f2(x0, x1);
     const uint64_t kRound = f2(12582912.0f, 12582912.0f);  // 2^23 + 2^22
     const uint64_t rnd = fadd2_rm(xc, kRound);               // floor(x) in the low mantissa bits

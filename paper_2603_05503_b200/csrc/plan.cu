@@ -379,12 +379,20 @@ __global__ void plan_validate_kernel(Geo g, int64_t n_cells, PlanDev p, uint32_t
         const int32_t* brp = p.blk_row_ptr + cell * (g.NB + 1);
         const int32_t* irp = p.ivl_row_ptr + cell * (g.NB + 1);
         uint32_t bad = 0;
-        if (p.blk_base[cell + 1] < p.blk_base[cell] || p.ivl_base[cell + 1] < p.ivl_base[cell])
-            bad |= 1;
+        const int64_t bb0 = p.blk_base[cell], bb1 = p.blk_base[cell + 1];
+        const int64_t ib0 = p.ivl_base[cell], ib1 = p.ivl_base[cell + 1];
+        if (bb1 < bb0 || ib1 < ib0 || bb0 < 0 || ib0 < 0) bad |= 1;
         if (p.blk_base[n_cells] > p.blk_capacity || p.ivl_base[n_cells] > p.ivl_capacity) bad |= 2;
+        if (cell == 0 && r == 0 && (p.blk_base[0] != 0 || p.ivl_base[0] != 0)) bad |= 2048;
+        if (r == 0 && (brp[0] != 0 || irp[0] != 0)) bad |= 2048;
         const int32_t b0 = brp[r], b1 = brp[r + 1], i0 = irp[r], i1 = irp[r + 1];
-        if (b1 < b0 || i1 < i0) bad |= 4;
-        if (p.kind[cell] == 0) {
+        // row pointers inside the cell's own list (no read below this check leaves it)
+        if (b1 < b0 || i1 < i0 || b0 < 0 || i0 < 0 || (int64_t)b1 > bb1 - bb0 ||
+            (int64_t)i1 > ib1 - ib0)
+            bad |= 4;
+        if (p.kind[cell] > 1) bad |= 512;
+        if (p.kind[cell] == 1 && (p.anchor_k[cell] < 1 || p.anchor_k[cell] > g.H)) bad |= 1024;
+        if (p.kind[cell] == 0 && !(bad & 4)) {
             if (b1 == b0) bad |= 8;  // empty MASK row
             if (brp[g.NB] != p.blk_base[cell + 1] - p.blk_base[cell]) bad |= 16;
             if (!bad) {

@@ -75,27 +75,49 @@ def sequence_shard(x: torch.Tensor, world: int, rank: int) -> torch.Tensor:
 
 
 def make_layer_step(q_loc, k_loc, v_loc, world: int, attention, group=None):
-    """Closure running one head-sharded layer: scatter Q, K, V -> attention(q, k, v) on this
-    rank's heads -> gather O.  `attention` maps [B, N, H/P, d] tensors to an output of the same
-    shape (the rank's csa_sparse_attn_fwd)."""
+    """Closure running one head-sharded layer with ONE stacked exchange of Q, K and V
+    (SURVEY 8.6): the send buffer interleaves the three tensors per token,
+    [P_dst, B, N/P, 3, H/P, d], so a single all_to_all_single moves them and the receive buffer
+    [P_src, B, N/P, 3, H/P, d] is, for batch 1, the token-ordered [1, N, 3, H/P, d]: Q, K and V
+    are strided views of it (token stride 3 H/P d elements) that the kernel's TMA maps read
+    directly, with no unpack copy.  The attention output [B, N, H/P, d] is, for batch 1, already
+    the send layout [P_dst, N/P, H/P, d] of the return exchange.  `attention` maps [B, N, H/P, d]
+    views (any token stride, head_dim contiguous) to a contiguous output of that shape (the
+    rank's csa_sparse_attn_fwd).  Returns this rank's [B, N/P, H, d] output."""
+    b, n_loc, h, d = q_loc.shape
+    hp = h // world
+    n = n_loc * world
+    send = torch.empty((world, b, n_loc, 3, hp, d), dtype=q_loc.dtype, device=q_loc.device)
+    recv = torch.empty_like(send)
+    o_recv = torch.empty((world, b, n_loc, hp, d), dtype=q_loc.dtype, device=q_loc.device)
 
     def step():
-        qh = scatter_heads(q_loc, world, group)
-        kh = scatter_heads(k_loc, world, group)
-        vh = scatter_heads(v_loc, world, group)
-        return gather_heads(attention(qh, kh, vh), world, group)
+        for s_, x in enumerate((q_loc, k_loc, v_loc)):
+            send[:, :, :, s_].copy_(x.view(b, n_loc, world, hp, d).permute(2, 0, 1, 3, 4))
+        dist.all_to_all_single(recv, send, group=group)
+        if b == 1:
+            qkv = recv.view(1, n, 3, hp, d)              # token order = source-rank order
+        else:
+            qkv = recv.permute(1, 0, 2, 3, 4, 5).reshape(b, n, 3, hp, d)
+        o = attention(qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2])
+        o_send = o.view(world, n_loc, hp, d) if b == 1 else \
+            o.view(b, world, n_loc, hp, d).transpose(0, 1).contiguous()
+        dist.all_to_all_single(o_recv.view(world, -1), o_send.reshape(world, -1), group=group)
+        # [P_src = head group, B, N/P, H/P, d] -> [B, N/P, H, d]
+        return o_recv.permute(1, 2, 0, 3, 4).reshape(b, n_loc, h, d)
 
     return step
 
 
 def make_layer_step_chunked(q_loc, k_loc, v_loc, world: int, attention, chunks: int, group=None):
     """One head-sharded layer with the exchange overlapped with the attention: this
-    rank's H/P heads are split into `chunks` head chunks; the all-to-all of chunk c+1's Q, K, V
-    (and of chunk c-1's output) runs on a communication stream while chunk c's attention runs on
-    the current stream.  attention(c, qh, kh, vh) maps chunk c's [B, N, H/(P chunks), d] tensors
-    (heads c*hc .. of this rank) to an output of the same shape.  Every rank must use the same
-    `chunks`; the result equals make_layer_step's bit for bit (head-local attention, the same
-    bytes moved).  On CPU tensors (gloo) the same schedule runs without streams."""
+    rank's H/P heads are split into `chunks` head chunks; the stacked all-to-all of chunk c+1's
+    Q, K, V (one all_to_all_single per chunk, layout as in make_layer_step) and the return
+    exchange of chunk c-1's output run on a communication stream while chunk c's attention runs
+    on the current stream.  attention(c, qh, kh, vh) maps chunk c's [B, N, H/(P chunks), d]
+    views (heads c*hc .. of this rank) to a contiguous output of that shape.  Every rank must use
+    the same `chunks`; the result equals make_layer_step's bit for bit (head-local attention, the
+    same bytes moved).  On CPU tensors (gloo) the same schedule runs without streams."""
     b, n_loc, h, d = q_loc.shape
     hp = h // world
     if hp % chunks:
@@ -104,20 +126,20 @@ def make_layer_step_chunked(q_loc, k_loc, v_loc, world: int, attention, chunks: 
     cuda = q_loc.is_cuda
     comm = torch.cuda.Stream(device=q_loc.device) if cuda else None
     n = n_loc * world
-    # send buffers, chunk c: [P_dst, B, N/P, hc, d] = heads p*hp + c*hc .. of this rank's tokens
-    send = [[torch.empty((world, b, n_loc, hc, d), dtype=x.dtype, device=x.device)
-             for x in (q_loc, k_loc, v_loc)] for _ in range(chunks)]
-    recv = [[torch.empty_like(s) for s in sc] for sc in send]
-    o_send = [torch.empty((world, b, n_loc, hc, d), dtype=q_loc.dtype, device=q_loc.device)
-              for _ in range(chunks)]
-    o_recv = [torch.empty_like(s) for s in o_send]
-    out = torch.empty((b, n_loc, h, d), dtype=q_loc.dtype, device=q_loc.device)
+    kw = dict(dtype=q_loc.dtype, device=q_loc.device)
+    # chunk c send: [P_dst, B, N/P, 3, hc, d] = heads p*hp + c*hc .. of this rank's tokens
+    send = [torch.empty((world, b, n_loc, 3, hc, d), **kw) for _ in range(chunks)]
+    recv = [torch.empty_like(x) for x in send]
+    o_send = [torch.empty((world, b, n_loc, hc, d), **kw) for _ in range(chunks)]
+    o_recv = [torch.empty_like(x) for x in o_send]
+    out = torch.empty((b, n_loc, h, d), **kw)
 
     def ctx(stream):
         return torch.cuda.stream(stream) if cuda else _Null()
 
-    def head_major(r):  # [P_src, B, N/P, hc, d] -> [B, N, hc, d] (token order = source order)
-        return r.view(1, n, hc, d) if b == 1 else r.permute(1, 0, 2, 3, 4).reshape(b, n, hc, d)
+    def views(r):  # [P_src, B, N/P, 3, hc, d] -> Q, K, V [B, N, hc, d] (token order)
+        qkv = r.view(1, n, 3, hc, d) if b == 1 else r.permute(1, 0, 2, 3, 4, 5).reshape(b, n, 3, hc, d)
+        return qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2]
 
     def step():
         cur = torch.cuda.current_stream(q_loc.device) if cuda else None
@@ -126,10 +148,11 @@ def make_layer_step_chunked(q_loc, k_loc, v_loc, world: int, attention, chunks: 
             comm.wait_stream(cur)  # inputs written on the current stream
         with ctx(comm):
             for c in range(chunks):
-                for x, sbuf, rbuf in zip((q_loc, k_loc, v_loc), send[c], recv[c]):
-                    sbuf.copy_(x.view(b, n_loc, world, hp, d)[:, :, :, c * hc:(c + 1) * hc]
-                               .permute(2, 0, 1, 3, 4))
-                    dist.all_to_all_single(rbuf, sbuf, group=group)
+                for s_, x in enumerate((q_loc, k_loc, v_loc)):
+                    send[c][:, :, :, s_].copy_(
+                        x.view(b, n_loc, world, hp, d)[:, :, :, c * hc:(c + 1) * hc]
+                        .permute(2, 0, 1, 3, 4))
+                dist.all_to_all_single(recv[c], send[c], group=group)
                 if cuda:
                     e = torch.cuda.Event()
                     e.record(comm)
@@ -137,7 +160,7 @@ def make_layer_step_chunked(q_loc, k_loc, v_loc, world: int, attention, chunks: 
         for c in range(chunks):
             if cuda:
                 cur.wait_event(ev_in[c])
-            oh = attention(c, *(head_major(r) for r in recv[c]))
+            oh = attention(c, *views(recv[c]))
             o_send[c].copy_(oh.view(b, world, n_loc, hc, d).permute(1, 0, 2, 3, 4))
             if cuda:
                 e = torch.cuda.Event()

@@ -102,6 +102,24 @@ def test_plan_compile_bit_exact(csa, lay):
     check_plan_against_oracle(csa, lay, counts, 32, sim=sim, anchor_k=min(5, lay.H))
 
 
+@pytest.mark.parametrize("field,value", [("kind", 2), ("anchor_k", 0), ("anchor_k", 99),
+                                         ("blk_base", -1), ("blk_row_ptr", 5), ("ivl_row_ptr", 3)])
+def test_validate_rejects_corrupt_plan_fields(csa, field, value):
+    """csa_validate_plan flags out-of-range kinds / anchor counts and bases or row pointers that
+    do not start at 0 (a CRC-valid file with anchor_k = 0 used to pass)."""
+    lay = Layout(2, 9, 40, 128)
+    rng = np.random.default_rng(2)
+    counts = u16_dev((rng.random((2, lay.NB, lay.NB)) < 0.5).astype(np.uint16))
+    sim = torch.tensor([0.0, 1.0], dtype=torch.float64, device="cuda")
+    plan = csa.compile_plan(lay, counts, 1, similarity=sim, gamma=0.87, anchor_k=3)
+    csa.validate_plan(plan)
+    t = getattr(plan, field)
+    idx = 1 if field in ("kind", "anchor_k") else 0   # cell 1 is REPETITIVE
+    t[idx] = value
+    with pytest.raises(csa.CsaError, match="CORRUPT_PLAN"):
+        csa.validate_plan(plan)
+
+
 def test_plan_compile_wan720_synthetic(csa):
     cfg = CONFIGS["wan720"]
     counts = inputs.synthetic_counts(cfg.layout, 4, cfg.sparsity, 64, seed=3)
@@ -314,6 +332,53 @@ def test_attention_full_size_sampled(csa, name):
     assert torch.isfinite(out).all()
     if cfg.d == 128:
         assert fallback_count(csa, q) == 0  # realistic rows never overshoot the reference max
+
+
+def test_attention_wan720_structured_peaked_sampled(csa):
+    """Wan 720p at full size on generator-G Q/K (peak-logit scale alpha up to 1.6, sink keys,
+    two repetitive heads), plan CALIBRATED from the same prompt (a2-a6 through the C ABI, eps of
+    t = 25 of 50), production launch.  Rows keep block 0 (the sinks), so their first kept tile
+    -- the fixed softmax reference of reading Q29 -- sits far below the row's peak near the
+    diagonal: this exercises the shift at full size with peaked logits, not just i.i.d. scores.
+    Oracle on sampled units incl. the ragged last block and anchor rows."""
+    cfg = CONFIGS["wan720"]
+    lay = cfg.layout
+    heads = 8
+    alphas = np.linspace(0.8, 1.6, heads)
+    q, k, v = inputs.structured_qk(lay, heads, 128, 9, 0, alpha=alphas, repetitive=(2, 5),
+                                   device="cuda")
+    nb = lay.NB
+    counts = u16_zeros(heads * nb * nb)
+    lse_c = torch.empty(heads * lay.N, dtype=torch.float32, device="cuda")
+    eps = oracle.epsilon(25, 50, oracle.A_of_N(lay.N), 0.99, 16)
+    csa.calib_accumulate(lay, q, k, eps, counts, lse_out=lse_c)
+    sim = torch.zeros(heads, dtype=torch.float64, device="cuda")
+    csa.spatial_similarity(lay, q, k, lse_c, 5, sim)
+    s = sim / float(lay.F * lay.H)
+    plan = csa.compile_plan(lay, counts, 1, similarity=s, gamma=0.87, anchor_k=5)
+    work = csa.build_work_list(plan, 0, heads)
+    lse = torch.empty(heads * lay.N, dtype=torch.float32, device="cuda")
+    out = csa.sparse_attn_fwd(q, k, v, plan, work, lse_out=lse)
+    torch.cuda.synchronize()
+    kinds = plan.kind_host
+    assert kinds[2] == 1 and kinds[5] == 1, kinds   # the generated repetitive heads are detected
+    cnt = u16_np(counts).reshape(heads, nb, nb)
+    masks = (cnt >= 1).astype(np.uint8)
+    for h in range(heads):   # the compiler's row repair (reading Q7) never triggers here
+        if not kinds[h]:
+            assert masks[h].sum(axis=1).min() >= 1
+    lse = lse.view(heads, lay.N).cpu().numpy()
+    units = [(0, 0), (0, nb - 1), (2, 0), (5, nb - 1), (7, nb // 2), (7, nb - 1)]
+    rng = np.random.default_rng(4)
+    units += [(int(rng.integers(heads)), int(rng.integers(nb))) for _ in range(8)]
+    for h, r in units:
+        rows = (r * lay.B, min((r + 1) * lay.B, lay.N))
+        rep_k = 5 if kinds[h] else None
+        ref, ref_lse = oracle_head(lay, q, k, v, 0, h, mask=masks[h], rep_k=rep_k, rows=rows)
+        got = out[0, rows[0]:rows[1], h].double().cpu().numpy()
+        assert_close(got, ref, f"h{h} r{r}")
+        assert np.abs(lse[h, rows[0]:rows[1]] - ref_lse).max() <= 1e-3, (h, r)
+    assert torch.isfinite(out).all()
 
 
 # ---------------------------------------------------------------- a2-a5 calibration

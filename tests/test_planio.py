@@ -64,10 +64,16 @@ def test_calibration_state_round_trip(tmp_path):
                             .reshape(-1).view(np.int16)).view(torch.uint16)
     sim = torch.linspace(0.1, 3.0, 4, dtype=torch.float64)
     path = os.path.join(tmp_path, "cal.csac")
-    planio.save_calibration(path, lay, keep, sim, 7)
-    lay2, keep2, sim2, n = planio.load_calibration(path, device="cpu")
+    st = {"T": 50, "L": 40, "H": 4, "anchor_k": 5, "rho": 0.5, "eps_A": 0.842192, "eps_C": 0.99,
+          "eps_k": 16.0}
+    planio.save_calibration(path, lay, keep, sim, 7, settings=st)
+    assert not os.path.exists(path + ".tmp")   # written atomically (tmp + rename)
+    lay2, keep2, sim2, n = planio.load_calibration(path, device="cpu", expect=st)
     assert lay2 == lay and n == 7 and torch.equal(sim2, sim)
     assert torch.equal(keep2.view(torch.int16), keep.view(torch.int16))
+    for key, val in (("rho", 0.6), ("eps_A", 0.9), ("T", 4), ("anchor_k", 3)):
+        with pytest.raises(ValueError, match=key):   # resuming under other settings is refused
+            planio.load_calibration(path, device="cpu", expect={**st, key: val})
     with pytest.raises(ValueError):
         planio.save_calibration(path, Layout(2, 9, 40, 128), keep, sim, 7)  # wrong geometry
 

@@ -34,8 +34,18 @@ def _worker(rank, world, port, batch, results):
         ok_roundtrip = torch.equal(back, x_loc)
         # a head-local op (per-head scaling by the head index) commutes with the exchange
         scale = torch.arange(h0, h1, dtype=x.dtype).view(1, 1, -1, 1) + 1
-        step = ulysses.make_layer_step(x_loc, x_loc, x_loc, world, lambda q, k, v: q * scale)
+        seen = {}
+
+        def attn(q, k, v):  # the stacked exchange hands the kernel strided views (no unpack)
+            seen["stride"] = q.stride()
+            seen["qkv"] = (torch.equal(q, x[:, :, h0:h1]) and torch.equal(k, x[:, :, h0:h1])
+                           and torch.equal(v, x[:, :, h0:h1]))
+            return q * scale
+
+        step = ulysses.make_layer_step(x_loc, x_loc, x_loc, world, attn)
         y_loc = step()
+        hp_ = h1 - h0
+        ok_views = seen["qkv"] and (batch > 1 or seen["stride"][1] == 3 * hp_ * d)
         ref = (x * (torch.arange(h, dtype=x.dtype).view(1, 1, -1, 1) + 1))
         ok_layer = torch.equal(y_loc, ulysses.sequence_shard(ref, world, rank))
         # a balanced head order (folded into the projections in a model): rank r receives the
@@ -52,7 +62,7 @@ def _worker(rank, world, port, batch, results):
                 lambda c, q, k, v, hc=(h1 - h0) // chunks: q * (scale[:, :, c * hc:(c + 1) * hc]),
                 chunks)
             ok_chunk &= torch.equal(stepc(), y_loc)
-        results[rank] = (ok_scatter, ok_roundtrip, ok_layer and ok_perm and ok_chunk)
+        results[rank] = (ok_scatter, ok_roundtrip, ok_layer and ok_perm and ok_chunk and ok_views)
     finally:
         dist.destroy_process_group()
 
