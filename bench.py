@@ -70,6 +70,19 @@ def peaks():
     return p
 
 
+def mufu_peak():
+    """Measured MUFU ex2/s of the whole GPU under load (profiles/mufu_peak_b200.json, written by
+    scripts/mufu_peak.cu); fallback: 16 ex2/clk/SM x 148 SMs x 1965 MHz (B200_PROFILING.md max
+    clock), stated as such."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "mufu_peak_b200.json")) as fh:
+            m = json.load(fh)
+        return {"ex2_per_s": float(m["ex2_per_s"]),
+                "src": f"measured (profiles/mufu_peak_b200.json, {m.get('sm_mhz_last')} MHz)"}
+    except (OSError, KeyError, ValueError):
+        return {"ex2_per_s": 16.0 * 148 * 1965e6, "src": "16 ex2/clk/SM x 148 x 1965 MHz"}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
 
@@ -466,18 +479,15 @@ def main():
         del q, k, v
         q = k = v = None
 
-        def run_heads(qh, kh, vh):
-            return csa.sparse_attn_fwd(qh, kh, vh, plan, work, out=out)
+        def run_heads(qh, kh, vh, o=None):
+            return csa.sparse_attn_fwd(qh, kh, vh, plan, work, out=out if o is None else o)
 
         hc = hp // chunks
         works = [csa.build_work_list(plan, c * hc, hc, order=csa.default_order(lay, d))
                  for c in range(chunks)]
-        outs_c = [torch.empty((B, lay.N, hc, d), dtype=torch.bfloat16, device=dev)
-                  for _ in range(chunks)]
 
-        def run_chunk(c, qh, kh, vh):  # heads c*hc .. of this rank: cells c*hc ..
-            return csa.sparse_attn_fwd(qh, kh, vh, plan, works[c], cell_base=c * hc,
-                                       out=outs_c[c])
+        def run_chunk(c, qh, kh, vh, o):  # heads c*hc .. of this rank: cells c*hc ..
+            return csa.sparse_attn_fwd(qh, kh, vh, plan, works[c], cell_base=c * hc, out=o)
 
         def layer_step(a, b_, c_):
             if chunks == 1:
@@ -680,12 +690,13 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
     calib_exps = 1.0 * H * float(lay.N) ** 2                 # one exp per score
     ph["calib_exp_per_s"] = calib_exps / (t_cal * 1e-3)
     ph["calib_qk_tflops"] = round(2.0 * d * H * float(lay.N) ** 2 / (t_cal * 1e-3) / 1e12, 1)
-    # exp roofline of a2-a3: MUFU ex2 = 16 / clk / SM at the SM clock sampled during
-    # the timed attention region (a quarter to 3/8 of the exps run on the FMA pipe instead)
-    sm_mhz = (result.get("clocks") or {}).get("sm_mhz") or 1965.0
-    mufu = 16.0 * torch.cuda.get_device_properties(dev).multi_processor_count * sm_mhz * 1e6
-    ph["calib_mufu_peak_exp_per_s"] = mufu
-    ph["calib_exp_frac_of_mufu"] = round(ph["calib_exp_per_s"] / mufu, 4)
+    # exp roofline of a2-a3: the MEASURED MUFU ex2 throughput of this pool's B200s
+    # under load (scripts/mufu_peak.cu -> profiles/mufu_peak_b200.json: 16 ex2 / clk / SM at the
+    # sustained clock), a fixed denominator for every run
+    mufu = mufu_peak()
+    ph["calib_mufu_peak_exp_per_s"] = mufu["ex2_per_s"]
+    ph["calib_mufu_peak_src"] = mufu["src"]
+    ph["calib_exp_frac_of_mufu"] = round(ph["calib_exp_per_s"] / mufu["ex2_per_s"], 4)
     cnt = torch.from_numpy((masks.astype(np.uint16) * np.uint16(64)).reshape(-1).view(np.int16)).to(dev).view(torch.uint16)
     sim = torch.tensor([1.0 if h in rep else 0.0 for h in range(H)], dtype=torch.float64, device=dev)
     torch.cuda.synchronize()

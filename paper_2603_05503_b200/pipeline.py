@@ -25,7 +25,7 @@ from typing import Callable
 
 import torch
 
-from . import csa
+from . import csa, ulysses
 from .inputs import Layout
 
 # "the same schedule for both 480p and 720p distilled LightX2V: A=0.763, C=0.863, k=5.64"
@@ -57,9 +57,32 @@ class PlanDictionary:
     prompts: int
     similarity: torch.Tensor   # fp64 [T * L * H]
     keep_count: torch.Tensor   # uint16 [T * L * H, N_B, N_Bkv]
+    gamma: float = 0.87
+    anchor_k: int = 5
 
     def cell_base(self, t: int, l: int) -> int:
         return (t * self.L + l) * self.H
+
+    def shard(self, world: int, rank: int, perm: list | None = None) -> "PlanDictionary":
+        """This rank's part of the dictionary for head-sharded inference: the cells
+        (t, l, h) of heads perm[rank H/P:(rank+1) H/P] (default: contiguous heads), compiled by
+        csa_compile_plan from those cells' keep counts and similarity -- cell-local, so every
+        cell's plan is the full dictionary's bit for bit.  (Calibration itself is head-sharded
+        with no collective: a rank can equally calibrate only its heads.)"""
+        H = self.H
+        if H % world:
+            raise ValueError(f"{H} heads not divisible by {world} ranks")
+        hp = H // world
+        perm = list(range(H)) if perm is None else list(perm)
+        mine = torch.tensor(perm[rank * hp:(rank + 1) * hp], device=self.keep_count.device)
+        kc = self.keep_count.view(self.T * self.L, H, self.lay.NB, -1)
+        keep = kc.view(torch.int16)[:, mine].contiguous().view(torch.uint16)
+        sim = self.similarity.view(self.T * self.L, H)[:, mine].contiguous().view(-1)
+        plan = csa.compile_plan(self.lay, keep.view(-1), self.min_count, similarity=sim,
+                                gamma=self.gamma, anchor_k=self.anchor_k)
+        return PlanDictionary(self.lay, self.T, self.L, hp, plan, self.eps, self.min_count,
+                              self.prompts, sim, keep.view(-1, self.lay.NB, keep.shape[-1]),
+                              self.gamma, self.anchor_k)
 
     def kept_fraction(self, t: int | None = None) -> float:
         """Kept area / dense area over the cells of timestep t (all cells if None)."""
@@ -99,7 +122,7 @@ def calibrate(lay: Layout, T: int, L: int, H: int, prompts: int,
     s = sim_sum / float(lay.F * lay.H * prompts)
     plan = csa.compile_plan(lay, keep, min_count, similarity=s, gamma=gamma, anchor_k=anchor_k)
     return PlanDictionary(lay, T, L, H, plan, eps, min_count, prompts, s,
-                          keep.view(cells, nb, nbk))
+                          keep.view(cells, nb, nbk), gamma, anchor_k)
 
 
 class DenoiseStep:
@@ -147,3 +170,81 @@ class DenoiseStep:
         d, b = self.q[0].shape[3], self.q[0].shape[0]
         area = self.dic.plan.kept_area.view(self.dic.T, -1)[t]
         return 4.0 * d * b * float(area.sum().item())
+
+
+class ShardedDenoiseStep:
+    """One denoising step of L attention layers head-sharded over the P ranks of a process group
+    (SURVEY 8.6 / f4 on N GPUs).  Activations are sequence-sharded: layer l reads q[l % S],
+    k[l % S], v[l % S] ([B, N/P, H, d], heads in the exchange order the rank dictionary was
+    sharded with) and writes o[l % S].  Per layer: ONE stacked Q/K/V all-to-all per head chunk
+    (ulysses.LayerExchange: the kernel reads the receive buffer and writes the return send
+    buffer in place), csa_sparse_attn_fwd over the rank's cells (t, l, chunk heads) with both
+    CFG branches in one launch (batch 2), the return all-to-all; with chunks > 1 the
+    exchange of chunk c+1 overlaps the attention of chunk c (communication stream).  A DiT's
+    layer l+1 reads layer l's output, so the overlap that exists is inside a layer (between head
+    chunks) -- layers run in order.  run(t) launches eagerly; capture(t) records the whole step,
+    NCCL calls included, in one CUDA graph.
+
+    attention(t, l, c, q, k, v, out) replaces the kernel call (CPU gloo rehearsal of the schedule
+    in tests/: the oracle stands in for the kernel); default: csa_sparse_attn_fwd."""
+
+    def __init__(self, dic_rank: PlanDictionary | None, world: int, q: list, k: list, v: list,
+                 o: list, chunks: int = 1, group=None, attention=None, T: int | None = None,
+                 L: int | None = None):
+        self.dic, self.world, self.chunks, self.group = dic_rank, world, chunks, group
+        self.T = dic_rank.T if dic_rank is not None else T
+        self.L = dic_rank.L if dic_rank is not None else L
+        h = q[0].shape[2]
+        self.hp = h // world
+        if self.hp % chunks:
+            raise ValueError(f"{self.hp} heads per rank not divisible into {chunks} chunks")
+        self.hc = self.hp // chunks
+        self.cur = (0, 0)
+        cuda = q[0].is_cuda
+        if attention is None:
+            if dic_rank is None or dic_rank.H != self.hp:
+                raise ValueError("the rank dictionary must hold H/P heads per (t, l)")
+            self.work = [[[csa.build_work_list(dic_rank.plan, dic_rank.cell_base(t, l) + c * self.hc,
+                                               self.hc)
+                           for c in range(chunks)] for l in range(self.L)] for t in range(self.T)]
+            attention = self._kernel
+        self.attention = attention
+        self.stream = torch.cuda.Stream(device=q[0].device) if cuda else None
+        comm = torch.cuda.Stream(device=q[0].device) if cuda else None
+
+        def attn(c, qh, kh, vh, out):
+            t, l = self.cur
+            self.attention(t, l, c, qh, kh, vh, out)
+
+        self.steps = [ulysses.make_layer_step_chunked(q[s], k[s], v[s], world, attn, chunks,
+                                                      group=group, out=o[s], comm=comm)
+                      for s in range(len(q))]
+        self.graphs: dict = {}
+
+    def _kernel(self, t, l, c, qh, kh, vh, out):
+        dic = self.dic
+        csa.sparse_attn_fwd(qh, kh, vh, dic.plan, self.work[t][l][c],
+                            cell_base=dic.cell_base(t, l) + c * self.hc, out=out)
+
+    def _launch(self, t: int) -> None:
+        S = len(self.steps)
+        for l in range(self.L):
+            self.cur = (t, l)
+            self.steps[l % S]()
+
+    def run(self, t: int) -> None:
+        self._launch(t)
+
+    def capture(self, t: int) -> torch.cuda.CUDAGraph:
+        if t not in self.graphs:
+            with torch.cuda.stream(self.stream):
+                self._launch(t)  # warm: workspaces allocated, NCCL communicators up
+            self.stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                self._launch(t)
+            self.graphs[t] = g
+        return self.graphs[t]
+
+    def replay(self, t: int) -> None:
+        self.capture(t).replay()

@@ -74,72 +74,93 @@ def sequence_shard(x: torch.Tensor, world: int, rank: int) -> torch.Tensor:
     return x[:, rank * s:(rank + 1) * s].contiguous()
 
 
-def make_layer_step(q_loc, k_loc, v_loc, world: int, attention, group=None):
-    """Closure running one head-sharded layer with ONE stacked exchange of Q, K and V
-    (SURVEY 8.6): the send buffer interleaves the three tensors per token,
-    [P_dst, B, N/P, 3, H/P, d], so a single all_to_all_single moves them and the receive buffer
-    [P_src, B, N/P, 3, H/P, d] is, for batch 1, the token-ordered [1, N, 3, H/P, d]: Q, K and V
-    are strided views of it (token stride 3 H/P d elements) that the kernel's TMA maps read
-    directly, with no unpack copy.  The attention output [B, N, H/P, d] is, for batch 1, already
-    the send layout [P_dst, N/P, H/P, d] of the return exchange.  `attention` maps [B, N, H/P, d]
-    views (any token stride, head_dim contiguous) to a contiguous output of that shape (the
-    rank's csa_sparse_attn_fwd).  Returns this rank's [B, N/P, H, d] output."""
+class LayerExchange:
+    """Buffers and views of one head-sharded layer exchange for `heads_per_chunk`
+    of this rank's heads.  Send layout [P_dst, N/P, B, 3, hc, d]: Q, K, V of a token are
+    interleaved and the batch (the CFG branches) sits inside the token, so ONE
+    all_to_all_single moves all three and the receive buffer [P_src, N/P, B, 3, hc, d] IS the
+    token-ordered [N, B, 3, hc, d]: qkv(s) is the strided [B, N, hc, d] view the kernel's TMA
+    maps read in place (stride_b = 3 hc d, stride_n = 3 B hc d).  The attention writes its output
+    straight into o_send [P_dst, N/P, B, hc, d] through the strided view out_view() (stride_b =
+    hc d, stride_n = B hc d): the return exchange needs no pack either."""
+
+    def __init__(self, b: int, n_loc: int, world: int, hc: int, d: int, dtype, device):
+        self.b, self.n_loc, self.world, self.hc, self.d = b, n_loc, world, hc, d
+        kw = dict(dtype=dtype, device=device)
+        self.send = torch.empty((world, n_loc, b, 3, hc, d), **kw)
+        self.recv = torch.empty_like(self.send)
+        self.o_send = torch.empty((world, n_loc, b, hc, d), **kw)
+        self.o_recv = torch.empty_like(self.o_send)
+
+    def pack(self, xs, world: int, hp: int, h0: int) -> None:
+        """send[p, t, b, s] = x_s[b, t, p hp + h0 : p hp + h0 + hc] for s = Q, K, V."""
+        b, n_loc, hc, d = self.b, self.n_loc, self.hc, self.d
+        for s_, x in enumerate(xs):
+            self.send[:, :, :, s_].copy_(
+                x.view(b, n_loc, world, hp, d)[:, :, :, h0:h0 + hc].permute(2, 1, 0, 3, 4))
+
+    def qkv(self, s_: int) -> torch.Tensor:
+        n = self.world * self.n_loc
+        return self.recv.view(n, self.b, 3, self.hc, self.d)[:, :, s_].transpose(0, 1)
+
+    def out_view(self) -> torch.Tensor:
+        n = self.world * self.n_loc
+        return self.o_send.view(n, self.b, self.hc, self.d).transpose(0, 1)
+
+    def unpack(self, out: torch.Tensor, hp: int, h0: int) -> None:
+        """o_recv [P_src = head group, N/P, B, hc, d] -> out[b, t, p hp + h0 ..] of this rank's
+        token shard [B, N/P, H, d]."""
+        b, n_loc, world, hc, d = self.b, self.n_loc, self.world, self.hc, self.d
+        out.view(b, n_loc, world, hp, d)[:, :, :, h0:h0 + hc].copy_(
+            self.o_recv.permute(2, 1, 0, 3, 4))
+
+
+def make_layer_step(q_loc, k_loc, v_loc, world: int, attention, group=None, out=None):
+    """Closure running one head-sharded layer: ONE stacked all-to-all of Q, K, V (LayerExchange),
+    attention(q, k, v, out) on this rank's heads -- q, k, v and out are strided [B, N, H/P, d]
+    views of the exchange buffers, read and written in place by the kernel (the rank's
+    csa_sparse_attn_fwd) -- then the return all-to-all.  Returns this rank's [B, N/P, H, d]."""
     b, n_loc, h, d = q_loc.shape
     hp = h // world
-    n = n_loc * world
-    send = torch.empty((world, b, n_loc, 3, hp, d), dtype=q_loc.dtype, device=q_loc.device)
-    recv = torch.empty_like(send)
-    o_recv = torch.empty((world, b, n_loc, hp, d), dtype=q_loc.dtype, device=q_loc.device)
+    ex = LayerExchange(b, n_loc, world, hp, d, q_loc.dtype, q_loc.device)
+    if out is None:
+        out = torch.empty((b, n_loc, h, d), dtype=q_loc.dtype, device=q_loc.device)
 
     def step():
-        for s_, x in enumerate((q_loc, k_loc, v_loc)):
-            send[:, :, :, s_].copy_(x.view(b, n_loc, world, hp, d).permute(2, 0, 1, 3, 4))
-        dist.all_to_all_single(recv, send, group=group)
-        if b == 1:
-            qkv = recv.view(1, n, 3, hp, d)              # token order = source-rank order
-        else:
-            qkv = recv.permute(1, 0, 2, 3, 4, 5).reshape(b, n, 3, hp, d)
-        o = attention(qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2])
-        o_send = o.view(world, n_loc, hp, d) if b == 1 else \
-            o.view(b, world, n_loc, hp, d).transpose(0, 1).contiguous()
-        dist.all_to_all_single(o_recv.view(world, -1), o_send.reshape(world, -1), group=group)
-        # [P_src = head group, B, N/P, H/P, d] -> [B, N/P, H, d]
-        return o_recv.permute(1, 2, 0, 3, 4).reshape(b, n_loc, h, d)
+        ex.pack((q_loc, k_loc, v_loc), world, hp, 0)
+        dist.all_to_all_single(ex.recv, ex.send, group=group)
+        attention(ex.qkv(0), ex.qkv(1), ex.qkv(2), ex.out_view())
+        dist.all_to_all_single(ex.o_recv, ex.o_send, group=group)
+        ex.unpack(out, hp, 0)
+        return out
 
     return step
 
 
-def make_layer_step_chunked(q_loc, k_loc, v_loc, world: int, attention, chunks: int, group=None):
+def make_layer_step_chunked(q_loc, k_loc, v_loc, world: int, attention, chunks: int, group=None,
+                            out=None, comm=None):
     """One head-sharded layer with the exchange overlapped with the attention: this
-    rank's H/P heads are split into `chunks` head chunks; the stacked all-to-all of chunk c+1's
-    Q, K, V (one all_to_all_single per chunk, layout as in make_layer_step) and the return
-    exchange of chunk c-1's output run on a communication stream while chunk c's attention runs
-    on the current stream.  attention(c, qh, kh, vh) maps chunk c's [B, N, H/(P chunks), d]
-    views (heads c*hc .. of this rank) to a contiguous output of that shape.  Every rank must use
-    the same `chunks`; the result equals make_layer_step's bit for bit (head-local attention, the
-    same bytes moved).  On CPU tensors (gloo) the same schedule runs without streams."""
+    rank's H/P heads are split into `chunks` head chunks, each with its own LayerExchange; the
+    stacked all-to-all of chunk c+1 (and the return exchange of chunk c-1) runs on a
+    communication stream while chunk c's attention runs on the current stream.
+    attention(c, q, k, v, out) handles heads c*hc .. of this rank (strided views, written in
+    place).  Every rank must use the same `chunks`; the result equals make_layer_step's bit for
+    bit (head-local attention, the same bytes moved).  On CPU tensors (gloo) the same schedule
+    runs without streams."""
     b, n_loc, h, d = q_loc.shape
     hp = h // world
     if hp % chunks:
         raise ValueError(f"{hp} heads per rank not divisible into {chunks} chunks")
     hc = hp // chunks
     cuda = q_loc.is_cuda
-    comm = torch.cuda.Stream(device=q_loc.device) if cuda else None
-    n = n_loc * world
-    kw = dict(dtype=q_loc.dtype, device=q_loc.device)
-    # chunk c send: [P_dst, B, N/P, 3, hc, d] = heads p*hp + c*hc .. of this rank's tokens
-    send = [torch.empty((world, b, n_loc, 3, hc, d), **kw) for _ in range(chunks)]
-    recv = [torch.empty_like(x) for x in send]
-    o_send = [torch.empty((world, b, n_loc, hc, d), **kw) for _ in range(chunks)]
-    o_recv = [torch.empty_like(x) for x in o_send]
-    out = torch.empty((b, n_loc, h, d), **kw)
+    if cuda and comm is None:
+        comm = torch.cuda.Stream(device=q_loc.device)
+    exs = [LayerExchange(b, n_loc, world, hc, d, q_loc.dtype, q_loc.device) for _ in range(chunks)]
+    if out is None:
+        out = torch.empty((b, n_loc, h, d), dtype=q_loc.dtype, device=q_loc.device)
 
     def ctx(stream):
         return torch.cuda.stream(stream) if cuda else _Null()
-
-    def views(r):  # [P_src, B, N/P, 3, hc, d] -> Q, K, V [B, N, hc, d] (token order)
-        qkv = r.view(1, n, 3, hc, d) if b == 1 else r.permute(1, 0, 2, 3, 4, 5).reshape(b, n, 3, hc, d)
-        return qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2]
 
     def step():
         cur = torch.cuda.current_stream(q_loc.device) if cuda else None
@@ -147,21 +168,17 @@ def make_layer_step_chunked(q_loc, k_loc, v_loc, world: int, attention, chunks: 
         if cuda:
             comm.wait_stream(cur)  # inputs written on the current stream
         with ctx(comm):
-            for c in range(chunks):
-                for s_, x in enumerate((q_loc, k_loc, v_loc)):
-                    send[c][:, :, :, s_].copy_(
-                        x.view(b, n_loc, world, hp, d)[:, :, :, c * hc:(c + 1) * hc]
-                        .permute(2, 0, 1, 3, 4))
-                dist.all_to_all_single(recv[c], send[c], group=group)
+            for c, ex in enumerate(exs):
+                ex.pack((q_loc, k_loc, v_loc), world, hp, c * hc)
+                dist.all_to_all_single(ex.recv, ex.send, group=group)
                 if cuda:
                     e = torch.cuda.Event()
                     e.record(comm)
                     ev_in.append(e)
-        for c in range(chunks):
+        for c, ex in enumerate(exs):
             if cuda:
                 cur.wait_event(ev_in[c])
-            oh = attention(c, *views(recv[c]))
-            o_send[c].copy_(oh.view(b, world, n_loc, hc, d).permute(1, 0, 2, 3, 4))
+            attention(c, ex.qkv(0), ex.qkv(1), ex.qkv(2), ex.out_view())
             if cuda:
                 e = torch.cuda.Event()
                 e.record(cur)
@@ -169,10 +186,8 @@ def make_layer_step_chunked(q_loc, k_loc, v_loc, world: int, attention, chunks: 
             with ctx(comm):
                 if cuda:
                     comm.wait_event(ev_out[c])
-                dist.all_to_all_single(o_recv[c], o_send[c], group=group)
-                # [P_src = head group, B, N/P, hc, d] -> heads p*hp + c*hc .. of this rank's tokens
-                out.view(b, n_loc, world, hp, d)[:, :, :, c * hc:(c + 1) * hc].copy_(
-                    o_recv[c].permute(1, 2, 0, 3, 4))
+                dist.all_to_all_single(ex.o_recv, ex.o_send, group=group)
+                ex.unpack(out, hp, c * hc)
         if cuda:
             cur.wait_stream(comm)
         return out

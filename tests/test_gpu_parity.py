@@ -652,6 +652,31 @@ def test_head_sharded_launches_are_bitwise_equal_to_the_full_launch(csa, world):
         assert torch.equal(part, full[:, :, sl])
 
 
+@pytest.mark.parametrize("batch", [1, 2])
+def test_exchange_layout_views_read_and_written_in_place(csa, batch):
+    """The stacked Ulysses exchange (ulysses.LayerExchange) hands the kernel Q, K, V as strided
+    views of one receive buffer [N, B, 3, H/P, d] (batch inside the token) and lets it write O
+    into the send buffer of the return exchange [N, B, H/P, d]: the TMA maps and the epilogue
+    take those strides, and the result is the contiguous call's bit for bit."""
+    from paper_2603_05503_b200 import ulysses
+
+    lay = Layout(21, 30, 52, 128)
+    heads = 4
+    q, k, v = qkv(batch, lay.N, heads, 128, seed=62, device="cuda")
+    rng = np.random.default_rng(5)
+    masks = (rng.random((heads, lay.NB, lay.NB)) < 0.3).astype(np.uint8)
+    masks[:, np.arange(lay.NB), np.arange(lay.NB)] = 1
+    ref, _, plan = run_attention(csa, lay, q, k, v, masks=masks, rep=[1], anchor_k=5)
+    ex = ulysses.LayerExchange(batch, lay.N, 1, heads, 128, torch.bfloat16, "cuda")
+    ex.pack((q, k, v), 1, heads, 0)
+    ex.recv.copy_(ex.send)                       # a world-1 exchange
+    qs, ks, vs, os_ = ex.qkv(0), ex.qkv(1), ex.qkv(2), ex.out_view()
+    assert qs.stride() == (3 * heads * 128, 3 * batch * heads * 128, 128, 1)
+    csa.sparse_attn_fwd(qs, ks, vs, plan, csa.build_work_list(plan, 0, heads), out=os_)
+    torch.cuda.synchronize()
+    assert torch.equal(os_, ref)
+
+
 def test_host_streaming_api_equals_device_call(csa):
     """csa.sparse_attn_fwd_host (pinned host in/out, head chunks with overlapped copies) gives
     the device call's output bit for bit (per-head arithmetic is schedule- and chunk-free)."""
@@ -859,3 +884,79 @@ def test_rect_edge_layouts_calibrate_compile_attend(csa, lay):
     assert_close(out[0, :, 0].double().cpu().numpy(), ref0, "mask head")
     ref1, _ = oracle_head(lay, q, k, v, 0, 1, rep_k=1)
     assert_close(out[0, :, 1].double().cpu().numpy(), ref1, "anchor head")
+
+
+@pytest.mark.parametrize("chunks", [1, 2])
+def test_sharded_denoise_step_nccl_graph(csa, chunks):
+    """f4 on the head-sharded runtime through a real NCCL group (one rank here; the exchange,
+    chunk overlap and CUDA-graph capture of the NCCL calls are the N-rank code path): the
+    sharded step's output equals the single-GPU DenoiseStep's bit for bit, eager and as a
+    replayed graph; rank dictionaries from PlanDictionary.shard hold the full dictionary's cells
+    bit for bit (P = 2, LPT order); sampled rows against the fp64 oracle."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2603_05503_b200 import pipeline
+
+    lay, H, d, T, L, prompts = Layout(2, 9, 40, 128), 4, 128, 2, 2, 2
+
+    def qk(p, t, l):
+        q, k, _ = inputs.structured_qk(lay, H, d, head_seed=10 * t + l, prompt_seed=p,
+                                       alpha=[2.0, 1.6, 1.1, 1.4], repetitive=(2,), device="cuda")
+        return q, k
+
+    dic = pipeline.calibrate(lay, T, L, H, prompts, qk, pipeline.DISTILLED, gamma=0.95)
+    bufs = [qkv(2, lay.N, H, d, seed=200 + l, device="cuda") for l in range(L)]
+    ref_o = [torch.empty_like(b[0]) for b in bufs]
+    single = pipeline.DenoiseStep(dic, [b[0] for b in bufs], [b[1] for b in bufs],
+                                  [b[2] for b in bufs], ref_o)
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        outs = [torch.empty_like(b[0]) for b in bufs]
+        step = pipeline.ShardedDenoiseStep(dic.shard(1, 0), 1, [b[0] for b in bufs],
+                                           [b[1] for b in bufs], [b[2] for b in bufs], outs,
+                                           chunks=chunks)
+        for t in range(T):
+            single.run(t)
+            step.run(t)
+            torch.cuda.synchronize()
+            for l in range(L):
+                assert torch.equal(outs[l], ref_o[l]), (t, l)
+            eager = [o.clone() for o in outs]
+            for o in outs:
+                o.zero_()
+            step.replay(t)
+            torch.cuda.synchronize()
+            for l in range(L):
+                assert torch.equal(outs[l], eager[l]), (t, l)
+    finally:
+        dist.destroy_process_group()
+    # rank dictionaries of a 2-way split in LPT order: cell-local compile, the same plans
+    perm = [0, 3, 1, 2]
+    nb = lay.NB
+    full_bits = unpack_bits(dic.plan.mask_bits.cpu().numpy(), nb).reshape(T, L, H, nb, nb)
+    full_kind = dic.plan.kind.cpu().numpy().reshape(T, L, H)
+    for r in range(2):
+        part = dic.shard(2, r, perm)
+        bits = unpack_bits(part.plan.mask_bits.cpu().numpy(), nb).reshape(T, L, 2, nb, nb)
+        kind = part.plan.kind.cpu().numpy().reshape(T, L, 2)
+        for j, h in enumerate(perm[2 * r:2 * r + 2]):
+            assert np.array_equal(kind[:, :, j], full_kind[:, :, h])
+            assert np.array_equal(bits[:, :, j], full_bits[:, :, h])
+    kind = full_kind
+    for t in range(T):
+        single.run(t)
+        torch.cuda.synchronize()
+        for l in range(L):
+            for h in range(H):
+                b, r = (t + h) % 2, (l + h) % nb
+                rows = (r * lay.B, min((r + 1) * lay.B, lay.N))
+                ref, _ = oracle_head(lay, *bufs[l], b, h, mask=full_bits[t, l, h],
+                                     rep_k=5 if kind[t, l, h] else None, rows=rows)
+                assert_close(ref_o[l][b, rows[0]:rows[1], h].double().cpu().numpy(), ref,
+                             f"t{t} l{l} h{h}")
