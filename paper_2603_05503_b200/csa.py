@@ -391,7 +391,8 @@ def default_order(lay: Layout, d: int) -> int:
     """Work-list order of the production path: 2 (head-major, longest row first within a head,
     one CTA per query block at a time)."""
     del lay, d
-    return 2
+    import os
+    return int(os.environ.get("CSA_ORDER", "2"))
 
 
 def build_work_list(plan: Plan, cell_base: int, n_heads: int, order: int = 2,

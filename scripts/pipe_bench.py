@@ -16,10 +16,11 @@ masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity or 0.69, seed=0)
 cnt = torch.from_numpy((masks.astype(np.uint16) * np.uint16(64)).reshape(-1).view(np.int16)).cuda()
 plan = csa.compile_plan(lay, cnt.view(torch.uint16), 32)
 work = csa.build_work_list(plan, 0, cfg.heads, order=int(os.environ.get("ORDER", "3")))
-q, k, v = inputs.qkv(1, lay.N, cfg.heads, cfg.d, seed=11, device="cuda")
+D = int(os.environ.get("D", cfg.d))
+q, k, v = inputs.qkv(1, lay.N, cfg.heads, D, seed=11, device="cuda")
 out = torch.empty_like(q)
 sizes = np.array([lay.block_size(c) for c in range(lay.NB)], np.int64)
-flop = 4.0 * cfg.d * float(np.einsum("hrc,r,c->", masks.astype(np.int64), sizes, sizes))
+flop = 4.0 * D * float(np.einsum("hrc,r,c->", masks.astype(np.int64), sizes, sizes))
 modes = [int(x) for x in os.environ.get("MODES", "0,1,2,3,4").split(",")]
 for mode in modes:
     csa.lib().csa_debug_trace(None, mode)
