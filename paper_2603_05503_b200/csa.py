@@ -384,15 +384,14 @@ class WorkList:
     items: torch.Tensor   # uint32 codes (stored as int32)
     n_work: torch.Tensor  # device int32 [1]
     max_work: int
-    pairs: bool = False   # order 3: items stand for rows (2p, 2p+1) (no kernel consumes them yet)
+    pairs: bool = False   # order 3: items stand for rows (2p, 2p+1) (no kernel in this build)
 
 
 def default_order(lay: Layout, d: int) -> int:
     """Work-list order of the production path: 2 (head-major, longest row first within a head,
     one CTA per query block at a time)."""
     del lay, d
-    import os
-    return int(os.environ.get("CSA_ORDER", "2"))
+    return 2
 
 
 def build_work_list(plan: Plan, cell_base: int, n_heads: int, order: int = 2,

@@ -149,7 +149,6 @@ const char* csa_version(void) { return "csa-b200 0.1 (sm_100a)"; }
 csa_status_t csa_debug_trace(void* buf, int32_t mode) {
     cudaError_t e = csa::set_attn_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_attn5_trace(buf, mode);
-    if (e == cudaSuccess) e = csa::set_attn6_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_calib_trace(buf, mode);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyToSymbol");
     return ok();
@@ -398,8 +397,9 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
                                  size_t workspace_bytes, csa_stream_t stream) {
     csa_status_t st = check_layout(L, head_dim, n_heads);
     if (st != CSA_OK) return st;
-    if (pair_items && !(L.block == 128 && is_square(L) && (head_dim == 128 || head_dim == 64)))
-        return fail(CSA_ERR_UNSUPPORTED, "pair work items need block 128 x 128, head_dim 128 / 64");
+    if (pair_items)
+        return fail(CSA_ERR_UNSUPPORTED,
+                    "pair work items: no kernel in this build (scripts/experiments/attn6_pair.cu)");
     // block 128 (square, or B_q = 128 x B_kv): fixed-reference kernels + exact-max fallback
     // passes, which keep their list in the workspace; block 64: attn.cu
     const bool b128 = L.block == 128;
@@ -466,8 +466,7 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
         csa::Fallback fb{base, base + 1, base + 1 + flag_words};
         e = cudaMemsetAsync(base, 0, 4 * (1 + flag_words), (cudaStream_t)stream);
         if (e == cudaSuccess)
-            e = pair_items   ? csa::launch_attn_pair(a, tq, tk, tv, grid, fb, (cudaStream_t)stream)
-                : is_square(L) ? csa::launch_attn_sepp(a, tq, tk, tv, grid, fb, (cudaStream_t)stream)
+            e = is_square(L) ? csa::launch_attn_sepp(a, tq, tk, tv, grid, fb, (cudaStream_t)stream)
                              : csa::launch_attn_rect(a, tq, tk, tv, grid, fb, 0,
                                                      (cudaStream_t)stream);
         csa::AttnArgs re = a;

@@ -145,13 +145,6 @@ cudaError_t set_attn5_trace(void* buf, int mode);
 cudaError_t launch_attn_sepp(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
                              const CUtensorMap& tv, int grid, const Fallback& fb,
                              cudaStream_t s);
-// Block 128 x 128, head_dim 128 or 64, PAIR items (csa_build_work_list order 3): two query
-// blocks per CTA, one softmax group each, one K/V stream over the union of their lists
-// (attn6.cu).  Flagged rows are appended to fb as single-item codes.
-cudaError_t set_attn6_trace(void* buf, int mode);
-cudaError_t launch_attn_pair(const AttnArgs& a, const CUtensorMap& tq, const CUtensorMap& tk,
-                             const CUtensorMap& tv, int grid, const Fallback& fb,
-                             cudaStream_t s);
 // Non-square blocks B_q = 128 x B_kv (attn_rect.cu), head_dim 128.  mode 0: fixed reference
 // max (first kept tile), overshooting items appended to fb; mode 1: exact row max of every item
 // of the (fallback) list, parked in the item's first output row; mode 2: recompute the list

@@ -301,76 +301,6 @@ def test_attention_batch2_shares_plan_and_is_deterministic(csa, lay, d):
         assert torch.equal(single[0], out[b])
 
 
-def pair_test_masks(heads, nb, seed):
-    """Row pairs (2p, 2p+1) with every overlap: identical rows, disjoint rows, one row a subset
-    of the other, random rows; the diagonal kept (Q7 repair never needed)."""
-    rng = np.random.default_rng(seed)
-    m = (rng.random((heads, nb, nb)) < 0.5).astype(np.uint8)
-    for h in range(heads):
-        for p in range(nb // 2):
-            r0, r1 = 2 * p, 2 * p + 1
-            kind = (h + p) % 4
-            if kind == 0:
-                m[h, r1] = m[h, r0]
-            elif kind == 1:
-                m[h, r0] = np.arange(nb) % 2 == 0
-                m[h, r1] = np.arange(nb) % 2 == 1
-            elif kind == 2:
-                m[h, r1] = m[h, r0] | (rng.random(nb) < 0.3)
-    m[:, np.arange(nb), np.arange(nb)] = 1
-    return m
-
-
-@pytest.mark.parametrize("lay,heads", [(Layout(2, 9, 40, 128), 3), (Layout(3, 7, 100, 128), 3),
-                                       (Layout(3, 7, 100, 128), 40)])
-@pytest.mark.parametrize("d", [128, 64])
-def test_pair_items_against_oracle(csa, lay, heads, d):
-    """attn6.cu (pair items, order 3): two query blocks per CTA over the union of their lists --
-    identical / disjoint / nested / random row pairs, an odd block count (the last pair has one
-    member), ragged N, a REPETITIVE head (anchor tiles paired), batch 2; every row against the
-    oracle, run-to-run bitwise determinism, and the same rows as the single-item kernel within
-    bf16 rounding of the output.  40 heads: 360 items over <= 148 CTAs (several items per CTA,
-    the K/V ring and the issuers' positions carried across items)."""
-    q, k, v = qkv(2, lay.N, heads, d, seed=31, device="cuda")
-    masks = pair_test_masks(heads, lay.NB, seed=8)
-    out, lse, plan = run_attention(csa, lay, q, k, v, masks=masks, rep=[1], anchor_k=2, order=3,
-                                   lse=True)
-    lse = lse.view(2, heads, lay.N).cpu().numpy()
-    for b in range(2):
-        for h in range(heads):
-            ref, ref_lse = oracle_head(lay, q, k, v, b, h, mask=masks[h],
-                                       rep_k=2 if h == 1 else None)
-            assert_close(out[b, :, h].double().cpu().numpy(), ref, f"b{b} h{h}")
-            assert np.abs(lse[b, h] - ref_lse).max() <= 1e-3, (b, h)
-    again, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[1], anchor_k=2, order=3)
-    assert torch.equal(out, again)
-    single, _, _ = run_attention(csa, lay, q, k, v, masks=masks, rep=[1], anchor_k=2, order=2)
-    assert (out.float() - single.float()).abs().max().item() <= 1e-2
-    assert fallback_count(csa, q) == 0
-
-
-@pytest.mark.parametrize("d", [128, 64])
-def test_pair_items_overflow_fallback(csa, d):
-    """Scores growing block by block far beyond 2^56 of the first kept tile: every pair member
-    is flagged and recomputed by the exact-max passes (single-item codes in the fallback list)."""
-    lay = Layout(2, 9, 40, 128)
-    heads, nb = 2, lay.NB
-    q, k, v = qkv(1, lay.N, heads, d, seed=21, device="cuda")
-    gain = torch.ones(lay.N, device="cuda")
-    for c in range(nb):
-        gain[c * 128:(c + 1) * 128] = 1.0 + 40.0 * c / nb
-    k = (k.float() * gain.view(1, -1, 1, 1)).to(torch.bfloat16)
-    rng = np.random.default_rng(5)
-    masks = (rng.random((heads, nb, nb)) < 0.6).astype(np.uint8)
-    masks[:, :, 0] = 1
-    masks[:, :, nb - 1] = 1
-    out, _, _ = run_attention(csa, lay, q, k, v, masks=masks, order=3)
-    assert fallback_count(csa, q) > 0
-    for h in range(heads):
-        ref, _ = oracle_head(lay, q, k, v, 0, h, mask=masks[h])
-        assert_close(out[0, :, h].double().cpu().numpy(), ref, f"d{d} h{h}")
-
-
 def sample_units(lay, heads, n, seed):
     rng = np.random.default_rng(seed)
     units = {(0, lay.NB - 1), (heads - 1, 0)}
@@ -379,18 +309,16 @@ def sample_units(lay, heads, n, seed):
     return sorted(units)
 
 
-@pytest.mark.parametrize("order", [2, 3])
 @pytest.mark.parametrize("name", ["wan480", "wan720", "mochi"])
-def test_attention_full_size_sampled(csa, name, order):
+def test_attention_full_size_sampled(csa, name):
     """BASELINE configs at full size, bench launch configuration; oracle on sampled (h, r)
-    (Mochi: generator-S masks at the paper's 69 % sparsity).  order 3: pair items (attn6.cu)."""
+    (Mochi: generator-S masks at the paper's 69 % sparsity)."""
     cfg = CONFIGS[name]
     lay = cfg.layout
     q, k, v = qkv(1, lay.N, cfg.heads, cfg.d, seed=11, device="cuda")
     masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity or 0.69, seed=0)
     rep = [h for h in (3, 17, 29, 38) if h < cfg.heads]
-    out, lse, plan = run_attention(csa, lay, q, k, v, masks=masks, rep=rep, anchor_k=5, lse=True,
-                                   order=order)
+    out, lse, plan = run_attention(csa, lay, q, k, v, masks=masks, rep=rep, anchor_k=5, lse=True)
     lse = lse.view(cfg.heads, lay.N).cpu().numpy()
     errs = []
     for h, r in sample_units(lay, cfg.heads, 10, seed=2):
@@ -406,8 +334,7 @@ def test_attention_full_size_sampled(csa, name, order):
         assert fallback_count(csa, q) == 0  # realistic rows never overshoot the reference max
 
 
-@pytest.mark.parametrize("order", [2, 3])
-def test_attention_wan720_structured_peaked_sampled(csa, order):
+def test_attention_wan720_structured_peaked_sampled(csa):
     """Wan 720p at full size on generator-G Q/K (peak-logit scale alpha up to 1.6, sink keys,
     two repetitive heads), plan CALIBRATED from the same prompt (a2-a6 through the C ABI, eps of
     t = 25 of 50), production launch.  Rows keep block 0 (the sinks), so their first kept tile
@@ -429,7 +356,7 @@ def test_attention_wan720_structured_peaked_sampled(csa, order):
     csa.spatial_similarity(lay, q, k, lse_c, 5, sim)
     s = sim / float(lay.F * lay.H)
     plan = csa.compile_plan(lay, counts, 1, similarity=s, gamma=0.87, anchor_k=5)
-    work = csa.build_work_list(plan, 0, heads, order=order)
+    work = csa.build_work_list(plan, 0, heads)
     lse = torch.empty(heads * lay.N, dtype=torch.float32, device="cuda")
     out = csa.sparse_attn_fwd(q, k, v, plan, work, lse_out=lse)
     torch.cuda.synchronize()
