@@ -684,6 +684,12 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
     sim_c = torch.zeros(H, dtype=torch.float64, device=dev)
     t_sim, _, _ = time_loop(lambda: csa.spatial_similarity(lay, q[:1], k[:1], lse_c, 5, sim_c), 1, 1,
                          stream)
+    sim_f = torch.zeros(H, dtype=torch.float64, device=dev)
+    t_fused, _, _ = time_loop(lambda: csa.calib_accumulate_sim(lay, q[:1], k[:1], eps, counts_c, 5,
+                                                               sim_f), 1, 1, stream)
+    ph["calib_sim_fused_ms"] = round(t_fused, 3)           # a2-a5 + f1 in one pass (2 exps/score)
+    ph["calib_sim_fused_exp_frac_of_mufu"] = None          # filled below
+    ph["calib_plus_sim_two_calls_ms"] = round(t_cal + t_sim, 3)
     ph["spatial_similarity_ms"] = round(t_sim, 3)          # f1: 2 exps per score
     ph["calib_accumulate_ms"] = round(t_cal, 3)             # single exponential pass (scratch)
     ph["calib_accumulate_two_pass_ms"] = round(t_cal2, 3)   # LSE pass + E pass
@@ -697,6 +703,8 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
     ph["calib_mufu_peak_exp_per_s"] = mufu["ex2_per_s"]
     ph["calib_mufu_peak_src"] = mufu["src"]
     ph["calib_exp_frac_of_mufu"] = round(ph["calib_exp_per_s"] / mufu["ex2_per_s"], 4)
+    ph["calib_sim_fused_exp_frac_of_mufu"] = round(2.0 * calib_exps / (t_fused * 1e-3)
+                                                   / mufu["ex2_per_s"], 4)
     cnt = torch.from_numpy((masks.astype(np.uint16) * np.uint16(64)).reshape(-1).view(np.int16)).to(dev).view(torch.uint16)
     sim = torch.tensor([1.0 if h in rep else 0.0 for h in range(H)], dtype=torch.float64, device=dev)
     torch.cuda.synchronize()

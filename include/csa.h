@@ -114,7 +114,7 @@ typedef struct {
 
 /* Which workspace a call needs (csa_workspace_size). */
 enum { CSA_WS_CALIB = 0, CSA_WS_COMPILE = 1, CSA_WS_WORK_LIST = 2, CSA_WS_ATTN = 3,
-       CSA_WS_SIMILARITY = 4, CSA_WS_MERGE = 5 };
+       CSA_WS_SIMILARITY = 4, CSA_WS_MERGE = 5, CSA_WS_CALIB_SIM = 6 };
 
 /* ------------------------------------------------------------------------------------------
  * csa_calib_accumulate -- one calibration prompt at one (t, l), all heads.
@@ -165,6 +165,26 @@ CSA_API csa_status_t csa_spatial_similarity(csa_layout_t L, int32_t n_heads, int
                                     const float* lse, int32_t anchor_k, double* sim_sum,
                                     float* cos_out, void* workspace, size_t workspace_bytes,
                                     csa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * csa_calib_accumulate_sim -- csa_calib_accumulate (lse computed in-kernel) AND
+ * csa_spatial_similarity of the same prompt in ONE pass over the key tiles per (head, query
+ * block) (the similarity statistic is computed alongside the
+ * calibration statistics): per key tile both S = Q K^T and the anchor tokens' scores
+ * S_a = Q_a K^T, each score's exponential taken once.  Outputs and their definitions are those
+ * of the two calls: keep_count (+= the selection at eps), optional energy_out / lse_out, sim_sum
+ * (+= sum over (f,i) of cos), optional cos_out; equal to the two-call sequence up to fp32
+ * rounding order (the selection is taken on this pass's own E).
+ * Block 128 x 128 (head_dim 128 or 64) runs the fused kernel; other layouts run the two calls'
+ * kernels in sequence (same results).  anchor_k in [1, rows].
+ * Workspace (required): csa_workspace_size(CSA_WS_CALIB_SIM, L, n_heads, head_dim) bytes,
+ * 16-byte aligned, contents irrelevant. */
+CSA_API csa_status_t csa_calib_accumulate_sim(csa_layout_t L, int32_t n_heads, int32_t head_dim,
+                                      float softmax_scale, csa_tensor_t q, csa_tensor_t k,
+                                      double eps, uint16_t* keep_count, float* energy_out,
+                                      float* lse_out, int32_t anchor_k, double* sim_sum,
+                                      float* cos_out, void* workspace, size_t workspace_bytes,
+                                      csa_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------
  * csa_compile_plan -- keep counts -> plan, for cells [0, n_cells).

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libcsa.so")
 BUILD = os.path.join(HERE, "build")
-SOURCES = ["api.cu", "plan.cu", "calib.cu", "attn.cu", "sim.cu", "compact.cu", "attn_rect.cu", "attn5.cu"]
+SOURCES = ["api.cu", "plan.cu", "calib.cu", "attn.cu", "sim.cu", "compact.cu", "attn_rect.cu", "attn5.cu", "calibsim.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -53,7 +53,7 @@ class _PlanT(ctypes.Structure):
 EXPORTS = ["csa_calib_accumulate", "csa_compile_plan", "csa_build_work_list",
            "csa_sparse_attn_fwd", "csa_workspace_size", "csa_validate_plan", "csa_last_error",
            "csa_version", "csa_debug_trace", "csa_spatial_similarity", "csa_merge_intervals",
-           "csa_share_timesteps", "csa_copy_heads"]
+           "csa_share_timesteps", "csa_copy_heads", "csa_calib_accumulate_sim"]
 
 _lib = None
 
@@ -75,6 +75,10 @@ def lib() -> ctypes.CDLL:
     L.csa_calib_accumulate.restype = st
     L.csa_calib_accumulate.argtypes = [_LayoutT, i32, i32, ctypes.c_float, _TensorT, _TensorT, vp,
                                        ctypes.c_double, vp, vp, vp, vp, ctypes.c_size_t, vp]
+    L.csa_calib_accumulate_sim.restype = st
+    L.csa_calib_accumulate_sim.argtypes = [_LayoutT, i32, i32, ctypes.c_float, _TensorT, _TensorT,
+                                           ctypes.c_double, vp, vp, vp, i32, vp, vp, vp,
+                                           ctypes.c_size_t, vp]
     L.csa_compile_plan.restype = st
     L.csa_compile_plan.argtypes = [_LayoutT, i64, vp, i32, vp, ctypes.c_double, i32, i32,
                                    ctypes.POINTER(_PlanT), vp, ctypes.c_size_t, vp]
@@ -161,6 +165,31 @@ def calib_accumulate(lay: Layout, q: torch.Tensor, k: torch.Tensor, eps: float,
                                       _ptr(energy_out), _ptr(lse_out), _ptr(ws), ws_bytes,
                                       _stream(stream)),
            "csa_calib_accumulate")
+
+
+def calib_accumulate_sim(lay: Layout, q: torch.Tensor, k: torch.Tensor, eps: float,
+                         keep_count: torch.Tensor, anchor_k: int, sim_sum: torch.Tensor,
+                         energy_out: torch.Tensor | None = None,
+                         lse_out: torch.Tensor | None = None, cos_out: torch.Tensor | None = None,
+                         scale: float | None = None, stream=None) -> None:
+    """csa_calib_accumulate_sim: calib_accumulate (a2-a5) and spatial_similarity (f1) of one
+    prompt in one pass over the key tiles."""
+    _, n, heads, d = q.shape
+    assert n == lay.N and keep_count.dtype == torch.uint16 and keep_count.is_contiguous()
+    assert keep_count.numel() == heads * lay.NB * lay.NBK
+    assert sim_sum.dtype == torch.float64 and sim_sum.numel() == heads
+    for t, shape in ((lse_out, heads * n), (energy_out, heads * lay.NB * lay.NBK),
+                     (cos_out, heads * lay.F * lay.H)):
+        if t is not None:
+            assert t.dtype == torch.float32 and t.is_contiguous() and t.numel() == shape
+    sc = default_scale(d) if scale is None else scale
+    nbytes = lib().csa_workspace_size(6, _layout(lay), heads, d)
+    ws = _calib_workspace(q.device, nbytes, key="calib_sim")
+    _check(lib().csa_calib_accumulate_sim(_layout(lay), heads, d, sc, _tensor(q), _tensor(k),
+                                          float(eps), _ptr(keep_count), _ptr(energy_out),
+                                          _ptr(lse_out), int(anchor_k), _ptr(sim_sum),
+                                          _ptr(cos_out), _ptr(ws), nbytes, _stream(stream)),
+           "csa_calib_accumulate_sim")
 
 
 def spatial_similarity(lay: Layout, q: torch.Tensor, k: torch.Tensor, lse: torch.Tensor,

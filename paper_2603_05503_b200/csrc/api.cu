@@ -170,6 +170,19 @@ size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_
         if (check_layout(L, 0, 0) != CSA_OK || n_heads < 1) return 0;
         return (size_t)n_heads * (size_t)L.frames * L.rows * L.cols * 3 * sizeof(float);
     }
+    if (which == CSA_WS_CALIB_SIM) {       // fused pass: row partials + similarity partials
+        if (check_layout(L, 0, 0) != CSA_OK || n_heads < 1) return 0;
+        DeviceInfo di;
+        if (device_info(&di) != CSA_OK) return 0;
+        const csa::Geo g = csa::make_geo(L);
+        size_t scr = csa::calib_scratch_bytes(g, n_heads, di.sms);  // >= the fused kernel's
+        scr = (scr + 255) / 256 * 256;
+        csa_layout_t sq = L;
+        sq.block_kv = 0;
+        // + an LSE buffer for layouts that run the two calls' kernels in sequence
+        return scr + csa_workspace_size(CSA_WS_SIMILARITY, sq, n_heads, head_dim) +
+               (size_t)n_heads * g.N * sizeof(float);
+    }
     if (which == CSA_WS_CALIB) {           // single-pass calibration: (t, m) row partials
         if (check_layout(L, 0, 0) != CSA_OK || n_heads < 1) return 0;
         DeviceInfo di;
@@ -219,6 +232,76 @@ csa_status_t csa_calib_accumulate(csa_layout_t L, int32_t n_heads, int32_t head_
     }
     cudaError_t e = csa::launch_calib(a, head_dim, tq, tk, di.sms, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "calib launch");
+    return ok();
+}
+
+csa_status_t csa_calib_accumulate_sim(csa_layout_t L, int32_t n_heads, int32_t head_dim,
+                                      float softmax_scale, csa_tensor_t q, csa_tensor_t k,
+                                      double eps, uint16_t* keep_count, float* energy_out,
+                                      float* lse_out, int32_t anchor_k, double* sim_sum,
+                                      float* cos_out, void* workspace, size_t workspace_bytes,
+                                      csa_stream_t stream) {
+    csa_status_t st = check_layout(L, head_dim, n_heads);
+    if (st != CSA_OK) return st;
+    if (n_heads < 1) return fail(CSA_ERR_INVALID_ARGUMENT, "n_heads must be >= 1");
+    if (!(softmax_scale > 0.0f)) return fail(CSA_ERR_INVALID_ARGUMENT, "softmax_scale <= 0");
+    if (!(eps > 0.0)) return fail(CSA_ERR_INVALID_ARGUMENT, "eps must be > 0");
+    if (!keep_count || !sim_sum)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "keep_count and sim_sum are required");
+    if (anchor_k < 1 || anchor_k > L.rows)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "anchor_k %d outside [1, rows=%d]", anchor_k, L.rows);
+    const size_t need = csa_workspace_size(CSA_WS_CALIB_SIM, L, n_heads, head_dim);
+    if (!workspace || workspace_bytes < need)
+        return fail(CSA_ERR_INVALID_ARGUMENT,
+                    "workspace smaller than csa_workspace_size(CSA_WS_CALIB_SIM) = %zu", need);
+    if (reinterpret_cast<uintptr_t>(workspace) % 16 != 0)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "workspace must be 16-byte aligned");
+    if (!q.ptr || (q.stride_n * 2) % 16 || (q.stride_h * 2) % 16)
+        return fail(CSA_ERR_INVALID_ARGUMENT, "q: null or strides not 16-byte multiples");
+    DeviceInfo di;
+    if ((st = device_info(&di)) != CSA_OK) return st;
+    const csa::Geo g = csa::make_geo(L);
+    size_t scr = (csa::calib_scratch_bytes(g, n_heads, di.sms) + 255) / 256 * 256;
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    csa_layout_t sq = L;
+    sq.block_kv = 0;
+    const size_t part_bytes = csa_workspace_size(CSA_WS_SIMILARITY, sq, n_heads, head_dim);
+    if (!(is_square(L) && L.block == 128 && (head_dim == 128 || head_dim == 64))) {
+        // other layouts: the two calls' kernels in sequence on the same stream
+        float* lse = lse_out ? lse_out : reinterpret_cast<float*>(ws + scr + part_bytes);
+        st = csa_calib_accumulate(L, n_heads, head_dim, softmax_scale, q, k, nullptr, eps,
+                                  keep_count, energy_out, lse, ws, scr, stream);
+        if (st != CSA_OK) return st;
+        return csa_spatial_similarity(sq, n_heads, head_dim, softmax_scale, q, k, lse, anchor_k,
+                                      sim_sum, cos_out, ws + scr, part_bytes, stream);
+    }
+    CUtensorMap tq, tk;
+    if ((st = make_map(&tq, q, 1, g.N, n_heads, head_dim, g.B, "q")) != CSA_OK) return st;
+    if ((st = make_map(&tk, k, 1, g.N, n_heads, head_dim, g.B, "k")) != CSA_OK) return st;
+    csa::CalibArgs a;
+    a.g = g;
+    a.n_heads = n_heads;
+    a.scale_log2 = softmax_scale * 1.4426950408889634f;
+    a.lse_in = nullptr;
+    a.eps = eps;
+    a.keep_count = keep_count;
+    a.energy_out = energy_out;
+    a.lse_out = lse_out;
+    a.scratch = reinterpret_cast<float2*>(ws);
+    csa::SimArgs s;
+    s.g = g;
+    s.n_heads = n_heads;
+    s.scale_log2 = a.scale_log2;
+    s.q = static_cast<const __nv_bfloat16*>(q.ptr);
+    s.q_sn = q.stride_n;
+    s.q_sh = q.stride_h;
+    s.lse = nullptr;
+    s.anchor_k = anchor_k;
+    s.partials = reinterpret_cast<float*>(ws + scr);
+    s.sim_sum = sim_sum;
+    s.cos_out = cos_out;
+    cudaError_t e = csa::launch_calib_sim(a, s, head_dim, tq, tk, di.sms, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "calibration + similarity launch");
     return ok();
 }
 

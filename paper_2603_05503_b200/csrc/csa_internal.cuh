@@ -109,6 +109,15 @@ struct SimArgs {
 };
 cudaError_t launch_similarity(const SimArgs& a, int head_dim, const CUtensorMap& tq,
                               const CUtensorMap& tk, int num_sms, cudaStream_t s);
+// sim_reduce_kernel alone: partials -> cos(f, i) and sim_sum (one CTA per head).
+cudaError_t launch_similarity_reduce(const SimArgs& a, cudaStream_t s);
+// a2-a5 + f1 in one pass (calibsim.cu; block 128 x 128, head_dim 128 / 64): a.scratch holds
+// calib_sim_scratch_bytes (one float per (row, key block) and CTA), s.partials the
+// [n_heads][N][3] similarity partials; ends with the similarity reduce.
+size_t calib_sim_scratch_bytes(const Geo& g, int32_t n_heads, int num_sms);
+cudaError_t launch_calib_sim(const CalibArgs& a, const SimArgs& s, int head_dim,
+                             const CUtensorMap& tq, const CUtensorMap& tk, int num_sms,
+                             cudaStream_t st);
 
 struct AttnArgs {
     Geo g;

@@ -317,6 +317,11 @@ cudaError_t launch_t(const SimArgs& a, const CUtensorMap& tq, const CUtensorMap&
 
 }  // namespace
 
+cudaError_t launch_similarity_reduce(const SimArgs& a, cudaStream_t s) {
+    sim_reduce_kernel<<<a.n_heads, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_similarity(const SimArgs& a, int head_dim, const CUtensorMap& tq,
                               const CUtensorMap& tk, int num_sms, cudaStream_t s) {
     const int64_t items = (int64_t)a.n_heads * a.g.NB;

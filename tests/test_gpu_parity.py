@@ -504,6 +504,97 @@ def test_spatial_similarity_against_oracle(csa, lay, heads, d, kind):
             assert np.abs(cos - 1.0).max() <= 1e-5  # every row is its own anchor
 
 
+@pytest.mark.parametrize("lay,d", [(Layout(2, 9, 40, 128), 128), (Layout(2, 9, 40, 128), 64),
+                                   (Layout(3, 7, 100, 128), 128), (Layout(1, 3, 40, 128), 128),
+                                   (Layout(2, 5, 25, 64), 64), (Layout(2, 9, 40, 128, 80), 128)])
+def test_calib_sim_fused_against_oracle(csa, lay, d):
+    """csa_calib_accumulate_sim (a2-a5 + f1 in one pass; calibsim.cu at block 128 x 128, the two
+    calls' kernels in sequence otherwise): E, LSE, the selection and cos(f, i) against the fp64
+    oracle, and the same outputs as calib_accumulate + spatial_similarity within fp32 rounding
+    order.  N_B = 1 (one ragged block: group 1 has no key tile), odd N_B, ragged N, d 64,
+    block 64 and B_kv = 80."""
+    heads, kA = 2, 2
+    q, k, _ = inputs.structured_qk(lay, heads, d, 3, 1, alpha=[0.9, 1.4], repetitive=(1,),
+                                   device="cuda")
+    nb, nbk = lay.NB, lay.NBK
+    eps = oracle.epsilon(20, 50, oracle.A_of_N(lay.N), 0.99, 16)
+    cnt_f = u16_zeros(heads * nb * nbk)
+    E_f = torch.empty(heads * nb * nbk, dtype=torch.float32, device="cuda")
+    lse_f = torch.empty(heads * lay.N, dtype=torch.float32, device="cuda")
+    sim_f = torch.zeros(heads, dtype=torch.float64, device="cuda")
+    cos_f = torch.empty(heads * lay.F * lay.H, dtype=torch.float32, device="cuda")
+    csa.calib_accumulate_sim(lay, q, k, eps, cnt_f, kA, sim_f, energy_out=E_f, lse_out=lse_f,
+                             cos_out=cos_f)
+    # the two-call sequence on the same prompt
+    cnt_s = u16_zeros(heads * nb * nbk)
+    E_s = torch.empty_like(E_f)
+    lse_s = torch.empty_like(lse_f)
+    sim_s = torch.zeros_like(sim_f)
+    cos_s = torch.empty_like(cos_f)
+    csa.calib_accumulate(lay, q, k, eps, cnt_s, energy_out=E_s, lse_out=lse_s)
+    csa.spatial_similarity(lay, q, k, lse_s, kA, sim_s, cos_out=cos_s)
+    torch.cuda.synchronize()
+    E = E_f.view(heads, nb, nbk).double().cpu().numpy()
+    cnt = u16_np(cnt_f).reshape(heads, nb, nbk)
+    cos = cos_f.view(heads, lay.F, lay.H).double().cpu().numpy()
+    assert np.abs(E - E_s.view(heads, nb, nbk).double().cpu().numpy()).max() <= 5e-6
+    assert np.abs(lse_f.cpu().numpy() - lse_s.cpu().numpy()).max() <= 1e-4
+    assert np.abs(cos - cos_s.view(heads, lay.F, lay.H).double().cpu().numpy()).max() <= 2e-6
+    scale = 1.0 / np.sqrt(d)
+    lse = lse_f.view(heads, lay.N).cpu().numpy()
+    for h in range(heads):
+        qh, kh = head64(q, 0, h), head64(k, 0, h)
+        E_ref = oracle.block_energy(qh, kh, scale, lay.B, block_kv=lay.BK or None)
+        assert np.abs(E[h] - E_ref).max() <= 5e-5, h
+        for r in range(nb):  # bit-exact selection on the pass's own E
+            assert np.array_equal(oracle.select(E[h, r], eps), cnt[h, r]), (h, r)
+        assert np.abs(lse[h] - oracle.row_lse(qh, kh, scale)).max() <= 1e-3
+        ref = np.array([[oracle.spatial_cos(lay.F, lay.H, lay.W, qh, kh, scale, kA, f, i)
+                         for i in range(lay.H)] for f in range(lay.F)])
+        assert np.abs(cos[h] - ref).max() <= 2e-5, h
+        assert abs(sim_f[h].item() / (lay.F * lay.H) - ref.mean()) <= 2e-5
+
+
+@pytest.mark.parametrize("name", ["wan720", "mochi"])
+def test_calib_sim_fused_full_size_sampled(csa, name):
+    """Full-size fused pass (generator-G Q/K, one repetitive head): every row's selection
+    bit-exact on the pass's own E, sampled E rows and cos(f, i) against the oracle, and all cos
+    within fp32 rounding of the two-call sequence."""
+    cfg = CONFIGS[name]
+    lay = cfg.layout
+    heads, kA = 4, 5
+    q, k, _ = inputs.structured_qk(lay, heads, cfg.d, 5, 0, alpha=[0.8, 1.0, 1.2, 1.5],
+                                   repetitive=(2,), device="cuda")
+    nb = lay.NB
+    eps = oracle.epsilon(25, 50, oracle.A_of_N(lay.N), 0.99, 16)
+    counts = u16_zeros(heads * nb * nb)
+    energy = torch.empty(heads * nb * nb, dtype=torch.float32, device="cuda")
+    sim = torch.zeros(heads, dtype=torch.float64, device="cuda")
+    cos_f = torch.empty(heads * lay.F * lay.H, dtype=torch.float32, device="cuda")
+    csa.calib_accumulate_sim(lay, q, k, eps, counts, kA, sim, energy_out=energy, cos_out=cos_f)
+    lse_s = torch.empty(heads * lay.N, dtype=torch.float32, device="cuda")
+    csa.calib_accumulate(lay, q, k, eps, u16_zeros(heads * nb * nb), lse_out=lse_s)
+    cos_s = torch.empty_like(cos_f)
+    csa.spatial_similarity(lay, q, k, lse_s, kA, torch.zeros_like(sim), cos_out=cos_s)
+    torch.cuda.synchronize()
+    E = energy.view(heads, nb, nb).double().cpu().numpy()
+    cnt = u16_np(counts).reshape(heads, nb, nb)
+    cos = cos_f.view(heads, lay.F, lay.H).double().cpu().numpy()
+    assert np.abs(cos - cos_s.view(heads, lay.F, lay.H).double().cpu().numpy()).max() <= 2e-6
+    for h in range(heads):
+        for r in range(nb):
+            assert np.array_equal(oracle.select(E[h, r], eps), cnt[h, r])
+    scale = 1.0 / np.sqrt(cfg.d)
+    for h, r in ((0, 0), (3, nb - 1), (2, nb // 2)):
+        qh, kh = head64(q, 0, h), head64(k, 0, h)
+        E_ref = oracle.block_energy(qh, kh, scale, lay.B, block_rows=(r, r + 1))
+        assert np.abs(E[h, r] - E_ref[0]).max() <= 5e-5
+    for h, f, i in ((0, 0, 0), (2, lay.F - 1, lay.H // 2), (3, lay.F // 2, lay.H - 1)):
+        qh, kh = head64(q, 0, h), head64(k, 0, h)
+        ref = oracle.spatial_cos(lay.F, lay.H, lay.W, qh, kh, scale, kA, f, i)
+        assert abs(cos[h, f, i] - ref) <= 2e-5, (h, f, i)
+
+
 def test_spatial_similarity_repetitive_structure_and_accumulation(csa):
     lay = Layout(2, 9, 40, 128)
     heads = 2
