@@ -167,14 +167,12 @@ def workload(cfg, args, heads_lo, heads_hi, rank_dev):
                            device=rank_dev).view(torch.uint16)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    lse = torch.empty(cfg.heads * lay.N, dtype=torch.float32, device=rank_dev)
     sim_sum = torch.zeros(cfg.heads, dtype=torch.float64, device=rank_dev)
     for p in range(n_prompts):
         qc, kc, _ = inputs.structured_qk(lay, cfg.heads, cfg.d, head_seed=1, prompt_seed=p,
                                          alpha=alphas, repetitive=tuple(sorted(rep)),
                                          device=rank_dev)
-        csa.calib_accumulate(lay, qc, kc, eps, counts_t, lse_out=lse)   # a2-a5
-        csa.spatial_similarity(lay, qc, kc, lse, 5, sim_sum)            # f1
+        csa.calib_accumulate_sim(lay, qc, kc, eps, counts_t, 5, sim_sum)  # a2-a5 + f1, one pass
         del qc, kc
     torch.cuda.synchronize()
     calib_s = time.perf_counter() - t0

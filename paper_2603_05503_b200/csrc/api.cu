@@ -150,6 +150,7 @@ csa_status_t csa_debug_trace(void* buf, int32_t mode) {
     cudaError_t e = csa::set_attn_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_attn5_trace(buf, mode);
     if (e == cudaSuccess) e = csa::set_calib_trace(buf, mode);
+    if (e == cudaSuccess) e = csa::set_calib_sim_trace(buf, mode);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyToSymbol");
     return ok();
 }
@@ -183,7 +184,7 @@ size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads, int32_
         return scr + csa_workspace_size(CSA_WS_SIMILARITY, sq, n_heads, head_dim) +
                (size_t)n_heads * g.N * sizeof(float);
     }
-    if (which == CSA_WS_CALIB) {           // single-pass calibration: (t, m) row partials
+    if (which == CSA_WS_CALIB) {           // single-pass calibration: per-(row, key block) log2-sum-exp
         if (check_layout(L, 0, 0) != CSA_OK || n_heads < 1) return 0;
         DeviceInfo di;
         if (device_info(&di) != CSA_OK) return 0;

@@ -114,6 +114,28 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
     return pk2((uint32_t)p + e0, (uint32_t)(p >> 32) + e1);
 }
 
+// 2^x for a pair of x on the FMA pipe with a degree-5 polynomial for 2^frac (relative
+// minimax fit on [0,1), max rel. error 1.7e-7 -- as accurate as ex2.approx, which the energies
+// need: unlike P in the attention kernel they are not rounded to bf16 afterwards).
+__device__ __forceinline__ uint64_t exp2_poly5(uint64_t x) {
+    // clamp at -126: the fit's p(0) = 0.99999994 < 1, so floor(x) = -127 would borrow out of
+    // the exponent field (0x3F7FFFFF - 0x3F800000 = NaN bits); at -126 the result is a
+    // denormal that the .ftz arithmetic downstream reads as 0 (masked keys hold -inf).
+    const float x0 = fmaxf(lo_f(x), -126.0f), x1 = fmaxf(hi_f(x), -126.0f);
+    const uint64_t xc = f2(x0, x1);
+    const uint64_t kRound = f2(12582912.0f, 12582912.0f);  // 2^23 + 2^22
+    const uint64_t rnd = fadd2_rm(xc, kRound);               // floor(x) in the low mantissa bits
+    const uint64_t frac = fsub2(xc, fsub2(rnd, kRound));     // in [0, 1)
+    uint64_t p = f2(0.0018775767f, 0.0018775767f);
+    p = ffma2(p, frac, f2(0.0089893406f, 0.0089893406f));
+    p = ffma2(p, frac, f2(0.055826318f, 0.055826318f));
+    p = ffma2(p, frac, f2(0.24015361f, 0.24015361f));
+    p = ffma2(p, frac, f2(0.69315308f, 0.69315308f));
+    p = ffma2(p, frac, f2(0.99999994f, 0.99999994f));
+    const uint32_t e0 = (uint32_t)rnd << 23, e1 = (uint32_t)(rnd >> 32) << 23;
+    return pk2((uint32_t)p + e0, (uint32_t)(p >> 32) + e1);
+}
+
 // Debug timeline (csa_debug_trace): clock64 stamps of CTA 0's pipeline events; nullptr = off.
 // Each translation unit defines its own `static __device__` g_trace / g_debug_mode (debug only).
 // Compiled in only for trace builds (CSA_TRACE_BUILD=1 python -m paper_2603_05503_b200._build

@@ -13,9 +13,10 @@
 //
 // Passes over the N_B key tiles of an item (each tile: S = Q K^T by tcgen05 into TMEM):
 //   lse_in given      one pass: per-row sums of exp(s - lse) reduced to E_{r,c} tile by tile.
-//   scratch given     one pass: per (row, tile) the partial sum t_ic = sum_j 2^(s_ij*l2e - m_ic)
-//                     and the running max m_ic it was taken against go to global scratch; after the
-//                     pass lse is known and E_{r,c} = sum_i t_ic 2^(m_ic - lse2_i) / |I_r|.
+//   scratch given     one pass: per (row, tile) the tile's log2-sum-exp u_ic = m_ic + log2(t_ic),
+//                     t_ic = sum_j 2^(s_ij*l2e - m_ic) against the running max m_ic, goes to global
+//                     scratch (4 bytes); after the pass lse is known and
+//                     E_{r,c} = sum_i 2^(u_ic - lse2_i) / |I_r|.
 //   neither           two passes (online LSE, then E) -- twice the exponentials.
 // Roles (persistent, one CTA per SM, 12 warps): warp 0 TMA producer, warp 1 MMA issuer, warp 2
 // TMEM allocator, warps 4-7 / 8-11 two row groups taking alternate tiles.  Exp-bound: packed
@@ -74,28 +75,6 @@ struct CalibSmem {
     static_assert(BKV == BK || (BK == 128 && BKV % 16 == 0 && kQCol + D / 2 <= 512), "B_kv");
     static_assert(kAlloc <= 232448, "smem");
 };
-
-// 2^x for a pair of x on the FMA pipe with a degree-5 polynomial for 2^frac (relative
-// minimax fit on [0,1), max rel. error 1.7e-7 -- as accurate as ex2.approx, which the energies
-// need: unlike P in the attention kernel they are not rounded to bf16 afterwards).
-__device__ __forceinline__ uint64_t exp2_poly5(uint64_t x) {
-    // clamp at -126: the fit's p(0) = 0.99999994 < 1, so floor(x) = -127 would borrow out of
-    // the exponent field (0x3F7FFFFF - 0x3F800000 = NaN bits); at -126 the result is a
-    // denormal that the .ftz arithmetic downstream reads as 0 (masked keys hold -inf).
-    const float x0 = fmaxf(lo_f(x), -126.0f), x1 = fmaxf(hi_f(x), -126.0f);
-    const uint64_t xc = f2(x0, x1);
-    const uint64_t kRound = f2(12582912.0f, 12582912.0f);  // 2^23 + 2^22
-    const uint64_t rnd = fadd2_rm(xc, kRound);               // floor(x) in the low mantissa bits
-    const uint64_t frac = fsub2(xc, fsub2(rnd, kRound));     // in [0, 1)
-    uint64_t p = f2(0.0018775767f, 0.0018775767f);
-    p = ffma2(p, frac, f2(0.0089893406f, 0.0089893406f));
-    p = ffma2(p, frac, f2(0.055826318f, 0.055826318f));
-    p = ffma2(p, frac, f2(0.24015361f, 0.24015361f));
-    p = ffma2(p, frac, f2(0.69315308f, 0.69315308f));
-    p = ffma2(p, frac, f2(0.99999994f, 0.99999994f));
-    const uint32_t e0 = (uint32_t)rnd << 23, e1 = (uint32_t)(rnd >> 32) << 23;
-    return pk2((uint32_t)p + e0, (uint32_t)(p >> 32) + e1);
-}
 
 // sum of 2^(s*sl2 - m) over the BK columns of a row (masked columns hold -inf)
 template <int BK>
@@ -288,7 +267,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t s_lane = tmem + ((uint32_t)(quarter * 32) << 16);
         const float sl2 = a.scale_log2;
         const int32_t tail_valid = g.N - (g.NBK - 1) * BKV;
-        float2* scr = use_scratch ? a.scratch + (int64_t)blockIdx.x * g.NBK * 128 : nullptr;
+        // scratch: one float per (row, key block) -- the tile's log2-sum-exp u = m + log2(t)
+        float* scr = use_scratch ? reinterpret_cast<float*>(a.scratch) +
+                                       (int64_t)blockIdx.x * g.NBK * 128
+                                 : nullptr;
         uint32_t scount = 0;
         int32_t local = 0;
         for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
@@ -345,7 +327,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     const float t = exp_sum<BKV>(s, sl2, m_use);
                     l_run += t;
-                    if (use_scratch) scr[(int64_t)c * 128 + row] = make_float2(t, m_use);
+                    if (use_scratch)
+                        scr[(int64_t)c * 128 + row] = t > 0.0f ? m_use + __log2f(t) : -INFINITY;
                     if (local == 0 && (warp & 3) == 0 && lane == 0) CSA_TRACE(grp, c, 3);
                 }
                 row_m[grp * 128 + row] = m_run;
@@ -385,16 +368,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int32_t c = c0 + 8 * u;
-                        float2 tm[4];
+                        float uu[4];
 #pragma unroll
                         for (int q4 = 0; q4 < 4; ++q4)
-                            tm[q4] = (c < g.NBK && okr[q4])
-                                         ? scr[(int64_t)c * 128 + lane + 32 * q4]
-                                         : make_float2(0.0f, 0.0f);
+                            uu[q4] = (c < g.NBK && okr[q4]) ? scr[(int64_t)c * 128 + lane + 32 * q4]
+                                                           : -INFINITY;
                         float acc = 0.0f;
 #pragma unroll
-                        for (int q4 = 0; q4 < 4; ++q4)
-                            acc = fmaf(tm[q4].x, ex2_approx(tm[q4].y - lr[q4]), acc);
+                        for (int q4 = 0; q4 < 4; ++q4) acc += ex2_approx(uu[q4] - lr[q4]);
                         v[u] = acc;
                     }
 #pragma unroll
@@ -507,7 +488,7 @@ static int calib_grid(const Geo& g, int32_t n_heads, int num_sms) {
 }
 
 size_t calib_scratch_bytes(const Geo& g, int32_t n_heads, int num_sms) {
-    return (size_t)calib_grid(g, n_heads, num_sms) * g.NBK * 128 * sizeof(float2);
+    return (size_t)calib_grid(g, n_heads, num_sms) * g.NBK * 128 * sizeof(float);
 }
 
 cudaError_t set_calib_trace(void* buf, int mode) {

@@ -38,6 +38,23 @@ namespace {
 using namespace attn;
 
 constexpr int kThreadsCS = 384;
+#ifndef CSA_CS_EMU
+#define CSA_CS_EMU 0
+#endif
+constexpr int kCSEmu = CSA_CS_EMU;  // pairs p with (p & 7) >= 8 - kCSEmu -> exp2_poly5 (FMA pipe)
+
+static __device__ unsigned long long* g_trace_cs;
+#ifdef CSA_ENABLE_TRACE
+#define TRACE_CS(slot, k, e)                                                                 \
+    do {                                                                                     \
+        if (g_trace_cs != nullptr && blockIdx.x == 0 && (k) < 1024)                          \
+            g_trace_cs[((slot) * 1024 + (k)) * 8 + (e)] = clock64();                         \
+    } while (0)
+#else
+#define TRACE_CS(slot, k, e) \
+    do {                     \
+    } while (0)
+#endif
 
 template <int D>
 struct CalibSimSmem {
@@ -194,10 +211,13 @@ __global__ void __launch_bounds__(kThreadsCS, 1)
                 for (int32_t c = 0; c < g.NB; ++c) {
                     const int grp = c & 1;
                     const uint32_t use = grp ? sused1++ : sused0++;
+                    if (lane == 0) TRACE_CS(2, cons, 0);
                     mbar_wait(s_empty + grp, (use & 1) ^ 1);
+                    if (lane == 0) TRACE_CS(2, cons, 1);
                     const uint32_t slot = cons % S, ph = (cons / S) & 1;
                     ++cons;
                     mbar_wait(k_full + slot, ph);
+                    if (lane == 0) TRACE_CS(2, cons - 1, 2);
                     tc_fence_after();
                     if (elect_one()) {
                         const uint32_t kb = k_base + slot * C::kKVBytes;
@@ -208,6 +228,7 @@ __global__ void __launch_bounds__(kThreadsCS, 1)
                         if (c == g.NB - 1) mma_commit(q_empty);
                     }
                     __syncwarp();
+                    if (lane == 0) TRACE_CS(2, cons - 1, 3);
                 }
             }
         }
@@ -233,34 +254,42 @@ __global__ void __launch_bounds__(kThreadsCS, 1)
             float m = -INFINITY, ma = -INFINITY;
             float l = 0.0f;
             uint64_t nn2 = 0, la2 = 0, na2 = 0, dd2 = 0;  // packed (even, odd column) partials
+            const bool tr = quarter == 0 && lane == 0;
+            (void)tr;
             for (int32_t c = grp; c < g.NB; c += 2) {
+                if (tr) TRACE_CS(grp, scount, 0);
                 mbar_wait(s_full + grp, scount & 1);
+                if (tr) TRACE_CS(grp, scount, 1);
                 ++scount;
                 tc_fence_after();
                 const bool ragged = c == g.NB - 1 && tail_valid < BK;
                 uint64_t tt2 = 0;  // this tile's partial sum against m
-#pragma unroll 1
+                // chunks software-pipelined: chunk ch+1's TMEM loads are in flight while chunk
+                // ch is computed (tcgen05.wait::ld waits for all of a thread's loads, so the
+                // next load is issued after the wait and waited for after the math)
+                uint32_t so[2][32], sx[2][32];
+                tmem_ld32(s_lane, so[0]);
+                tmem_ld32(s_lane + 128, sx[0]);
+                tmem_ld_wait(so[0]);
+                tmem_ld_wait(sx[0]);
+#pragma unroll
                 for (int ch = 0; ch < 4; ++ch) {
-                    uint32_t so[32], sx[32];
-                    tmem_ld32(s_lane + ch * 32, so);
-                    tmem_ld32(s_lane + 128 + ch * 32, sx);
-                    tmem_ld_wait(so);
-                    tmem_ld_wait(sx);
-                    if (ch == 3) {  // S / S_a of this group free for its next tile
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(s_empty + grp);
+                    uint32_t(&co)[32] = so[ch & 1];
+                    uint32_t(&cx)[32] = sx[ch & 1];
+                    if (ch < 3) {
+                        tmem_ld32(s_lane + (ch + 1) * 32, so[(ch + 1) & 1]);
+                        tmem_ld32(s_lane + 128 + (ch + 1) * 32, sx[(ch + 1) & 1]);
                     }
                     if (ragged) {
 #pragma unroll
                         for (int x = 0; x < 32; ++x)
                             if (ch * 32 + x >= tail_valid) {  // keys >= N do not exist (Q2)
-                                so[x] = 0xff800000u;
-                                sx[x] = 0xff800000u;
+                                co[x] = 0xff800000u;
+                                cx[x] = 0xff800000u;
                             }
                     }
-                    const float mt = max32cs(so) * sl2;
-                    const float mat = max32cs(sx) * sl2;
+                    const float mt = max32cs(co) * sl2;
+                    const float mat = max32cs(cx) * sl2;
                     if (mt > m + kRescaleThreshold) {  // lazy reference of the row
                         const float f = ex2_approx(m - mt);  // 0 on the first chunk (m = -inf)
                         const uint64_t f1 = f2(f, f), fq = f2(f * f, f * f);
@@ -281,20 +310,37 @@ __global__ void __launch_bounds__(kThreadsCS, 1)
                     const uint64_t negm = f2(-m, -m), negma = f2(-ma, -ma);
 #pragma unroll
                     for (int x = 0; x < 32; x += 2) {
-                        const uint64_t to = ffma2(pk2(so[x], so[x + 1]), sl2x2, negm);
-                        const uint64_t ta = ffma2(pk2(sx[x], sx[x + 1]), sl2x2, negma);
-                        const uint64_t p = f2(ex2_approx(lo_f(to)), ex2_approx(hi_f(to)));
-                        const uint64_t pa = f2(ex2_approx(lo_f(ta)), ex2_approx(hi_f(ta)));
+                        const uint64_t to = ffma2(pk2(co[x], co[x + 1]), sl2x2, negm);
+                        const uint64_t ta = ffma2(pk2(cx[x], cx[x + 1]), sl2x2, negma);
+                        uint64_t p, pa;
+                        if (((x / 2) & 7) >= 8 - kCSEmu) {  // FMA-pipe exponentials (A/B knob)
+                            p = exp2_poly5(to);
+                            pa = exp2_poly5(ta);
+                        } else {
+                            p = f2(ex2_approx(lo_f(to)), ex2_approx(hi_f(to)));
+                            pa = f2(ex2_approx(lo_f(ta)), ex2_approx(hi_f(ta)));
+                        }
                         tt2 = fadd2(tt2, p);
                         nn2 = ffma2(p, p, nn2);
                         la2 = fadd2(la2, pa);
                         na2 = ffma2(pa, pa, na2);
                         dd2 = ffma2(p, pa, dd2);
                     }
+                    if (ch < 3) {
+                        tmem_ld_wait(so[(ch + 1) & 1]);
+                        tmem_ld_wait(sx[(ch + 1) & 1]);
+                        if (ch == 2) {  // S / S_a of this group free for its next tile
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(s_empty + grp);
+                            if (tr) TRACE_CS(grp, scount - 1, 2);
+                        }
+                    }
                 }
                 const float tt = hsum(tt2);
                 l += tt;
                 scr[(int64_t)c * 128 + row] = tt > 0.0f ? m + __log2f(tt) : -INFINITY;
+                if (tr) TRACE_CS(grp, scount - 1, 3);
             }
             // ------------------------------------------- merge the two groups (fixed order)
             float nn = hsum(nn2), la = hsum(la2), na = hsum(na2), dd = hsum(dd2);
@@ -451,6 +497,12 @@ cudaError_t launch_cs(const CalibArgs& a, const SimArgs& s, const CUtensorMap& t
 }
 
 }  // namespace
+
+cudaError_t set_calib_sim_trace(void* buf, int mode) {
+    (void)mode;
+    unsigned long long* p = static_cast<unsigned long long*>(buf);
+    return cudaMemcpyToSymbol(g_trace_cs, &p, sizeof(p));
+}
 
 size_t calib_sim_scratch_bytes(const Geo& g, int32_t n_heads, int num_sms) {
     const int64_t items = (int64_t)n_heads * g.NB;

@@ -79,7 +79,8 @@ struct CalibArgs {
     uint16_t* keep_count;
     float* energy_out;
     float* lse_out;
-    float2* scratch;  // [grid][N_B][128] (t, m) partials; nullptr -> two passes (or lse_in)
+    float2* scratch;  // [grid][N_B][128] float log2-sum-exp partials (typed float2 for 8-byte
+                      // alignment); nullptr -> two passes (or lse_in)
 };
 size_t calib_scratch_bytes(const Geo& g, int32_t n_heads, int num_sms);
 cudaError_t set_calib_trace(void* buf, int mode);
@@ -115,6 +116,7 @@ cudaError_t launch_similarity_reduce(const SimArgs& a, cudaStream_t s);
 // calib_sim_scratch_bytes (one float per (row, key block) and CTA), s.partials the
 // [n_heads][N][3] similarity partials; ends with the similarity reduce.
 size_t calib_sim_scratch_bytes(const Geo& g, int32_t n_heads, int num_sms);
+cudaError_t set_calib_sim_trace(void* buf, int mode);
 cudaError_t launch_calib_sim(const CalibArgs& a, const SimArgs& s, int head_dim,
                              const CUtensorMap& tq, const CUtensorMap& tk, int num_sms,
                              cudaStream_t st);

@@ -98,25 +98,23 @@ def calibrate(lay: Layout, T: int, L: int, H: int, prompts: int,
     """Offline calibration of the whole dictionary.
 
     qk_fn(prompt, t, l) -> conditional-branch Q, K bf16 [1, N, H, d] of that layer at that step.
-    Per (prompt, t, l): csa_calib_accumulate adds the prompt's per-row selections at eps(t) to the
-    cells' keep counts (a2-a5) and csa_spatial_similarity adds its cosines (f1) from the pass's own
-    row LSE.  Then s = sim_sum / (F H |D|), min_count = ceil(rho |D|) and one csa_compile_plan over
+    Per (prompt, t, l): one csa_calib_accumulate_sim pass adds the prompt's per-row selections at
+    eps(t) to the cells' keep counts (a2-a5) and its cosines to the similarity sums (f1).  Then s = sim_sum / (F H |D|), min_count = ceil(rho |D|) and one csa_compile_plan over
     every cell (a6; s > gamma -> REPETITIVE)."""
     eps = epsilon_schedule(T, *constants)
     nb, nbk = lay.NB, lay.NBK  # query blocks x key blocks (non-square B_q x B_kv: P:1294-1328)
     cells = T * L * H
     keep = torch.zeros(cells * nb * nbk, dtype=torch.int16, device=device).view(torch.uint16)
     sim_sum = torch.zeros(cells, dtype=torch.float64, device=device)
-    lse = torch.empty(H * lay.N, dtype=torch.float32, device=device)
     per = H * nb * nbk
     for p in range(prompts):
         for t in range(T):
             for l in range(L):
                 q, k = qk_fn(p, t, l)
                 c0 = (t * L + l) * H
-                csa.calib_accumulate(lay, q, k, eps[t], keep[c0 * nb * nbk:c0 * nb * nbk + per],
-                                     lse_out=lse)
-                csa.spatial_similarity(lay, q, k, lse, anchor_k, sim_sum[c0:c0 + H])
+                csa.calib_accumulate_sim(lay, q, k, eps[t],
+                                         keep[c0 * nb * nbk:c0 * nb * nbk + per], anchor_k,
+                                         sim_sum[c0:c0 + H])
     # smallest integer >= rho |D| (Eq. eq:mask_threshold in count space, reading Q6)
     min_count = math.ceil(rho * prompts - 1e-12)
     s = sim_sum / float(lay.F * lay.H * prompts)

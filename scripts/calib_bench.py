@@ -37,6 +37,8 @@ def main():
     ap.add_argument("--steps-T", type=int, default=50)
     ap.add_argument("--heads-per-rank", type=int, default=0, help="0: H / WORLD_SIZE")
     ap.add_argument("--no-sim", action="store_true")
+    ap.add_argument("--separate", action="store_true",
+                    help="csa_calib_accumulate + csa_spatial_similarity instead of the fused pass")
     ap.add_argument("--json-out", default=None)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -67,11 +69,16 @@ def main():
             c0 = (t * L + l) * hr
             e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             e[0].record()
-            csa.calib_accumulate(lay, q, k, eps[t], keep[c0 * nb * nb:(c0 + hr) * nb * nb],
-                                 lse_out=lse)
-            e[1].record()
-            if not args.no_sim:
-                csa.spatial_similarity(lay, q, k, lse, 5, sim_sum[c0:c0 + hr])
+            if args.no_sim or args.separate:
+                csa.calib_accumulate(lay, q, k, eps[t], keep[c0 * nb * nb:(c0 + hr) * nb * nb],
+                                     lse_out=lse)
+                e[1].record()
+                if not args.no_sim:
+                    csa.spatial_similarity(lay, q, k, lse, 5, sim_sum[c0:c0 + hr])
+            else:  # a2-a5 + f1 in one pass (csa_calib_accumulate_sim); counted as calibration
+                csa.calib_accumulate_sim(lay, q, k, eps[t], keep[c0 * nb * nb:(c0 + hr) * nb * nb],
+                                         5, sim_sum[c0:c0 + hr])
+                e[1].record()
             e[2].record()
             ev.append(e)
             del q, k
