@@ -246,9 +246,10 @@ CSA_API csa_status_t csa_share_timesteps(csa_layout_t L, int32_t n_groups, int32
  * order 1: natural (h asc, index asc);
  * order 2: head-major, longest-first within a head (h asc, cost desc, index asc) -- the L2-local
  *          order the dynamic scheduler of csa_sparse_attn_fwd is built for;
- * order 3: PAIR items for the CTA-pair kernel (block 128, head_dim 128): item (h, p) stands for
- *          rows (2p, 2p+1) of a MASK head or anchor tiles (2p, 2p+1) of a REPETITIVE head,
- *          p < ceil(units/2), cost = sum of the members' costs; head-major, cost desc, p asc.
+ * order 3: PAIR items: item (h, p) stands for rows (2p, 2p+1) of a MASK head or anchor tiles
+ *          (2p, 2p+1) of a REPETITIVE head, p < ceil(units/2), cost = sum of the members' costs;
+ *          head-major, cost desc, p asc.  No attention kernel of this build consumes them
+ *          (the pair-item kernel measured slower and was removed: DESIGN.md section 5).
  * Encoding: kind<<31 | h<<20 | (r, u or p).  work_list: uint32 [capacity]; n_work: device int32.
  * Requires n_heads <= 2048 and at most 32768 items. */
 CSA_API csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan, int64_t cell_base,
@@ -269,26 +270,19 @@ CSA_API csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan,
  *   lse_out     optional fp32 [batch][n_heads][N], natural log over the kept keys
  *   work_list   items from csa_build_work_list; n_work device int32 (count)
  *   max_work    host upper bound of *n_work (sizes the persistent grid)
- *   pair_items  0: single items (orders 0-2), one CTA per item;  1: pair items (order 3), two
- *               CTAs of a cluster per item (cta_group::2 MMAs, each CTA loads half of every K/V
- *               tile); requires block 128 and head_dim 128.  Results are identical per row.
+ *   pair_items  must be 0 (single items, orders 0-2); 1 -> CSA_ERR_UNSUPPORTED in this build.
  * Workspace: csa_workspace_size(CSA_WS_ATTN, L, n_heads, ...) bytes of device memory (8-byte
  * aligned).  Bytes [0, 256) hold the dynamic scheduler's counters: zero-filled before the first
  * use, left zero-filled when the launch completes (one buffer serves every launch on one stream).
- * NULL -> static round-robin assignment of work items to CTAs (pair items are always assigned
- * statically).
- * Kernels (block 128, head_dim 128, single items): with a workspace, the fixed-reference kernel
- * (attn5.cu -- attn4.cu with env CSA_ATTN4 -- each row's softmax shift is the max of its first
- * kept tile, P:647-653 is shift-invariant); an item whose later scores exceed that shift by more than 2^56 in exp2 terms
- * is listed in bytes [256, size) (rewritten every launch, needs max_work <= n_heads * N_B) and
- * recomputed on the same stream by the running-max kernel (attn3.cu).  Without a workspace the
- * running-max kernel runs the whole launch.  Each mode is deterministic; the two agree within
- * bf16 rounding of P (not bitwise).
- * Non-square blocks (block 128 x block_kv) run attn_rect.cu and block 128 / head_dim 64 runs
- * attn5.cu<64> (the same fixed-reference design; attn_rect.cu with B_kv-wide key tiles; the workspace is REQUIRED for non-square
- * layouts): overshooting items are recomputed on the same stream by an exact-row-max pass (the
- * row max is parked in the first 4 bytes of the row's first output row) and a pass against that
- * max.  Other shapes (block 64) run attn.cu. */
+ * NULL -> static round-robin assignment of work items to CTAs (block 64 only).
+ * Kernels: block 128 x 128 (head_dim 128 or 64) runs attn5.cu, block 128 x block_kv runs
+ * attn_rect.cu -- both with each row's softmax shift fixed at the max of its first kept tile
+ * (P:647-653 is shift-invariant); the workspace is REQUIRED for block 128.  An item whose later
+ * scores exceed that shift by more than 2^56 in exp2 terms is listed in bytes [256, size)
+ * (rewritten every launch, needs max_work <= n_heads * N_B) and recomputed on the same stream by
+ * attn_rect.cu's exact-row-max pass (the row max is parked in the first 4 bytes of the row's
+ * first output row) and a pass against that max.  Block 64 runs attn.cu (running max).  Every
+ * path is deterministic (bitwise run to run, independent of the item order). */
 CSA_API csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
                                  int32_t head_dim, float softmax_scale, csa_tensor_t q,
                                  csa_tensor_t k, csa_tensor_t v, csa_tensor_t o, float* lse_out,

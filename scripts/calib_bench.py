@@ -108,8 +108,11 @@ def main():
         "cells": cells, "calib_s_per_prompt": round(calib_ms / 1e3, 3),
         "similarity_s_per_prompt": round(sim_ms / 1e3, 3),
         "calib_qk_tflops": round(2.0 * d * scores / (calib_ms * 1e-3) / 1e12, 1),
-        "calib_exp_per_s": scores / (calib_ms * 1e-3),
-        "calib_exp_frac_of_mufu": round(scores / (calib_ms * 1e-3) / mufu, 4),
+        "fused_a2_a5_f1": not (args.no_sim or args.separate),
+        # exponentials per score: 1 in csa_calib_accumulate, 2 in the fused pass (p and p_a)
+        "calib_exp_per_s": scores * (1 if args.no_sim or args.separate else 2) / (calib_ms * 1e-3),
+        "calib_exp_frac_of_mufu": round(scores * (1 if args.no_sim or args.separate else 2)
+                                        / (calib_ms * 1e-3) / mufu, 4),
         "mufu_peak_exp_per_s_at_idle_clock": mufu,
         "compile_ms_incl_size_readback": round(compile_ms, 1),
         "keep_count_bytes": keep.numel() * 2, "plan_bytes": plan.nbytes(),
