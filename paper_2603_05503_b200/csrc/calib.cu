@@ -271,6 +271,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* scr = use_scratch ? reinterpret_cast<float*>(a.scratch) +
                                        (int64_t)blockIdx.x * g.NBK * 128
                                  : nullptr;
+        // scratch kept in L2 (evict_last) and its lines discarded once read: no DRAM write-back
+        const uint64_t pol_scr = policy_evict_last();
+        const bool discard_ok = (reinterpret_cast<uintptr_t>(scr) & 127u) == 0u;  // 128-B lines
         uint32_t scount = 0;
         int32_t local = 0;
         for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
@@ -328,7 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float t = exp_sum<BKV>(s, sl2, m_use);
                     l_run += t;
                     if (use_scratch)
-                        scr[(int64_t)c * 128 + row] = t > 0.0f ? m_use + __log2f(t) : -INFINITY;
+                        st_global_hint(scr + (int64_t)c * 128 + row,
+                                       t > 0.0f ? m_use + __log2f(t) : -INFINITY, pol_scr);
                     if (local == 0 && (warp & 3) == 0 && lane == 0) CSA_TRACE(grp, c, 3);
                 }
                 row_m[grp * 128 + row] = m_run;
@@ -386,6 +390,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int u = 0; u < 4; ++u)
                             if (c0 + 8 * u < g.NBK) erow[c0 + 8 * u] = v[u] / (float)rows_valid;
+                    }
+                    if (discard_ok && lane < 16) {  // the 4 columns' 512-B scratch rows are dead
+                        const int32_t c = c0 + 8 * (lane >> 2);
+                        if (c < g.NBK) discard_l2_line(scr + (int64_t)c * 128 + 32 * (lane & 3));
                     }
                 }
             } else {

@@ -245,6 +245,9 @@ __global__ void __launch_bounds__(kThreadsCS, 1)
         const uint64_t sl2x2 = f2(sl2, sl2);
         const int32_t tail_valid = g.N - (g.NB - 1) * BK;
         float* scr = reinterpret_cast<float*>(a.scratch) + (int64_t)blockIdx.x * g.NB * 128;
+        // scratch kept in L2 (evict_last) and its lines discarded once read: no DRAM write-back
+        const uint64_t pol_scr = policy_evict_last();
+        const bool discard_ok = (reinterpret_cast<uintptr_t>(scr) & 127u) == 0u;  // 128-B lines
         uint32_t scount = 0;
         for (int32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
             const int32_t h = item / g.NB, r = item % g.NB;
@@ -339,7 +342,8 @@ __global__ void __launch_bounds__(kThreadsCS, 1)
                 }
                 const float tt = hsum(tt2);
                 l += tt;
-                scr[(int64_t)c * 128 + row] = tt > 0.0f ? m + __log2f(tt) : -INFINITY;
+                st_global_hint(scr + (int64_t)c * 128 + row, tt > 0.0f ? m + __log2f(tt) : -INFINITY,
+                               pol_scr);
                 if (tr) TRACE_CS(grp, scount - 1, 3);
             }
             // ------------------------------------------- merge the two groups (fixed order)
@@ -417,6 +421,10 @@ __global__ void __launch_bounds__(kThreadsCS, 1)
 #pragma unroll
                         for (int u = 0; u < 4; ++u)
                             if (c0 + 8 * u < g.NB) erow[c0 + 8 * u] = v[u] / (float)rows_valid;
+                    }
+                    if (discard_ok && lane < 16) {  // the 4 columns' 512-B scratch rows are dead
+                        const int32_t c = c0 + 8 * (lane >> 2);
+                        if (c < g.NB) discard_l2_line(scr + (int64_t)c * 128 + 32 * (lane & 3));
                     }
                 }
             }

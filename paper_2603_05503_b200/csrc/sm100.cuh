@@ -110,6 +110,17 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     return p;
 }
 
+// Global store with an L2 eviction-priority policy (createpolicy above).
+__device__ __forceinline__ void st_global_hint(float* p, float v, uint64_t policy) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(policy)
+                 : "memory");
+}
+// Invalidate the 128-byte L2 line at p (128-byte aligned) without writing it back: for scratch
+// whose contents are dead once read.
+__device__ __forceinline__ void discard_l2_line(const void* p) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
 // -------------------------------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {  // whole warp
