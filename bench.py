@@ -711,6 +711,18 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
     torch.cuda.synchronize()
     ph["compile_plan_ms_incl_readback"] = round((time.perf_counter() - t0) * 1e3, 3)
     ph["plan_bytes"] = plan.nbytes()
+    # the same plan in the intervals-only form (no CSR index; the kernel walks the 1-D skip
+    # list): its bytes and its attention launch, bitwise the same output
+    plan_iv = csa.compile_plan(lay, cnt, 32, similarity=sim, gamma=0.87, anchor_k=5, csr=False)
+    work_iv = csa.build_work_list(plan_iv, 0, H, order=csa.default_order(lay, d))
+    if q.shape[2] == H:  # single-GPU layout (the exchange path holds rank-local views)
+        out_iv = torch.empty_like(out)
+        t_iv, _, _ = time_loop(lambda: csa.sparse_attn_fwd(q, k, v, plan_iv, work_iv, out=out_iv),
+                               max(2, args.steps // 2), 2, stream)
+        ph["attn_ms_intervals_only_plan"] = round(t_iv / max(2, args.steps // 2), 3)
+        ph["intervals_only_output_bitwise_equal"] = bool(torch.equal(
+            out_iv, csa.sparse_attn_fwd(q, k, v, plan, work, out=torch.empty_like(out))))
+    ph["plan_bytes_intervals_only"] = plan_iv.nbytes()
     result["phases"] = ph
     # ---- e2e through the public API with host buffers (H2D of Q/K/V, D2H of O in the region)
     # csa.sparse_attn_fwd_host streams head chunks: H2D of chunk c+1 and D2H of chunk c-1

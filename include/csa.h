@@ -90,7 +90,10 @@ typedef struct {
  *   mask_bits   [n_cells][N_B][ceil(N_B/32)] kept bit (r,c) = word c/32 bit c%32 (LSB first)
  *   blk_base    [n_cells + 1]            cell offset into blk_idx; blk_base[n_cells] = total
  *   blk_row_ptr [n_cells][N_B + 1]       CSR row pointers relative to blk_base[cell]
- *   blk_idx     [blk_capacity]           kept key-block indices c, ascending per row
+ *   blk_idx     [blk_capacity]           kept key-block indices c, ascending per row; OPTIONAL:
+ *                                        NULL with blk_capacity 0 makes an intervals-only plan --
+ *                                        the attention kernels then walk ivl (the 1-D skip list,
+ *                                        P:947-950) and blk_row_ptr keeps only the row counts
  *   ivl_base    [n_cells + 1]            cell offset (in intervals) into ivl
  *   ivl_row_ptr [n_cells][N_B + 1]       interval row pointers relative to ivl_base[cell]
  *   ivl         [2 * ivl_capacity]       skip-list intervals (start, end) half-open, maximal runs
@@ -196,8 +199,8 @@ CSA_API csa_status_t csa_calib_accumulate_sim(csa_layout_t L, int32_t n_heads, i
  *   phase 0 (COUNT): writes kind, anchor_k, mask_bits, row pointers, kept_area, blk_base,
  *                    ivl_base (blk_idx / ivl may be NULL).  The caller reads blk_base[n_cells]
  *                    and ivl_base[n_cells] to size blk_idx / ivl.
- *   phase 1 (FILL):  writes blk_idx and ivl (writes beyond the capacities are dropped; a plan
- *                    filled with too small a capacity fails csa_validate_plan).
+ *   phase 1 (FILL):  writes blk_idx (if not NULL) and ivl (writes beyond the capacities are
+ *                    dropped; a plan filled with too small a capacity fails csa_validate_plan).
  * keep_count: uint16 [n_cells][N_B][N_B]. */
 CSA_API csa_status_t csa_compile_plan(csa_layout_t L, int64_t n_cells, const uint16_t* keep_count,
                               int32_t min_count, const double* similarity, double gamma,
@@ -308,7 +311,8 @@ CSA_API size_t csa_workspace_size(int32_t which, csa_layout_t L, int32_t n_heads
  * anchor_k in [1, rows]; blk_base[0] = ivl_base[0] = 0, bases non-negative, monotone and within
  * the capacities; every cell's row pointers start at 0, are monotone and stay inside the cell's
  * list; MASK rows non-empty with indices ascending and < N_B (N_Bkv) and set in mask_bits;
- * intervals maximal/ordered and equal to the decoded blk_idx.  No read leaves the plan's buffers
+ * intervals maximal/ordered and equal to the decoded blk_idx (intervals-only plans: the intervals
+ * cover exactly the row count, inside mask_bits).  No read leaves the plan's buffers
  * once a bound is found broken.  Synchronises `stream`.  CSA_OK or CSA_ERR_CORRUPT_PLAN. */
 CSA_API csa_status_t csa_validate_plan(const csa_plan_t* plan, csa_layout_t L, int64_t n_cells,
                                csa_stream_t stream);

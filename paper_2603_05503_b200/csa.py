@@ -275,8 +275,9 @@ class Plan:
 
 def compile_plan(lay: Layout, keep_count: torch.Tensor, min_count: int,
                  similarity: torch.Tensor | None = None, gamma: float = 0.87, anchor_k: int = 5,
-                 stream=None) -> Plan:
-    """csa_compile_plan phase 0 (count) -> size read-back -> phase 1 (fill)."""
+                 stream=None, csr: bool = True) -> Plan:
+    """csa_compile_plan phase 0 (count) -> size read-back -> phase 1 (fill).  csr=False: an
+    intervals-only plan (no blk_idx: the kernels walk the 1-D skip list)."""
     dev = keep_count.device
     nb, nbk = lay.NB, lay.NBK
     n_cells = keep_count.numel() // (nb * nbk)
@@ -302,7 +303,7 @@ def compile_plan(lay: Layout, keep_count: torch.Tensor, min_count: int,
                                   ctypes.byref(s), None, 0, _stream(stream)), "csa_compile_plan(0)")
     tot_b = int(p.blk_base[n_cells].item())
     tot_i = int(p.ivl_base[n_cells].item())
-    p.blk_idx = e(max(tot_b, 1), dtype=torch.uint16, device=dev)
+    p.blk_idx = e(max(tot_b, 1) if csr else 0, dtype=torch.uint16, device=dev)
     p.ivl = e(max(2 * tot_i, 2), dtype=torch.uint16, device=dev)
     s = p.struct()
     _check(lib().csa_compile_plan(_layout(lay), n_cells, None, int(min_count), None, float(gamma),

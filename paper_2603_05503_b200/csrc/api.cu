@@ -131,7 +131,8 @@ bool plan_ptrs_ok(const csa_plan_t* p, bool need_lists) {
     if (!p || !p->kind || !p->anchor_k || !p->mask_bits || !p->blk_base || !p->blk_row_ptr ||
         !p->ivl_base || !p->ivl_row_ptr || !p->kept_area)
         return false;
-    if (need_lists && (!p->blk_idx || !p->ivl)) return false;
+    // blk_idx may be absent (intervals-only plan: blk_capacity 0); the intervals may not
+    if (need_lists && (!p->ivl || (!p->blk_idx && p->blk_capacity != 0))) return false;
     return true;
 }
 

@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // whole warp walks the list (warp-uniform values live in uniform registers); one
             // elected lane issues -- a lane-0-only loop makes ptxas wrap each TMA in an
             // ELECT / R2UR / BRA.U.ANY loop.
+            TileCursor kcur(tl), vcur(tl);
             for (int32_t step = 0; step <= tl.n; ++step) {
                 for (int kv = 0; kv < 2; ++kv) {
                     int32_t j;
@@ -218,7 +219,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     const uint32_t slot = ld % S, ph = (ld / S) & 1;
                     ++ld;
-                    const int32_t c = tl.at(j);
+                    const int32_t c = kv == 0 ? kcur.next() : vcur.next();
+                    (void)j;
                     mbar_wait(kv_empty + slot, ph ^ 1);
                     if (elect_one()) {
                         uint8_t* dst = smem + L::kKVOff + slot * C::kKVBytes;
@@ -313,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const Item it = decode_item(a, item);
             const TileList tl = tile_list(a, it);
             // only the last listed tile can be the ragged block N_B - 1
-            const bool last_ragged = tail_valid < BK && tl.n > 0 && tl.at(tl.n - 1) == g.NB - 1;
+            const bool last_ragged = tail_valid < BK && tl.n > 0 && tl.last() == g.NB - 1;
             float m_run = -INFINITY, l_run = 0.0f;
             int32_t mine = 0;
             for (int32_t j = grp; j < tl.n; j += 2, ++mine) {

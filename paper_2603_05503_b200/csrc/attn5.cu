@@ -223,10 +223,10 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
                     if (lane == 0) mbar_arrive(q_full + qb);
                 }
                 // ring order = issue order: K0, K1, then per step s >= 2: K_s, V_{s-2}; V tail
-                auto load = [&](int kv, int32_t j) {
+                TileCursor kcur(tl), vcur(tl);
+                auto load = [&](int kv, int32_t c) {
                     const uint32_t slot = ld % S, ph = (ld / S) & 1;
                     ++ld;
-                    const int32_t c = tl.at(j);
                     mbar_wait(kv_empty + slot, ph ^ 1);
                     if (elect_one()) {
                         uint8_t* dst = smem + L::kKVOff + slot * L::kTile;
@@ -237,8 +237,8 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
                     __syncwarp();
                 };
                 for (int32_t step = 0; step < tl.n + 2; ++step) {
-                    if (step < tl.n) load(0, step);
-                    if (step >= 2) load(1, step - 2);
+                    if (step < tl.n) load(0, kcur.next());
+                    if (step >= 2) load(1, vcur.next());
                 }
             }
         } else if (warp == 1) {
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
             if (item < 0) break;
             const Item it = decode_item(a, item);
             const TileList tl = tile_list(a, it);
-            const bool last_ragged = tail_valid < BK && tl.n > 0 && tl.at(tl.n - 1) == g.NB - 1;
+            const bool last_ragged = tail_valid < BK && tl.n > 0 && tl.last() == g.NB - 1;
             float m_ref = 0.0f, l_run = 0.0f;
             bool bad = false;
             uint32_t s_ready = 0;  // probe result for the next tile's S

@@ -30,23 +30,58 @@ __device__ __forceinline__ Item decode_item(const AttnArgs& a, int32_t item) {
     return it;
 }
 
-// Kept key-block list of a MASK item (CSR), or all N_Bkv key blocks for a REPETITIVE item.
+// Kept key-block list of a MASK item, or all N_Bkv key blocks for a REPETITIVE item.  A MASK row
+// is read from the CSR index list when the plan has one, else from its 1-D interval list
+// ((start, end) pairs: the form the paper leaves its kernel for as future work) --
+// an intervals-only plan drops the CSR index array (2 bytes per kept block).  The kernels walk
+// a list sequentially with TileCursor; last() is the row's last kept block.
 struct TileList {
-    const uint16_t* idx;  // nullptr -> dense 0..n-1
-    int32_t n;
-    __device__ __forceinline__ int32_t at(int32_t j) const { return idx ? (int32_t)idx[j] : j; }
+    const uint16_t* idx;  // CSR indices; nullptr -> intervals (ivl) or dense 0..n-1 (ivl null)
+    const uint16_t* ivl;  // (start, end) pairs when idx == nullptr
+    int32_t n;            // kept tiles
+    int32_t n_ivl;
+    __device__ __forceinline__ int32_t last() const {
+        return idx ? (int32_t)idx[n - 1] : ivl ? (int32_t)ivl[2 * n_ivl - 1] - 1 : n - 1;
+    }
+};
+
+struct TileCursor {
+    const uint16_t* idx;
+    const uint16_t* ivl;
+    int32_t k, c, e;
+    __device__ __forceinline__ explicit TileCursor(const TileList& t)
+        : idx(t.idx), ivl(t.ivl), k(0), c(0), e(0) {}
+    __device__ __forceinline__ int32_t next() {
+        if (idx) return (int32_t)idx[k++];
+        if (!ivl) return k++;
+        if (c == e) {
+            c = ivl[2 * k];
+            e = ivl[2 * k + 1];
+            ++k;
+        }
+        return c++;
+    }
 };
 
 __device__ __forceinline__ TileList tile_list(const AttnArgs& a, const Item& it) {
     TileList t;
+    t.idx = nullptr;
+    t.ivl = nullptr;
+    t.n_ivl = 0;
     if (it.kind) {
-        t.idx = nullptr;
         t.n = a.g.NBK;
     } else {
         const int32_t* rp = a.plan.blk_row_ptr + it.cell * (a.g.NB + 1);
         const int32_t r0 = rp[it.idx], r1 = rp[it.idx + 1];
-        t.idx = a.plan.blk_idx + a.plan.blk_base[it.cell] + r0;
         t.n = r1 - r0;
+        if (a.plan.blk_idx != nullptr) {
+            t.idx = a.plan.blk_idx + a.plan.blk_base[it.cell] + r0;
+        } else {
+            const int32_t* irp = a.plan.ivl_row_ptr + it.cell * (a.g.NB + 1);
+            const int32_t i0 = irp[it.idx];
+            t.ivl = a.plan.ivl + 2 * (a.plan.ivl_base[it.cell] + i0);
+            t.n_ivl = irp[it.idx + 1] - i0;
+        }
     }
     return t;
 }

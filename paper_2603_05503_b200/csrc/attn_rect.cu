@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(SmemR<BKV, D>::kThreads, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(q_full);
                 }
+                TileCursor kcur(tl), vcur(tl);
                 for (int32_t step = 0; step <= tl.n; ++step) {
                     for (int kv = 0; kv < 2; ++kv) {
                         int32_t j;
@@ -297,7 +298,8 @@ __global__ void __launch_bounds__(SmemR<BKV, D>::kThreads, 1)
                         }
                         const uint32_t slot = ld % S, ph = (ld / S) & 1;
                         ++ld;
-                        const int32_t c = tl.at(j);
+                        const int32_t c = kv == 0 ? kcur.next() : vcur.next();
+                        (void)j;
                         mbar_wait(kv_empty + slot, ph ^ 1);
                         if (elect_one()) {
                             uint8_t* dst = smem + L::kKVOff + slot * L::kTile;
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(SmemR<BKV, D>::kThreads, 1)
             if (item < 0) break;
             const Item it = decode_item(a, item);
             const TileList tl = tile_list(a, it);
-            const bool last_ragged = tail_valid < BKV && tl.n > 0 && tl.at(tl.n - 1) == g.NBK - 1;
+            const bool last_ragged = tail_valid < BKV && tl.n > 0 && tl.last() == g.NBK - 1;
             // output rows of this thread's query row (MASK: the row itself; REPETITIVE: the
             // nearest-anchor group of spatial rows of the anchor query, Q10)
             int64_t tok0 = -1;

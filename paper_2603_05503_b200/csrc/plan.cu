@@ -382,7 +382,9 @@ __global__ void plan_validate_kernel(Geo g, int64_t n_cells, PlanDev p, uint32_t
         const int64_t bb0 = p.blk_base[cell], bb1 = p.blk_base[cell + 1];
         const int64_t ib0 = p.ivl_base[cell], ib1 = p.ivl_base[cell + 1];
         if (bb1 < bb0 || ib1 < ib0 || bb0 < 0 || ib0 < 0) bad |= 1;
-        if (p.blk_base[n_cells] > p.blk_capacity || p.ivl_base[n_cells] > p.ivl_capacity) bad |= 2;
+        if ((p.blk_idx != nullptr && p.blk_base[n_cells] > p.blk_capacity) ||
+            p.ivl_base[n_cells] > p.ivl_capacity)
+            bad |= 2;
         if (cell == 0 && r == 0 && (p.blk_base[0] != 0 || p.ivl_base[0] != 0)) bad |= 2048;
         if (r == 0 && (brp[0] != 0 || irp[0] != 0)) bad |= 2048;
         const int32_t b0 = brp[r], b1 = brp[r + 1], i0 = irp[r], i1 = irp[r + 1];
@@ -396,21 +398,24 @@ __global__ void plan_validate_kernel(Geo g, int64_t n_cells, PlanDev p, uint32_t
             if (b1 == b0) bad |= 8;  // empty MASK row
             if (brp[g.NB] != p.blk_base[cell + 1] - p.blk_base[cell]) bad |= 16;
             if (!bad) {
-                const uint16_t* bi = p.blk_idx + p.blk_base[cell];
+                // intervals-only plans (blk_idx == nullptr): the intervals alone
+                // must cover exactly the row's count, in order, inside the mask bits
+                const uint16_t* bi = p.blk_idx ? p.blk_idx + p.blk_base[cell] : nullptr;
                 const uint16_t* iv = p.ivl + 2 * p.ivl_base[cell];
+                const uint32_t* words = p.mask_bits + (cell * g.NB + r) * g.W32;
                 int32_t prev = -1, cover = 0, bj = b0;
                 for (int32_t t = i0; t < i1; ++t) {
                     const int32_t s = iv[2 * t], e = iv[2 * t + 1];
                     if (!(s < e) || e > g.NBK || s <= prev) bad |= 32;  // ordered, non-adjacent
                     prev = e;
                     for (int32_t c = s; c < e && !bad; ++c, ++bj) {
-                        if (bj >= b1 || bi[bj] != c) bad |= 64;  // CSR == decoded intervals
+                        if (bi != nullptr && (bj >= b1 || bi[bj] != c)) bad |= 64;  // CSR == ivl
+                        if (bi == nullptr && !((words[c >> 5] >> (c & 31)) & 1u)) bad |= 128;
                     }
                     cover += e - s;
                 }
                 if (cover != b1 - b0) bad |= 64;
-                const uint32_t* words = p.mask_bits + (cell * g.NB + r) * g.W32;
-                for (int32_t t = b0; t < b1 && !bad; ++t) {
+                for (int32_t t = b0; bi != nullptr && t < b1 && !bad; ++t) {
                     const int32_t c = bi[t];
                     if (c >= g.NBK || (t > b0 && c <= bi[t - 1])) bad |= 128;
                     if (!((words[c >> 5] >> (c & 31)) & 1u)) bad |= 128;

@@ -79,7 +79,8 @@ class PlanDictionary:
         keep = kc.view(torch.int16)[:, mine].contiguous().view(torch.uint16)
         sim = self.similarity.view(self.T * self.L, H)[:, mine].contiguous().view(-1)
         plan = csa.compile_plan(self.lay, keep.view(-1), self.min_count, similarity=sim,
-                                gamma=self.gamma, anchor_k=self.anchor_k)
+                                gamma=self.gamma, anchor_k=self.anchor_k,
+                                csr=self.plan.blk_idx.numel() > 0)
         return PlanDictionary(self.lay, self.T, self.L, hp, plan, self.eps, self.min_count,
                               self.prompts, sim, keep.view(-1, self.lay.NB, keep.shape[-1]),
                               self.gamma, self.anchor_k)
@@ -94,13 +95,14 @@ class PlanDictionary:
 def calibrate(lay: Layout, T: int, L: int, H: int, prompts: int,
               qk_fn: Callable[[int, int, int], tuple[torch.Tensor, torch.Tensor]],
               constants: tuple[float, float, float], rho: float = 0.5, gamma: float = 0.87,
-              anchor_k: int = 5, device="cuda") -> PlanDictionary:
+              anchor_k: int = 5, device="cuda", csr: bool = True) -> PlanDictionary:
     """Offline calibration of the whole dictionary.
 
     qk_fn(prompt, t, l) -> conditional-branch Q, K bf16 [1, N, H, d] of that layer at that step.
     Per (prompt, t, l): one csa_calib_accumulate_sim pass adds the prompt's per-row selections at
     eps(t) to the cells' keep counts (a2-a5) and its cosines to the similarity sums (f1).  Then s = sim_sum / (F H |D|), min_count = ceil(rho |D|) and one csa_compile_plan over
-    every cell (a6; s > gamma -> REPETITIVE)."""
+    every cell (a6; s > gamma -> REPETITIVE).  csr=False: an intervals-only dictionary (the
+    kernels walk the 1-D skip lists; ~1/8 of the CSR dictionary's bytes at 720p)."""
     eps = epsilon_schedule(T, *constants)
     nb, nbk = lay.NB, lay.NBK  # query blocks x key blocks (non-square B_q x B_kv: P:1294-1328)
     cells = T * L * H
@@ -118,7 +120,8 @@ def calibrate(lay: Layout, T: int, L: int, H: int, prompts: int,
     # smallest integer >= rho |D| (Eq. eq:mask_threshold in count space, reading Q6)
     min_count = math.ceil(rho * prompts - 1e-12)
     s = sim_sum / float(lay.F * lay.H * prompts)
-    plan = csa.compile_plan(lay, keep, min_count, similarity=s, gamma=gamma, anchor_k=anchor_k)
+    plan = csa.compile_plan(lay, keep, min_count, similarity=s, gamma=gamma, anchor_k=anchor_k,
+                            csr=csr)
     return PlanDictionary(lay, T, L, H, plan, eps, min_count, prompts, s,
                           keep.view(cells, nb, nbk), gamma, anchor_k)
 

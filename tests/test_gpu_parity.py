@@ -301,6 +301,84 @@ def test_attention_batch2_shares_plan_and_is_deterministic(csa, lay, d):
         assert torch.equal(single[0], out[b])
 
 
+def _plan_from_masks(csa, lay, masks, rep, anchor_k, csr):
+    heads = masks.shape[0]
+    sim = torch.tensor([1.0 if h in rep else 0.0 for h in range(heads)], dtype=torch.float64,
+                       device="cuda")
+    return csa.compile_plan(lay, u16_dev(masks.astype(np.uint16)), 1, similarity=sim, gamma=0.87,
+                            anchor_k=anchor_k, csr=csr)
+
+
+@pytest.mark.parametrize("lay,d", [(Layout(2, 9, 40, 128), 128), (Layout(2, 9, 40, 128), 64),
+                                   (Layout(2, 9, 40, 128, 80), 128), (Layout(2, 9, 40, 128, 192), 128),
+                                   (Layout(2, 5, 25, 64), 64), (Layout(3, 7, 100, 128), 128)])
+def test_intervals_only_plan_bitwise(csa, lay, d):
+    """Intervals-only plans (no blk_idx; the kernels walk the 1-D skip list) give the
+    CSR plan's outputs bit for bit on every attention kernel (attn5 d 128 / 64, attn_rect, attn at
+    block 64), with a REPETITIVE head, batch 2, and through the exact-max fallback passes
+    (scores growing 40x block by block); the validator accepts them; outputs match the oracle."""
+    heads = 3
+    q, k, v = qkv(2, lay.N, heads, d, seed=17, device="cuda")
+    rng = np.random.default_rng(6)
+    masks = (rng.random((heads, lay.NB, lay.NBK)) < 0.45).astype(np.uint8)
+    masks[:, :, 0] = 1
+    outs = {}
+    for csr in (True, False):
+        plan = _plan_from_masks(csa, lay, masks, [1], 2, csr)
+        csa.validate_plan(plan)
+        assert (plan.blk_idx.numel() > 0) == csr
+        lse = torch.empty(2 * heads * lay.N, dtype=torch.float32, device="cuda")
+        outs[csr] = (csa.sparse_attn_fwd(q, k, v, plan, csa.build_work_list(plan, 0, heads),
+                                         lse_out=lse), lse)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[True][0], outs[False][0])
+    assert torch.equal(outs[True][1], outs[False][1])
+    for h in (0, 2):
+        ref, _ = oracle_head(lay, q, k, v, 1, h, mask=masks[h])
+        assert_close(outs[False][0][1, :, h].double().cpu().numpy(), ref, f"h{h}")
+    if lay.B == 128:  # overshooting rows through the fallback list, intervals-only plan
+        gain = torch.ones(lay.N, device="cuda")
+        for c in range(lay.NBK):
+            gain[c * lay.Bkv:(c + 1) * lay.Bkv] = 1.0 + 40.0 * c / lay.NBK
+        kj = (k.float() * gain.view(1, -1, 1, 1)).to(torch.bfloat16)
+        res = []
+        for csr in (True, False):
+            plan = _plan_from_masks(csa, lay, masks, [], 2, csr)
+            res.append(csa.sparse_attn_fwd(q, kj, v, plan, csa.build_work_list(plan, 0, heads)))
+            torch.cuda.synchronize()
+            assert fallback_count(csa, q) > 0
+        assert torch.equal(res[0], res[1])
+        ref, _ = oracle_head(lay, q, kj, v, 0, 1, mask=masks[1])
+        assert_close(res[1][0, :, 1].double().cpu().numpy(), ref, "fallback")
+
+
+def test_intervals_only_plan_full_size_and_validation(csa):
+    """Wan 720p (generator-S masks, 4 anchor heads): the intervals-only plan is a fraction of the
+    CSR plan's bytes and gives the same attention bit for bit; a corrupted interval (end moved
+    by one) or a row count that no longer matches its intervals fails csa_validate_plan."""
+    cfg = CONFIGS["wan720"]
+    lay = cfg.layout
+    q, k, v = qkv(1, lay.N, cfg.heads, cfg.d, seed=11, device="cuda")
+    masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity, seed=0)
+    rep = [0, 13, 26, 39]
+    p_csr = _plan_from_masks(csa, lay, masks, rep, 5, True)
+    p_ivl = _plan_from_masks(csa, lay, masks, rep, 5, False)
+    csa.validate_plan(p_ivl)
+    assert p_ivl.nbytes() < 0.3 * p_csr.nbytes(), (p_ivl.nbytes(), p_csr.nbytes())
+    o1 = csa.sparse_attn_fwd(q, k, v, p_csr, csa.build_work_list(p_csr, 0, cfg.heads))
+    o2 = csa.sparse_attn_fwd(q, k, v, p_ivl, csa.build_work_list(p_ivl, 0, cfg.heads))
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    iv = p_ivl.ivl.view(torch.int16)
+    first_end = 1
+    old = int(iv[first_end].item())
+    iv[first_end] = old + 1                      # cover no longer equals the row count
+    with pytest.raises(csa.CsaError, match="CORRUPT_PLAN"):
+        csa.validate_plan(p_ivl)
+    iv[first_end] = old
+    csa.validate_plan(p_ivl)
+
+
 def sample_units(lay, heads, n, seed):
     rng = np.random.default_rng(seed)
     units = {(0, lay.NB - 1), (heads - 1, 0)}
