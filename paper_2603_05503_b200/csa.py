@@ -216,11 +216,16 @@ _CALIB_WS: dict = {}
 
 
 def _calib_workspace(device, nbytes: int, key: str = "calib") -> torch.Tensor:
-    """Cached scratch for the single-pass calibration / the similarity pass (grown on demand,
-    one per device and use)."""
-    key = f"{key}:{device}"
+    """Cached scratch for the single-pass calibration / the similarity pass (grown on demand),
+    one per (device, current stream, use): calls on one stream are ordered, so they can share
+    it; calls on different streams never do.  A replaced buffer is kept alive (a captured CUDA
+    graph may still hold its address)."""
+    s = torch.cuda.current_stream(device)
+    key = (key, torch.device(device).index, s.cuda_stream)
     buf = _CALIB_WS.get(key)
     if buf is None or buf.numel() < nbytes:
+        if buf is not None:
+            _RETIRED_WS.append(buf)
         buf = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
         _CALIB_WS[key] = buf
     return buf
