@@ -584,13 +584,14 @@ def test_spatial_similarity_against_oracle(csa, lay, heads, d, kind):
 
 @pytest.mark.parametrize("lay,d", [(Layout(2, 9, 40, 128), 128), (Layout(2, 9, 40, 128), 64),
                                    (Layout(3, 7, 100, 128), 128), (Layout(1, 3, 40, 128), 128),
+                                   (Layout(1, 2, 30, 128), 128),
                                    (Layout(2, 5, 25, 64), 64), (Layout(2, 9, 40, 128, 80), 128)])
 def test_calib_sim_fused_against_oracle(csa, lay, d):
     """csa_calib_accumulate_sim (a2-a5 + f1 in one pass; calibsim.cu at block 128 x 128, the two
     calls' kernels in sequence otherwise): E, LSE, the selection and cos(f, i) against the fp64
     oracle, and the same outputs as calib_accumulate + spatial_similarity within fp32 rounding
-    order.  N_B = 1 (one ragged block: group 1 has no key tile), odd N_B, ragged N, d 64,
-    block 64 and B_kv = 80."""
+    order.  N_B = 1 (one ragged block: group 1 has no key tile; N = 60: chunks past the last
+    key fully masked), odd N_B, ragged N, d 64, block 64 and B_kv = 80."""
     heads, kA = 2, 2
     q, k, _ = inputs.structured_qk(lay, heads, d, 3, 1, alpha=[0.9, 1.4], repetitive=(1,),
                                    device="cuda")
