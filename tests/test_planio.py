@@ -58,6 +58,21 @@ def test_plan_file_round_trip_and_corruption(tmp_path, lay):
             planio.load_plan(path, device="cpu", validate=False)
 
 
+def test_intervals_only_plan_file_round_trip(tmp_path):
+    """An intervals-only plan (no CSR index) is saved and loaded with an empty
+    blk_idx, and its struct hands the kernels a NULL index with capacity 0."""
+    lay = Layout(2, 9, 40, 128)
+    plan = _host_plan(lay, inputs.random_counts(lay.NB, 2, 8, seed=4), 3)
+    plan.blk_idx = torch.empty(0, dtype=torch.int16).view(torch.uint16)
+    path = os.path.join(tmp_path, "plan_ivl.csap")
+    planio.save_plan(plan, path)
+    back = planio.load_plan(path, device="cpu", validate=False)
+    assert back.blk_idx.numel() == 0
+    assert torch.equal(back.ivl.view(torch.int16), plan.ivl.view(torch.int16))
+    st = back.struct()
+    assert st.blk_idx is None and st.blk_capacity == 0 and st.ivl_capacity == plan.ivl.numel() // 2
+
+
 def test_calibration_state_round_trip(tmp_path):
     lay = Layout(2, 9, 40, 128, 96)
     keep = torch.from_numpy(inputs.random_counts(lay.NB, 4, 8, seed=3, nbk=lay.NBK)
