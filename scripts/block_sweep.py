@@ -7,7 +7,6 @@ table), compiled by csa_compile_plan and run through csa_sparse_attn_fwd:
   * attention ms (CUDA events, median of --steps after --warmup), effective TFLOP/s of the kept
     FLOPs (4 d sum kept_area) and its fraction of the measured bf16 peak;
   * the same kernel on the all-ones plan of that grid (dense) -> speedup and proportionality;
-  * at 128 x 128 also the generic B_kv kernel (CSA_ATTN_RECT) next to the production kernel;
   * parity: sampled (head, query-block) units against the fp64 oracle (bar: north-star).
 One JSON line per configuration; --json-out collects them.
 """
@@ -121,8 +120,6 @@ def main():
         plan1 = csa.compile_plan(lay, ones, 32)
         work1 = csa.build_work_list(plan1, 0, H)
         variants = [("production" if bkv == 128 else "attn_rect", {})]
-        if bkv == 128:
-            variants.append(("attn_rect", {"CSA_ATTN_RECT": "1"}))
         for name, env in variants:
             os.environ.update(env)
             try:

@@ -5,5 +5,4 @@ timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "rect or denoise" > gpurun_out/pytest_d64.log 2>&1
 echo "pytest exit $?" >> gpurun_out/pytest_d64.log
 timeout 300 python scripts/block_sweep.py --bkv 128,64,192 --d 64 > gpurun_out/d64_rect.log 2>&1
-CSA_ATTN_V3=1 timeout 300 python scripts/block_sweep.py --bkv 128 --d 64 > gpurun_out/d64_v3.log 2>&1
-tail -n 2 gpurun_out/smoke.log; tail -n 3 gpurun_out/pytest_d64.log; cat gpurun_out/d64_rect.log gpurun_out/d64_v3.log | cut -c1-330
+tail -n 2 gpurun_out/smoke.log; tail -n 3 gpurun_out/pytest_d64.log; cat gpurun_out/d64_rect.log | cut -c1-330

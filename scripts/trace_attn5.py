@@ -1,4 +1,4 @@
-"""Debug timeline of CTA 0's first 1024 tiles in attn5.cu (trace build, CSA_ATTN5=1): softmax
+"""Debug timeline of CTA 0's first 1024 tiles in attn5.cu (trace build): softmax
 (S wait start / S ready / S loaded / exps done / P published), QK issue (s_empty wait start /
 K ready), PV issue (p_full wait start / P ready / issued)."""
 import ctypes
@@ -11,7 +11,6 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2603_05503_b200 import csa, inputs  # noqa: E402
 
-os.environ["CSA_ATTN5"] = "1"
 cfg = inputs.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "wan720"]
 lay = cfg.layout
 masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity or 0.69, seed=0)
