@@ -1,7 +1,7 @@
 // attn6_pair.cu -- EXPERIMENT, not built into libcsa.so ("Pair items").
 // Measured slower than the production attn5.cu on the same box (Wan 720p d 128: 1064 vs 1282
 // TF/s; Wan 480p d 64: 704 vs 929), parity green; built and tested as csrc/attn6.cu at commit
-// 8f52c9f (scripts/ab_pair2.sh, scripts/trace_attn6.py, tests test_pair_items_*).
+// 8f52c9f (scripts/experiments/ab_pair2.sh, scripts/experiments/trace_attn6.py, tests test_pair_items_*).
 //
 // a7 + a8 for block 128 (head_dim 128 and 64) on PAIR items: two query blocks per
 // CTA share one K/V stream over the union of their kept-block lists.
