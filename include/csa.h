@@ -295,6 +295,32 @@ CSA_API csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t 
                                  size_t workspace_bytes, csa_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------
+ * csa_sparse_attn_fwd_scatter -- csa_sparse_attn_fwd (same arithmetic, bit for bit) whose output
+ * rows are written straight into the sequence-sharded receive buffers of n_peers ranks: the
+ * row of token t goes to o_peers[t / (N / n_peers)] at local token t % (N / n_peers).  This fuses
+ * the return all-to-all of the head-sharded (Ulysses) layer into the attention epilogue (SURVEY
+ * 8.6; heads are independent): with symmetric / peer-mapped buffers the stores travel over
+ * NVLink as each tile row is finished, and the consumer only needs a cross-rank barrier after
+ * the launch (stream-ordered; the caller's).
+ *   o_peers     DEVICE array [n_peers] of bf16 pointers (peer-accessible from this device),
+ *               each pointing at THIS rank's first head inside peer p's receive buffer (e.g.
+ *               recv_p + h0 * head_dim for a [batch, N / n_peers, H_total, head_dim] buffer);
+ *               16-byte aligned
+ *   o_stride_*  element strides of every receive buffer (batch, token, head); multiples of 8
+ *   n_peers     >= 1, must divide N; block 128 layouts only (square or B_kv) -- the fallback
+ *               passes scatter the same way
+ * Other arguments as csa_sparse_attn_fwd (lse_out stays local, [batch][n_heads][N]). */
+CSA_API csa_status_t csa_sparse_attn_fwd_scatter(csa_layout_t L, int32_t batch, int32_t n_heads,
+                                         int32_t head_dim, float softmax_scale, csa_tensor_t q,
+                                         csa_tensor_t k, csa_tensor_t v, void* const* o_peers,
+                                         int32_t n_peers, int64_t o_stride_b, int64_t o_stride_n,
+                                         int64_t o_stride_h, float* lse_out,
+                                         const csa_plan_t* plan, int64_t cell_base,
+                                         const uint32_t* work_list, const int32_t* n_work,
+                                         int32_t max_work, void* workspace,
+                                         size_t workspace_bytes, csa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
  * csa_copy_heads -- runtime helper for streaming a layer through the API from host memory:
  * copies heads [h0, h1) of a bf16 [1, N, n_heads, head_dim] tensor (head_dim contiguous, rows of
  * n_heads * head_dim) between pinned host memory and device memory of the same layout, as one

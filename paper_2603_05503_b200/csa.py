@@ -53,7 +53,8 @@ class _PlanT(ctypes.Structure):
 EXPORTS = ["csa_calib_accumulate", "csa_compile_plan", "csa_build_work_list",
            "csa_sparse_attn_fwd", "csa_workspace_size", "csa_validate_plan", "csa_last_error",
            "csa_version", "csa_debug_trace", "csa_spatial_similarity", "csa_merge_intervals",
-           "csa_share_timesteps", "csa_copy_heads", "csa_calib_accumulate_sim"]
+           "csa_share_timesteps", "csa_copy_heads", "csa_calib_accumulate_sim",
+           "csa_sparse_attn_fwd_scatter"]
 
 _lib = None
 
@@ -89,6 +90,11 @@ def lib() -> ctypes.CDLL:
     L.csa_sparse_attn_fwd.argtypes = [_LayoutT, i32, i32, i32, ctypes.c_float, _TensorT, _TensorT,
                                       _TensorT, _TensorT, vp, ctypes.POINTER(_PlanT), i64, vp, vp,
                                       i32, i32, vp, ctypes.c_size_t, vp]
+    L.csa_sparse_attn_fwd_scatter.restype = st
+    L.csa_sparse_attn_fwd_scatter.argtypes = [_LayoutT, i32, i32, i32, ctypes.c_float, _TensorT,
+                                              _TensorT, _TensorT, vp, i32, i64, i64, i64, vp,
+                                              ctypes.POINTER(_PlanT), i64, vp, vp, i32, vp,
+                                              ctypes.c_size_t, vp]
     L.csa_spatial_similarity.restype = st
     L.csa_spatial_similarity.argtypes = [_LayoutT, i32, i32, ctypes.c_float, _TensorT, _TensorT,
                                          vp, i32, vp, vp, vp, ctypes.c_size_t, vp]
@@ -469,6 +475,33 @@ def sparse_attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: Pla
                                      0 if ws is None else ws.numel(), _stream(stream)),
            "csa_sparse_attn_fwd")
     return out
+
+
+def sparse_attn_fwd_scatter(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: Plan,
+                            work: WorkList, peer_ptrs: torch.Tensor, recv_like: torch.Tensor,
+                            cell_base: int = 0, lse_out: torch.Tensor | None = None,
+                            scale: float | None = None, stream=None) -> None:
+    """csa_sparse_attn_fwd_scatter: the attention of q/k/v [batch, N, heads, d] with each output
+    row stored into the receive buffer of the rank owning its token: peer_ptrs is a device int64
+    tensor [P] of pointers (this rank's first head inside each rank's [batch, N/P, H, d] receive
+    buffer), recv_like any tensor with the receive buffers' strides (the Ulysses return exchange
+    fused into the epilogue)."""
+    b, n, heads, d = q.shape
+    assert n == plan.lay.N and k.shape == q.shape and v.shape == q.shape
+    assert peer_ptrs.dtype == torch.int64 and peer_ptrs.is_cuda and peer_ptrs.dim() == 1
+    if lse_out is not None:
+        assert lse_out.dtype == torch.float32 and lse_out.numel() == b * heads * n
+    sc = default_scale(d) if scale is None else scale
+    s = plan.struct()
+    ws = _sched_workspace(q.device, lib().csa_workspace_size(3, _layout(plan.lay), heads, d), stream)
+    st_b, st_n, st_h, _ = recv_like.stride()
+    _check(lib().csa_sparse_attn_fwd_scatter(_layout(plan.lay), b, heads, d, sc, _tensor(q),
+                                             _tensor(k), _tensor(v), _ptr(peer_ptrs),
+                                             peer_ptrs.numel(), st_b, st_n, st_h, _ptr(lse_out),
+                                             ctypes.byref(s), cell_base, _ptr(work.items),
+                                             _ptr(work.n_work), work.max_work, _ptr(ws),
+                                             ws.numel(), _stream(stream)),
+           "csa_sparse_attn_fwd_scatter")
 
 
 _SCHED_WS: dict = {}

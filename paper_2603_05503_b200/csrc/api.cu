@@ -473,13 +473,18 @@ csa_status_t csa_build_work_list(csa_layout_t L, const csa_plan_t* plan, int64_t
     return ok();
 }
 
-csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
-                                 int32_t head_dim, float softmax_scale, csa_tensor_t q,
-                                 csa_tensor_t k, csa_tensor_t v, csa_tensor_t o, float* lse_out,
-                                 const csa_plan_t* plan, int64_t cell_base,
-                                 const uint32_t* work_list, const int32_t* n_work,
-                                 int32_t max_work, int32_t pair_items, void* workspace,
-                                 size_t workspace_bytes, csa_stream_t stream) {
+}  // extern "C"
+
+namespace {
+// csa_sparse_attn_fwd and csa_sparse_attn_fwd_scatter: o_peer == nullptr -> output in o;
+// otherwise token t's row goes to o_peer[t / (N / n_peers)] (device array of n_peers pointers)
+// at local token t % (N / n_peers), with o's strides.
+csa_status_t attn_fwd_impl(csa_layout_t L, int32_t batch, int32_t n_heads, int32_t head_dim,
+                           float softmax_scale, csa_tensor_t q, csa_tensor_t k, csa_tensor_t v,
+                           csa_tensor_t o, void* const* o_peer, int32_t n_peers, float* lse_out,
+                           const csa_plan_t* plan, int64_t cell_base, const uint32_t* work_list,
+                           const int32_t* n_work, int32_t max_work, int32_t pair_items,
+                           void* workspace, size_t workspace_bytes, csa_stream_t stream) {
     csa_status_t st = check_layout(L, head_dim, n_heads);
     if (st != CSA_OK) return st;
     if (pair_items)
@@ -499,9 +504,15 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
     if (cell_base < 0 || cell_base + n_heads > plan->n_cells)
         return fail(CSA_ERR_INVALID_ARGUMENT, "cells outside the plan");
     if (max_work < 0) return fail(CSA_ERR_INVALID_ARGUMENT, "max_work < 0");
-    if (!o.ptr || reinterpret_cast<uintptr_t>(o.ptr) % 16 || o.stride_n % 8 ||
-        (n_heads > 1 && o.stride_h % 8) || (batch > 1 && o.stride_b % 8))
+    if ((o_peer == nullptr && (!o.ptr || reinterpret_cast<uintptr_t>(o.ptr) % 16)) ||
+        o.stride_n % 8 || (n_heads > 1 && o.stride_h % 8) || (batch > 1 && o.stride_b % 8))
         return fail(CSA_ERR_INVALID_ARGUMENT, "o: null or not 16-byte aligned");
+    if (o_peer != nullptr) {
+        const int64_t n_tok = (int64_t)L.frames * L.rows * L.cols;
+        if (!b128 || n_peers < 1 || n_tok % n_peers != 0)
+            return fail(CSA_ERR_INVALID_ARGUMENT,
+                        "output scatter: block 128 and N divisible by n_peers (%d)", n_peers);
+    }
     if (!q.ptr || q.stride_n % 8 || (n_heads > 1 && q.stride_h % 8))
         return fail(CSA_ERR_INVALID_ARGUMENT, "q: null or strides not 16-byte multiples");
     DeviceInfo di;
@@ -532,6 +543,8 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
     a.work_list = work_list;
     a.n_work = n_work;
     a.sched = static_cast<uint32_t*>(workspace);
+    a.o_peer = reinterpret_cast<__nv_bfloat16* const*>(o_peer);
+    a.o_peer_tokens = o_peer ? (int64_t)g.N / n_peers : 0;
     const int64_t items = (int64_t)max_work * batch;
     const int grid = (int)(items < di.sms ? items : di.sms);
     cudaError_t e;
@@ -565,6 +578,41 @@ csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
     }
     if (e != cudaSuccess) return cuda_fail(e, "attention launch");
     return ok();
+}
+}  // namespace
+
+extern "C" {
+
+csa_status_t csa_sparse_attn_fwd(csa_layout_t L, int32_t batch, int32_t n_heads,
+                                 int32_t head_dim, float softmax_scale, csa_tensor_t q,
+                                 csa_tensor_t k, csa_tensor_t v, csa_tensor_t o, float* lse_out,
+                                 const csa_plan_t* plan, int64_t cell_base,
+                                 const uint32_t* work_list, const int32_t* n_work,
+                                 int32_t max_work, int32_t pair_items, void* workspace,
+                                 size_t workspace_bytes, csa_stream_t stream) {
+    return attn_fwd_impl(L, batch, n_heads, head_dim, softmax_scale, q, k, v, o, nullptr, 0,
+                         lse_out, plan, cell_base, work_list, n_work, max_work, pair_items,
+                         workspace, workspace_bytes, stream);
+}
+
+csa_status_t csa_sparse_attn_fwd_scatter(csa_layout_t L, int32_t batch, int32_t n_heads,
+                                         int32_t head_dim, float softmax_scale, csa_tensor_t q,
+                                         csa_tensor_t k, csa_tensor_t v, void* const* o_peers,
+                                         int32_t n_peers, int64_t o_stride_b, int64_t o_stride_n,
+                                         int64_t o_stride_h, float* lse_out,
+                                         const csa_plan_t* plan, int64_t cell_base,
+                                         const uint32_t* work_list, const int32_t* n_work,
+                                         int32_t max_work, void* workspace,
+                                         size_t workspace_bytes, csa_stream_t stream) {
+    if (o_peers == nullptr) return fail(CSA_ERR_INVALID_ARGUMENT, "o_peers is null");
+    csa_tensor_t o;
+    o.ptr = nullptr;
+    o.stride_b = o_stride_b;
+    o.stride_n = o_stride_n;
+    o.stride_h = o_stride_h;
+    return attn_fwd_impl(L, batch, n_heads, head_dim, softmax_scale, q, k, v, o, o_peers,
+                         n_peers, lse_out, plan, cell_base, work_list, n_work, max_work, 0,
+                         workspace, workspace_bytes, stream);
 }
 
 csa_status_t csa_validate_plan(const csa_plan_t* plan, csa_layout_t L, int64_t n_cells,

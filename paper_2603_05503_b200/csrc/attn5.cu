@@ -452,7 +452,6 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
                     dst_stride_rows = g.W;
                 }
             }
-            __nv_bfloat16* obase = a.o + (int64_t)it.b * a.o_sb + (int64_t)it.h * a.o_sh;
             const uint64_t inv2 = f2(inv, inv);
             {
                 constexpr int NO = D / CH;  // output columns of this thread's part (32 or 16)
@@ -475,7 +474,7 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
                 }
                 for (int32_t dI = 0; dI < n_dst; ++dI) {
                     uint4* dst = reinterpret_cast<uint4*>(
-                        obase + (tok0 + (int64_t)dI * dst_stride_rows) * a.o_sn + col);
+                        out_row(a, it.b, it.h, tok0 + (int64_t)dI * dst_stride_rows) + col);
 #pragma unroll
                     for (int v = 0; v < NO / 8; ++v)
                         dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2],

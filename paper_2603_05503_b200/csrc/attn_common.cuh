@@ -86,6 +86,19 @@ __device__ __forceinline__ TileList tile_list(const AttnArgs& a, const Item& it)
     return t;
 }
 
+// Address of the output row of token tok (batch b, head h): the local O tensor, or -- output
+// scatter -- the receive buffer of the rank that owns tok's sequence shard.
+__device__ __forceinline__ __nv_bfloat16* out_row(const AttnArgs& a, int32_t b, int32_t h,
+                                                  int64_t tok) {
+    __nv_bfloat16* base = a.o;
+    if (a.o_peer != nullptr) {
+        const int64_t p = tok / a.o_peer_tokens;
+        base = a.o_peer[p];
+        tok -= p * a.o_peer_tokens;
+    }
+    return base + (int64_t)b * a.o_sb + (int64_t)h * a.o_sh + tok * a.o_sn;
+}
+
 __device__ __forceinline__ int32_t anchor_row(int32_t H, int32_t k, int32_t m) {
     return (int32_t)(((int64_t)(2 * m + 1) * H) / (2 * k));
 }

@@ -436,9 +436,8 @@ __global__ void __launch_bounds__(SmemR<BKV, D>::kThreads, 1)
                     dst_stride_rows = g.W;
                 }
             }
-            __nv_bfloat16* obase = a.o + (int64_t)it.b * a.o_sb + (int64_t)it.h * a.o_sh;
-            uint32_t* park = tok0 >= 0 ? reinterpret_cast<uint32_t*>(obase + tok0 * a.o_sn)
-                                       : nullptr;
+            uint32_t* park =
+                tok0 >= 0 ? reinterpret_cast<uint32_t*>(out_row(a, it.b, it.h, tok0)) : nullptr;
             float m_ref = 0.0f, l_run = 0.0f, m_run = -INFINITY;
             bool have_ref = mode != 0, bad = false;
             if (mode == 2 && park != nullptr) m_ref = __uint_as_float(*park);
@@ -538,7 +537,7 @@ __global__ void __launch_bounds__(SmemR<BKV, D>::kThreads, 1)
                     }
                     for (int32_t dI = 0; dI < n_dst; ++dI) {
                         uint4* dst = reinterpret_cast<uint4*>(
-                            obase + (tok0 + (int64_t)dI * dst_stride_rows) * a.o_sn + col);
+                            out_row(a, it.b, it.h, tok0 + (int64_t)dI * dst_stride_rows) + col);
 #pragma unroll
                         for (int v = 0; v < 4; ++v)
                             dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1],

@@ -138,6 +138,12 @@ struct AttnArgs {
     const uint32_t* work_list;
     const int32_t* n_work;
     uint32_t* sched;  // [2] dynamic-scheduler counters (zero on entry and on exit) or nullptr
+    // Output scatter (csa_sparse_attn_fwd_scatter): when o_peer != nullptr, token t's output row
+    // goes to o_peer[t / o_peer_tokens] at local token t % o_peer_tokens (strides o_s*), i.e.
+    // straight into the sequence-sharded receive buffers of the ranks (Ulysses return exchange
+    // fused into the epilogue); o is unused then.
+    __nv_bfloat16* const* o_peer;
+    int64_t o_peer_tokens;
 };
 cudaError_t set_attn_trace(void* buf, int mode);
 cudaError_t launch_attn(const AttnArgs& a, int head_dim, const CUtensorMap& tq,
