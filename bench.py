@@ -55,6 +55,10 @@ def parse():
                          "(largest divisor of H/N up to 5)")
     ap.add_argument("--exchange", action="store_true",
                     help="run the head-sharded exchange path even at N = 1 (NCCL, one rank)")
+    ap.add_argument("--fused-out", action="store_true",
+                    help="exchange path with the return all-to-all fused into the attention "
+                         "epilogue (csa_sparse_attn_fwd_scatter into symmetric-memory receive "
+                         "buffers of every rank; SURVEY 8.6)")
     return ap.parse_args()
 
 
@@ -419,14 +423,14 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         torch.distributed.init_process_group("nccl", device_id=dev)
-    elif args.exchange:  # single-rank NCCL group: exercises the exchange path on one GPU
+    elif args.exchange or args.fused_out:  # single-rank NCCL group: the exchange path, 1 GPU
         import socket
         with socket.socket() as so:
             so.bind(("127.0.0.1", 0))
             port = so.getsockname()[1]
         torch.distributed.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}",
                                              rank=0, world_size=1, device_id=dev)
-    exchange = world > 1 or args.exchange
+    exchange = world > 1 or args.exchange or args.fused_out
     from paper_2603_05503_b200 import csa
 
     stream = torch.cuda.current_stream()
@@ -487,7 +491,12 @@ def main():
         def run_chunk(c, qh, kh, vh, o):  # heads c*hc .. of this rank: cells c*hc ..
             return csa.sparse_attn_fwd(qh, kh, vh, plan, works[c], cell_base=c * hc, out=o)
 
+        def run_scatter(qh, kh, vh, ptrs, recv):
+            csa.sparse_attn_fwd_scatter(qh, kh, vh, plan, work, ptrs, recv)
+
         def layer_step(a, b_, c_):
+            if args.fused_out:
+                return ulysses.make_layer_step_fused_out(a, b_, c_, world, run_scatter)
             if chunks == 1:
                 return ulysses.make_layer_step(a, b_, c_, world, run_heads)
             return ulysses.make_layer_step_chunked(a, b_, c_, world, run_chunk, chunks)
@@ -550,7 +559,10 @@ def main():
     }
     if exchange:
         result["config"]["exchange_overlap_chunks"] = chunks
-        result["config"]["exchange"] = "stacked QKV all_to_all_single (1 per chunk) + O return"
+        result["config"]["exchange"] = (
+            "stacked QKV all_to_all_single; O rows stored by the attention epilogue straight into "
+            "every rank's symmetric-memory receive buffer (return all-to-all fused)"
+            if args.fused_out else "stacked QKV all_to_all_single (1 per chunk) + O return")
         # roofline of the attention kernel on this rank (launches alone, no exchange), the
         # slowest rank's: achieved = its kept FLOPs / its mean launch time
         _, per_k, _ = time_loop(lambda: run_heads(qh0, kh0, vh0), args.steps, 2, stream)

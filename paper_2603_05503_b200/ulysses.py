@@ -195,6 +195,41 @@ def make_layer_step_chunked(q_loc, k_loc, v_loc, world: int, attention, chunks: 
     return step
 
 
+def make_layer_step_fused_out(q_loc, k_loc, v_loc, world: int, attention_scatter, group=None):
+    """One head-sharded layer whose RETURN exchange is fused into the attention epilogue (SURVEY
+    8.6 stretch): the output tensor [B, N/P, H, d] of every rank is a symmetric-memory buffer,
+    and the kernel (csa_sparse_attn_fwd_scatter) stores each finished output row of token t
+    straight into the buffer of the rank owning t's sequence shard, at this rank's head columns
+    -- over NVLink peer mappings, as the tiles complete.  The Q/K/V exchange stays the stacked
+    all_to_all_single of LayerExchange.  A device-side barrier of the symmetric buffers orders
+    the peers' stores before the consumer's reads (and the previous layer's reads before the
+    next stores).  attention_scatter(q, k, v, peer_ptrs, recv_like) runs this rank's heads.
+    Returns step() -> this rank's [B, N/P, H, d] (the symmetric buffer itself)."""
+    import torch.distributed._symmetric_memory as symm_mem
+
+    b, n_loc, h, d = q_loc.shape
+    hp = h // world
+    grp = group if group is not None else dist.group.WORLD
+    rank = dist.get_rank(grp)
+    ex = LayerExchange(b, n_loc, world, hp, d, q_loc.dtype, q_loc.device)
+    out = symm_mem.empty((b, n_loc, h, d), dtype=q_loc.dtype, device=q_loc.device)
+    hdl = symm_mem.rendezvous(out, grp.group_name)
+    esz = out.element_size()
+    # this rank's first head inside every rank's receive buffer
+    peer_ptrs = torch.tensor([int(hdl.buffer_ptrs[p]) + rank * hp * d * esz for p in range(world)],
+                             dtype=torch.int64, device=q_loc.device)
+
+    def step():
+        ex.pack((q_loc, k_loc, v_loc), world, hp, 0)
+        dist.all_to_all_single(ex.recv, ex.send, group=group)
+        hdl.barrier(channel=0)   # every peer is done reading its previous output
+        attention_scatter(ex.qkv(0), ex.qkv(1), ex.qkv(2), peer_ptrs, out)
+        hdl.barrier(channel=1)   # every peer's rows have landed in this rank's buffer
+        return out
+
+    return step
+
+
 class _Null:
     def __enter__(self):
         return self

@@ -379,6 +379,88 @@ def test_intervals_only_plan_full_size_and_validation(csa):
     csa.validate_plan(p_ivl)
 
 
+@pytest.mark.parametrize("lay,peers", [(Layout(2, 9, 40, 128), 1), (Layout(2, 9, 40, 128), 2),
+                                       (Layout(2, 9, 40, 128), 8), (Layout(3, 7, 100, 128), 4),
+                                       (Layout(2, 9, 40, 128, 80), 4)])
+def test_output_scatter_into_rank_buffers(csa, lay, peers):
+    """csa_sparse_attn_fwd_scatter with P "virtual ranks" on one GPU (the kernel only sees a
+    pointer table, local or peer-mapped alike): every output row lands in the receive buffer of
+    the rank owning its token, at this rank's head columns, bit for bit the rows of
+    csa_sparse_attn_fwd; other heads untouched.  REPETITIVE broadcast rows crossing shard
+    boundaries, batch 2, and the exact-max fallback passes (scores growing 40x block by block:
+    mode 1 parks each row's max in its first output row -- inside a rank's buffer -- and mode 2
+    reads it back)."""
+    hp, d, b = 3, 128, 2
+    rank = peers - 1                                  # this rank's heads: [rank hp, rank hp + hp)
+    H = hp * peers
+    n_loc = lay.N // peers
+    q, k, v = qkv(b, lay.N, hp, d, seed=23, device="cuda")
+    rng = np.random.default_rng(3)
+    masks = (rng.random((hp, lay.NB, lay.NBK)) < 0.5).astype(np.uint8)
+    masks[:, :, 0] = 1
+    for jump in (0.0, 40.0):
+        kk = k
+        if jump:
+            gain = torch.ones(lay.N, device="cuda")
+            for c in range(lay.NBK):
+                gain[c * lay.Bkv:(c + 1) * lay.Bkv] = 1.0 + jump * c / lay.NBK
+            kk = (k.float() * gain.view(1, -1, 1, 1)).to(torch.bfloat16)
+        plan = _plan_from_masks(csa, lay, masks, [] if jump else [1], 2, True)
+        work = csa.build_work_list(plan, 0, hp)
+        ref = csa.sparse_attn_fwd(q, kk, v, plan, work)
+        torch.cuda.synchronize()
+        nfb = fallback_count(csa, q)
+        bufs = [torch.zeros((b, n_loc, H, d), dtype=torch.bfloat16, device="cuda")
+                for _ in range(peers)]
+        ptrs = torch.tensor([t.data_ptr() + rank * hp * d * 2 for t in bufs], dtype=torch.int64,
+                            device="cuda")
+        csa.sparse_attn_fwd_scatter(q, kk, v, plan, work, ptrs, bufs[0])
+        torch.cuda.synchronize()
+        assert fallback_count(csa, q) == nfb and ((nfb > 0) == (jump > 0))
+        for p_, t in enumerate(bufs):
+            assert torch.equal(t[:, :, rank * hp:(rank + 1) * hp],
+                               ref[:, p_ * n_loc:(p_ + 1) * n_loc]), (jump, p_)
+            others = torch.cat([t[:, :, :rank * hp], t[:, :, (rank + 1) * hp:]], dim=2)
+            assert not others.any()
+
+
+def test_fused_out_layer_step_single_rank_nccl(csa):
+    """ulysses.make_layer_step_fused_out through a real NCCL group and symmetric memory (one
+    rank: the only peer is itself): the same output as the stacked-exchange layer step, bit for
+    bit, over repeated steps (the barriers order the buffer's reuse)."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2603_05503_b200 import ulysses
+    lay = Layout(3, 7, 100, 128)
+    H, d = 4, 128
+    q, k, v = qkv(2, lay.N, H, d, seed=29, device="cuda")
+    rng = np.random.default_rng(9)
+    masks = (rng.random((H, lay.NB, lay.NB)) < 0.5).astype(np.uint8)
+    masks[:, :, 0] = 1
+    plan = _plan_from_masks(csa, lay, masks, [2], 2, True)
+    work = csa.build_work_list(plan, 0, H)
+    ref = csa.sparse_attn_fwd(q, k, v, plan, work)
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        def attn(qv, kv, vv, ptrs, recv):
+            csa.sparse_attn_fwd_scatter(qv, kv, vv, plan, work, ptrs, recv)
+
+        step = ulysses.make_layer_step_fused_out(q, k, v, 1, attn)
+        for _ in range(3):
+            out = step()
+            torch.cuda.synchronize()
+            assert torch.equal(out, ref)
+            out.zero_()
+    finally:
+        dist.destroy_process_group()
+
+
 def sample_units(lay, heads, n, seed):
     rng = np.random.default_rng(seed)
     units = {(0, lay.NB - 1), (heads - 1, 0)}
