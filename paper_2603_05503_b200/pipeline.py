@@ -102,7 +102,8 @@ def calibrate(lay: Layout, T: int, L: int, H: int, prompts: int,
     Per (prompt, t, l): one csa_calib_accumulate_sim pass adds the prompt's per-row selections at
     eps(t) to the cells' keep counts (a2-a5) and its cosines to the similarity sums (f1).  Then s = sim_sum / (F H |D|), min_count = ceil(rho |D|) and one csa_compile_plan over
     every cell (a6; s > gamma -> REPETITIVE).  csr=False: an intervals-only dictionary (the
-    kernels walk the 1-D skip lists; ~1/8 of the CSR dictionary's bytes at 720p)."""
+    kernels walk the 1-D skip lists; 0.24 of the CSR plan bytes at Wan 720p: the
+    mask bits and row pointers remain)."""
     eps = epsilon_schedule(T, *constants)
     nb, nbk = lay.NB, lay.NBK  # query blocks x key blocks (non-square B_q x B_kv: P:1294-1328)
     cells = T * L * H
