@@ -66,3 +66,34 @@ def test_host_side_argument_checks(libcsa):
     L = libcsa._LayoutT(0, 5, 25, 64)
     assert lib.csa_compile_plan(L, 1, None, 1, None, 0.87, 5, 0, None, None, 0, None) == 1
     assert lib.csa_workspace_size(0, libcsa._LayoutT(2, 5, 25, 64), 1, 64) == 0
+
+
+def test_host_side_argument_checks_fused_and_scatter(libcsa):
+    """The round-2 entry points reject bad arguments before touching a device."""
+    lib = libcsa.lib()
+    T = libcsa._TensorT
+    z = T(None, 0, 0, 0)
+    L = libcsa._LayoutT(2, 9, 40, 128)
+    # csa_calib_accumulate_sim: anchor_k outside [1, rows], missing sim_sum, eps <= 0
+    st = lib.csa_calib_accumulate_sim(L, 2, 128, 0.088, z, z, 0.9, 1, None, None, 0, 1, None,
+                                      None, 0, None)
+    assert st == 1 and b"anchor_k" in lib.csa_last_error()
+    st = lib.csa_calib_accumulate_sim(L, 2, 128, 0.088, z, z, 0.9, 1, None, None, 3, None, None,
+                                      None, 0, None)
+    assert st == 1 and b"sim_sum" in lib.csa_last_error()
+    st = lib.csa_calib_accumulate_sim(L, 2, 128, 0.088, z, z, 0.0, 1, None, None, 3, 1, None,
+                                      None, 0, None)
+    assert st == 1 and b"eps" in lib.csa_last_error()
+    # csa_sparse_attn_fwd_scatter: no peer table; N not divisible by the peer count; block 64
+    plan = libcsa._PlanT()
+    st = lib.csa_sparse_attn_fwd_scatter(L, 1, 2, 128, 0.088, z, z, z, None, 2, 0, 256, 128,
+                                         None, None, 0, None, None, 1, None, 0, None)
+    assert st == 1 and b"o_peers" in lib.csa_last_error()
+    ptrs = ctypes.c_void_p(8)  # never dereferenced: the checks fail first
+    st = lib.csa_sparse_attn_fwd_scatter(L, 1, 2, 128, 0.088, z, z, z, ptrs, 2, 0, 256, 128,
+                                         None, ctypes.byref(plan), 0, ptrs, ptrs, 1, ptrs, 4096,
+                                         None)
+    assert st == 1  # null plan buffers
+    st = lib.csa_sparse_attn_fwd(L, 1, 2, 128, 0.088, z, z, z, z, None, ctypes.byref(plan), 0,
+                                 None, None, 1, 1, None, 0, None)
+    assert st == 2 and b"pair" in lib.csa_last_error()
