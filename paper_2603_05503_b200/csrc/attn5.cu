@@ -472,9 +472,15 @@ __global__ void __launch_bounds__(Smem5<D>::kThreads, 1)
                     const uint64_t v = fmul2(pk2(r0[x], r0[x + 1]), inv2);
                     packed[x / 2] = pack_bf16(lo_f(v), hi_f(v));
                 }
+                // local output: one base pointer per item; output scatter: out_row per row
+                __nv_bfloat16* obase = a.o_peer == nullptr
+                                           ? a.o + (int64_t)it.b * a.o_sb + (int64_t)it.h * a.o_sh
+                                           : nullptr;
                 for (int32_t dI = 0; dI < n_dst; ++dI) {
+                    const int64_t tok = tok0 + (int64_t)dI * dst_stride_rows;
                     uint4* dst = reinterpret_cast<uint4*>(
-                        out_row(a, it.b, it.h, tok0 + (int64_t)dI * dst_stride_rows) + col);
+                        (obase != nullptr ? obase + tok * a.o_sn : out_row(a, it.b, it.h, tok)) +
+                        col);
 #pragma unroll
                     for (int v = 0; v < NO / 8; ++v)
                         dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2],
