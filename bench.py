@@ -654,6 +654,26 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
                           "frac_of_sustained": round(achieved / pk["bf16_tflops_sustained"], 4),
                           "kernel": attention_kernel_name(lay, cfg.d),
                           "algorithmic_flop_per_launch": flop_all}
+    # ---- same-box context: cuBLAS bf16 GEMM burst on THIS box right now (the pool's
+    # MEASURED_PEAKS figure stays the roofline peak; boxes differ by several percent)
+    try:
+        ga = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+        gb = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+        best = None
+        for _ in range(12):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            torch.matmul(ga, gb)
+            e1.record(stream)
+            e1.synchronize()
+            t = e0.elapsed_time(e1)
+            best = t if best is None else min(best, t)
+        gemm = 2.0 * 8192 ** 3 / (best * 1e-3) / 1e12
+        result["roofline"]["same_box_bf16_gemm_tflops"] = round(gemm, 1)
+        result["roofline"]["frac_of_same_box_gemm"] = round(result["roofline"]["achieved"] / gemm, 4)
+        del ga, gb
+    except Exception as e:  # context only
+        result["roofline"]["same_box_bf16_gemm_tflops"] = f"unavailable: {e}"
     # ---- dense comparators: our kernel on an all-ones plan, and torch SDPA (cuDNN/flash)
     H, d, B = cfg.heads, cfg.d, args.batch
     ones = torch.full((H * lay.NB * lay.NB,), 64, dtype=torch.int16, device=dev).view(torch.uint16)
