@@ -1212,3 +1212,56 @@ def test_sharded_denoise_step_nccl_graph(csa, chunks):
                                      rep_k=5 if kind[t, l, h] else None, rows=rows)
                 assert_close(ref_o[l][b, rows[0]:rows[1], h].double().cpu().numpy(), ref,
                              f"t{t} l{l} h{h}")
+
+
+def test_max_block_grid_whole_path(csa):
+    """The largest grid the 16-bit skip lists allow: N_B = 2047 blocks (N = 262 016, one frame
+    of 2047 x 128 tokens).  Fused calibration + similarity (every row's selection bit-exact on
+    the pass's own E, sampled E rows and one cos(f, i) against the oracle), plan compile (the
+    MASK cell bit-exact against the oracle compiler), attention on the CSR and the
+    intervals-only plan (bitwise equal; sampled rows against the oracle)."""
+    lay = Layout(1, 2047, 128, 128)
+    assert lay.NB == 2047
+    heads, d, kA = 2, 128, 5
+    q, k, v = inputs.structured_qk(lay, heads, d, 7, 0, alpha=[1.3, 1.3], repetitive=(1,),
+                                   device="cuda")
+    nb = lay.NB
+    counts = u16_zeros(heads * nb * nb)
+    energy = torch.empty(heads * nb * nb, dtype=torch.float32, device="cuda")
+    sim = torch.zeros(heads, dtype=torch.float64, device="cuda")
+    cos = torch.empty(heads * lay.F * lay.H, dtype=torch.float32, device="cuda")
+    csa.calib_accumulate_sim(lay, q, k, 0.9, counts, kA, sim, energy_out=energy, cos_out=cos)
+    torch.cuda.synchronize()
+    E = energy.view(heads, nb, nb).double().cpu().numpy()
+    cnt = u16_np(counts).reshape(heads, nb, nb)
+    for h in range(heads):
+        for r in range(nb):
+            assert np.array_equal(oracle.select(E[h, r], 0.9), cnt[h, r]), (h, r)
+    scale = 1.0 / np.sqrt(d)
+    qh, kh = head64(q, 0, 0), head64(k, 0, 0)
+    for r in (0, nb - 1):
+        E_ref = oracle.block_energy(qh, kh, scale, lay.B, block_rows=(r, r + 1))
+        assert np.abs(E[0, r] - E_ref[0]).max() <= 5e-5, r
+    c_ref = oracle.spatial_cos(lay.F, lay.H, lay.W, qh, kh, scale, kA, 0, 1000)
+    assert abs(cos.view(heads, lay.H)[0, 1000].item() - c_ref) <= 2e-5
+    s = sim / float(lay.F * lay.H)
+    plans = {}
+    for csr in (True, False):
+        plans[csr] = csa.compile_plan(lay, counts, 1, similarity=s, gamma=0.87, anchor_k=kA,
+                                      csr=csr)
+        csa.validate_plan(plans[csr])
+    p = plans[True]
+    ref_cell = oracle.compile_cell(cnt[0], lay.N, lay.B, lay.F, lay.H, lay.W, 1)
+    assert np.array_equal(p.blk_row_ptr.cpu().numpy()[:nb + 1], ref_cell["blk_row_ptr"])
+    assert np.array_equal(u16_np(p.blk_idx)[:int(p.blk_base[1].item())], ref_cell["blk_idx"])
+    outs = [csa.sparse_attn_fwd(q, k, v, plans[c], csa.build_work_list(plans[c], 0, heads))
+            for c in (True, False)]
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    kinds = p.kind_host
+    mask0 = (cnt[0] >= 1).astype(np.uint8)
+    for h, r in ((0, 0), (0, nb // 2), (0, nb - 1), (1, 3)):
+        rows = (r * lay.B, min((r + 1) * lay.B, lay.N))
+        ref, _ = oracle_head(lay, q, k, v, 0, h, mask=mask0 if not kinds[h] else None,
+                             rep_k=kA if kinds[h] else None, rows=rows)
+        assert_close(outs[0][0, rows[0]:rows[1], h].double().cpu().numpy(), ref, f"h{h} r{r}")
