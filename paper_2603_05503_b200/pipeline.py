@@ -188,11 +188,16 @@ class ShardedDenoiseStep:
     NCCL calls included, in one CUDA graph.
 
     attention(t, l, c, q, k, v, out) replaces the kernel call (CPU gloo rehearsal of the schedule
-    in tests/: the oracle stands in for the kernel); default: csa_sparse_attn_fwd."""
+    in tests/: the oracle stands in for the kernel); default: csa_sparse_attn_fwd.
+
+    fused_out=True (CUDA, one head chunk): the return all-to-all is fused into the attention
+    epilogue (ulysses.make_layer_step_fused_out, csa_sparse_attn_fwd_scatter): the layer outputs
+    are symmetric-memory buffers owned by the step -- self.o[s] replaces the caller's o[s] (pass
+    o=None) -- written by every rank's kernel directly."""
 
     def __init__(self, dic_rank: PlanDictionary | None, world: int, q: list, k: list, v: list,
-                 o: list, chunks: int = 1, group=None, attention=None, T: int | None = None,
-                 L: int | None = None):
+                 o: list | None, chunks: int = 1, group=None, attention=None,
+                 T: int | None = None, L: int | None = None, fused_out: bool = False):
         self.dic, self.world, self.chunks, self.group = dic_rank, world, chunks, group
         self.T = dic_rank.T if dic_rank is not None else T
         self.L = dic_rank.L if dic_rank is not None else L
@@ -203,6 +208,7 @@ class ShardedDenoiseStep:
         self.hc = self.hp // chunks
         self.cur = (0, 0)
         cuda = q[0].is_cuda
+        library_kernel = attention is None
         if attention is None:
             if dic_rank is None or dic_rank.H != self.hp:
                 raise ValueError("the rank dictionary must hold H/P heads per (t, l)")
@@ -218,9 +224,27 @@ class ShardedDenoiseStep:
             t, l = self.cur
             self.attention(t, l, c, qh, kh, vh, out)
 
-        self.steps = [ulysses.make_layer_step_chunked(q[s], k[s], v[s], world, attn, chunks,
-                                                      group=group, out=o[s], comm=comm)
-                      for s in range(len(q))]
+        if fused_out:
+            if not cuda or chunks != 1 or not library_kernel:
+                raise ValueError("fused_out: CUDA tensors, chunks = 1, the library kernel")
+
+            def attn_scatter(qh, kh, vh, ptrs, recv):
+                t, l = self.cur
+                csa.sparse_attn_fwd_scatter(qh, kh, vh, self.dic.plan, self.work[t][l][0], ptrs,
+                                            recv, cell_base=self.dic.cell_base(t, l))
+
+            self.steps, self.o = [], []
+            for s_ in range(len(q)):
+                st = ulysses.make_layer_step_fused_out(q[s_], k[s_], v[s_], world, attn_scatter,
+                                                       group=group)
+                self.steps.append(st)
+                self.o.append(st.out)
+        else:
+            self.steps = [ulysses.make_layer_step_chunked(q[s_], k[s_], v[s_], world, attn,
+                                                          chunks, group=group, out=o[s_],
+                                                          comm=comm)
+                          for s_ in range(len(q))]
+            self.o = o
         self.graphs: dict = {}
 
     def _kernel(self, t, l, c, qh, kh, vh, out):

@@ -227,6 +227,7 @@ def make_layer_step_fused_out(q_loc, k_loc, v_loc, world: int, attention_scatter
         hdl.barrier(channel=1)   # every peer's rows have landed in this rank's buffer
         return out
 
+    step.out = out  # the symmetric output buffer (this rank's [B, N/P, H, d])
     return step
 
 

@@ -1138,7 +1138,7 @@ def test_rect_edge_layouts_calibrate_compile_attend(csa, lay):
     assert_close(out[0, :, 1].double().cpu().numpy(), ref1, "anchor head")
 
 
-@pytest.mark.parametrize("chunks", [1, 2])
+@pytest.mark.parametrize("chunks", [1, 2, 0])  # 0: return exchange fused into the epilogue
 def test_sharded_denoise_step_nccl_graph(csa, chunks):
     """f4 on the head-sharded runtime through a real NCCL group (one rank here; the exchange,
     chunk overlap and CUDA-graph capture of the NCCL calls are the N-rank code path): the
@@ -1170,9 +1170,12 @@ def test_sharded_denoise_step_nccl_graph(csa, chunks):
                             device_id=torch.device("cuda", 0))
     try:
         outs = [torch.empty_like(b[0]) for b in bufs]
+        fused = chunks == 0   # the return exchange fused into the epilogue (symmetric memory)
         step = pipeline.ShardedDenoiseStep(dic.shard(1, 0), 1, [b[0] for b in bufs],
-                                           [b[1] for b in bufs], [b[2] for b in bufs], outs,
-                                           chunks=chunks)
+                                           [b[1] for b in bufs], [b[2] for b in bufs],
+                                           None if fused else outs, chunks=max(chunks, 1),
+                                           fused_out=fused)
+        outs = step.o
         for t in range(T):
             single.run(t)
             step.run(t)
