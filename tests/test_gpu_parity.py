@@ -1268,3 +1268,110 @@ def test_max_block_grid_whole_path(csa):
         ref, _ = oracle_head(lay, q, k, v, 0, h, mask=mask0 if not kinds[h] else None,
                              rep_k=kA if kinds[h] else None, rows=rows)
         assert_close(outs[0][0, rows[0]:rows[1], h].double().cpu().numpy(), ref, f"h{h} r{r}")
+
+
+def _fuzz_cases(n=64, seed=2026):
+    """Seeded random attention problems: geometry (ragged N up to 4000), block 64 / 128, B_kv,
+    head_dim, heads, batch, mask density, an anchor head, CSR or intervals-only plan."""
+    rng = np.random.default_rng(seed)
+    cases = []
+    while len(cases) < n:
+        B = int(rng.choice([64, 128]))
+        BK = 0
+        if B == 128 and rng.random() < 0.4:
+            BK = int(rng.choice([64, 80, 96, 112, 144, 160, 176, 192]))
+        lay = Layout(int(rng.integers(1, 4)), int(rng.integers(1, 10)), int(rng.integers(5, 140)),
+                     B, BK)
+        if lay.N > 4000:
+            continue
+        heads = int(rng.integers(1, 4))
+        cases.append(dict(lay=lay, d=int(rng.choice([64, 128])), heads=heads,
+                          batch=int(rng.integers(1, 3)), dens=float(rng.uniform(0.03, 1.0)),
+                          rep=heads >= 2 and rng.random() < 0.5, csr=bool(rng.random() < 0.5),
+                          kA=int(rng.integers(1, lay.H + 1)), seed=int(rng.integers(1 << 20))))
+    return cases
+
+
+_FUZZ = _fuzz_cases()
+
+
+@pytest.mark.parametrize("case", range(len(_FUZZ)))
+def test_attention_fuzz_against_oracle(csa, case):
+    """Seeded random problems through compile + attention on every kernel (attn.cu at block 64,
+    attn5.cu, attn_rect.cu), every output row and LSE of every (batch, head) against the fp64
+    oracle on the plan's effective masks (rows emptied by a sparse random mask are repaired by
+    the compiler, reading Q7)."""
+    c = _FUZZ[case]
+    lay, d, heads, batch = c["lay"], c["d"], c["heads"], c["batch"]
+    q, k, v = qkv(batch, lay.N, heads, d, seed=c["seed"] % 997, device="cuda")
+    rng = np.random.default_rng(c["seed"])
+    masks = (rng.random((heads, lay.NB, lay.NBK)) < c["dens"]).astype(np.uint8)
+    reps = [heads - 1] if c["rep"] else []
+    plan = _plan_from_masks(csa, lay, masks, reps, c["kA"], c["csr"])
+    csa.validate_plan(plan)
+    bits = unpack_bits(plan.mask_bits.cpu().numpy(), lay.NBK).reshape(heads, lay.NB, lay.NBK)
+    lse = torch.empty(batch * heads * lay.N, dtype=torch.float32, device="cuda")
+    out = csa.sparse_attn_fwd(q, k, v, plan, csa.build_work_list(plan, 0, heads), lse_out=lse)
+    torch.cuda.synchronize()
+    lse = lse.view(batch, heads, lay.N).cpu().numpy()
+    for b in range(batch):
+        for h in range(heads):
+            rep = h in reps
+            ref, ref_lse = oracle_head(lay, q, k, v, b, h, mask=None if rep else bits[h],
+                                       rep_k=c["kA"] if rep else None)
+            assert_close(out[b, :, h].double().cpu().numpy(), ref, f"{c} b{b} h{h}")
+            assert np.abs(lse[b, h] - ref_lse).max() <= 1e-3, (c, b, h)
+
+
+
+def _calib_fuzz_cases(n=16, seed=77):
+    rng = np.random.default_rng(seed)
+    cases = []
+    while len(cases) < n:
+        B = int(rng.choice([64, 128, 128]))
+        BK = 0
+        if B == 128 and rng.random() < 0.25:
+            BK = int(rng.choice([64, 80, 144, 192]))
+        lay = Layout(int(rng.integers(1, 4)), int(rng.integers(1, 8)), int(rng.integers(5, 120)),
+                     B, BK)
+        if lay.N > 2000:
+            continue
+        d = 128 if BK else int(rng.choice([64, 128]))
+        cases.append(dict(lay=lay, d=d, heads=int(rng.integers(1, 3)),
+                          eps=float(rng.uniform(0.5, 0.99)), kA=int(rng.integers(1, lay.H + 1)),
+                          alpha=float(rng.uniform(0.6, 1.6)), seed=int(rng.integers(1 << 20))))
+    return cases
+
+
+_CFUZZ = _calib_fuzz_cases()
+
+
+@pytest.mark.parametrize("case", range(len(_CFUZZ)))
+def test_calib_sim_fuzz_against_oracle(csa, case):
+    """Seeded random problems through csa_calib_accumulate_sim (the fused kernel at block 128 x
+    128, the two calls' kernels otherwise): E within 5e-5 of the oracle, every row's selection
+    bit-exact on the pass's own E, every cos(f, i) within 2e-5."""
+    c = _CFUZZ[case]
+    lay, d, heads, kA = c["lay"], c["d"], c["heads"], c["kA"]
+    q, k, _ = inputs.structured_qk(lay, heads, d, c["seed"] % 101, 0, alpha=[c["alpha"]] * heads,
+                                   repetitive=(), device="cuda")
+    nb, nbk = lay.NB, lay.NBK
+    cnt = u16_zeros(heads * nb * nbk)
+    E_t = torch.empty(heads * nb * nbk, dtype=torch.float32, device="cuda")
+    sim = torch.zeros(heads, dtype=torch.float64, device="cuda")
+    cos_t = torch.empty(heads * lay.F * lay.H, dtype=torch.float32, device="cuda")
+    csa.calib_accumulate_sim(lay, q, k, c["eps"], cnt, kA, sim, energy_out=E_t, cos_out=cos_t)
+    torch.cuda.synchronize()
+    E = E_t.view(heads, nb, nbk).double().cpu().numpy()
+    counts = u16_np(cnt).reshape(heads, nb, nbk)
+    cos = cos_t.view(heads, lay.F, lay.H).double().cpu().numpy()
+    scale = 1.0 / np.sqrt(d)
+    for h in range(heads):
+        qh, kh = head64(q, 0, h), head64(k, 0, h)
+        E_ref = oracle.block_energy(qh, kh, scale, lay.B, block_kv=lay.BK or None)
+        assert np.abs(E[h] - E_ref).max() <= 5e-5, (c, h)
+        for r in range(nb):
+            assert np.array_equal(oracle.select(E[h, r], c["eps"]), counts[h, r]), (c, h, r)
+        ref = np.array([[oracle.spatial_cos(lay.F, lay.H, lay.W, qh, kh, scale, kA, f, i)
+                         for i in range(lay.H)] for f in range(lay.F)])
+        assert np.abs(cos[h] - ref).max() <= 2e-5, (c, h)
