@@ -15,6 +15,13 @@
  *                            launch's (head, query-block) items.
  *   csa_sparse_attn_fwd   -- block-sparse attention forward over the kept blocks and
  *                            anchor-row attention + broadcast for repetitive heads.
+ * Also: csa_calib_accumulate_sim (calibration statistics and the repetitive-head similarity
+ * statistic, in one pass), csa_spatial_similarity (the statistic alone, from a given
+ * LSE), csa_merge_intervals / csa_share_timesteps (plan compaction),
+ * csa_sparse_attn_fwd_scatter (attention whose output rows go straight to the ranks' receive
+ * buffers: the head-sharded layer's return exchange fused into the epilogue), csa_validate_plan,
+ * csa_copy_heads, csa_workspace_size.  Plans may omit the CSR index (intervals-only: the kernels
+ * walk the 1-D interval lists).
  *
  * Conventions (all entry points):
  *   - Ownership: the caller owns every buffer (e.g. torch.empty on the device); the library never
@@ -31,8 +38,9 @@
  *   - Supported: sm_100 devices; head_dim in {64, 128}; block in {64, 128}; N_B <= 2047.
  *   - Non-square blocks (block_kv != 0 and != block): every entry point accepts block 128,
  *     block_kv a multiple of 16 in [64, 192], N_Bkv <= 2047 (head_dim 128 for calibration and
- *     attention; csa_sparse_attn_fwd then needs its workspace).  csa_spatial_similarity ignores
- *     block_kv (the statistic is defined over all N keys).
+ *     attention; csa_sparse_attn_fwd then needs its workspace).  csa_spatial_similarity (and the
+ *     similarity part of csa_calib_accumulate_sim) ignores block_kv (the statistic is defined
+ *     over all N keys).
  *     Everywhere below, "N_B x N_B" of a plan or keep-count cell reads "N_B x N_Bkv" (rows are
  *     query blocks, columns key blocks), and mask rows hold ceil(N_Bkv/32) words.
  */
