@@ -95,7 +95,8 @@ class PlanDictionary:
 def calibrate(lay: Layout, T: int, L: int, H: int, prompts: int,
               qk_fn: Callable[[int, int, int], tuple[torch.Tensor, torch.Tensor]],
               constants: tuple[float, float, float], rho: float = 0.5, gamma: float = 0.87,
-              anchor_k: int = 5, device="cuda", csr: bool = True) -> PlanDictionary:
+              anchor_k: int = 5, device="cuda", csr: bool = True,
+              heads: list | None = None) -> PlanDictionary:
     """Offline calibration of the whole dictionary.
 
     qk_fn(prompt, t, l) -> conditional-branch Q, K bf16 [1, N, H, d] of that layer at that step.
@@ -103,9 +104,17 @@ def calibrate(lay: Layout, T: int, L: int, H: int, prompts: int,
     eps(t) to the cells' keep counts (a2-a5) and its cosines to the similarity sums (f1).  Then s = sim_sum / (F H |D|), min_count = ceil(rho |D|) and one csa_compile_plan over
     every cell (a6; s > gamma -> REPETITIVE).  csr=False: an intervals-only dictionary (the
     kernels walk the 1-D skip lists; 0.24 of the CSR plan bytes at Wan 720p: the
-    mask bits and row pointers remain)."""
+    mask bits and row pointers remain).
+
+    heads: head-sharded calibration (BASELINE configs[4]) -- this rank calibrates and
+    compiles only the cells of these heads of qk_fn's H (in this order), with no collective; the
+    result equals calibrate(...).shard(P, r, perm) bit for bit (every step is cell-local)."""
     eps = epsilon_schedule(T, *constants)
     nb, nbk = lay.NB, lay.NBK  # query blocks x key blocks (non-square B_q x B_kv: P:1294-1328)
+    sel = None
+    if heads is not None:
+        sel = torch.tensor(list(heads), dtype=torch.long, device=device)
+        H = len(heads)
     cells = T * L * H
     keep = torch.zeros(cells * nb * nbk, dtype=torch.int16, device=device).view(torch.uint16)
     sim_sum = torch.zeros(cells, dtype=torch.float64, device=device)
@@ -114,6 +123,8 @@ def calibrate(lay: Layout, T: int, L: int, H: int, prompts: int,
         for t in range(T):
             for l in range(L):
                 q, k = qk_fn(p, t, l)
+                if sel is not None:  # this rank's heads (a model's head-sharded projections)
+                    q, k = q.index_select(2, sel), k.index_select(2, sel)
                 c0 = (t * L + l) * H
                 csa.calib_accumulate_sim(lay, q, k, eps[t],
                                          keep[c0 * nb * nbk:c0 * nb * nbk + per], anchor_k,

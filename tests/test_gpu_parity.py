@@ -1375,3 +1375,33 @@ def test_calib_sim_fuzz_against_oracle(csa, case):
         ref = np.array([[oracle.spatial_cos(lay.F, lay.H, lay.W, qh, kh, scale, kA, f, i)
                          for i in range(lay.H)] for f in range(lay.F)])
         assert np.abs(cos[h] - ref).max() <= 2e-5, (c, h)
+
+
+
+def test_head_sharded_calibration_equals_the_dictionary_shard(csa):
+    """pipeline.calibrate(heads=...) on each rank's heads (no collective) gives the same keep
+    counts, similarity and compiled plans as the full dictionary's shard, bit for bit."""
+    from paper_2603_05503_b200 import pipeline
+    lay = Layout(2, 9, 40, 128)
+    T, L, H, d, prompts = 2, 2, 4, 128, 2
+
+    def qk(p, t, l):
+        q, k, _ = inputs.structured_qk(lay, H, d, head_seed=10 * t + l, prompt_seed=p,
+                                       alpha=[2.0, 1.6, 1.1, 1.4], repetitive=(2,), device="cuda")
+        return q, k
+
+    full = pipeline.calibrate(lay, T, L, H, prompts, qk, pipeline.DISTILLED, gamma=0.95)
+    perm = [0, 3, 1, 2]
+    for r in range(2):
+        mine = perm[2 * r:2 * r + 2]
+        part = pipeline.calibrate(lay, T, L, H, prompts, qk, pipeline.DISTILLED, gamma=0.95,
+                                  heads=mine)
+        ref = full.shard(2, r, perm)
+        torch.cuda.synchronize()
+        assert torch.equal(part.keep_count.view(torch.int16), ref.keep_count.view(torch.int16))
+        assert torch.equal(part.similarity, ref.similarity)
+        for name in ("kind", "anchor_k", "mask_bits", "blk_row_ptr", "blk_idx", "ivl", "kept_area"):
+            a, b = getattr(part.plan, name), getattr(ref.plan, name)
+            if a.dtype == torch.uint16:
+                a, b = a.view(torch.int16), b.view(torch.int16)
+            assert torch.equal(a, b), (r, name)
