@@ -1,7 +1,6 @@
 """The bench line contract (task README / SURVEY 8.5) checked on the committed round-end lines in
 profiles/ (CPU: no GPU needed to read them): required keys, units, the roofline object computed
 from the algorithmic FLOPs, the parity gate, the CPU baseline and the end-to-end measurement."""
-import glob
 import json
 import os
 
