@@ -1,6 +1,8 @@
 """Host-side logic on CPU: the synthetic plan generator (generator S) on square and non-square
 grids, the bench's FLOP accounting against the oracle compiler's kept area, and the head
 balancing used by the multi-GPU bench."""
+import os
+
 import numpy as np
 import pytest
 
@@ -64,3 +66,19 @@ def test_balance_heads_on_bench_costs():
         nat = [sum(cost[r * hp:(r + 1) * hp]) for r in range(world)]
         assert sorted(perm) == list(range(cfg.heads))
         assert max(loads) <= max(nat) and max(loads) / (sum(cost) / world) < 1.03
+
+
+def test_bench_multi_gpu_request_fails_loudly_without_gpus():
+    """`bench.py --gpus 2` outside torchrun with fewer than 2 visible GPUs must refuse (never
+    report a smaller job under a larger n_gpus)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    res = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                          "--steps", "1", "--warmup", "3"], capture_output=True, text=True,
+                         env=env, timeout=300)
+    assert res.returncode != 0
+    assert "refusing" in res.stderr + res.stdout
