@@ -14,7 +14,7 @@ cfg = inputs.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "wan720"]
 lay = cfg.layout
 masks = inputs.synthetic_masks(lay, cfg.heads, cfg.sparsity or 0.69, seed=0)
 cnt = torch.from_numpy((masks.astype(np.uint16) * np.uint16(64)).reshape(-1).view(np.int16)).cuda()
-plan = csa.compile_plan(lay, cnt.view(torch.uint16), 32)
+plan = csa.compile_plan(lay, cnt.view(torch.uint16), 32, csr=os.environ.get("CSR", "1") == "1")
 work = csa.build_work_list(plan, 0, cfg.heads, order=int(os.environ.get("ORDER", "3")))
 D = int(os.environ.get("D", cfg.d))
 q, k, v = inputs.qkv(1, lay.N, cfg.heads, D, seed=11, device="cuda")
