@@ -606,7 +606,10 @@ def main():
     if rank == 0 and not exchange and not args.no_extras:
         extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_all, dense_flop,
                kept_fraction, per, pk, stream, dev, csa)
-        result["cpu_baseline"] = cpu_base
+        result["cpu_baseline"] = dict(cpu_base)
+        # extrapolated, not measured: the whole layer's kept FLOPs at the sampled rate
+        result["cpu_baseline"]["extrapolated_layer_s_all_threads"] = round(
+            flop_all / (cpu_base["value"] * 1e12), 1)
     if rank == 0:
         if not parity["pass"]:  # a perf number without passing parity is not reported
             result["value"] = None
