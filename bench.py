@@ -752,9 +752,18 @@ def extras(result, args, cfg, lay, masks, rep, plan, work, q, k, v, out, flop_al
     work_iv = csa.build_work_list(plan_iv, 0, H, order=csa.default_order(lay, d))
     if q.shape[2] == H:  # single-GPU layout (the exchange path holds rank-local views)
         out_iv = torch.empty_like(out)
-        t_iv, _, _ = time_loop(lambda: csa.sparse_attn_fwd(q, k, v, plan_iv, work_iv, out=out_iv),
-                               max(2, args.steps // 2), 2, stream)
-        ph["attn_ms_intervals_only_plan"] = round(t_iv / max(2, args.steps // 2), 3)
+        # alternating A/B (CSR plan, intervals-only plan) so both see the same clocks
+        reps = max(2, args.steps // 2)
+        t_cs, t_ivs = [], []
+        for _ in range(3):
+            t_a, _, _ = time_loop(lambda: csa.sparse_attn_fwd(q, k, v, plan, work, out=out_iv),
+                                  reps, 1, stream)
+            t_b, _, _ = time_loop(lambda: csa.sparse_attn_fwd(q, k, v, plan_iv, work_iv,
+                                                              out=out_iv), reps, 1, stream)
+            t_cs.append(t_a / reps)
+            t_ivs.append(t_b / reps)
+        ph["attn_ms_csr_plan_alternating"] = round(statistics.median(t_cs), 3)
+        ph["attn_ms_intervals_only_plan"] = round(statistics.median(t_ivs), 3)
         ph["intervals_only_output_bitwise_equal"] = bool(torch.equal(
             out_iv, csa.sparse_attn_fwd(q, k, v, plan, work, out=torch.empty_like(out))))
     ph["plan_bytes_intervals_only"] = plan_iv.nbytes()
